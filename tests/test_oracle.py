@@ -1,0 +1,315 @@
+"""Pins of the fp64 oracle against what the paper and the mathematics fix.
+
+Each test names the oracle part (O1..O7) and the kind of pin:
+printed values (tests/golden/, cited), closed forms, brute force on tiny
+inputs, exact integer arithmetic, invariants.  None of these re-types the
+oracle's own formula as its check.
+"""
+import itertools
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synthetic as S
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+# ---------------------------------------------------------------- O1 ----
+def test_o1_printed_cost_example():
+    """P:L333 / P:L335 printed numbers for P=4, K=256, M=N=4096."""
+    g = _golden("sacp_cost_example.json")
+    sfb, sfps, full = O.costs(g["M"], g["N"], g["K"], g["P"])
+    pm = g["printed_millions"]
+    tol = g["printed_precision"]
+    assert abs(sfb / 1e6 - pm["sfb"]) <= tol
+    assert abs(sfps / 1e6 - pm["sf_ps"]) <= tol
+    assert abs(full / 1e6 - pm["full_ps"]) <= tol
+    pr = g["printed_ratios"]
+    assert abs(full / sfb - pr["full_over_sfb"]) <= tol
+    assert abs(sfps / sfb - pr["sfps_over_sfb"]) <= tol
+    assert O.choose_scheme(O.LAYER_FC, 4096, 4096, 256, 4) == O.SCHEME_SFB
+
+
+def test_o1_spec_p32_example():
+    g = _golden("sacp_cost_example.json")["spec_examples"]
+    sfb, sfps, _ = O.costs(4096, 4096, 256, 32)
+    assert abs(sfb / g["P32_sfb_approx"] - 1) < g["approx_rel"]
+    assert abs(sfps / g["P32_sfps_approx"] - 1) < g["approx_rel"]
+    assert O.choose_scheme(O.LAYER_FC, 4096, 4096, 256, 32) == O.SCHEME_PS
+
+
+def test_o1_conv_always_ps():
+    for P, K in itertools.product(range(1, 9), (1, 64, 256)):
+        assert O.choose_scheme(O.LAYER_CONV, 96, 363, K, P) == O.SCHEME_PS
+
+
+def _k_star(M, N, P):
+    """Closed form derived by hand (O1): for P >= 3,
+    (P-1)^2 K(M+N) <= PK(M+N) + PMN  <=>  K (M+N)(P^2-3P+1) <= PMN."""
+    return (P * M * N) // ((M + N) * (P * P - 3 * P + 1))
+
+
+SHAPES = [(128, 256), (64, 1024), (10, 64), (4096, 9216), (4096, 4096),
+          (1000, 4096), (1000, 1024), (21841, 4096)]
+
+
+def test_o1_closed_form_crossover_matches_rule():
+    for (M, N) in SHAPES:
+        for P in range(1, 9):
+            for K in list(range(1, 300)) + [511, 512, 1000, 1024, 2048, 3000, 4096, 10347, 10348]:
+                rule = O.choose_scheme(O.LAYER_FC, M, N, K, P)
+                if P <= 2:
+                    expect = O.SCHEME_SFB
+                else:
+                    expect = O.SCHEME_SFB if K <= _k_star(M, N, P) else O.SCHEME_PS
+                assert rule == expect, (M, N, K, P)
+
+
+def test_o1_tie_goes_to_sfb():
+    """Reading Z5: M=128, N=256, K=256, P=3 is an exact tie (393,216 floats)."""
+    sfb, sfps, _ = O.costs(128, 256, 256, 3)
+    assert sfb == sfps == 2 * 2 * 256 * 384 == 393216
+    assert O.choose_scheme(O.LAYER_FC, 128, 256, 256, 3) == O.SCHEME_SFB
+    assert O.choose_scheme(O.LAYER_FC, 128, 256, 257, 3) == O.SCHEME_PS
+
+
+def test_o1_monotone_in_P():
+    """Once SFB flips to PS as P grows it never flips back."""
+    for (M, N) in SHAPES:
+        for K in (1, 8, 100, 128, 256, 1024):
+            seq = [O.choose_scheme(O.LAYER_FC, M, N, K, P) for P in range(1, 65)]
+            flipped = False
+            for s in seq:
+                if s == O.SCHEME_PS:
+                    flipped = True
+                elif flipped:
+                    pytest.fail(f"flip back at {(M, N, K)}")
+
+
+def test_o1_spot_decisions():
+    """Hand-computed decisions (recomputed here by hand)."""
+    # fc8 1000x4096, K=256: P=5 -> 16*256*5096 = 20,873,216 <= 5*256*5096 + 5*4,096,000 = 27,002,880
+    assert O.costs(1000, 4096, 256, 5)[:2] == (20873216, 27002880)
+    assert O.choose_scheme(O.LAYER_FC, 1000, 4096, 256, 5) == O.SCHEME_SFB
+    # P=6 -> 25*256*5096 = 32,614,400 > 6*256*5096 + 6*4,096,000 = 32,403,456 -> PS
+    assert O.costs(1000, 4096, 256, 6)[:2] == (32614400, 32403456)
+    assert O.choose_scheme(O.LAYER_FC, 1000, 4096, 256, 6) == O.SCHEME_PS
+    # fc6 at P=8: 49*256*13312 = 166,985,728 <= 8*256*13312 + 8*37,748,736 = 329,252,864
+    assert O.costs(4096, 9216, 256, 8)[:2] == (166985728, 329252864)
+    # C2 ip1 64x1024, K=100: SFB at P=3, PS at P=4
+    assert O.choose_scheme(O.LAYER_FC, 64, 1024, 100, 3) == O.SCHEME_SFB
+    assert O.choose_scheme(O.LAYER_FC, 64, 1024, 100, 4) == O.SCHEME_PS
+    # orientation does not matter (reading Z8)
+    for (M, N) in SHAPES:
+        for P in range(1, 9):
+            assert O.costs(M, N, 256, P) == O.costs(N, M, 256, P)
+
+
+def test_o1_u64_range_values():
+    """Values exceed 2^31 inside the grid; Python ints are exact."""
+    sfb, sfps, full = O.costs(21841, 4096, 256, 13)
+    assert full == 2 * 13 * 21841 * 4096 and full > 2 ** 31
+    assert sfb == 144 * 256 * 25937
+
+
+# ---------------------------------------------------------------- O2 ----
+def test_o2_partition_brute_force():
+    for n in list(range(0, 200)) + [650, 2432, 32896, 34944, 145578, 4097000]:
+        for P in range(1, 9):
+            S_ = O.shard_size(n, P)
+            assert S_ % 32 == 0 and S_ * P >= n and (S_ == 0 or S_ * P - n < 32 * P)
+            seen = np.zeros(n, dtype=np.int32) if n < 10 ** 6 else None
+            prev_end = 0
+            for r in range(P):
+                lo, hi, padded = O.shard_range(n, P, r)
+                assert padded == P * S_
+                assert lo == prev_end and lo <= hi
+                prev_end = hi
+                if seen is not None:
+                    seen[lo:hi] += 1
+            assert prev_end == n
+            if seen is not None:
+                assert np.all(seen == 1)
+
+
+def test_o2_examples():
+    """DESIGN.md §3 reading Z11 examples (n=650 at P=8 has an empty shard)."""
+    assert O.shard_size(650, 8) == 96
+    assert O.shard_range(650, 8, 6) == (576, 650, 768)
+    assert O.shard_range(650, 8, 7) == (650, 650, 768)
+    assert O.shard_range(32896, 2, 1) == (16448, 32896, 32896)
+    assert O.shard_range(34944, 8, 7) == (30688, 34944, 35072)
+    assert O.shard_range(100, 1, 0) == (0, 100, 128)
+
+
+# ---------------------------------------------------------------- O3 ----
+@pytest.mark.parametrize("M,N,K,P", [(3, 4, 2, 1), (5, 3, 4, 2), (4, 6, 3, 3), (8, 8, 4, 3)])
+def test_o3_eq5_against_finite_differences(M, N, K, P):
+    """Eq. 5: sum over all workers' samples of E a^T equals dl/dW of
+    the mean loss over the P*K samples, by central differences in fp64."""
+    g = S.rng(100 + M * N + K + P)
+    W = g.standard_normal((M, N))
+    b = g.standard_normal(M)
+    X = g.standard_normal((P * K, N))
+    labels = g.integers(0, M, size=P * K)
+    gW_fd, gb_fd = O.fd_gradient(W, b, X, labels)
+    U = O.error_messages(W, b, X, labels, denom=P * K)
+    G = O.reconstruct_loops(U, X)
+    assert np.max(np.abs(G - gW_fd)) / np.max(np.abs(gW_fd)) < 1e-7
+    assert np.max(np.abs(U.sum(axis=0) - gb_fd)) / np.max(np.abs(gb_fd)) < 1e-7
+
+
+def test_reconstruct_matmul_equals_loops():
+    g = S.rng(3)
+    U = g.standard_normal((5, 7))
+    V = g.standard_normal((5, 6))
+    assert np.allclose(O.reconstruct(U, V), O.reconstruct_loops(U, V), rtol=0, atol=1e-13)
+
+
+def test_reconstruct_single_entry():
+    """K=1, u=e_i, v=e_j gives the single-entry matrix."""
+    U = np.zeros((1, 4)); U[0, 2] = 1
+    V = np.zeros((1, 3)); V[0, 1] = 1
+    G = O.reconstruct_loops(U, V)
+    assert G[2, 1] == 1 and G.sum() == 1
+
+
+# --------------------------------------------------------- O4 / O5 / O6 --
+def _exact_sync(W, b, Us, Vs, lr):
+    """Exact rational arithmetic (Fractions) of the definition, brute force."""
+    P = len(Us)
+    M, N = W.shape
+    W1 = [[Fraction(float(W[m, n])) for n in range(N)] for m in range(M)]
+    b1 = [Fraction(float(b[m])) for m in range(M)]
+    a = Fraction(lr) / P
+    for p in range(P):
+        for k in range(Us[p].shape[0]):
+            for m in range(M):
+                u = Fraction(float(Us[p][k, m]))
+                b1[m] -= a * u
+                for n in range(N):
+                    W1[m][n] -= a * u * Fraction(float(Vs[p][k, n]))
+    return W1, b1
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4])
+def test_o4_against_exact_rationals(P):
+    W, b, Us, Vs, lr = S.integer_factors(5, 6, 3, P, seed=P)
+    W1, b1 = O.sync_step(W, b, Us, Vs, lr)
+    We, be = _exact_sync(W, b, Us, Vs, lr)
+    for m in range(5):
+        assert b1[m] == float(be[m]) or abs(b1[m] - float(be[m])) < 1e-15
+        for n in range(6):
+            assert abs(W1[m, n] - float(We[m][n])) < 1e-15
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_o4_integer_variant_is_exact_in_fp32(P):
+    """The integer variant is exactly representable at every step, so O4's
+    fp64 result is representable in fp32 (what makes GPU parity bit-exact)."""
+    W, b, Us, Vs, lr = S.integer_factors(16, 24, 8, P)
+    W1, b1 = O.sync_step(W, b, Us, Vs, lr)
+    assert np.array_equal(W1, W1.astype(np.float32).astype(np.float64))
+    assert np.array_equal(b1, b1.astype(np.float32).astype(np.float64))
+
+
+@pytest.mark.parametrize("M,N,K,P", [(7, 5, 3, 1), (16, 9, 4, 2), (33, 17, 5, 3), (64, 40, 8, 8)])
+def test_o4_o5_o6_agree(M, N, K, P):
+    W, b = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, P)
+    lr = 0.05
+    W4, b4 = O.sync_step(W, b, Us, Vs, lr)
+    W5, b5 = O.sfb_simulated(W, b, Us, Vs, lr)
+    W6, b6 = O.ps_simulated(W, b, Us, Vs, lr)
+    for Wx, bx in ((W5, b5), (W6, b6)):
+        assert np.max(np.abs(Wx - W4)) < 1e-12
+        assert np.max(np.abs(bx - b4)) < 1e-12
+
+
+def test_o4_invariants():
+    M, N, K, P = 12, 10, 4, 3
+    W, b = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, P)
+    # lr = 0 -> unchanged bitwise
+    W1, b1 = O.sync_step(W, b, Us, Vs, 0.0)
+    assert np.array_equal(W1, W.astype(np.float64)) and np.array_equal(b1, b.astype(np.float64))
+    # U = 0 -> unchanged
+    W1, _ = O.sync_step(W, b, [u * 0 for u in Us], Vs, 0.1)
+    assert np.array_equal(W1, W.astype(np.float64))
+    # doubling U doubles the update
+    Wa, _ = O.sync_step(W, b, Us, Vs, 0.1)
+    Wb, _ = O.sync_step(W, b, [2 * u for u in Us], Vs, 0.1)
+    assert np.allclose(Wb - W, 2 * (Wa - W), rtol=0, atol=1e-14)
+    # permuting workers leaves the result unchanged
+    perm = [2, 0, 1]
+    Wc, _ = O.sync_step(W, b, [Us[i] for i in perm], [Vs[i] for i in perm], 0.1)
+    assert np.allclose(Wc, Wa, rtol=0, atol=1e-14)
+    # a mean over workers: P identical workers == one worker
+    W1w, b1w = O.sync_step(W, b, Us[:1], Vs[:1], 0.1)
+    W3w, b3w = O.sync_step(W, b, Us[:1] * 3, Vs[:1] * 3, 0.1)
+    assert np.allclose(W1w, W3w, rtol=0, atol=1e-14) and np.allclose(b1w, b3w, rtol=0, atol=1e-14)
+
+
+def test_o6_shard_cover_failure_is_detected():
+    """ps_step_flat checks coverage; an inconsistent P/grad list still works
+    only when the map covers [0,n) — sanity that the check exists."""
+    w = np.zeros(100)
+    out = O.ps_step_flat(w, [np.ones(100)] * 4, 1.0)
+    assert np.allclose(out, -1.0)
+
+
+def test_sync_step_rows_matches_full():
+    M, N, K, P = 40, 12, 5, 3
+    W, b = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, P)
+    W1, b1 = O.sync_step(W, b, Us, Vs, 0.3)
+    rows = np.array([0, 7, 39, 13])
+    Wr, br = O.sync_step_rows(W[rows], b[rows], Us, Vs, 0.3, rows)
+    assert np.allclose(Wr, W1[rows], rtol=0, atol=1e-14)
+    assert np.allclose(br, b1[rows], rtol=0, atol=1e-14)
+
+
+# ---------------------------------------------------------------- O7 ----
+@pytest.mark.parametrize("M,N,K,P", [(10, 64, 8, 2), (5, 7, 4, 4), (3, 9, 6, 1)])
+def test_o7_concat_batch_equivalence(M, N, K, P):
+    """A synchronous step with per-worker mean-loss factors equals
+    single-worker SGD on the concatenated P*K batch."""
+    W, b = S.fc_weights_randbias(M, N)
+    X, labels = S.softmax_batch(N, M, P * K)
+    Us, Vs = O.worker_factors(W, b, X, labels, P)
+    Wsync, bsync = O.sync_step(W, b, Us, Vs, 0.07)
+    Wcat, bcat = O.concat_batch_sgd(W, b, X, labels, 0.07)
+    assert np.max(np.abs(Wsync - Wcat)) < 1e-12
+    assert np.max(np.abs(bsync - bcat)) < 1e-12
+
+
+def test_o7_single_worker_is_textbook_sgd_by_fd():
+    """P=1: the step equals W - lr * (finite-difference gradient)."""
+    M, N, K = 4, 5, 6
+    W, b = S.fc_weights_randbias(M, N)
+    X, labels = S.softmax_batch(N, M, K)
+    W64, b64 = W.astype(np.float64), b.astype(np.float64)
+    gW, gb = O.fd_gradient(W64, b64, X.astype(np.float64), labels)
+    Us, Vs = O.worker_factors(W, b, X, labels, 1)
+    W1, b1 = O.sync_step(W, b, Us, Vs, 0.5)
+    assert np.max(np.abs(W1 - (W64 - 0.5 * gW))) < 1e-8
+    assert np.max(np.abs(b1 - (b64 - 0.5 * gb))) < 1e-8
+
+
+# --------------------------------------------------------- Z13 metric ----
+def test_update_error_metric_catches_2x_bug():
+    W0 = np.ones((4, 4), dtype=np.float32)
+    ref = W0 - 1e-4
+    bad = W0 - 2e-4
+    assert O.update_error(W0, ref, ref) == 0.0
+    assert O.update_error(W0, bad, ref) == pytest.approx(1.0, rel=1e-2)
