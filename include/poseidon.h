@@ -1,0 +1,247 @@
+/*
+ * poseidon.h — C ABI of libposeidon.so, a B200-native (sm_100a) implementation
+ * of Poseidon's per-layer gradient synchronisation (Zhang et al., arXiv
+ * 1512.06216): SACP (Alg. 3), sufficient-factor broadcasting (SFB, Sec. 4.3.1),
+ * sharded parameter-server sync (PS, Alg. 1 master / Alg. 3 lines 1-3) and
+ * distributed wait-free backprop scheduling (DWBP, Alg. 2).
+ *
+ * Citations "P:Lnnn" are lines of the paper's LaTeX source; readings
+ * "Zn" are listed in DESIGN.md §3.
+ *
+ * General conventions
+ *  - Every function returns poseidon_status_t (0 == POSEIDON_OK) unless stated.
+ *    On failure nothing has been enqueued and poseidon_last_error() returns a
+ *    thread-local message.  No C++ exception crosses this boundary.
+ *  - All float pointers passed to sync/kernel entry points are fp32 DEVICE
+ *    pointers on the context's device, 16-byte aligned, contiguous, row-major.
+ *    The caller owns them; the library never frees caller memory.
+ *  - Streams are CUDA runtime streams (cudaStream_t), passed as
+ *    poseidon_stream_t; NULL means the legacy default stream.
+ *  - Asynchrony: sync_* / backprop_hook / kernel entry points only ENQUEUE work
+ *    and return immediately.  Results are valid after poseidon_wait_layer() on
+ *    the consuming stream (or after synchronising the stream passed in).
+ *  - A context is used from one host thread.  Collectives are issued in call
+ *    order, which must be identical on every rank (top -> bottom layer order).
+ *  - FC layer shapes follow the paper: W is M x N with M = output dim (length
+ *    of the error message E_{i+1}) and N = input dim (reading Z8).
+ *  - The update is plain SGD with the worker mean: W <- W + alpha * sum,
+ *    alpha = -lr / P (readings Z1-Z4).
+ */
+#ifndef POSEIDON_H_
+#define POSEIDON_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* poseidon_stream_t;
+
+typedef enum {
+  POSEIDON_OK = 0,
+  POSEIDON_ERR_INVALID_ARG = -1,
+  POSEIDON_ERR_NOT_INITIALIZED = -2,
+  POSEIDON_ERR_CUDA = -3,
+  POSEIDON_ERR_NCCL = -4,
+  POSEIDON_ERR_SHAPE = -5,
+  POSEIDON_ERR_ALIGNMENT = -6,
+  POSEIDON_ERR_UNSUPPORTED = -7,
+  POSEIDON_ERR_STATE = -8
+} poseidon_status_t;
+
+typedef enum { POSEIDON_SCHEME_PS = 0, POSEIDON_SCHEME_SFB = 1 } poseidon_scheme_t;
+typedef enum { POSEIDON_LAYER_CONV = 0, POSEIDON_LAYER_FC = 1 } poseidon_layer_kind_t;
+
+/* Reconstruction kernel of the SFB path (step 3 of P:L331).
+ *  TF32: K1, tcgen05.mma kind::tf32, TMA-fed, TMEM accumulators, fused SGD
+ *        epilogue; factors rounded to TF32 (RN) when packed (reading Z12).
+ *        Tolerance 2e-3 (Z13 metric).
+ *  FP32: K1r, CUDA-core fp32 FMA tiles, fused SGD epilogue.  Tolerance 1e-5. */
+typedef enum { POSEIDON_RECON_TF32 = 0, POSEIDON_RECON_FP32 = 1 } poseidon_recon_t;
+
+/* Float counts of Alg. 3's cost rule, exact in 64 bits:
+ *  sfb     = (P-1)^2 K (M+N)
+ *  sf_ps   = P K (M+N) + P M N
+ *  full_ps = 2 P M N           (reported only, never decides) */
+typedef struct { uint64_t sfb, sf_ps, full_ps; } poseidon_costs_t;
+
+/* Topology of one process/GPU.  nccl_id is the 128-byte ncclUniqueId created
+ * by rank 0 with poseidon_get_unique_id() and broadcast by the caller (e.g.
+ * torch.distributed); ignored when world == 1.  flags: POSEIDON_FLAG_*. */
+typedef struct {
+  int32_t rank, world, device;
+  uint8_t nccl_id[128];
+  uint32_t flags;
+} poseidon_topology_t;
+
+#define POSEIDON_FLAG_DWBP_OFF 0x1u   /* ablation: sync starts only at iteration_end (Fig. dwbp (a)) */
+#define POSEIDON_FLAG_NO_PRIORITY 0x2u /* sync streams at default instead of highest priority */
+
+typedef struct poseidon_ctx* poseidon_ctx_t;
+
+/* Per-iteration statistics from device events (milliseconds).
+ *  exposed_ms    = max(0, max_i t(done_i) - t(bwd_end))  (sync time not hidden by backward)
+ *  sync_total_ms = sum_i (t(done_i) - t(start_i))
+ *  queue_ms      = sum_i (t(start_i) - t(ready_i))
+ *  recon_ms      = sum of K1/K1r (+bias) kernel times; ps_update_ms = sum of K2 times
+ *  first_ready_to_bwd_end_ms = t(bwd_end) - min_i t(ready_i)
+ *  nccl_bytes_*  = bytes this rank handed to / received from NCCL */
+typedef struct {
+  float exposed_ms, sync_total_ms, queue_ms, recon_ms, ps_update_ms, first_ready_to_bwd_end_ms;
+  uint64_t nccl_bytes_sent, nccl_bytes_recv;
+  int32_t n_layers;
+  int32_t iteration;
+} poseidon_iter_stats_t;
+
+/* Per-layer statistics of one iteration (milliseconds, device events). */
+typedef struct {
+  float ready_to_start_ms, comm_ms, kernel_ms, start_to_done_ms, done_after_bwd_end_ms;
+  int32_t scheme;
+  int32_t launched;
+} poseidon_layer_stats_t;
+
+/* ======================= the five named entry points ======================= */
+
+/* Create a context for this process's GPU.  world must equal topo->world.
+ * world > 1 creates an NCCL communicator from topo->nccl_id (collective over
+ * all ranks) and requires single-node all-pairs peer access
+ * (POSEIDON_ERR_UNSUPPORTED otherwise; there is no other backend). */
+poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, poseidon_ctx_t* out);
+
+/* SACP decision, Alg. 3: kind != FC -> PS; FC -> SFB iff
+ * (P-1)^2 K(M+N) <= PK(M+N) + PMN (tie -> SFB, Z5), else PS (the else branch
+ * is executed as full-gradient PS, Z7).  Pure host integer code: needs no
+ * context and no GPU.  Returns the scheme (>= 0) or a negative status for
+ * M, N, K < 0, P < 1 or u64 overflow.  costs may be NULL. */
+int32_t poseidon_choose_scheme(int32_t kind, int64_t M, int64_t N, int64_t K, int32_t P,
+                               poseidon_costs_t* costs);
+
+/* SFB sync of one registered FC layer (Alg. 3 lines 6-8).
+ *  U: K x M, row k = worker's error message E_{i+1} of sample k (dl/dy of the
+ *     mean loss; the library never rescales by K, Z2).
+ *  V: K x N, row k = layer input a_i of sample k.
+ *  W: M x N (NULL -> bound W), bias: M (NULL -> bound bias or none).
+ * Enqueues on `producer`: pack of U, V into this rank's slot of the gather
+ * buffers (+ per-worker bias column sums, optional TF32 RN rounding).  Then on
+ * the library's streams: all-gather of all ranks' factors (NCCL, skipped at
+ * P == 1) and the fused reconstruction + SGD  W += alpha * Ug^T Vg,
+ * b += alpha * sum_rows Ug.  U and V may be reused after the producer stream
+ * passes this point.  K must equal the registered K. */
+poseidon_status_t poseidon_sync_fc_sfb(poseidon_ctx_t ctx, int32_t layer_id, const float* U,
+                                       const float* V, float* W, float* bias, float lr,
+                                       poseidon_stream_t producer);
+
+/* PS sync of one layer's flat buffer (Alg. 1 master P:L208-211, Alg. 3 lines
+ * 1-3): grad and W are padded flat buffers of padded_n = P*S floats
+ * (poseidon_shard_range) holding the layer's W row-major then bias, n real
+ * elements, zero padding in grad.  In place: reduce-scatter(sum) of grad,
+ * this rank's shard W[b,e) += alpha * gsum[b,e) (K2), all-gather of W.
+ * grad/W NULL -> bound buffers.  After the call grad holds partial sums; it is
+ * zeroed by the library iff the buffers were bound with POSEIDON_PS_ZERO_GRAD. */
+poseidon_status_t poseidon_sync_ps(poseidon_ctx_t ctx, int32_t layer_id, float* grad, float* W,
+                                   int64_t n, float lr, poseidon_stream_t producer);
+
+/* DWBP trigger (Alg. 2 line 9): "layer `layer_id`'s gradient inputs
+ * are complete on `stream`".  PS layers sync their bound buffers; SFB layers
+ * sync the factors the caller wrote into poseidon_sfb_slot() (the library
+ * finalises the slot: column sums + optional rounding).  Starts the layer's
+ * sync on the library streams right away (or at iteration_end under
+ * POSEIDON_FLAG_DWBP_OFF). */
+poseidon_status_t poseidon_backprop_hook(poseidon_ctx_t ctx, int32_t layer_id, poseidon_stream_t stream);
+
+/* ================================ helpers ================================= */
+
+/* ncclGetUniqueId into out[128] (call on rank 0 only). */
+poseidon_status_t poseidon_get_unique_id(uint8_t out[128]);
+
+/* Shard map (reading Z11): S = 32*ceil(n/(32P)), padded_n = P*S, rank r owns
+ * [min(rS,n), min((r+1)S,n)) (possibly empty).  Pure host code. */
+poseidon_status_t poseidon_shard_range(int64_t n, int32_t P, int32_t rank, int64_t* begin,
+                                       int64_t* end, int64_t* padded_n);
+
+/* Register layer `layer_id` (0 <= id < 4096): kind, M x N weight, per-worker
+ * batch K, has_bias.  scheme_override: -1 -> SACP rule, else the scheme to use
+ * (C2 forces PS).  chosen_scheme may be NULL.  SFB layers get library-owned
+ * gather buffers Ug[P*K x M_pad], Vg[P*K x N_pad], Bs[P x M_pad] with
+ * M_pad = roundup(M,4).  A layer may be re-registered only while idle. */
+poseidon_status_t poseidon_register_layer(poseidon_ctx_t ctx, int32_t layer_id, int32_t kind,
+                                          int64_t M, int64_t N, int64_t K, int32_t has_bias,
+                                          int32_t scheme_override, int32_t* chosen_scheme);
+
+/* Zero-copy pack target of an SFB layer: this rank's U slot (K rows, row
+ * stride *ld_u = M_pad floats) and V slot (K rows, stride *ld_v = N_pad). */
+poseidon_status_t poseidon_sfb_slot(poseidon_ctx_t ctx, int32_t layer_id, float** U_slot,
+                                    int64_t* ld_u, float** V_slot, int64_t* ld_v);
+
+#define POSEIDON_PS_ZERO_GRAD 0x1u
+/* Bind a PS layer's padded flat buffers (caller-owned, padded_n floats each). */
+poseidon_status_t poseidon_bind_ps_buffers(poseidon_ctx_t ctx, int32_t layer_id, float* grad,
+                                           float* W, int64_t n, uint32_t flags);
+/* Bind an SFB layer's parameters (W: M x N, bias: M or NULL). */
+poseidon_status_t poseidon_bind_sfb_params(poseidon_ctx_t ctx, int32_t layer_id, float* W, float* bias);
+
+poseidon_status_t poseidon_set_lr(poseidon_ctx_t ctx, float lr);           /* lr used by backprop_hook */
+poseidon_status_t poseidon_set_recon(poseidon_ctx_t ctx, int32_t layer_id /* -1: all */, int32_t recon);
+
+/* Next-forward barrier: `consumer` waits until layer_id's latest sync is done
+ * (under DWBP_OFF: until every layer's sync of the last iteration is done). */
+poseidon_status_t poseidon_wait_layer(poseidon_ctx_t ctx, int32_t layer_id, poseidon_stream_t consumer);
+
+/* Mark the end of backward on `compute` (records bwd_end; under DWBP_OFF
+ * launches the deferred syncs), close the iteration and, if out != NULL,
+ * block until its syncs are done and fill the statistics. */
+poseidon_status_t poseidon_iteration_end(poseidon_ctx_t ctx, poseidon_stream_t compute, poseidon_iter_stats_t* out);
+
+/* Statistics of a finished iteration, `ago` iterations back (0 = the last one
+ * closed by iteration_end; at most 31).  Blocks on that iteration's events. */
+poseidon_status_t poseidon_get_iter_stats(poseidon_ctx_t ctx, int32_t ago, poseidon_iter_stats_t* out);
+poseidon_status_t poseidon_get_layer_stats(poseidon_ctx_t ctx, int32_t ago, int32_t layer_id,
+                                           poseidon_layer_stats_t* out);
+
+/* Number of library kernels launched so far by this process (all contexts). */
+uint64_t poseidon_launch_count(void);
+
+poseidon_status_t poseidon_finalize(poseidon_ctx_t ctx);
+const char* poseidon_last_error(void);
+int32_t poseidon_version(void);
+
+/* ============ kernel-level entry points (tests, microbenchmarks) ============
+ * These run the hot-path kernels on caller buffers without a communicator:
+ * "simulated workers" lay the P workers' data rank-major in one buffer, the
+ * way the all-gather leaves it, so multi-worker arithmetic is exercised on
+ * one GPU.  No context needed. */
+
+/* SFB with P_sim simulated workers on one GPU: U_all [P_sim*K x M] and
+ * V_all [P_sim*K x N] (worker p = rows [pK,(p+1)K)), W [M x N], bias [M]|NULL.
+ * Packs each worker block (K3, column sums, rounding for TF32) into scratch
+ * gather buffers, then runs the reconstruction (K1 or K1r) and the bias
+ * update with alpha = -lr / P_sim.  Scratch is owned by the library. */
+poseidon_status_t poseidon_sfb_simulated(const float* U_all, const float* V_all, int32_t P_sim,
+                                         int64_t K, int64_t M, int64_t N, float* W, float* bias,
+                                         float lr, int32_t recon, poseidon_stream_t stream);
+
+/* PS with P_sim simulated workers: grads [P_sim x padded_n] (padded flat
+ * buffers), W [padded_n].  For every shard r of the map, W[b_r,e_r) +=
+ * alpha * sum_p grads[p][b_r,e_r) summed in worker order (the fused
+ * reduce + K2 a single GPU can do for all shards), alpha = -lr / P_sim. */
+poseidon_status_t poseidon_ps_simulated(const float* grads, int32_t P_sim, float* W, int64_t n,
+                                        float lr, poseidon_stream_t stream);
+
+/* K2 alone: W[i] = fmaf(alpha, g[i], W[i]) for i in [0,count); if stats !=
+ * NULL (2 floats, device, caller-zeroed) accumulates sum((alpha g)^2) and the
+ * count of non-finite updates via warp-shuffle reductions. */
+poseidon_status_t poseidon_ps_shard_update(const float* g, float* W, int64_t count, float alpha,
+                                           float* stats, poseidon_stream_t stream);
+
+/* Reconstruction alone on already-gathered, already-rounded buffers:
+ * W[M x N] += alpha * Ug^T Vg with Ug [rows x ldu], Vg [rows x ldv]
+ * (ldu >= M, ldv >= N, multiples of 4). */
+poseidon_status_t poseidon_reconstruct_sgd(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv,
+                                           int64_t rows, int64_t M, int64_t N, float* W, float alpha,
+                                           int32_t recon, poseidon_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POSEIDON_H_ */

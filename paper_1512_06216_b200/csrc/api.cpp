@@ -1,0 +1,747 @@
+// libposeidon C ABI: context, per-layer plans, NCCL communicator, DWBP
+// scheduling (Alg. 2) and the two sync schemes of SACP (Alg. 3).
+//
+// Streams of a context:
+//   producer (caller's)  K3 pack of SFB factors; ready_i recorded here
+//   comm_stream          all collectives in call order (identical on every
+//                        rank), plus the PS shard update K2 between the
+//                        reduce-scatter and the all-gather
+//   recon_stream         K1 / K1r + bias update of SFB layers, so the next
+//                        layer's collective does not queue behind a GEMM
+// Both library streams run at the highest priority: the tail of DWBP is the
+// bottom layers' sync, which is on the critical path of the next forward.
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace poseidon {
+
+std::atomic<uint64_t> g_launches{0};
+
+thread_local std::string t_err;
+
+void set_error(const std::string& msg) { t_err = msg; }
+poseidon_status_t fail(poseidon_status_t code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+poseidon_status_t cuda_fail(cudaError_t e, const char* what) {
+  return fail(POSEIDON_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace poseidon
+
+using namespace poseidon;
+
+namespace {
+
+constexpr int RING = 8;           // iterations of events kept for statistics
+constexpr int MAX_LAYERS = 4096;
+
+#define CU_TRY(expr)                                      \
+  do {                                                    \
+    cudaError_t e_ = (expr);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr);   \
+  } while (0)
+#define NC_TRY(expr)                                                                          \
+  do {                                                                                        \
+    ncclResult_t r_ = (expr);                                                                 \
+    if (r_ != ncclSuccess)                                                                    \
+      return fail(POSEIDON_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_));     \
+  } while (0)
+
+struct EvSet {
+  cudaEvent_t ready = nullptr, start = nullptr, gathered = nullptr, kstart = nullptr, kend = nullptr,
+              done = nullptr;
+};
+
+struct Layer {
+  bool registered = false;
+  int kind = 0, scheme = 0, recon = POSEIDON_RECON_TF32;
+  int64_t M = 0, N = 0, K = 0;
+  bool has_bias = false;
+  // SFB: library-owned gather buffers (rank-major)
+  int64_t M_pad = 0, N_pad = 0;
+  float *Ug = nullptr, *Vg = nullptr, *Bs = nullptr;
+  float *W = nullptr, *bias = nullptr;  // bound SFB params
+  // PS: caller-owned padded flat buffers
+  float *grad = nullptr, *Wps = nullptr;
+  int64_t n = 0, S = 0, padded = 0, begin = 0, end = 0;
+  uint32_t ps_flags = 0;
+  EvSet ev[RING];
+  bool events_created = false;
+  int64_t last_iter = -1;  // iteration of the latest sync
+  // deferred (DWBP off) work
+  bool pending = false;
+  float pending_lr = 0.f;
+  float* pending_W = nullptr;
+  float* pending_bias = nullptr;
+  float* pending_grad = nullptr;
+};
+
+struct IterRecord {
+  int64_t iter = -1;
+  std::vector<int32_t> layers;
+  uint64_t sent = 0, recv = 0;
+  cudaEvent_t bwd_end = nullptr;
+  bool closed = false;
+};
+
+}  // namespace
+
+struct poseidon_ctx {
+  int rank = 0, world = 1, device = 0;
+  uint32_t flags = 0;
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr, recon_stream = nullptr;
+  float lr = 0.f;
+  std::vector<Layer> layers;
+  int64_t iter = 0;  // current (open) iteration
+  IterRecord rec[RING];
+  std::vector<int32_t> pending_order;  // DWBP off: hook order of deferred syncs
+};
+
+namespace {
+
+poseidon_status_t check_ctx(poseidon_ctx_t c) {
+  if (!c) return fail(POSEIDON_ERR_NOT_INITIALIZED, "context is NULL");
+  return POSEIDON_OK;
+}
+
+poseidon_status_t check_layer(poseidon_ctx_t c, int32_t id, Layer** out) {
+  if (!c) return fail(POSEIDON_ERR_NOT_INITIALIZED, "context is NULL");
+  if (id < 0 || id >= MAX_LAYERS) return fail(POSEIDON_ERR_INVALID_ARG, "layer_id out of range [0,4096)");
+  if (id >= (int32_t)c->layers.size() || !c->layers[id].registered)
+    return fail(POSEIDON_ERR_STATE, "layer " + std::to_string(id) + " is not registered");
+  *out = &c->layers[id];
+  return POSEIDON_OK;
+}
+
+poseidon_status_t ensure_events(Layer& L) {
+  if (L.events_created) return POSEIDON_OK;
+  for (int i = 0; i < RING; ++i) {
+    EvSet& e = L.ev[i];
+    cudaEvent_t* all[] = {&e.ready, &e.start, &e.gathered, &e.kstart, &e.kend, &e.done};
+    for (cudaEvent_t* p : all) CU_TRY(cudaEventCreate(p));
+  }
+  L.events_created = true;
+  return POSEIDON_OK;
+}
+
+IterRecord& open_record(poseidon_ctx_t c) {
+  IterRecord& r = c->rec[c->iter % RING];
+  if (r.iter != c->iter) {
+    r.iter = c->iter;
+    r.layers.clear();
+    r.sent = r.recv = 0;
+    r.closed = false;
+  }
+  return r;
+}
+
+// Producer-side prologue shared by both schemes: the previous sync of this
+// layer must be finished before its buffers are rewritten.
+poseidon_status_t producer_guard(poseidon_ctx_t c, Layer& L, cudaStream_t producer) {
+  if (L.last_iter >= 0) CU_TRY(cudaStreamWaitEvent(producer, L.ev[L.last_iter % RING].done, 0));
+  return POSEIDON_OK;
+}
+
+// Comm + update part of an SFB sync (steps 2 and 3 of P:L330-331).
+poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* W, float* bias, float lr,
+                                  cudaEvent_t wait_ev) {
+  EvSet& e = L.ev[c->iter % RING];
+  const int P = c->world;
+  CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
+  CU_TRY(cudaEventRecord(e.start, c->comm_stream));
+  IterRecord& r = open_record(c);
+  if (P > 1) {
+    const size_t ucount = (size_t)(L.K * L.M_pad), vcount = (size_t)(L.K * L.N_pad), bcount = (size_t)L.M_pad;
+    NC_TRY(ncclGroupStart());
+    NC_TRY(ncclAllGather(L.Ug + (size_t)c->rank * ucount, L.Ug, ucount, ncclFloat32, c->comm, c->comm_stream));
+    NC_TRY(ncclAllGather(L.Vg + (size_t)c->rank * vcount, L.Vg, vcount, ncclFloat32, c->comm, c->comm_stream));
+    NC_TRY(ncclAllGather(L.Bs + (size_t)c->rank * bcount, L.Bs, bcount, ncclFloat32, c->comm, c->comm_stream));
+    NC_TRY(ncclGroupEnd());
+    const uint64_t per = (uint64_t)(ucount + vcount + bcount) * 4u;
+    r.sent += per;  // handed to NCCL once; NCCL forwards it to P-1 peers
+    r.recv += per * (uint64_t)(P - 1);
+  }
+  CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+  CU_TRY(cudaStreamWaitEvent(c->recon_stream, e.gathered, 0));
+  CU_TRY(cudaEventRecord(e.kstart, c->recon_stream));
+  const float alpha = -lr / (float)P;
+  const int64_t rows = (int64_t)P * L.K;
+  cudaError_t err;
+  if (L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(L.Ug, L.M_pad, L.Vg, L.N_pad, L.M, L.N, W))
+    err = launch_recon_tcgen05(L.Ug, L.M_pad, L.Vg, L.N_pad, rows, L.M, L.N, W, alpha, c->recon_stream);
+  else
+    err = launch_recon_simt(L.Ug, L.M_pad, L.Vg, L.N_pad, rows, L.M, L.N, W, L.N, alpha, c->recon_stream);
+  if (err != cudaSuccess) return cuda_fail(err, "reconstruct+sgd launch");
+  if (bias) {
+    err = launch_bias_update(L.Bs, L.M_pad, P, bias, L.M, alpha, c->recon_stream);
+    if (err != cudaSuccess) return cuda_fail(err, "bias update launch");
+  }
+  CU_TRY(cudaEventRecord(e.kend, c->recon_stream));
+  CU_TRY(cudaEventRecord(e.done, c->recon_stream));
+  r.layers.push_back(id);
+  return POSEIDON_OK;
+}
+
+// PS sync (Alg. 3 lines 1-3 / Alg. 1 master): RS -> K2 -> AG, all on comm_stream.
+poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* grad, float* W, float lr,
+                                 cudaEvent_t wait_ev) {
+  EvSet& e = L.ev[c->iter % RING];
+  const int P = c->world;
+  CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
+  CU_TRY(cudaEventRecord(e.start, c->comm_stream));
+  IterRecord& r = open_record(c);
+  if (P > 1) {
+    NC_TRY(ncclReduceScatter(grad, grad + (size_t)c->rank * L.S, (size_t)L.S, ncclFloat32, ncclSum, c->comm,
+                             c->comm_stream));
+    r.sent += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
+    r.recv += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
+  }
+  CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+  CU_TRY(cudaEventRecord(e.kstart, c->comm_stream));
+  const float alpha = -lr / (float)P;
+  cudaError_t err = launch_ps_shard_update(grad + L.begin, W + L.begin, L.end - L.begin, alpha, nullptr,
+                                           c->comm_stream);
+  if (err != cudaSuccess) return cuda_fail(err, "ps shard update launch");
+  CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
+  if (P > 1) {
+    NC_TRY(ncclAllGather(W + (size_t)c->rank * L.S, W, (size_t)L.S, ncclFloat32, c->comm, c->comm_stream));
+    r.sent += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
+    r.recv += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
+  }
+  if (L.ps_flags & POSEIDON_PS_ZERO_GRAD) CU_TRY(cudaMemsetAsync(grad, 0, (size_t)L.padded * 4u, c->comm_stream));
+  CU_TRY(cudaEventRecord(e.done, c->comm_stream));
+  r.layers.push_back(id);
+  return POSEIDON_OK;
+}
+
+poseidon_status_t sfb_after_pack(poseidon_ctx_t c, int32_t id, Layer& L, float* W, float* bias, float lr,
+                                 cudaStream_t producer) {
+  EvSet& e = L.ev[c->iter % RING];
+  CU_TRY(cudaEventRecord(e.ready, producer));
+  L.last_iter = c->iter;
+  if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
+    L.pending = true;
+    L.pending_lr = lr;
+    L.pending_W = W;
+    L.pending_bias = bias;
+    c->pending_order.push_back(id);
+    open_record(c);
+    return POSEIDON_OK;
+  }
+  return launch_sfb_comm(c, id, L, W, bias, lr, e.ready);
+}
+
+poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t ldU, const float* V, int64_t ldV,
+                           cudaStream_t producer) {
+  const bool round = (L.recon == POSEIDON_RECON_TF32);
+  float* u_slot = L.Ug + (size_t)c->rank * L.K * L.M_pad;
+  float* v_slot = L.Vg + (size_t)c->rank * L.K * L.N_pad;
+  float* b_slot = L.Bs + (size_t)c->rank * L.M_pad;
+  cudaError_t err = launch_pack(U, ldU, u_slot, L.M_pad, L.K, L.M, round, b_slot, producer);
+  if (err != cudaSuccess) return cuda_fail(err, "pack U launch");
+  err = launch_pack(V, ldV, v_slot, L.N_pad, L.K, L.N, round, nullptr, producer);
+  if (err != cudaSuccess) return cuda_fail(err, "pack V launch");
+  return POSEIDON_OK;
+}
+
+void free_layer(Layer& L) {
+  if (L.Ug) cudaFree(L.Ug);
+  if (L.Vg) cudaFree(L.Vg);
+  if (L.Bs) cudaFree(L.Bs);
+  L.Ug = L.Vg = L.Bs = nullptr;
+  if (L.events_created) {
+    for (int i = 0; i < RING; ++i) {
+      EvSet& e = L.ev[i];
+      cudaEvent_t all[] = {e.ready, e.start, e.gathered, e.kstart, e.kend, e.done};
+      for (cudaEvent_t ev : all)
+        if (ev) cudaEventDestroy(ev);
+      e = EvSet{};
+    }
+    L.events_created = false;
+  }
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();
+    return 0.f;
+  }
+  return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t poseidon_version(void) { return 10000; }
+const char* poseidon_last_error(void) { return poseidon::t_err.c_str(); }
+uint64_t poseidon_launch_count(void) { return g_launches.load(); }
+
+poseidon_status_t poseidon_get_unique_id(uint8_t out[128]) {
+  if (!out) return fail(POSEIDON_ERR_INVALID_ARG, "out is NULL");
+  ncclUniqueId id;
+  NC_TRY(ncclGetUniqueId(&id));
+  static_assert(sizeof(id.internal) == 128, "ncclUniqueId size");
+  memcpy(out, id.internal, 128);
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, poseidon_ctx_t* out) {
+  if (!topo || !out) return fail(POSEIDON_ERR_INVALID_ARG, "topo/out is NULL");
+  if (world < 1 || topo->world != world || topo->rank < 0 || topo->rank >= world)
+    return fail(POSEIDON_ERR_INVALID_ARG, "inconsistent world/rank");
+  int ndev = 0;
+  CU_TRY(cudaGetDeviceCount(&ndev));
+  if (topo->device < 0 || topo->device >= ndev) return fail(POSEIDON_ERR_INVALID_ARG, "device out of range");
+  CU_TRY(cudaSetDevice(topo->device));
+  cudaDeviceProp prop;
+  CU_TRY(cudaGetDeviceProperties(&prop, topo->device));
+  if (prop.major != 10)
+    return fail(POSEIDON_ERR_UNSUPPORTED, "libposeidon is built for sm_100a (B200); device is sm_" +
+                                              std::to_string(prop.major) + std::to_string(prop.minor));
+  if (world > 1 && ndev >= world) {
+    // single-node all-pairs peer access (NVLink/NVSwitch); no other backend
+    for (int d = 0; d < world; ++d) {
+      if (d == topo->device) continue;
+      int ok = 0;
+      CU_TRY(cudaDeviceCanAccessPeer(&ok, topo->device, d));
+      if (!ok) return fail(POSEIDON_ERR_UNSUPPORTED, "GPUs are not all-pairs peer connected");
+    }
+  }
+  auto* c = new poseidon_ctx();
+  c->rank = topo->rank;
+  c->world = world;
+  c->device = topo->device;
+  c->flags = topo->flags;
+  c->layers.resize(64);
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  const int prio = (c->flags & POSEIDON_FLAG_NO_PRIORITY) ? lo : hi;
+  cudaError_t e1 = cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, prio);
+  cudaError_t e2 = cudaStreamCreateWithPriority(&c->recon_stream, cudaStreamNonBlocking, prio);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    delete c;
+    return cuda_fail(e1 != cudaSuccess ? e1 : e2, "stream create");
+  }
+  for (auto& r : c->rec) {
+    if (cudaEventCreate(&r.bwd_end) != cudaSuccess) {
+      delete c;
+      return fail(POSEIDON_ERR_CUDA, "event create");
+    }
+  }
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(id.internal, topo->nccl_id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, topo->rank);
+    if (r != ncclSuccess) {
+      delete c;
+      return fail(POSEIDON_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+  }
+  *out = c;
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_finalize(poseidon_ctx_t c) {
+  if (!c) return POSEIDON_OK;
+  cudaSetDevice(c->device);
+  if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+  if (c->recon_stream) cudaStreamSynchronize(c->recon_stream);
+  for (auto& L : c->layers) free_layer(L);
+  for (auto& r : c->rec)
+    if (r.bwd_end) cudaEventDestroy(r.bwd_end);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->recon_stream) cudaStreamDestroy(c->recon_stream);
+  delete c;
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t kind, int64_t M, int64_t N,
+                                          int64_t K, int32_t has_bias, int32_t scheme_override,
+                                          int32_t* chosen_scheme) {
+  poseidon_status_t st = check_ctx(c);
+  if (st) return st;
+  if (id < 0 || id >= MAX_LAYERS) return fail(POSEIDON_ERR_INVALID_ARG, "layer_id out of range [0,4096)");
+  if (kind != POSEIDON_LAYER_CONV && kind != POSEIDON_LAYER_FC) return fail(POSEIDON_ERR_INVALID_ARG, "bad kind");
+  if (M <= 0 || N <= 0 || K <= 0) return fail(POSEIDON_ERR_SHAPE, "M, N, K must be positive");
+  if (scheme_override < -1 || scheme_override > 1) return fail(POSEIDON_ERR_INVALID_ARG, "bad scheme_override");
+  int32_t rule = poseidon_choose_scheme(kind, M, N, K, c->world, nullptr);
+  if (rule < 0) return (poseidon_status_t)rule;
+  const int32_t scheme = scheme_override >= 0 ? scheme_override : rule;
+  if (scheme == POSEIDON_SCHEME_SFB && kind != POSEIDON_LAYER_FC)
+    return fail(POSEIDON_ERR_INVALID_ARG, "SFB needs an FC layer (Alg. 3)");
+  cudaSetDevice(c->device);
+  if (id >= (int32_t)c->layers.size()) c->layers.resize((size_t)id + 1);
+  Layer& L = c->layers[id];
+  if (L.registered && L.last_iter >= 0) {
+    // re-registration: wait for the layer to be idle
+    cudaEventSynchronize(L.ev[L.last_iter % RING].done);
+  }
+  free_layer(L);
+  L = Layer{};
+  L.kind = kind;
+  L.M = M;
+  L.N = N;
+  L.K = K;
+  L.has_bias = has_bias != 0;
+  L.scheme = scheme;
+  if (scheme == POSEIDON_SCHEME_SFB) {
+    L.M_pad = round_up(M, 4);
+    L.N_pad = round_up(N, 4);
+    const size_t P = (size_t)c->world;
+    const size_t ub = P * (size_t)(K * L.M_pad) * 4, vb = P * (size_t)(K * L.N_pad) * 4, bb = P * (size_t)L.M_pad * 4;
+    CU_TRY(cudaMalloc(&L.Ug, ub));
+    CU_TRY(cudaMalloc(&L.Vg, vb));
+    CU_TRY(cudaMalloc(&L.Bs, bb));
+    CU_TRY(cudaMemset(L.Ug, 0, ub));  // padding columns stay zero forever
+    CU_TRY(cudaMemset(L.Vg, 0, vb));
+    CU_TRY(cudaMemset(L.Bs, 0, bb));
+  }
+  st = ensure_events(L);
+  if (st) return st;
+  L.registered = true;
+  if (chosen_scheme) *chosen_scheme = scheme;
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_sfb_slot(poseidon_ctx_t c, int32_t id, float** U_slot, int64_t* ld_u, float** V_slot,
+                                    int64_t* ld_v) {
+  Layer* L;
+  poseidon_status_t st = check_layer(c, id, &L);
+  if (st) return st;
+  if (L->scheme != POSEIDON_SCHEME_SFB) return fail(POSEIDON_ERR_STATE, "layer is not an SFB layer");
+  if (U_slot) *U_slot = L->Ug + (size_t)c->rank * L->K * L->M_pad;
+  if (V_slot) *V_slot = L->Vg + (size_t)c->rank * L->K * L->N_pad;
+  if (ld_u) *ld_u = L->M_pad;
+  if (ld_v) *ld_v = L->N_pad;
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_bind_ps_buffers(poseidon_ctx_t c, int32_t id, float* grad, float* W, int64_t n,
+                                           uint32_t flags) {
+  Layer* L;
+  poseidon_status_t st = check_layer(c, id, &L);
+  if (st) return st;
+  if (L->scheme != POSEIDON_SCHEME_PS) return fail(POSEIDON_ERR_STATE, "layer is not a PS layer");
+  if (!grad || !W) return fail(POSEIDON_ERR_INVALID_ARG, "grad/W is NULL");
+  if (!aligned16(grad) || !aligned16(W)) return fail(POSEIDON_ERR_ALIGNMENT, "PS buffers must be 16-byte aligned");
+  const int64_t expect = L->M * L->N + (L->has_bias ? L->M : 0);
+  if (n != expect) return fail(POSEIDON_ERR_SHAPE, "n != M*N (+M if bias)");
+  L->grad = grad;
+  L->Wps = W;
+  L->n = n;
+  L->ps_flags = flags;
+  int64_t b, e, padded;
+  poseidon_shard_range(n, c->world, c->rank, &b, &e, &padded);
+  L->S = padded / c->world;
+  L->padded = padded;
+  L->begin = b;
+  L->end = e;
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_bind_sfb_params(poseidon_ctx_t c, int32_t id, float* W, float* bias) {
+  Layer* L;
+  poseidon_status_t st = check_layer(c, id, &L);
+  if (st) return st;
+  if (L->scheme != POSEIDON_SCHEME_SFB) return fail(POSEIDON_ERR_STATE, "layer is not an SFB layer");
+  if (!W) return fail(POSEIDON_ERR_INVALID_ARG, "W is NULL");
+  if (bias && !L->has_bias) return fail(POSEIDON_ERR_INVALID_ARG, "layer registered without bias");
+  L->W = W;
+  L->bias = bias;
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_set_lr(poseidon_ctx_t c, float lr) {
+  poseidon_status_t st = check_ctx(c);
+  if (st) return st;
+  c->lr = lr;
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_set_recon(poseidon_ctx_t c, int32_t id, int32_t recon) {
+  poseidon_status_t st = check_ctx(c);
+  if (st) return st;
+  if (recon != POSEIDON_RECON_TF32 && recon != POSEIDON_RECON_FP32) return fail(POSEIDON_ERR_INVALID_ARG, "bad recon");
+  if (id == -1) {
+    for (auto& L : c->layers) L.recon = recon;
+    return POSEIDON_OK;
+  }
+  Layer* L;
+  st = check_layer(c, id, &L);
+  if (st) return st;
+  L->recon = recon;
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_sync_fc_sfb(poseidon_ctx_t c, int32_t id, const float* U, const float* V, float* W,
+                                       float* bias, float lr, poseidon_stream_t producer) {
+  Layer* L;
+  poseidon_status_t st = check_layer(c, id, &L);
+  if (st) return st;
+  if (L->scheme != POSEIDON_SCHEME_SFB) return fail(POSEIDON_ERR_STATE, "layer is not an SFB layer");
+  if (!U || !V) return fail(POSEIDON_ERR_INVALID_ARG, "U/V is NULL");
+  if (!W) W = L->W;
+  if (!bias) bias = L->bias;
+  if (!W) return fail(POSEIDON_ERR_INVALID_ARG, "no W given or bound");
+  if (bias && !L->has_bias) return fail(POSEIDON_ERR_INVALID_ARG, "layer registered without bias");
+  if (!aligned16(W)) return fail(POSEIDON_ERR_ALIGNMENT, "W must be 16-byte aligned");
+  cudaStream_t ps = reinterpret_cast<cudaStream_t>(producer);
+  st = producer_guard(c, *L, ps);
+  if (st) return st;
+  st = pack_sfb(c, *L, U, L->M, V, L->N, ps);
+  if (st) return st;
+  return sfb_after_pack(c, id, *L, W, bias, lr, ps);
+}
+
+poseidon_status_t poseidon_sync_ps(poseidon_ctx_t c, int32_t id, float* grad, float* W, int64_t n, float lr,
+                                   poseidon_stream_t producer) {
+  Layer* L;
+  poseidon_status_t st = check_layer(c, id, &L);
+  if (st) return st;
+  if (L->scheme != POSEIDON_SCHEME_PS) return fail(POSEIDON_ERR_STATE, "layer is not a PS layer");
+  if (grad || W) {
+    if (!grad || !W) return fail(POSEIDON_ERR_INVALID_ARG, "pass both grad and W, or neither");
+    if (grad != L->grad || W != L->Wps || n != L->n) {
+      st = poseidon_bind_ps_buffers(c, id, grad, W, n, L->ps_flags);
+      if (st) return st;
+    }
+  }
+  if (!L->grad) return fail(POSEIDON_ERR_STATE, "no PS buffers given or bound");
+  if (n != L->n) return fail(POSEIDON_ERR_SHAPE, "n does not match the bound buffers");
+  cudaStream_t ps = reinterpret_cast<cudaStream_t>(producer);
+  EvSet& e = L->ev[c->iter % RING];
+  CU_TRY(cudaEventRecord(e.ready, ps));
+  L->last_iter = c->iter;
+  if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
+    L->pending = true;
+    L->pending_lr = lr;
+    L->pending_grad = L->grad;
+    L->pending_W = L->Wps;
+    c->pending_order.push_back(id);
+    open_record(c);
+    return POSEIDON_OK;
+  }
+  return launch_ps_comm(c, id, *L, L->grad, L->Wps, lr, e.ready);
+}
+
+poseidon_status_t poseidon_backprop_hook(poseidon_ctx_t c, int32_t id, poseidon_stream_t stream) {
+  Layer* L;
+  poseidon_status_t st = check_layer(c, id, &L);
+  if (st) return st;
+  if (L->scheme == POSEIDON_SCHEME_PS) return poseidon_sync_ps(c, id, nullptr, nullptr, L->n, c->lr, stream);
+  // SFB: the caller wrote its factors into the slot; finalise in place (colsum + rounding)
+  if (!L->W) return fail(POSEIDON_ERR_STATE, "SFB layer has no bound W (poseidon_bind_sfb_params)");
+  cudaStream_t ps = reinterpret_cast<cudaStream_t>(stream);
+  float* u_slot = L->Ug + (size_t)c->rank * L->K * L->M_pad;
+  float* v_slot = L->Vg + (size_t)c->rank * L->K * L->N_pad;
+  // the slot was written by the caller after its own wait_layer; still order after the last sync
+  st = producer_guard(c, *L, ps);
+  if (st) return st;
+  st = pack_sfb(c, *L, u_slot, L->M_pad, v_slot, L->N_pad, ps);
+  if (st) return st;
+  return sfb_after_pack(c, id, *L, L->W, L->bias, c->lr, ps);
+}
+
+poseidon_status_t poseidon_wait_layer(poseidon_ctx_t c, int32_t id, poseidon_stream_t consumer) {
+  Layer* L;
+  poseidon_status_t st = check_layer(c, id, &L);
+  if (st) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(consumer);
+  if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
+    // traditional BP (Fig. dwbp (a)): the next iteration waits for every layer
+    const IterRecord& r = c->rec[(c->iter + RING - 1) % RING];
+    if (r.iter == c->iter - 1)
+      for (int32_t lid : r.layers) CU_TRY(cudaStreamWaitEvent(cs, c->layers[lid].ev[r.iter % RING].done, 0));
+    return POSEIDON_OK;
+  }
+  if (L->last_iter >= 0) CU_TRY(cudaStreamWaitEvent(cs, L->ev[L->last_iter % RING].done, 0));
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_iteration_end(poseidon_ctx_t c, poseidon_stream_t compute, poseidon_iter_stats_t* out) {
+  poseidon_status_t st = check_ctx(c);
+  if (st) return st;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(compute);
+  IterRecord& r = open_record(c);
+  CU_TRY(cudaEventRecord(r.bwd_end, cs));
+  if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
+    // deferred syncs in the order the hooks fired, all after the whole backward
+    for (int32_t id : c->pending_order) {
+      Layer& L = c->layers[id];
+      if (!L.pending) continue;
+      L.pending = false;
+      st = (L.scheme == POSEIDON_SCHEME_SFB)
+               ? launch_sfb_comm(c, id, L, L.pending_W, L.pending_bias, L.pending_lr, r.bwd_end)
+               : launch_ps_comm(c, id, L, L.pending_grad, L.pending_W, L.pending_lr, r.bwd_end);
+      if (st) return st;
+    }
+    c->pending_order.clear();
+  }
+  r.closed = true;
+  c->iter += 1;
+  if (out) return poseidon_get_iter_stats(c, 0, out);
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_get_iter_stats(poseidon_ctx_t c, int32_t ago, poseidon_iter_stats_t* out) {
+  poseidon_status_t st = check_ctx(c);
+  if (st) return st;
+  if (!out) return fail(POSEIDON_ERR_INVALID_ARG, "out is NULL");
+  if (ago < 0 || ago >= RING - 1) return fail(POSEIDON_ERR_INVALID_ARG, "ago out of range");
+  const int64_t it = c->iter - 1 - ago;
+  if (it < 0) return fail(POSEIDON_ERR_STATE, "no such iteration");
+  IterRecord& r = c->rec[it % RING];
+  if (r.iter != it || !r.closed) return fail(POSEIDON_ERR_STATE, "iteration record overwritten");
+  memset(out, 0, sizeof(*out));
+  CU_TRY(cudaEventSynchronize(r.bwd_end));
+  float exposed = 0.f, first_ready = 0.f;
+  for (int32_t id : r.layers) {
+    Layer& L = c->layers[id];
+    EvSet& e = L.ev[it % RING];
+    CU_TRY(cudaEventSynchronize(e.done));
+    exposed = std::max(exposed, elapsed(r.bwd_end, e.done));
+    first_ready = std::max(first_ready, elapsed(e.ready, r.bwd_end));
+    out->sync_total_ms += elapsed(e.start, e.done);
+    out->queue_ms += elapsed(e.ready, e.start);
+    if (L.scheme == POSEIDON_SCHEME_SFB)
+      out->recon_ms += elapsed(e.kstart, e.kend);
+    else
+      out->ps_update_ms += elapsed(e.kstart, e.kend);
+  }
+  out->exposed_ms = exposed;
+  out->first_ready_to_bwd_end_ms = first_ready;
+  out->nccl_bytes_sent = r.sent;
+  out->nccl_bytes_recv = r.recv;
+  out->n_layers = (int32_t)r.layers.size();
+  out->iteration = (int32_t)it;
+  ncclResult_t async_err = ncclSuccess;
+  if (c->comm && ncclCommGetAsyncError(c->comm, &async_err) == ncclSuccess && async_err != ncclSuccess)
+    return fail(POSEIDON_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(async_err));
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_get_layer_stats(poseidon_ctx_t c, int32_t ago, int32_t id, poseidon_layer_stats_t* out) {
+  Layer* L;
+  poseidon_status_t st = check_layer(c, id, &L);
+  if (st) return st;
+  if (!out) return fail(POSEIDON_ERR_INVALID_ARG, "out is NULL");
+  if (ago < 0 || ago >= RING - 1) return fail(POSEIDON_ERR_INVALID_ARG, "ago out of range");
+  const int64_t it = c->iter - 1 - ago;
+  if (it < 0) return fail(POSEIDON_ERR_STATE, "no such iteration");
+  IterRecord& r = c->rec[it % RING];
+  if (r.iter != it || !r.closed) return fail(POSEIDON_ERR_STATE, "iteration record overwritten");
+  memset(out, 0, sizeof(*out));
+  out->scheme = L->scheme;
+  bool found = false;
+  for (int32_t lid : r.layers) found |= (lid == id);
+  if (!found) return POSEIDON_OK;
+  EvSet& e = L->ev[it % RING];
+  CU_TRY(cudaEventSynchronize(e.done));
+  CU_TRY(cudaEventSynchronize(r.bwd_end));
+  out->launched = 1;
+  out->ready_to_start_ms = elapsed(e.ready, e.start);
+  out->comm_ms = elapsed(e.start, e.gathered);
+  out->kernel_ms = elapsed(e.kstart, e.kend);
+  out->start_to_done_ms = elapsed(e.start, e.done);
+  out->done_after_bwd_end_ms = elapsed(r.bwd_end, e.done);
+  return POSEIDON_OK;
+}
+
+// ------------------------------------------- kernel-level entry points ----
+poseidon_status_t poseidon_sfb_simulated(const float* U_all, const float* V_all, int32_t P, int64_t K, int64_t M,
+                                         int64_t N, float* W, float* bias, float lr, int32_t recon,
+                                         poseidon_stream_t stream) {
+  if (!U_all || !V_all || !W || P < 1 || K < 0 || M <= 0 || N <= 0)
+    return fail(POSEIDON_ERR_INVALID_ARG, "sfb_simulated: bad arguments");
+  if (recon != POSEIDON_RECON_TF32 && recon != POSEIDON_RECON_FP32) return fail(POSEIDON_ERR_INVALID_ARG, "bad recon");
+  if (!aligned16(W)) return fail(POSEIDON_ERR_ALIGNMENT, "W must be 16-byte aligned");
+  if (K == 0) return POSEIDON_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t M_pad = round_up(M, 4), N_pad = round_up(N, 4);
+  const size_t ub = (size_t)P * K * M_pad * 4, vb = (size_t)P * K * N_pad * 4, bb = (size_t)P * M_pad * 4;
+  float *Ug = nullptr, *Vg = nullptr, *Bs = nullptr;
+  CU_TRY(cudaMallocAsync(&Ug, ub, s));
+  CU_TRY(cudaMallocAsync(&Vg, vb, s));
+  CU_TRY(cudaMallocAsync(&Bs, bb, s));
+  CU_TRY(cudaMemsetAsync(Ug, 0, ub, s));
+  CU_TRY(cudaMemsetAsync(Vg, 0, vb, s));
+  const bool round = recon == POSEIDON_RECON_TF32;
+  cudaError_t err = cudaSuccess;
+  for (int p = 0; p < P && err == cudaSuccess; ++p) {
+    err = launch_pack(U_all + (size_t)p * K * M, M, Ug + (size_t)p * K * M_pad, M_pad, K, M, round,
+                      Bs + (size_t)p * M_pad, s);
+    if (err == cudaSuccess)
+      err = launch_pack(V_all + (size_t)p * K * N, N, Vg + (size_t)p * K * N_pad, N_pad, K, N, round, nullptr, s);
+  }
+  const float alpha = -lr / (float)P;
+  if (err == cudaSuccess) {
+    if (round && recon_tcgen05_supported(Ug, M_pad, Vg, N_pad, M, N, W))
+      err = launch_recon_tcgen05(Ug, M_pad, Vg, N_pad, (int64_t)P * K, M, N, W, alpha, s);
+    else
+      err = launch_recon_simt(Ug, M_pad, Vg, N_pad, (int64_t)P * K, M, N, W, N, alpha, s);
+  }
+  if (err == cudaSuccess && bias) err = launch_bias_update(Bs, M_pad, P, bias, M, alpha, s);
+  cudaFreeAsync(Ug, s);
+  cudaFreeAsync(Vg, s);
+  cudaFreeAsync(Bs, s);
+  if (err != cudaSuccess) return cuda_fail(err, "sfb_simulated launch");
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_ps_simulated(const float* grads, int32_t P, float* W, int64_t n, float lr,
+                                        poseidon_stream_t stream) {
+  if (!grads || !W || P < 1 || n < 0) return fail(POSEIDON_ERR_INVALID_ARG, "ps_simulated: bad arguments");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int64_t b, e, padded;
+  poseidon_shard_range(n, P, 0, &b, &e, &padded);
+  const float alpha = -lr / (float)P;
+  for (int r = 0; r < P; ++r) {
+    poseidon_shard_range(n, P, r, &b, &e, &padded);
+    cudaError_t err = launch_ps_sim_update(grads + b, padded, P, W + b, e - b, alpha, s);
+    if (err != cudaSuccess) return cuda_fail(err, "ps_simulated launch");
+  }
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_ps_shard_update(const float* g, float* W, int64_t count, float alpha, float* stats,
+                                           poseidon_stream_t stream) {
+  if (!g || !W || count < 0) return fail(POSEIDON_ERR_INVALID_ARG, "ps_shard_update: bad arguments");
+  cudaError_t err = launch_ps_shard_update(g, W, count, alpha, stats, reinterpret_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "ps_shard_update launch");
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_reconstruct_sgd(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t rows,
+                                           int64_t M, int64_t N, float* W, float alpha, int32_t recon,
+                                           poseidon_stream_t stream) {
+  if (!Ug || !Vg || !W || rows < 0 || M <= 0 || N <= 0 || ldu < M || ldv < N)
+    return fail(POSEIDON_ERR_INVALID_ARG, "reconstruct_sgd: bad arguments");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t err;
+  if (recon == POSEIDON_RECON_TF32) {
+    if (!recon_tcgen05_supported(Ug, ldu, Vg, ldv, M, N, W))
+      return fail(POSEIDON_ERR_ALIGNMENT, "tcgen05 path needs 16-B aligned buffers, ldu/ldv/N multiples of 4");
+    err = launch_recon_tcgen05(Ug, ldu, Vg, ldv, rows, M, N, W, alpha, s);
+  } else if (recon == POSEIDON_RECON_FP32) {
+    err = launch_recon_simt(Ug, ldu, Vg, ldv, rows, M, N, W, N, alpha, s);
+  } else {
+    return fail(POSEIDON_ERR_INVALID_ARG, "bad recon");
+  }
+  if (err != cudaSuccess) return cuda_fail(err, "reconstruct_sgd launch");
+  return POSEIDON_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,53 @@
+// Internal declarations shared by the libposeidon translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "poseidon.h"
+
+namespace poseidon {
+
+// ---- error plumbing (thread-local message, status codes) ----
+void set_error(const std::string& msg);
+poseidon_status_t fail(poseidon_status_t code, const std::string& msg);
+poseidon_status_t cuda_fail(cudaError_t e, const char* what);
+
+extern std::atomic<uint64_t> g_launches;
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---- kernels (each returns the launch error) ----
+
+// K2: W[i] = fmaf(alpha, g[i], W[i]), i in [0, count). stats: optional 2 floats.
+cudaError_t launch_ps_shard_update(const float* g, float* W, int64_t count, float alpha, float* stats,
+                                   cudaStream_t s);
+// PS with P simulated workers: W[i] = fmaf(alpha, sum_p g[p*ld + i], W[i]), i in [0,count).
+cudaError_t launch_ps_sim_update(const float* g, int64_t ld, int32_t P, float* W, int64_t count,
+                                 float alpha, cudaStream_t s);
+
+// K3: pack K rows of src (row stride ld_src) into dst (row stride ld_dst), columns [0, cols);
+// optional TF32 round-to-nearest; if colsum != NULL also writes colsum[c] = sum_k src[k][c]
+// (fp32, fixed row order, of the UNROUNDED values).
+cudaError_t launch_pack(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int64_t K,
+                        int64_t cols, bool round_tf32, float* colsum, cudaStream_t s);
+// bias[m] = fmaf(alpha, sum_p bs[p*ld + m], bias[m]) for m in [0, M), p in worker order.
+cudaError_t launch_bias_update(const float* bs, int64_t ld, int32_t P, float* bias, int64_t M,
+                               float alpha, cudaStream_t s);
+
+// K1r: W[M x N] += alpha * Ug^T Vg on CUDA cores (fp32 FMA).
+cudaError_t launch_recon_simt(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t rows,
+                              int64_t M, int64_t N, float* W, int64_t ldw, float alpha, cudaStream_t s);
+
+// K1: tcgen05 TF32 version.  Returns cudaErrorNotSupported when the shape/alignment cannot be
+// described by TMA (caller reports it).  Tensor maps are (re)encoded per call (cheap host work).
+cudaError_t launch_recon_tcgen05(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t rows,
+                                 int64_t M, int64_t N, float* W, float alpha, cudaStream_t s);
+bool recon_tcgen05_supported(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t M,
+                             int64_t N, const float* W);
+
+}  // namespace poseidon

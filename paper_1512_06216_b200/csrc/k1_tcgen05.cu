@@ -1,0 +1,434 @@
+// K1 — SFB reconstruction fused with the SGD update on the 5th-generation
+// tensor cores (step (3) of SFB; Alg. 3 line 8; Eq. 5).
+//
+//   W[M x N] += alpha * Ug^T Vg      Ug: rows x M (ld ldu), Vg: rows x N (ld ldv)
+//
+// "rows" = P*K: every worker's sufficient factors, rank-major, exactly as the
+// all-gather leaves them.  Both operands are MN-major (M resp. N contiguous),
+// which tcgen05 supports for TF32 (instruction-descriptor bits 15/16), so the
+// gathered buffers are consumed in place with no transpose.
+//
+// Design (sm_100a, one CTA per SM, persistent, 256 threads):
+//   warp 0      TMA producer: Ug/Vg slabs of BK=32 rows -> 3-stage smem ring
+//               (128B swizzle; 4 boxes of 32x32 for A, 8 for B; 48 KB/stage)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (M=128, N=256, K=8, kind::tf32, fp32 accumulate in TMEM,
+//               double-buffered accumulators: 2 x 256 columns = all 512)
+//   warp 2      TMA producer for the W tile, 32-column chunks (16 KB) into a
+//               4-slot ring, running ahead of the epilogue (W does not depend
+//               on the accumulator, so its HBM read overlaps the MMA)
+//   warps 4-7   epilogue: tcgen05.ld 32 accumulator columns per row,
+//               W = fmaf(alpha, acc, W) in shared memory, TMA store back.
+// The epilogue of tile i overlaps the MMAs of tile i+1 (TMEM double buffer),
+// which is what keeps the kernel at the HBM roofline when P*K is small
+// (W read-modify-write, 8 B/element) and at the tensor roofline when it is
+// large.  Tile order: N-tile fastest within an M-tile row.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "internal.h"
+
+namespace poseidon {
+
+namespace {
+
+constexpr int BM = 128;         // UMMA M (rows of W per tile)
+constexpr int BN = 256;         // UMMA N (cols of W per tile)
+constexpr int BK = 32;          // factor rows per pipeline stage
+constexpr int UK = 8;           // K per tcgen05.mma for tf32
+constexpr int STAGES = 3;
+constexpr int WSLOTS = 4;
+constexpr int A_BOX_BYTES = 32 * BK * 4;               // 4 KB: 32 m x 32 k
+constexpr int B_BOX_BYTES = 32 * BK * 4;
+constexpr int A_STAGE_BYTES = (BM / 32) * A_BOX_BYTES;   // 16 KB
+constexpr int B_STAGE_BYTES = (BN / 32) * B_BOX_BYTES;   // 32 KB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int W_CHUNK_COLS = 32;
+constexpr int W_CHUNK_BYTES = BM * W_CHUNK_COLS * 4;     // 16 KB
+constexpr int CHUNKS_PER_TILE = BN / W_CHUNK_COLS;       // 8
+constexpr int TMEM_COLS = 512;
+constexpr int NUM_THREADS = 256;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + WSLOTS * W_CHUNK_BYTES + 1024 /*barriers*/ + 1024 /*align*/;
+
+// ---------------------------------------------------------------- PTX ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra.uni DONE;\n"
+      "bra.uni LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int32_t x, int32_t y,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem], kind::tf32, cta_group::1
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 32 consecutive 32-bit columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Shared-memory matrix descriptor (tcgen05), SWIZZLE_128B, MN-major canonical layout
+// ((8,m),(8,k)) : ((1,LBO),(8,SBO)) in 16-byte units: LBO = stride between 32-float
+// MN chunks (one TMA box = BK rows x 128 B), SBO = stride between 8-row K groups (1 KB).
+__device__ __forceinline__ uint64_t make_desc_mn_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D=f32, A=B=tf32, A and B MN-major, N=BN, M=BM.
+__host__ __device__ constexpr uint32_t make_idesc() {
+  return (1u << 4)              // c_format = F32
+         | (2u << 7)            // a_format = TF32
+         | (2u << 10)           // b_format = TF32
+         | (1u << 15)           // a_major = MN
+         | (1u << 16)           // b_major = MN
+         | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+struct Params {
+  int32_t M, N, rows;
+  int32_t m_tiles, n_tiles, num_tiles, num_kb;
+  int32_t a_boxes_valid_last, b_boxes_valid_last;  // boxes of the last m/n tile that are not fully OOB
+  float alpha;
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    recon_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmW, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_ops = smem;                                        // STAGES x (A | B)
+  uint8_t* smem_w = smem + STAGES * STAGE_BYTES;                   // WSLOTS x 16 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_w + WSLOTS * W_CHUNK_BYTES);
+  uint64_t* full = bars;                      // [STAGES]
+  uint64_t* empty = full + STAGES;            // [STAGES]
+  uint64_t* tfull = empty + STAGES;           // [2]
+  uint64_t* tempty = tfull + 2;               // [2]
+  uint64_t* wfull = tempty + 2;               // [WSLOTS]
+  uint64_t* wempty = wfull + WSLOTS;          // [WSLOTS]
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(wempty + WSLOTS);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < WSLOTS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_smem)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+
+  if (warp == 0) {
+    // ===================== operand TMA producer =====================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_last();
+      uint32_t stage = 0, phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+        const int a_boxes = (mt == p.m_tiles - 1) ? p.a_boxes_valid_last : BM / 32;
+        const int b_boxes = (nt == p.n_tiles - 1) ? p.b_boxes_valid_last : BN / 32;
+        const uint32_t tx = (uint32_t)(a_boxes * A_BOX_BYTES + b_boxes * B_BOX_BYTES);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], tx);
+          uint8_t* sa = smem_ops + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_STAGE_BYTES;
+          for (int j = 0; j < a_boxes; ++j)
+            tma_load_2d(&tmA, &full[stage], sa + j * A_BOX_BYTES, mt * BM + 32 * j, kb * BK, pol);
+          for (int j = 0; j < b_boxes; ++j)
+            tma_load_2d(&tmB, &full[stage], sb + j * B_BOX_BYTES, nt * BN + 32 * j, kb * BK, pol);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc();
+      uint32_t stage = 0, phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem_ops + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_STAGE_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k) {
+            const uint64_t ad = make_desc_mn_sw128(sa + k * 1024, A_BOX_BYTES, 1024);
+            const uint64_t bd = make_desc_mn_sw128(sb + k * 1024, B_BOX_BYTES, 1024);
+            tc_mma_tf32(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp == 2) {
+    // ===================== W tile TMA producer =====================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t g = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+        const int n0 = nt * BN;
+        int nch = (p.N - n0 + W_CHUNK_COLS - 1) / W_CHUNK_COLS;
+        if (nch > CHUNKS_PER_TILE) nch = CHUNKS_PER_TILE;
+        for (int c = 0; c < nch; ++c, ++g) {
+          const uint32_t slot = g % WSLOTS, ph = (g / WSLOTS) & 1;
+          mbar_wait(&wempty[slot], ph ^ 1);
+          mbar_expect_tx(&wfull[slot], W_CHUNK_BYTES);
+          tma_load_2d(&tmW, &wfull[slot], smem_w + slot * W_CHUNK_BYTES, n0 + c * W_CHUNK_COLS, mt * BM, pol);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue (128 threads, one W row each) =====================
+    const int q = warp - 4;                 // TMEM lane quarter
+    const int row = q * 32 + lane;          // row within the tile
+    uint32_t g = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+      const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+      const int n0 = nt * BN;
+      int nch = (p.N - n0 + W_CHUNK_COLS - 1) / W_CHUNK_COLS;
+      if (nch > CHUNKS_PER_TILE) nch = CHUNKS_PER_TILE;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      for (int c = 0; c < nch; ++c, ++g) {
+        const uint32_t slot = g % WSLOTS, ph = (g / WSLOTS) & 1;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * W_CHUNK_COLS), r);
+        tmem_ld_wait();
+        mbar_wait(&wfull[slot], ph);
+        uint8_t* wrow = smem_w + slot * W_CHUNK_BYTES + row * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4* p4 = reinterpret_cast<float4*>(wrow + ((j ^ (row & 7)) << 4));
+          float4 w = *p4;
+          w.x = fmaf(p.alpha, __uint_as_float(r[4 * j + 0]), w.x);
+          w.y = fmaf(p.alpha, __uint_as_float(r[4 * j + 1]), w.y);
+          w.z = fmaf(p.alpha, __uint_as_float(r[4 * j + 2]), w.z);
+          w.w = fmaf(p.alpha, __uint_as_float(r[4 * j + 3]), w.w);
+          *p4 = w;
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (q == 0 && lane == 0) {
+          tma_store_2d(&tmW, smem_w + slot * W_CHUNK_BYTES, n0 + c * W_CHUNK_COLS, mt * BM);
+          bulk_commit();
+          bulk_wait_read<1>();                 // the previous chunk's store has read its slot
+          if (g > 0) mbar_arrive(&wempty[(g - 1) % WSLOTS]);
+        }
+      }
+      // accumulator buffer free for the MMA of tile it+2
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+    if (q == 0 && lane == 0) bulk_wait_all();
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------- host side ----
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool encode_2d(CUtensorMap* map, const float* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+               uint32_t box_inner, uint32_t box_outer) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int sm_count_k1() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace
+
+bool recon_tcgen05_supported(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t M, int64_t N,
+                             const float* W) {
+  return aligned16(Ug) && aligned16(Vg) && aligned16(W) && ldu % 4 == 0 && ldv % 4 == 0 && N % 4 == 0 &&
+         ldu >= M && ldv >= N && M < (1 << 30) && N < (1 << 30);
+}
+
+cudaError_t launch_recon_tcgen05(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t rows,
+                                 int64_t M, int64_t N, float* W, float alpha, cudaStream_t s) {
+  if (M <= 0 || N <= 0 || rows <= 0) return cudaSuccess;
+  if (!recon_tcgen05_supported(Ug, ldu, Vg, ldv, M, N, W) || rows >= (1ll << 31)) return cudaErrorNotSupported;
+  CUtensorMap tmA, tmB, tmW;
+  if (!encode_2d(&tmA, Ug, (uint64_t)ldu, (uint64_t)rows, (uint64_t)ldu * 4, 32, BK) ||
+      !encode_2d(&tmB, Vg, (uint64_t)ldv, (uint64_t)rows, (uint64_t)ldv * 4, 32, BK) ||
+      !encode_2d(&tmW, W, (uint64_t)N, (uint64_t)M, (uint64_t)N * 4, W_CHUNK_COLS, BM))
+    return cudaErrorNotSupported;
+  Params p;
+  p.M = (int32_t)M;
+  p.N = (int32_t)N;
+  p.rows = (int32_t)rows;
+  p.m_tiles = (int32_t)((M + BM - 1) / BM);
+  p.n_tiles = (int32_t)((N + BN - 1) / BN);
+  p.num_tiles = p.m_tiles * p.n_tiles;
+  p.num_kb = (int32_t)((rows + BK - 1) / BK);
+  // boxes of the last tiles that touch valid memory (fully out-of-bounds boxes are skipped;
+  // they would only feed accumulator rows/cols that are never stored)
+  const int64_t m_rem = ldu - (int64_t)(p.m_tiles - 1) * BM;  // columns of Ug that exist in the last m tile
+  const int64_t n_rem = ldv - (int64_t)(p.n_tiles - 1) * BN;
+  p.a_boxes_valid_last = (int32_t)std::min<int64_t>(BM / 32, (m_rem + 31) / 32);
+  p.b_boxes_valid_last = (int32_t)std::min<int64_t>(BN / 32, (n_rem + 31) / 32);
+  p.alpha = alpha;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(recon_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int grid = std::min(p.num_tiles, sm_count_k1());
+  recon_tcgen05_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(tmA, tmB, tmW, p);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+}  // namespace poseidon

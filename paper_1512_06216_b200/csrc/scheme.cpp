@@ -1,0 +1,57 @@
+// SACP cost rule (Alg. 3; costs P:L333 and P:L335) and the shard
+// map of a PS layer (reading Z11).  Pure host integer code: no context, no GPU.
+#include <limits>
+
+#include "internal.h"
+
+namespace {
+
+bool mul_u64(uint64_t a, uint64_t b, uint64_t* out) { return !__builtin_mul_overflow(a, b, out); }
+bool add_u64(uint64_t a, uint64_t b, uint64_t* out) { return !__builtin_add_overflow(a, b, out); }
+
+}  // namespace
+
+extern "C" int32_t poseidon_choose_scheme(int32_t kind, int64_t M, int64_t N, int64_t K, int32_t P,
+                                          poseidon_costs_t* costs) {
+  using namespace poseidon;
+  if (M < 0 || N < 0 || K < 0 || P < 1) {
+    fail(POSEIDON_ERR_INVALID_ARG, "choose_scheme: need M, N, K >= 0 and P >= 1");
+    return POSEIDON_ERR_INVALID_ARG;
+  }
+  const uint64_t m = (uint64_t)M, n = (uint64_t)N, k = (uint64_t)K, p = (uint64_t)P;
+  uint64_t mpn, pm1sq, sfb, pk, pkmn, pmn, sfps, full;
+  // C_sfb = (P-1)^2 K (M+N)
+  bool ok = add_u64(m, n, &mpn) && mul_u64(p - 1, p - 1, &pm1sq) && mul_u64(pm1sq, k, &sfb) &&
+            mul_u64(sfb, mpn, &sfb);
+  // C_sfps = P K (M+N) + P M N
+  ok = ok && mul_u64(p, k, &pk) && mul_u64(pk, mpn, &pkmn) && mul_u64(p, m, &pmn) && mul_u64(pmn, n, &pmn) &&
+       add_u64(pkmn, pmn, &sfps);
+  // C_full = 2 P M N
+  ok = ok && mul_u64(2, pmn, &full);
+  if (!ok) {
+    fail(POSEIDON_ERR_INVALID_ARG, "choose_scheme: cost overflows 64 bits");
+    return POSEIDON_ERR_INVALID_ARG;
+  }
+  if (costs) {
+    costs->sfb = sfb;
+    costs->sf_ps = sfps;
+    costs->full_ps = full;
+  }
+  if (kind != POSEIDON_LAYER_FC) return POSEIDON_SCHEME_PS;       // Alg. 3 lines 1-3
+  return sfb <= sfps ? POSEIDON_SCHEME_SFB : POSEIDON_SCHEME_PS;   // Alg. 3 line 5, tie -> SFB
+}
+
+extern "C" poseidon_status_t poseidon_shard_range(int64_t n, int32_t P, int32_t rank, int64_t* begin,
+                                                  int64_t* end, int64_t* padded_n) {
+  using namespace poseidon;
+  if (n < 0 || P < 1 || rank < 0 || rank >= P)
+    return fail(POSEIDON_ERR_INVALID_ARG, "shard_range: need n >= 0, P >= 1, 0 <= rank < P");
+  const int64_t A = 32;
+  const int64_t S = A * ((n + A * P - 1) / (A * P));
+  const int64_t b = rank * S < n ? rank * S : n;
+  const int64_t e = (rank + 1) * S < n ? (rank + 1) * S : n;
+  if (begin) *begin = b;
+  if (end) *end = e;
+  if (padded_n) *padded_n = S * P;
+  return POSEIDON_OK;
+}

@@ -1,0 +1,79 @@
+"""CPU-side checks of the C-ABI boundary: the library loads, exports every
+symbol include/poseidon.h declares, and its pure host functions (SACP rule,
+shard map) agree bit-exactly with the oracle.  No GPU compute is called."""
+import itertools
+
+import pytest
+
+import oracle as O
+import paper_1512_06216_b200 as pz
+from paper_1512_06216_b200 import binding as B
+
+
+def test_library_exports_every_header_symbol():
+    names = B.header_functions()
+    assert len(names) >= 25
+    for n in names:
+        assert hasattr(B.lib, n), n
+    for n in ("poseidon_init", "poseidon_choose_scheme", "poseidon_sync_fc_sfb", "poseidon_sync_ps",
+              "poseidon_backprop_hook"):
+        assert n in names
+
+
+def test_version():
+    assert B.lib.poseidon_version() >= 10000
+
+
+SHAPES = [(128, 256), (256, 128), (64, 1024), (10, 64), (4096, 9216), (4096, 4096),
+          (1000, 4096), (1000, 1024), (21841, 4096), (1, 1)]
+
+
+def test_choose_scheme_bit_exact_vs_oracle():
+    Ks = list(range(1, 65)) + [100, 128, 255, 256, 257, 512, 1000, 1024, 2048, 4096]
+    for (M, N) in SHAPES:
+        for P in range(1, 65):
+            for K in Ks:
+                for kind in (O.LAYER_FC, O.LAYER_CONV):
+                    s, c = pz.choose_scheme(kind, M, N, K, P)
+                    assert s == O.choose_scheme(kind, M, N, K, P), (kind, M, N, K, P)
+                    assert c == O.costs(M, N, K, P)
+
+
+def test_choose_scheme_errors_and_overflow():
+    with pytest.raises(pz.PoseidonError):
+        pz.choose_scheme(1, -1, 5, 5, 2)
+    with pytest.raises(pz.PoseidonError):
+        pz.choose_scheme(1, 5, 5, 5, 0)
+    with pytest.raises(pz.PoseidonError):
+        pz.choose_scheme(1, 2 ** 40, 2 ** 40, 2 ** 20, 8)   # 2PMN overflows u64
+    # largest values still exact
+    s, c = pz.choose_scheme(1, 2 ** 20, 2 ** 20, 2 ** 20, 1000)
+    assert c == O.costs(2 ** 20, 2 ** 20, 2 ** 20, 1000)
+
+
+def test_shard_range_bit_exact_vs_oracle():
+    for n in list(range(0, 130)) + [650, 2432, 25632, 32896, 34944, 145578, 4097000, 37752832]:
+        for P in range(1, 9):
+            for r in range(P):
+                assert pz.shard_range(n, P, r) == O.shard_range(n, P, r)
+
+
+def test_shard_range_errors():
+    for args in ((-1, 2, 0), (10, 0, 0), (10, 2, 2), (10, 2, -1)):
+        with pytest.raises(pz.PoseidonError) as ei:
+            pz.shard_range(*args)
+        assert ei.value.code == B.ERR_INVALID_ARG
+
+
+def test_null_context_errors():
+    import ctypes
+    assert B.lib.poseidon_set_lr(None, ctypes.c_float(0.1)) == B.ERR_NOT_INITIALIZED
+    assert "NULL" in B.last_error()
+    assert B.lib.poseidon_backprop_hook(None, 0, None) == B.ERR_NOT_INITIALIZED
+    assert B.lib.poseidon_finalize(None) == B.OK
+
+
+def test_struct_layouts_match_header():
+    import ctypes
+    assert ctypes.sizeof(B.Topology) == 4 * 3 + 128 + 4
+    assert ctypes.sizeof(B.Costs) == 24

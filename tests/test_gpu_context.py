@@ -1,0 +1,106 @@
+"""GPU tests of the context-level C ABI at world == 1 (P = 1: no collective;
+SFB degenerates to K1 on local factors with alpha = -lr, PS to K2 over the
+whole buffer — reading Z10), compared with the fp64 oracle."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synthetic as S
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pz():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1512_06216_b200 as pz
+    return pz
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def test_context_sfb_and_ps_world1(pz):
+    ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device())
+    M, N, K = 128, 256, 8
+    assert ctx.register_layer(0, pz.LAYER_FC, M, N, K) == pz.SCHEME_SFB
+    assert ctx.register_layer(1, pz.LAYER_FC, M, N, K, scheme_override=pz.SCHEME_PS) == pz.SCHEME_PS
+    W, b = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, 1)
+    lr = 0.25
+    Wd, bd = dev(W), dev(b)
+    ctx.sync_fc_sfb(0, dev(Us[0]), dev(Vs[0]), Wd, bd, lr)
+    # PS path of the same layer: flat buffer W||b and its gradient
+    n = M * N + M
+    _, _, padded = pz.shard_range(n, 1, 0)
+    flatW = torch.zeros(padded, device="cuda")
+    flatW[:n] = dev(O.flatten_params(W, b).astype(np.float32))
+    G = Us[0].astype(np.float64).T @ Vs[0].astype(np.float64)
+    flatG = torch.zeros(padded, device="cuda")
+    flatG[:n] = dev(O.flatten_params(G, Us[0].astype(np.float64).sum(0)).astype(np.float32))
+    ctx.bind_ps_buffers(1, flatG, flatW, n, pz.PS_ZERO_GRAD)
+    ctx.sync_ps(1, flatG, flatW, n, lr)
+    ctx.wait_layer(0)
+    ctx.wait_layer(1)
+    st = ctx.iteration_end(stats=True)
+    assert st["n_layers"] == 2 and st["nccl_bytes_sent"] == 0
+    W1, b1 = O.sync_step(W, b, Us, Vs, lr)
+    assert O.update_error(W, host(Wd), W1) <= 2e-3
+    assert O.update_error(b, host(bd), b1) <= 1e-5
+    out = host(flatW)
+    assert O.update_error(W, out[:M * N].reshape(M, N), W1) <= 1e-5
+    assert O.update_error(b, out[M * N:n], b1) <= 1e-5
+    assert np.all(host(flatG) == 0)  # PS_ZERO_GRAD
+    ls = ctx.layer_stats(0)
+    assert ls["launched"] == 1 and ls["kernel_ms"] > 0
+    ctx.close()
+
+
+def test_context_hook_slot_path_and_dwbp_off(pz):
+    for flags in (0, pz.FLAG_DWBP_OFF):
+        ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device(), flags=flags)
+        M, N, K = 1000, 1024, 16
+        ctx.register_layer(3, pz.LAYER_FC, M, N, K)
+        W, b = S.fc_weights_randbias(M, N)
+        Us, Vs = S.hidden_factors(M, N, K, 1, seed=44)
+        Wd, bd = dev(W), dev(b)
+        ctx.bind_sfb_params(3, Wd, bd)
+        ctx.set_lr(0.1)
+        u_ptr, ldu, v_ptr, ldv = ctx.sfb_slot(3)
+        assert ldu == 1000 and ldv == 1024
+        # write the factors straight into the slot (zero-copy path)
+        from paper_1512_06216_b200.binding import device_view
+        device_view(u_ptr, (K, ldu)).copy_(dev(Us[0]))
+        device_view(v_ptr, (K, ldv)).copy_(dev(Vs[0]))
+        ctx.backprop_hook(3)
+        st = ctx.iteration_end(stats=True)
+        assert st["n_layers"] == 1
+        ctx.wait_layer(3)
+        W1, b1 = O.sync_step(W, b, Us, Vs, 0.1)
+        assert O.update_error(W, host(Wd), W1) <= 2e-3
+        assert O.update_error(b, host(bd), b1) <= 1e-5
+        ctx.close()
+
+
+def test_context_errors(pz):
+    ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device())
+    with pytest.raises(pz.PoseidonError) as ei:
+        ctx.backprop_hook(7)
+    assert ei.value.code == -8  # not registered
+    ctx.register_layer(7, pz.LAYER_CONV, 96, 363, 256)
+    with pytest.raises(pz.PoseidonError):
+        ctx.sync_fc_sfb(7, 1, 1, 1, None, 0.1)  # PS layer
+    with pytest.raises(pz.PoseidonError):
+        ctx.register_layer(8, pz.LAYER_CONV, 4, 4, 4, scheme_override=pz.SCHEME_SFB)
+    g = torch.zeros(96 * 363 + 96 + 64, device="cuda")
+    with pytest.raises(pz.PoseidonError):
+        ctx.bind_ps_buffers(7, g, g, 12345)  # wrong n
+    ctx.close()

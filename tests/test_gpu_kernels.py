@@ -1,0 +1,223 @@
+"""GPU parity of the hot-path kernels against the fp64 oracle (all through the
+C ABI).  Tolerances (BASELINE.json north_star, metric of reading Z13):
+  * integer variant: bit-exact on every path;
+  * fp32 CUDA-core paths (K1r, K2): max-normalised update error <= 1e-5;
+  * TF32 tensor-core path (K1): <= 2e-3.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import synthetic as S
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL_FP32 = 1e-5
+TOL_TF32 = 2e-3
+
+
+@pytest.fixture(scope="module")
+def pz():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_1512_06216_b200 as pz
+    return pz
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+# ------------------------------------------------------------------ K2 ----
+@pytest.mark.parametrize("count", [1, 3, 4, 5, 31, 1023, 1027, 4096, 65536 + 7, 1_000_003])
+def test_k2_integer_bit_exact(pz, count):
+    g = S.rng(count)
+    W = (g.integers(-1023, 1024, size=count) * 2.0 ** -10).astype(np.float32)
+    gr = g.integers(-64, 65, size=count).astype(np.float32)
+    alpha = -(2.0 ** -7)
+    Wd, gd = dev(W), dev(gr)
+    pz.ps_shard_update(gd, Wd, count, alpha)
+    ref = W.astype(np.float64) + alpha * gr.astype(np.float64)
+    assert np.array_equal(host(Wd).astype(np.float64), ref)
+
+
+def test_k2_unaligned_and_random(pz):
+    n = 100_001
+    W = S.dense_grads(n + 1, 1, seed=5, scale=1.0)[0]
+    gr = S.dense_grads(n + 1, 1, seed=6)[0]
+    Wd, gd = dev(W), dev(gr)
+    # offset by one float -> not 16-byte aligned -> scalar path
+    pz.ps_shard_update(gd[1:], Wd[1:], n, -0.01)
+    out = host(Wd)
+    ref = W.astype(np.float64)
+    ref[1:] += -0.01 * gr[1:].astype(np.float64)
+    assert out[0] == W[0]
+    assert O.update_error(W, out, ref) <= TOL_FP32
+
+
+def test_k2_stats_warp_reduction(pz):
+    n = 50_000
+    gr = S.dense_grads(n, 1, seed=9)[0]
+    gr[123] = np.inf
+    gr[40000] = np.nan
+    W = np.zeros(n, np.float32)
+    st = torch.zeros(2, device="cuda")
+    pz.ps_shard_update(dev(gr), dev(W), n, 0.5, stats=st)
+    s = host(st)
+    fin = np.isfinite(gr)
+    assert s[1] == 2.0
+    # sum of squares over the finite updates is reported only when all are finite; check separately
+    st2 = torch.zeros(2, device="cuda")
+    gr2 = np.where(fin, gr, 0).astype(np.float32)
+    pz.ps_shard_update(dev(gr2), dev(W), n, 0.5, stats=st2)
+    s2 = host(st2)
+    ref = float(np.sum((0.5 * gr2.astype(np.float64)) ** 2))
+    assert s2[1] == 0.0 and abs(s2[0] - ref) / ref < 1e-5
+
+
+def test_k2_zero_count_is_noop(pz):
+    W = dev(np.ones(8, np.float32))
+    pz.ps_shard_update(W, W, 0, 1.0)
+    assert np.all(host(W) == 1.0)
+
+
+# --------------------------------------------------------- PS simulated ----
+@pytest.mark.parametrize("n,P", [(650, 8), (2432, 8), (34944, 8), (145578, 3), (32896, 2), (100, 1), (37, 4)])
+def test_ps_simulated_integer_bit_exact(pz, n, P):
+    _, _, padded = O.shard_range(n, P, 0)
+    g = S.rng(n + P)
+    W = (g.integers(-1023, 1024, size=padded) * 2.0 ** -10).astype(np.float32)
+    grads = np.zeros((P, padded), np.float32)
+    for p, gp in enumerate(S.integer_grads(n, P, seed=n)):
+        grads[p, :n] = gp
+    lr = 2.0 ** -7 * (P if P in (1, 2, 4, 8) else 1)
+    Wd = dev(W)
+    pz.ps_simulated(dev(grads), P, Wd, n, lr)
+    out = host(Wd)
+    ref = O.ps_step_flat(W[:n], [grads[p, :n] for p in range(P)], lr)
+    if P in (1, 2, 4, 8):
+        assert np.array_equal(out[:n].astype(np.float64), ref)
+    else:
+        assert O.update_error(W[:n], out[:n], ref) <= TOL_FP32
+    assert np.array_equal(out[n:], W[n:])  # padding untouched
+
+
+def test_ps_simulated_random(pz):
+    n, P = 1_000_000, 8
+    _, _, padded = O.shard_range(n, P, 0)
+    W = np.zeros(padded, np.float32)
+    W[:n] = S.dense_grads(n, 1, seed=1, scale=0.05)[0]
+    grads = np.zeros((P, padded), np.float32)
+    for p, gp in enumerate(S.dense_grads(n, P, seed=2)):
+        grads[p, :n] = gp
+    Wd = dev(W)
+    pz.ps_simulated(dev(grads), P, Wd, n, 0.01)
+    out = host(Wd)
+    ref = O.ps_step_flat(W[:n], [grads[p, :n] for p in range(P)], 0.01)
+    assert O.update_error(W[:n], out[:n], ref) <= TOL_FP32
+
+
+# -------------------------------------------------------- SFB simulated ----
+SFB_CASES = [
+    # (M, N, K, P)   C1; ragged tiles; C2 ip2 (M not /4, N < 256); odd everything; tiny
+    (128, 256, 8, 2),
+    (1000, 1024, 16, 3),
+    (10, 64, 100, 2),
+    (333, 260, 7, 3),
+    (1, 4, 1, 1),
+    (130, 516, 33, 2),
+    (640, 4096, 32, 4),
+]
+
+
+@pytest.mark.parametrize("recon", ["fp32", "tf32"])
+@pytest.mark.parametrize("M,N,K,P", SFB_CASES)
+def test_sfb_simulated_vs_oracle(pz, recon, M, N, K, P):
+    W, b = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, P)
+    lr = 0.5
+    Wd, bd = dev(W), dev(b)
+    pz.sfb_simulated(dev(np.concatenate(Us)), dev(np.concatenate(Vs)), P, K, M, N, Wd, bd, lr,
+                     recon=pz.RECON_FP32 if recon == "fp32" else pz.RECON_TF32)
+    W1, b1 = O.sync_step(W, b, Us, Vs, lr)
+    tol = TOL_FP32 if recon == "fp32" else TOL_TF32
+    assert O.update_error(W, host(Wd), W1) <= tol
+    # the bias uses the unrounded fp32 column sums on both paths
+    assert O.update_error(b, host(bd), b1) <= TOL_FP32
+
+
+@pytest.mark.parametrize("recon", ["fp32", "tf32"])
+@pytest.mark.parametrize("M,N,K,P", [(128, 256, 8, 2), (1000, 1024, 64, 4), (10, 64, 100, 2),
+                                     (300, 520, 40, 8), (256, 512, 256, 8)])
+def test_sfb_integer_bit_exact(pz, recon, M, N, K, P):
+    W, b, Us, Vs, lr = S.integer_factors(M, N, K, P, seed=M + N)
+    Wd, bd = dev(W), dev(b)
+    pz.sfb_simulated(dev(np.concatenate(Us)), dev(np.concatenate(Vs)), P, K, M, N, Wd, bd, lr,
+                     recon=pz.RECON_FP32 if recon == "fp32" else pz.RECON_TF32)
+    W1, b1 = O.sync_step(W, b, Us, Vs, lr)
+    assert np.array_equal(host(Wd).astype(np.float64), W1)
+    assert np.array_equal(host(bd).astype(np.float64), b1)
+
+
+def test_sfb_sfb_equals_ps_on_same_layer(pz):
+    """Cross-path check (SURVEY 8(c) K2 numerics): SFB (TF32) and PS (fp32)
+    land within the TF32 gate of each other; PS within 1e-5 of the oracle."""
+    M, N, K, P = 256, 384, 32, 4
+    W, b = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, P)
+    lr = 0.3
+    Wd = dev(W)
+    pz.sfb_simulated(dev(np.concatenate(Us)), dev(np.concatenate(Vs)), P, K, M, N, Wd, None, lr)
+    n = M * N
+    _, _, padded = O.shard_range(n, P, 0)
+    grads = np.zeros((P, padded), np.float32)
+    for p in range(P):
+        grads[p, :n] = (Us[p].astype(np.float64).T @ Vs[p].astype(np.float64)).astype(np.float32).reshape(-1)
+    Wps = np.zeros(padded, np.float32)
+    Wps[:n] = W.reshape(-1)
+    Wpsd = dev(Wps)
+    pz.ps_simulated(dev(grads), P, Wpsd, n, lr)
+    W1, _ = O.sync_step(W, None, Us, Vs, lr)
+    sfb_out = host(Wd)
+    ps_out = host(Wpsd)[:n].reshape(M, N)
+    assert O.update_error(W, sfb_out, W1) <= TOL_TF32
+    assert O.update_error(W, ps_out, W1) <= TOL_FP32
+    assert O.update_error(W, sfb_out, ps_out) <= TOL_TF32
+
+
+def test_reconstruct_zero_rows_noop(pz):
+    W = dev(np.ones((8, 8), np.float32))
+    U = dev(np.ones((1, 8), np.float32))
+    pz.reconstruct_sgd(U, 8, U, 8, 0, 8, 8, W, 1.0)
+    assert np.all(host(W) == 1.0)
+
+
+# ------------------------------------------- full size, sampled rows ----
+def _sampled_rows(M, n=48, seed=0):
+    g = S.rng(seed)
+    rows = np.unique(np.concatenate([[0, M - 1, M // 2, 127, 128], g.integers(0, M, size=n)]))
+    return rows[rows < M]
+
+
+@pytest.mark.parametrize("M,N,K,P", [(4096, 9216, 256, 8),     # C3 fc6 at P=8 (bench launch shape x8 rows)
+                                     (4096, 9216, 256, 1),     # C3 fc6 at P=1 (bench N=1 launch)
+                                     (21841, 4096, 256, 2)])   # C5 softmax FC (M not a multiple of 4)
+def test_sfb_full_size_sampled_rows(pz, M, N, K, P):
+    W, b = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, P)
+    lr = 0.5
+    Wd, bd = dev(W), dev(b)
+    pz.sfb_simulated(dev(np.concatenate(Us)), dev(np.concatenate(Vs)), P, K, M, N, Wd, bd, lr)
+    out, outb = host(Wd), host(bd)
+    rows = _sampled_rows(M)
+    W1r, b1r = O.sync_step_rows(W[rows], b[rows], Us, Vs, lr, rows)
+    assert O.update_error(W[rows], out[rows], W1r) <= TOL_TF32
+    assert O.update_error(b[rows], outb[rows], b1r) <= TOL_FP32
+    # property at any size: rows never sampled still moved only where factors are non-zero
+    assert np.all(np.isfinite(out))
