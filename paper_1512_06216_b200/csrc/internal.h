@@ -46,7 +46,8 @@ cudaError_t launch_recon_simt(const float* Ug, int64_t ldu, const float* Vg, int
 // K1: tcgen05 TF32 version.  Returns cudaErrorNotSupported when the shape/alignment cannot be
 // described by TMA (caller reports it).  Tensor maps are (re)encoded per call (cheap host work).
 cudaError_t launch_recon_tcgen05(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t rows,
-                                 int64_t M, int64_t N, float* W, float alpha, cudaStream_t s);
+                                 int64_t M, int64_t N, float* W, float alpha, cudaStream_t s,
+                                 float* dbg = nullptr);
 bool recon_tcgen05_supported(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t M,
                              int64_t N, const float* W);
 

@@ -177,6 +177,7 @@ struct Params {
   int32_t m_tiles, n_tiles, num_tiles, num_kb;
   int32_t a_boxes_valid_last, b_boxes_valid_last;  // boxes of the last m/n tile that are not fully OOB
   float alpha;
+  float* dbg;  // debug dump (tile 0 of CTA 0): smem stage 0 of A|B, raw accumulator; NULL in production
 };
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -257,6 +258,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+          if (p.dbg != nullptr && it == 0 && kb == 0 && blockIdx.x == 0) {
+            const float* src = reinterpret_cast<const float*>(smem_ops + stage * STAGE_BYTES);
+            for (int i = 0; i < STAGE_BYTES / 4; ++i) p.dbg[i] = src[i];
+          }
           const uint32_t sa = smem_u32(smem_ops + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_STAGE_BYTES;
 #pragma unroll
@@ -309,6 +314,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * W_CHUNK_COLS), r);
         tmem_ld_wait();
+        if (p.dbg != nullptr && it == 0 && blockIdx.x == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) p.dbg[STAGE_BYTES / 4 + row * BN + c * 32 + j] = __uint_as_float(r[j]);
+        }
         mbar_wait(&wfull[slot], ph);
         uint8_t* wrow = smem_w + slot * W_CHUNK_BYTES + row * 128;
 #pragma unroll
@@ -396,7 +405,7 @@ bool recon_tcgen05_supported(const float* Ug, int64_t ldu, const float* Vg, int6
 }
 
 cudaError_t launch_recon_tcgen05(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t rows,
-                                 int64_t M, int64_t N, float* W, float alpha, cudaStream_t s) {
+                                 int64_t M, int64_t N, float* W, float alpha, cudaStream_t s, float* dbg) {
   if (M <= 0 || N <= 0 || rows <= 0) return cudaSuccess;
   if (!recon_tcgen05_supported(Ug, ldu, Vg, ldv, M, N, W) || rows >= (1ll << 31)) return cudaErrorNotSupported;
   CUtensorMap tmA, tmB, tmW;
@@ -419,6 +428,7 @@ cudaError_t launch_recon_tcgen05(const float* Ug, int64_t ldu, const float* Vg, 
   p.a_boxes_valid_last = (int32_t)std::min<int64_t>(BM / 32, (m_rem + 31) / 32);
   p.b_boxes_valid_last = (int32_t)std::min<int64_t>(BN / 32, (n_rem + 31) / 32);
   p.alpha = alpha;
+  p.dbg = dbg;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(recon_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -432,3 +442,12 @@ cudaError_t launch_recon_tcgen05(const float* Ug, int64_t ldu, const float* Vg, 
 }
 
 }  // namespace poseidon
+
+// Debug entry (not part of include/poseidon.h): runs K1 and dumps stage 0 of tile 0 and its raw
+// accumulator into dbg (STAGE_BYTES/4 + 128*256 floats).
+extern "C" int poseidon_debug_recon_tcgen05(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t rows,
+                                            int64_t M, int64_t N, float* W, float alpha, float* dbg) {
+  cudaError_t e = poseidon::launch_recon_tcgen05(Ug, ldu, Vg, ldv, rows, M, N, W, alpha, 0, dbg);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return (int)e;
+}
