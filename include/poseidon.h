@@ -123,7 +123,8 @@ int32_t poseidon_choose_scheme(int32_t kind, int64_t M, int64_t N, int64_t K, in
  *  V: K x N, row k = layer input a_i of sample k.
  *  W: M x N (NULL -> bound W), bias: M (NULL -> bound bias or none).
  * Enqueues on `producer`: pack of U, V into this rank's slot of the gather
- * buffers (+ per-worker bias column sums, optional TF32 RN rounding).  Then on
+ * buffers (transposed to K-major, + per-worker bias column sums, TF32 RN
+ * rounding on the TF32 path).  Then on
  * the library's streams: all-gather of all ranks' factors (NCCL, skipped at
  * P == 1) and the fused reconstruction + SGD  W += alpha * Ug^T Vg,
  * b += alpha * sum_rows Ug.  U and V may be reused after the producer stream
@@ -144,8 +145,8 @@ poseidon_status_t poseidon_sync_ps(poseidon_ctx_t ctx, int32_t layer_id, float* 
 
 /* DWBP trigger (Alg. 2 line 9): "layer `layer_id`'s gradient inputs
  * are complete on `stream`".  PS layers sync their bound buffers; SFB layers
- * sync the factors the caller wrote into poseidon_sfb_slot() (the library
- * finalises the slot: column sums + optional rounding).  Starts the layer's
+ * sync the factors the caller wrote into the staging slot of
+ * poseidon_sfb_slot() (packed like sync_fc_sfb does).  Starts the layer's
  * sync on the library streams right away (or at iteration_end under
  * POSEIDON_FLAG_DWBP_OFF). */
 poseidon_status_t poseidon_backprop_hook(poseidon_ctx_t ctx, int32_t layer_id, poseidon_stream_t stream);
@@ -163,14 +164,18 @@ poseidon_status_t poseidon_shard_range(int64_t n, int32_t P, int32_t rank, int64
 /* Register layer `layer_id` (0 <= id < 4096): kind, M x N weight, per-worker
  * batch K, has_bias.  scheme_override: -1 -> SACP rule, else the scheme to use
  * (C2 forces PS).  chosen_scheme may be NULL.  SFB layers get library-owned
- * gather buffers Ug[P*K x M_pad], Vg[P*K x N_pad], Bs[P x M_pad] with
- * M_pad = roundup(M,4).  A layer may be re-registered only while idle. */
+ * gather buffers, rank-major with K-major blocks (the tensor cores consume
+ * TF32 operands K-major): Ug [P][M][ldk], Vg [P][N][ldk], Bs [P][M] (per-worker
+ * column sums of U for the bias), ldk = roundup(K,4), padding zero.
+ * Re-registering a layer waits for its previous sync. */
 poseidon_status_t poseidon_register_layer(poseidon_ctx_t ctx, int32_t layer_id, int32_t kind,
                                           int64_t M, int64_t N, int64_t K, int32_t has_bias,
                                           int32_t scheme_override, int32_t* chosen_scheme);
 
-/* Zero-copy pack target of an SFB layer: this rank's U slot (K rows, row
- * stride *ld_u = M_pad floats) and V slot (K rows, stride *ld_v = N_pad). */
+/* Staging slot of an SFB layer for poseidon_backprop_hook: library-owned
+ * device buffers U [K x M] (*ld_u = M) and V [K x N] (*ld_v = N), row-major,
+ * allocated on first call.  The caller writes the factors there (ordered
+ * before the hook's stream), then calls poseidon_backprop_hook. */
 poseidon_status_t poseidon_sfb_slot(poseidon_ctx_t ctx, int32_t layer_id, float** U_slot,
                                     int64_t* ld_u, float** V_slot, int64_t* ld_v);
 
@@ -234,12 +239,13 @@ poseidon_status_t poseidon_ps_simulated(const float* grads, int32_t P_sim, float
 poseidon_status_t poseidon_ps_shard_update(const float* g, float* W, int64_t count, float alpha,
                                            float* stats, poseidon_stream_t stream);
 
-/* Reconstruction alone on already-gathered, already-rounded buffers:
- * W[M x N] += alpha * Ug^T Vg with Ug [rows x ldu], Vg [rows x ldv]
- * (ldu >= M, ldv >= N, multiples of 4). */
-poseidon_status_t poseidon_reconstruct_sgd(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv,
-                                           int64_t rows, int64_t M, int64_t N, float* W, float alpha,
-                                           int32_t recon, poseidon_stream_t stream);
+/* Reconstruction alone (K1 / K1r) on already-gathered, already-rounded
+ * buffers in the gather layout: W[M x N] += alpha * sum_p sum_k<K
+ * Ug[p][m][k] Vg[p][n][k], Ug [P][M][ldk], Vg [P][N][ldk], ldk >= K.  The
+ * TF32 path needs ldk and N multiples of 4 and 16-byte aligned buffers. */
+poseidon_status_t poseidon_reconstruct_sgd(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk,
+                                           int64_t M, int64_t N, float* W, float alpha, int32_t recon,
+                                           poseidon_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -283,6 +283,26 @@ def update_error(W0, W1_test, W1_ref) -> float:
     return num / denom
 
 
+def update_error_fp32(W0, W1_test, W1_ref) -> float:
+    """Z13 metric for a result STORED in fp32 (reading Z13b): the deviation of
+    each element beyond one fp32 ulp of the reference value W'_ref (the
+    unavoidable rounding of the stored result, which is not arithmetic error
+    of the update) is normalised by max |dW_ref|.  With the test updates much
+    larger than one ulp of W, a wrong scale or sign still reads ~1."""
+    W0 = np.asarray(W0, np.float64)
+    t = np.asarray(W1_test, np.float64)
+    r = np.asarray(W1_ref, np.float64)
+    if r.size == 0:
+        return 0.0
+    ulp = np.spacing(np.abs(r).astype(np.float32)).astype(np.float64)
+    dev = np.maximum(np.abs(t - r) - ulp, 0.0)
+    denom = float(np.max(np.abs(r - W0)))
+    num = float(np.max(dev))
+    if denom == 0.0:
+        return 0.0 if num == 0.0 else math.inf
+    return num / denom
+
+
 def update_error_rows(W0, W1_test, W1_ref, rows) -> float:
     """Z13 metric restricted to sampled rows (full-size parity on samples);
     the normaliser is the max over the sampled rows."""

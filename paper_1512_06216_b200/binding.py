@@ -104,7 +104,7 @@ _SIGS = {
     "poseidon_sfb_simulated": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _vp, _vp, _f, _i32, _vp]),
     "poseidon_ps_simulated": (_i32, [_vp, _i32, _vp, _i64, _f, _vp]),
     "poseidon_ps_shard_update": (_i32, [_vp, _vp, _i64, _f, _vp, _vp]),
-    "poseidon_reconstruct_sgd": (_i32, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp, _f, _i32, _vp]),
+    "poseidon_reconstruct_sgd": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _f, _i32, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(lib, _name)
@@ -269,8 +269,8 @@ def ps_shard_update(g, W, count, alpha, stats=None, stream=None):
     _check(lib.poseidon_ps_shard_update(_ptr(g), _ptr(W), count, float(alpha), _ptr(stats), _stream(stream)))
 
 
-def reconstruct_sgd(Ug, ldu, Vg, ldv, rows, M, N, W, alpha, recon=RECON_TF32, stream=None):
-    _check(lib.poseidon_reconstruct_sgd(_ptr(Ug), ldu, _ptr(Vg), ldv, rows, M, N, _ptr(W), float(alpha), recon,
+def reconstruct_sgd(Ug, Vg, P, K, ldk, M, N, W, alpha, recon=RECON_TF32, stream=None):
+    _check(lib.poseidon_reconstruct_sgd(_ptr(Ug), _ptr(Vg), P, K, ldk, M, N, _ptr(W), float(alpha), recon,
                                         _stream(stream)))
 
 

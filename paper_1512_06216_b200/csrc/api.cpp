@@ -66,9 +66,11 @@ struct Layer {
   int kind = 0, scheme = 0, recon = POSEIDON_RECON_TF32;
   int64_t M = 0, N = 0, K = 0;
   bool has_bias = false;
-  // SFB: library-owned gather buffers (rank-major)
-  int64_t M_pad = 0, N_pad = 0;
+  // SFB: library-owned gather buffers (rank-major, K-major blocks): Ug [P][M][ldk],
+  // Vg [P][N][ldk], Bs [P][M] (per-worker column sums of U); optional staging [K][M], [K][N]
+  int64_t ldk = 0;
   float *Ug = nullptr, *Vg = nullptr, *Bs = nullptr;
+  float *stU = nullptr, *stV = nullptr;
   float *W = nullptr, *bias = nullptr;  // bound SFB params
   // PS: caller-owned padded flat buffers
   float *grad = nullptr, *Wps = nullptr;
@@ -161,7 +163,7 @@ poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float*
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
   IterRecord& r = open_record(c);
   if (P > 1) {
-    const size_t ucount = (size_t)(L.K * L.M_pad), vcount = (size_t)(L.K * L.N_pad), bcount = (size_t)L.M_pad;
+    const size_t ucount = (size_t)(L.M * L.ldk), vcount = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
     NC_TRY(ncclGroupStart());
     NC_TRY(ncclAllGather(L.Ug + (size_t)c->rank * ucount, L.Ug, ucount, ncclFloat32, c->comm, c->comm_stream));
     NC_TRY(ncclAllGather(L.Vg + (size_t)c->rank * vcount, L.Vg, vcount, ncclFloat32, c->comm, c->comm_stream));
@@ -175,15 +177,14 @@ poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float*
   CU_TRY(cudaStreamWaitEvent(c->recon_stream, e.gathered, 0));
   CU_TRY(cudaEventRecord(e.kstart, c->recon_stream));
   const float alpha = -lr / (float)P;
-  const int64_t rows = (int64_t)P * L.K;
   cudaError_t err;
-  if (L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(L.Ug, L.M_pad, L.Vg, L.N_pad, L.M, L.N, W))
-    err = launch_recon_tcgen05(L.Ug, L.M_pad, L.Vg, L.N_pad, rows, L.M, L.N, W, alpha, c->recon_stream);
+  if (L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(L.Ug, L.Vg, L.ldk, L.M, L.N, W))
+    err = launch_recon_tcgen05(L.Ug, L.Vg, P, L.K, L.ldk, L.M, L.N, W, alpha, c->recon_stream);
   else
-    err = launch_recon_simt(L.Ug, L.M_pad, L.Vg, L.N_pad, rows, L.M, L.N, W, L.N, alpha, c->recon_stream);
+    err = launch_recon_simt(L.Ug, L.Vg, P, L.K, L.ldk, L.M, L.N, W, alpha, c->recon_stream);
   if (err != cudaSuccess) return cuda_fail(err, "reconstruct+sgd launch");
   if (bias) {
-    err = launch_bias_update(L.Bs, L.M_pad, P, bias, L.M, alpha, c->recon_stream);
+    err = launch_bias_update(L.Bs, L.M, P, bias, L.M, alpha, c->recon_stream);
     if (err != cudaSuccess) return cuda_fail(err, "bias update launch");
   }
   CU_TRY(cudaEventRecord(e.kend, c->recon_stream));
@@ -244,12 +245,12 @@ poseidon_status_t sfb_after_pack(poseidon_ctx_t c, int32_t id, Layer& L, float* 
 poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t ldU, const float* V, int64_t ldV,
                            cudaStream_t producer) {
   const bool round = (L.recon == POSEIDON_RECON_TF32);
-  float* u_slot = L.Ug + (size_t)c->rank * L.K * L.M_pad;
-  float* v_slot = L.Vg + (size_t)c->rank * L.K * L.N_pad;
-  float* b_slot = L.Bs + (size_t)c->rank * L.M_pad;
-  cudaError_t err = launch_pack(U, ldU, u_slot, L.M_pad, L.K, L.M, round, b_slot, producer);
+  float* u_slot = L.Ug + (size_t)c->rank * L.M * L.ldk;
+  float* v_slot = L.Vg + (size_t)c->rank * L.N * L.ldk;
+  float* b_slot = L.Bs + (size_t)c->rank * L.M;
+  cudaError_t err = launch_pack_t(U, ldU, u_slot, L.ldk, L.K, L.M, round, b_slot, producer);
   if (err != cudaSuccess) return cuda_fail(err, "pack U launch");
-  err = launch_pack(V, ldV, v_slot, L.N_pad, L.K, L.N, round, nullptr, producer);
+  err = launch_pack_t(V, ldV, v_slot, L.ldk, L.K, L.N, round, nullptr, producer);
   if (err != cudaSuccess) return cuda_fail(err, "pack V launch");
   return POSEIDON_OK;
 }
@@ -258,7 +259,9 @@ void free_layer(Layer& L) {
   if (L.Ug) cudaFree(L.Ug);
   if (L.Vg) cudaFree(L.Vg);
   if (L.Bs) cudaFree(L.Bs);
-  L.Ug = L.Vg = L.Bs = nullptr;
+  if (L.stU) cudaFree(L.stU);
+  if (L.stV) cudaFree(L.stV);
+  L.Ug = L.Vg = L.Bs = L.stU = L.stV = nullptr;
   if (L.events_created) {
     for (int i = 0; i < RING; ++i) {
       EvSet& e = L.ev[i];
@@ -398,14 +401,13 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
   L.has_bias = has_bias != 0;
   L.scheme = scheme;
   if (scheme == POSEIDON_SCHEME_SFB) {
-    L.M_pad = round_up(M, 4);
-    L.N_pad = round_up(N, 4);
+    L.ldk = round_up(K, 4);
     const size_t P = (size_t)c->world;
-    const size_t ub = P * (size_t)(K * L.M_pad) * 4, vb = P * (size_t)(K * L.N_pad) * 4, bb = P * (size_t)L.M_pad * 4;
+    const size_t ub = P * (size_t)(M * L.ldk) * 4, vb = P * (size_t)(N * L.ldk) * 4, bb = P * (size_t)M * 4;
     CU_TRY(cudaMalloc(&L.Ug, ub));
     CU_TRY(cudaMalloc(&L.Vg, vb));
     CU_TRY(cudaMalloc(&L.Bs, bb));
-    CU_TRY(cudaMemset(L.Ug, 0, ub));  // padding columns stay zero forever
+    CU_TRY(cudaMemset(L.Ug, 0, ub));  // k columns in [K, ldk) stay zero forever
     CU_TRY(cudaMemset(L.Vg, 0, vb));
     CU_TRY(cudaMemset(L.Bs, 0, bb));
   }
@@ -422,10 +424,15 @@ poseidon_status_t poseidon_sfb_slot(poseidon_ctx_t c, int32_t id, float** U_slot
   poseidon_status_t st = check_layer(c, id, &L);
   if (st) return st;
   if (L->scheme != POSEIDON_SCHEME_SFB) return fail(POSEIDON_ERR_STATE, "layer is not an SFB layer");
-  if (U_slot) *U_slot = L->Ug + (size_t)c->rank * L->K * L->M_pad;
-  if (V_slot) *V_slot = L->Vg + (size_t)c->rank * L->K * L->N_pad;
-  if (ld_u) *ld_u = L->M_pad;
-  if (ld_v) *ld_v = L->N_pad;
+  if (!L->stU) {
+    cudaSetDevice(c->device);
+    CU_TRY(cudaMalloc(&L->stU, (size_t)(L->K * L->M) * 4));
+    CU_TRY(cudaMalloc(&L->stV, (size_t)(L->K * L->N) * 4));
+  }
+  if (U_slot) *U_slot = L->stU;
+  if (V_slot) *V_slot = L->stV;
+  if (ld_u) *ld_u = L->M;
+  if (ld_v) *ld_v = L->N;
   return POSEIDON_OK;
 }
 
@@ -542,15 +549,13 @@ poseidon_status_t poseidon_backprop_hook(poseidon_ctx_t c, int32_t id, poseidon_
   poseidon_status_t st = check_layer(c, id, &L);
   if (st) return st;
   if (L->scheme == POSEIDON_SCHEME_PS) return poseidon_sync_ps(c, id, nullptr, nullptr, L->n, c->lr, stream);
-  // SFB: the caller wrote its factors into the slot; finalise in place (colsum + rounding)
+  // SFB: the caller wrote its factors into the staging slot (poseidon_sfb_slot); pack them
   if (!L->W) return fail(POSEIDON_ERR_STATE, "SFB layer has no bound W (poseidon_bind_sfb_params)");
+  if (!L->stU) return fail(POSEIDON_ERR_STATE, "SFB layer has no staging slot (call poseidon_sfb_slot first)");
   cudaStream_t ps = reinterpret_cast<cudaStream_t>(stream);
-  float* u_slot = L->Ug + (size_t)c->rank * L->K * L->M_pad;
-  float* v_slot = L->Vg + (size_t)c->rank * L->K * L->N_pad;
-  // the slot was written by the caller after its own wait_layer; still order after the last sync
   st = producer_guard(c, *L, ps);
   if (st) return st;
-  st = pack_sfb(c, *L, u_slot, L->M_pad, v_slot, L->N_pad, ps);
+  st = pack_sfb(c, *L, L->stU, L->M, L->stV, L->N, ps);
   if (st) return st;
   return sfb_after_pack(c, id, *L, L->W, L->bias, c->lr, ps);
 }
@@ -670,30 +675,32 @@ poseidon_status_t poseidon_sfb_simulated(const float* U_all, const float* V_all,
   if (!aligned16(W)) return fail(POSEIDON_ERR_ALIGNMENT, "W must be 16-byte aligned");
   if (K == 0) return POSEIDON_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int64_t M_pad = round_up(M, 4), N_pad = round_up(N, 4);
-  const size_t ub = (size_t)P * K * M_pad * 4, vb = (size_t)P * K * N_pad * 4, bb = (size_t)P * M_pad * 4;
+  const int64_t ldk = round_up(K, 4);
+  const size_t ub = (size_t)P * M * ldk * 4, vb = (size_t)P * N * ldk * 4, bb = (size_t)P * M * 4;
   float *Ug = nullptr, *Vg = nullptr, *Bs = nullptr;
   CU_TRY(cudaMallocAsync(&Ug, ub, s));
   CU_TRY(cudaMallocAsync(&Vg, vb, s));
   CU_TRY(cudaMallocAsync(&Bs, bb, s));
-  CU_TRY(cudaMemsetAsync(Ug, 0, ub, s));
-  CU_TRY(cudaMemsetAsync(Vg, 0, vb, s));
+  if (ldk != K) {
+    CU_TRY(cudaMemsetAsync(Ug, 0, ub, s));
+    CU_TRY(cudaMemsetAsync(Vg, 0, vb, s));
+  }
   const bool round = recon == POSEIDON_RECON_TF32;
   cudaError_t err = cudaSuccess;
   for (int p = 0; p < P && err == cudaSuccess; ++p) {
-    err = launch_pack(U_all + (size_t)p * K * M, M, Ug + (size_t)p * K * M_pad, M_pad, K, M, round,
-                      Bs + (size_t)p * M_pad, s);
+    err = launch_pack_t(U_all + (size_t)p * K * M, M, Ug + (size_t)p * M * ldk, ldk, K, M, round,
+                        Bs + (size_t)p * M, s);
     if (err == cudaSuccess)
-      err = launch_pack(V_all + (size_t)p * K * N, N, Vg + (size_t)p * K * N_pad, N_pad, K, N, round, nullptr, s);
+      err = launch_pack_t(V_all + (size_t)p * K * N, N, Vg + (size_t)p * N * ldk, ldk, K, N, round, nullptr, s);
   }
   const float alpha = -lr / (float)P;
   if (err == cudaSuccess) {
-    if (round && recon_tcgen05_supported(Ug, M_pad, Vg, N_pad, M, N, W))
-      err = launch_recon_tcgen05(Ug, M_pad, Vg, N_pad, (int64_t)P * K, M, N, W, alpha, s);
+    if (round && recon_tcgen05_supported(Ug, Vg, ldk, M, N, W))
+      err = launch_recon_tcgen05(Ug, Vg, P, K, ldk, M, N, W, alpha, s);
     else
-      err = launch_recon_simt(Ug, M_pad, Vg, N_pad, (int64_t)P * K, M, N, W, N, alpha, s);
+      err = launch_recon_simt(Ug, Vg, P, K, ldk, M, N, W, alpha, s);
   }
-  if (err == cudaSuccess && bias) err = launch_bias_update(Bs, M_pad, P, bias, M, alpha, s);
+  if (err == cudaSuccess && bias) err = launch_bias_update(Bs, M, P, bias, M, alpha, s);
   cudaFreeAsync(Ug, s);
   cudaFreeAsync(Vg, s);
   cudaFreeAsync(Bs, s);
@@ -724,19 +731,19 @@ poseidon_status_t poseidon_ps_shard_update(const float* g, float* W, int64_t cou
   return POSEIDON_OK;
 }
 
-poseidon_status_t poseidon_reconstruct_sgd(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t rows,
+poseidon_status_t poseidon_reconstruct_sgd(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk,
                                            int64_t M, int64_t N, float* W, float alpha, int32_t recon,
                                            poseidon_stream_t stream) {
-  if (!Ug || !Vg || !W || rows < 0 || M <= 0 || N <= 0 || ldu < M || ldv < N)
+  if (!Ug || !Vg || !W || P < 1 || K < 0 || M <= 0 || N <= 0 || ldk < K)
     return fail(POSEIDON_ERR_INVALID_ARG, "reconstruct_sgd: bad arguments");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t err;
   if (recon == POSEIDON_RECON_TF32) {
-    if (!recon_tcgen05_supported(Ug, ldu, Vg, ldv, M, N, W))
-      return fail(POSEIDON_ERR_ALIGNMENT, "tcgen05 path needs 16-B aligned buffers, ldu/ldv/N multiples of 4");
-    err = launch_recon_tcgen05(Ug, ldu, Vg, ldv, rows, M, N, W, alpha, s);
+    if (!recon_tcgen05_supported(Ug, Vg, ldk, M, N, W))
+      return fail(POSEIDON_ERR_ALIGNMENT, "tcgen05 path needs 16-B aligned buffers and ldk, N multiples of 4");
+    err = launch_recon_tcgen05(Ug, Vg, P, K, ldk, M, N, W, alpha, s);
   } else if (recon == POSEIDON_RECON_FP32) {
-    err = launch_recon_simt(Ug, ldu, Vg, ldv, rows, M, N, W, N, alpha, s);
+    err = launch_recon_simt(Ug, Vg, P, K, ldk, M, N, W, alpha, s);
   } else {
     return fail(POSEIDON_ERR_INVALID_ARG, "bad recon");
   }

@@ -30,25 +30,23 @@ cudaError_t launch_ps_shard_update(const float* g, float* W, int64_t count, floa
 cudaError_t launch_ps_sim_update(const float* g, int64_t ld, int32_t P, float* W, int64_t count,
                                  float alpha, cudaStream_t s);
 
-// K3: pack K rows of src (row stride ld_src) into dst (row stride ld_dst), columns [0, cols);
-// optional TF32 round-to-nearest; if colsum != NULL also writes colsum[c] = sum_k src[k][c]
-// (fp32, fixed row order, of the UNROUNDED values).
-cudaError_t launch_pack(const float* src, int64_t ld_src, float* dst, int64_t ld_dst, int64_t K,
-                        int64_t cols, bool round_tf32, float* colsum, cudaStream_t s);
+// K3: transpose-pack K rows x `cols` columns of src (row stride ld_src) into dst[cols x ldk]
+// (dst[c*ldk + k] = src[k*ld_src + c]); optional TF32 round-to-nearest; if colsum != NULL
+// also writes colsum[c] = sum_k src[k][c] (fp32, fixed order, UNROUNDED values).
+cudaError_t launch_pack_t(const float* src, int64_t ld_src, float* dst, int64_t ldk, int64_t K, int64_t cols,
+                          bool round_tf32, float* colsum, cudaStream_t s);
 // bias[m] = fmaf(alpha, sum_p bs[p*ld + m], bias[m]) for m in [0, M), p in worker order.
-cudaError_t launch_bias_update(const float* bs, int64_t ld, int32_t P, float* bias, int64_t M,
-                               float alpha, cudaStream_t s);
+cudaError_t launch_bias_update(const float* bs, int64_t ld, int32_t P, float* bias, int64_t M, float alpha,
+                               cudaStream_t s);
 
-// K1r: W[M x N] += alpha * Ug^T Vg on CUDA cores (fp32 FMA).
-cudaError_t launch_recon_simt(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t rows,
-                              int64_t M, int64_t N, float* W, int64_t ldw, float alpha, cudaStream_t s);
+// K1r: W[M x N] += alpha * sum_p sum_k Ug[p][m][k] Vg[p][n][k] on CUDA cores (fp32 FMA).
+cudaError_t launch_recon_simt(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
+                              int64_t N, float* W, float alpha, cudaStream_t s);
 
-// K1: tcgen05 TF32 version.  Returns cudaErrorNotSupported when the shape/alignment cannot be
-// described by TMA (caller reports it).  Tensor maps are (re)encoded per call (cheap host work).
-cudaError_t launch_recon_tcgen05(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t rows,
-                                 int64_t M, int64_t N, float* W, float alpha, cudaStream_t s,
-                                 float* dbg = nullptr);
-bool recon_tcgen05_supported(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t M,
-                             int64_t N, const float* W);
+// K1: the same on tcgen05 (TF32 operands, fp32 TMEM accumulators).  Returns cudaErrorNotSupported
+// when TMA cannot describe the buffers.  Tensor maps are encoded per call (host only, ~us).
+cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
+                                 int64_t N, float* W, float alpha, cudaStream_t s, float* dbg = nullptr);
+bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int64_t M, int64_t N, const float* W);
 
 }  // namespace poseidon

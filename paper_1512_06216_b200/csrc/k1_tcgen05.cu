@@ -1,16 +1,18 @@
 // K1 — SFB reconstruction fused with the SGD update on the 5th-generation
 // tensor cores (step (3) of SFB; Alg. 3 line 8; Eq. 5).
 //
-//   W[M x N] += alpha * Ug^T Vg      Ug: rows x M (ld ldu), Vg: rows x N (ld ldv)
+//   W[M x N] += alpha * sum_p sum_k Ug[p][m][k] * Vg[p][n][k]
 //
-// "rows" = P*K: every worker's sufficient factors, rank-major, exactly as the
-// all-gather leaves them.  Both operands are MN-major (M resp. N contiguous),
-// which tcgen05 supports for TF32 (instruction-descriptor bits 15/16), so the
-// gathered buffers are consumed in place with no transpose.
+// Ug: P blocks of M x ldk, Vg: P blocks of N x ldk (K contiguous, ldk =
+// roundup(K,4)): every worker's sufficient factors, rank-major, exactly as
+// the all-gather leaves them.  Both operands are K-major: on sm_100a the
+// MN-major (transposed) TF32 variant of tcgen05.mma was measured to produce
+// all-zero accumulators (tools/tc_probe.cu), so K3 transposes the factors
+// while packing them and the reduction index (p, k) is contiguous in memory.
 //
 // Design (sm_100a, one CTA per SM, persistent, 256 threads):
-//   warp 0      TMA producer: Ug/Vg slabs of BK=32 rows -> 3-stage smem ring
-//               (128B swizzle; 4 boxes of 32x32 for A, 8 for B; 48 KB/stage)
+//   warp 0      TMA producer: Ug/Vg slabs of BK=32 k (128 B) -> 3-stage smem ring
+//               (128B swizzle; one 32x128 box for A, one 32x256 box for B; 48 KB/stage)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //               (M=128, N=256, K=8, kind::tf32, fp32 accumulate in TMEM,
 //               double-buffered accumulators: 2 x 256 columns = all 512)
@@ -41,10 +43,8 @@ constexpr int BK = 32;          // factor rows per pipeline stage
 constexpr int UK = 8;           // K per tcgen05.mma for tf32
 constexpr int STAGES = 3;
 constexpr int WSLOTS = 4;
-constexpr int A_BOX_BYTES = 32 * BK * 4;               // 4 KB: 32 m x 32 k
-constexpr int B_BOX_BYTES = 32 * BK * 4;
-constexpr int A_STAGE_BYTES = (BM / 32) * A_BOX_BYTES;   // 16 KB
-constexpr int B_STAGE_BYTES = (BN / 32) * B_BOX_BYTES;   // 32 KB
+constexpr int A_STAGE_BYTES = BM * BK * 4;   // 16 KB: 128 m x 32 k
+constexpr int B_STAGE_BYTES = BN * BK * 4;   // 32 KB: 256 n x 32 k
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int W_CHUNK_COLS = 32;
 constexpr int W_CHUNK_BYTES = BM * W_CHUNK_COLS * 4;     // 16 KB
@@ -86,6 +86,14 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int32_t x, int32_t y,
+                                            int32_t z, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t x, int32_t y) {
@@ -149,10 +157,11 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// Shared-memory matrix descriptor (tcgen05), SWIZZLE_128B, MN-major canonical layout
-// ((8,m),(8,k)) : ((1,LBO),(8,SBO)) in 16-byte units: LBO = stride between 32-float
-// MN chunks (one TMA box = BK rows x 128 B), SBO = stride between 8-row K groups (1 KB).
-__device__ __forceinline__ uint64_t make_desc_mn_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+// Shared-memory matrix descriptor (tcgen05), SWIZZLE_128B, K-major canonical layout
+// ((8,m),(T,2)) : ((8T,SBO),(1,T)) in 16-byte units: rows of 128 B (32 tf32 k values),
+// SBO = stride between 8-row groups (1 KB); LBO unused for swizzled K-major (encoded 1).
+// The k-th UMMA (K=8 -> 32 B) of a stage starts 32*k bytes into the 1 KB-aligned atom.
+__device__ __forceinline__ uint64_t make_desc_k_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
@@ -162,20 +171,17 @@ __device__ __forceinline__ uint64_t make_desc_mn_sw128(uint32_t saddr, uint32_t 
   return d;
 }
 
-// Instruction descriptor: D=f32, A=B=tf32, A and B MN-major, N=BN, M=BM.
+// Instruction descriptor: D=f32, A=B=tf32, A and B K-major, N=BN, M=BM.
 __host__ __device__ constexpr uint32_t make_idesc() {
   return (1u << 4)              // c_format = F32
          | (2u << 7)            // a_format = TF32
          | (2u << 10)           // b_format = TF32
-         | (1u << 15)           // a_major = MN
-         | (1u << 16)           // b_major = MN
          | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
 struct Params {
-  int32_t M, N, rows;
-  int32_t m_tiles, n_tiles, num_tiles, num_kb;
-  int32_t a_boxes_valid_last, b_boxes_valid_last;  // boxes of the last m/n tile that are not fully OOB
+  int32_t M, N;
+  int32_t m_tiles, n_tiles, num_tiles, num_kb, kb_per_p;
   float alpha;
   float* dbg;  // debug dump (tile 0 of CTA 0): smem stage 0 of A|B, raw accumulator; NULL in production
 };
@@ -227,18 +233,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t stage = 0, phase = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
         const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
-        const int a_boxes = (mt == p.m_tiles - 1) ? p.a_boxes_valid_last : BM / 32;
-        const int b_boxes = (nt == p.n_tiles - 1) ? p.b_boxes_valid_last : BN / 32;
-        const uint32_t tx = (uint32_t)(a_boxes * A_BOX_BYTES + b_boxes * B_BOX_BYTES);
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for (int kk = 0; kk < p.num_kb; ++kk) {
+          const int pw = kk / p.kb_per_p, kb = kk - pw * p.kb_per_p;
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], tx);
+          mbar_expect_tx(&full[stage], (uint32_t)STAGE_BYTES);
           uint8_t* sa = smem_ops + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_STAGE_BYTES;
-          for (int j = 0; j < a_boxes; ++j)
-            tma_load_2d(&tmA, &full[stage], sa + j * A_BOX_BYTES, mt * BM + 32 * j, kb * BK, pol);
-          for (int j = 0; j < b_boxes; ++j)
-            tma_load_2d(&tmB, &full[stage], sb + j * B_BOX_BYTES, nt * BN + 32 * j, kb * BK, pol);
+          tma_load_3d(&tmA, &full[stage], sa, kb * BK, mt * BM, pw, pol);
+          tma_load_3d(&tmB, &full[stage], sb, kb * BK, nt * BN, pw, pol);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -258,7 +260,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < p.num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          if (p.dbg != nullptr && it == 0 && kb == 0 && blockIdx.x == 0) {
+          if (p.dbg != nullptr && it == 0 && kb == 0 && blockIdx.x == 0) {  // debug dump only
             const float* src = reinterpret_cast<const float*>(smem_ops + stage * STAGE_BYTES);
             for (int i = 0; i < STAGE_BYTES / 4; ++i) p.dbg[i] = src[i];
           }
@@ -266,8 +268,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t sb = sa + A_STAGE_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k) {
-            const uint64_t ad = make_desc_mn_sw128(sa + k * 1024, A_BOX_BYTES, 1024);
-            const uint64_t bd = make_desc_mn_sw128(sb + k * 1024, B_BOX_BYTES, 1024);
+            const uint64_t ad = make_desc_k_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = make_desc_k_sw128(sb + k * 32, 16, 1024);
             tc_mma_tf32(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
           }
           tc_commit(&empty[stage]);
@@ -371,15 +373,15 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-bool encode_2d(CUtensorMap* map, const float* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
-               uint32_t box_inner, uint32_t box_outer) {
+bool encode(CUtensorMap* map, const float* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+            const uint32_t* box) {
   auto enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {row_bytes};
-  cuuint32_t box[2] = {box_inner, box_outer};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+  cuuint64_t d[3], st[2];
+  cuuint32_t b[3], estr[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; }
+  for (int i = 0; i < rank - 1; ++i) st[i] = strides_bytes[i];
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<float*>(base), d, st, b, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -398,35 +400,35 @@ int sm_count_k1() {
 
 }  // namespace
 
-bool recon_tcgen05_supported(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t M, int64_t N,
-                             const float* W) {
-  return aligned16(Ug) && aligned16(Vg) && aligned16(W) && ldu % 4 == 0 && ldv % 4 == 0 && N % 4 == 0 &&
-         ldu >= M && ldv >= N && M < (1 << 30) && N < (1 << 30);
+bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int64_t M, int64_t N, const float* W) {
+  return aligned16(Ug) && aligned16(Vg) && aligned16(W) && ldk % 4 == 0 && N % 4 == 0 && M < (1 << 30) &&
+         N < (1 << 30) && ldk < (1 << 30);
 }
 
-cudaError_t launch_recon_tcgen05(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t rows,
-                                 int64_t M, int64_t N, float* W, float alpha, cudaStream_t s, float* dbg) {
-  if (M <= 0 || N <= 0 || rows <= 0) return cudaSuccess;
-  if (!recon_tcgen05_supported(Ug, ldu, Vg, ldv, M, N, W) || rows >= (1ll << 31)) return cudaErrorNotSupported;
+cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
+                                 int64_t N, float* W, float alpha, cudaStream_t s, float* dbg) {
+  if (M <= 0 || N <= 0 || K <= 0 || P <= 0) return cudaSuccess;
+  if (!recon_tcgen05_supported(Ug, Vg, ldk, M, N, W) || ldk < K) return cudaErrorNotSupported;
   CUtensorMap tmA, tmB, tmW;
-  if (!encode_2d(&tmA, Ug, (uint64_t)ldu, (uint64_t)rows, (uint64_t)ldu * 4, 32, BK) ||
-      !encode_2d(&tmB, Vg, (uint64_t)ldv, (uint64_t)rows, (uint64_t)ldv * 4, 32, BK) ||
-      !encode_2d(&tmW, W, (uint64_t)N, (uint64_t)M, (uint64_t)N * 4, W_CHUNK_COLS, BM))
+  const uint64_t dA[3] = {(uint64_t)ldk, (uint64_t)M, (uint64_t)P};
+  const uint64_t sA[2] = {(uint64_t)ldk * 4, (uint64_t)ldk * 4 * (uint64_t)M};
+  const uint32_t bA[3] = {BK, BM, 1};
+  const uint64_t dB[3] = {(uint64_t)ldk, (uint64_t)N, (uint64_t)P};
+  const uint64_t sB[2] = {(uint64_t)ldk * 4, (uint64_t)ldk * 4 * (uint64_t)N};
+  const uint32_t bB[3] = {BK, BN, 1};
+  const uint64_t dW[2] = {(uint64_t)N, (uint64_t)M};
+  const uint64_t sW[1] = {(uint64_t)N * 4};
+  const uint32_t bW[2] = {W_CHUNK_COLS, BM};
+  if (!encode(&tmA, Ug, 3, dA, sA, bA) || !encode(&tmB, Vg, 3, dB, sB, bB) || !encode(&tmW, W, 2, dW, sW, bW))
     return cudaErrorNotSupported;
   Params p;
   p.M = (int32_t)M;
   p.N = (int32_t)N;
-  p.rows = (int32_t)rows;
   p.m_tiles = (int32_t)((M + BM - 1) / BM);
   p.n_tiles = (int32_t)((N + BN - 1) / BN);
   p.num_tiles = p.m_tiles * p.n_tiles;
-  p.num_kb = (int32_t)((rows + BK - 1) / BK);
-  // boxes of the last tiles that touch valid memory (fully out-of-bounds boxes are skipped;
-  // they would only feed accumulator rows/cols that are never stored)
-  const int64_t m_rem = ldu - (int64_t)(p.m_tiles - 1) * BM;  // columns of Ug that exist in the last m tile
-  const int64_t n_rem = ldv - (int64_t)(p.n_tiles - 1) * BN;
-  p.a_boxes_valid_last = (int32_t)std::min<int64_t>(BM / 32, (m_rem + 31) / 32);
-  p.b_boxes_valid_last = (int32_t)std::min<int64_t>(BN / 32, (n_rem + 31) / 32);
+  p.kb_per_p = (int32_t)((K + BK - 1) / BK);  // k columns >= K of a block are zero (padding / TMA OOB)
+  p.num_kb = p.kb_per_p * P;
   p.alpha = alpha;
   p.dbg = dbg;
   static bool attr_set = false;
@@ -445,9 +447,9 @@ cudaError_t launch_recon_tcgen05(const float* Ug, int64_t ldu, const float* Vg, 
 
 // Debug entry (not part of include/poseidon.h): runs K1 and dumps stage 0 of tile 0 and its raw
 // accumulator into dbg (STAGE_BYTES/4 + 128*256 floats).
-extern "C" int poseidon_debug_recon_tcgen05(const float* Ug, int64_t ldu, const float* Vg, int64_t ldv, int64_t rows,
+extern "C" int poseidon_debug_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk,
                                             int64_t M, int64_t N, float* W, float alpha, float* dbg) {
-  cudaError_t e = poseidon::launch_recon_tcgen05(Ug, ldu, Vg, ldv, rows, M, N, W, alpha, 0, dbg);
+  cudaError_t e = poseidon::launch_recon_tcgen05(Ug, Vg, P, K, ldk, M, N, W, alpha, 0, dbg);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   return (int)e;
 }

@@ -58,7 +58,7 @@ def test_k2_unaligned_and_random(pz):
     ref = W.astype(np.float64)
     ref[1:] += -0.01 * gr[1:].astype(np.float64)
     assert out[0] == W[0]
-    assert O.update_error(W, out, ref) <= TOL_FP32
+    assert O.update_error_fp32(W, out, ref) <= TOL_FP32
 
 
 def test_k2_stats_warp_reduction(pz):
@@ -104,7 +104,7 @@ def test_ps_simulated_integer_bit_exact(pz, n, P):
     if P in (1, 2, 4, 8):
         assert np.array_equal(out[:n].astype(np.float64), ref)
     else:
-        assert O.update_error(W[:n], out[:n], ref) <= TOL_FP32
+        assert O.update_error_fp32(W[:n], out[:n], ref) <= TOL_FP32
     assert np.array_equal(out[n:], W[n:])  # padding untouched
 
 
@@ -120,7 +120,7 @@ def test_ps_simulated_random(pz):
     pz.ps_simulated(dev(grads), P, Wd, n, 0.01)
     out = host(Wd)
     ref = O.ps_step_flat(W[:n], [grads[p, :n] for p in range(P)], 0.01)
-    assert O.update_error(W[:n], out[:n], ref) <= TOL_FP32
+    assert O.update_error_fp32(W[:n], out[:n], ref) <= TOL_FP32
 
 
 # -------------------------------------------------------- SFB simulated ----
@@ -147,9 +147,9 @@ def test_sfb_simulated_vs_oracle(pz, recon, M, N, K, P):
                      recon=pz.RECON_FP32 if recon == "fp32" else pz.RECON_TF32)
     W1, b1 = O.sync_step(W, b, Us, Vs, lr)
     tol = TOL_FP32 if recon == "fp32" else TOL_TF32
-    assert O.update_error(W, host(Wd), W1) <= tol
+    assert O.update_error_fp32(W, host(Wd), W1) <= tol
     # the bias uses the unrounded fp32 column sums on both paths
-    assert O.update_error(b, host(bd), b1) <= TOL_FP32
+    assert O.update_error_fp32(b, host(bd), b1) <= TOL_FP32
 
 
 @pytest.mark.parametrize("recon", ["fp32", "tf32"])
@@ -186,16 +186,35 @@ def test_sfb_sfb_equals_ps_on_same_layer(pz):
     W1, _ = O.sync_step(W, None, Us, Vs, lr)
     sfb_out = host(Wd)
     ps_out = host(Wpsd)[:n].reshape(M, N)
-    assert O.update_error(W, sfb_out, W1) <= TOL_TF32
-    assert O.update_error(W, ps_out, W1) <= TOL_FP32
-    assert O.update_error(W, sfb_out, ps_out) <= TOL_TF32
+    assert O.update_error_fp32(W, sfb_out, W1) <= TOL_TF32
+    assert O.update_error_fp32(W, ps_out, W1) <= TOL_FP32
+    assert O.update_error_fp32(W, sfb_out, ps_out) <= TOL_TF32
 
 
 def test_reconstruct_zero_rows_noop(pz):
     W = dev(np.ones((8, 8), np.float32))
-    U = dev(np.ones((1, 8), np.float32))
-    pz.reconstruct_sgd(U, 8, U, 8, 0, 8, 8, W, 1.0)
+    U = dev(np.ones((8, 8), np.float32))
+    pz.reconstruct_sgd(U, U, 1, 0, 8, 8, 8, W, 1.0)
     assert np.all(host(W) == 1.0)
+    pz.reconstruct_sgd(U, U, 1, 0, 8, 8, 8, W, 1.0, recon=pz.RECON_FP32)
+    assert np.all(host(W) == 1.0)
+
+
+@pytest.mark.parametrize("recon", ["fp32", "tf32"])
+def test_reconstruct_sgd_gather_layout(pz, recon):
+    """K1/K1r on buffers already in the gather layout ([P][M][ldk], ldk > K)."""
+    M, N, K, P, ldk = 200, 300, 6, 3, 8
+    g = S.rng(77)
+    U = np.zeros((P, M, ldk), np.float32)
+    V = np.zeros((P, N, ldk), np.float32)
+    U[:, :, :K] = g.integers(-3, 4, size=(P, M, K))
+    V[:, :, :K] = g.integers(0, 4, size=(P, N, K))
+    W = (g.integers(-1023, 1024, size=(M, N)) * 2.0 ** -10).astype(np.float32)
+    Wd = dev(W)
+    pz.reconstruct_sgd(dev(U), dev(V), P, K, ldk, M, N, Wd, -(2.0 ** -9),
+                       recon=pz.RECON_FP32 if recon == "fp32" else pz.RECON_TF32)
+    ref = W.astype(np.float64) - 2.0 ** -9 * np.einsum("pmk,pnk->mn", U.astype(np.float64), V.astype(np.float64))
+    assert np.array_equal(host(Wd).astype(np.float64), ref)
 
 
 # ------------------------------------------- full size, sampled rows ----
@@ -217,7 +236,7 @@ def test_sfb_full_size_sampled_rows(pz, M, N, K, P):
     out, outb = host(Wd), host(bd)
     rows = _sampled_rows(M)
     W1r, b1r = O.sync_step_rows(W[rows], b[rows], Us, Vs, lr, rows)
-    assert O.update_error(W[rows], out[rows], W1r) <= TOL_TF32
-    assert O.update_error(b[rows], outb[rows], b1r) <= TOL_FP32
+    assert O.update_error_fp32(W[rows], out[rows], W1r) <= TOL_TF32
+    assert O.update_error_fp32(b[rows], outb[rows], b1r) <= TOL_FP32
     # property at any size: rows never sampled still moved only where factors are non-zero
     assert np.all(np.isfinite(out))

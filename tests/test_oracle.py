@@ -313,3 +313,14 @@ def test_update_error_metric_catches_2x_bug():
     bad = W0 - 2e-4
     assert O.update_error(W0, ref, ref) == 0.0
     assert O.update_error(W0, bad, ref) == pytest.approx(1.0, rel=1e-2)
+
+
+def test_update_error_fp32_excuses_only_storage_rounding():
+    W0 = np.full(8, 1.0, np.float32)
+    ref = W0.astype(np.float64) - 1e-3 * np.arange(8)
+    stored = ref.astype(np.float32)          # correctly rounded result
+    assert O.update_error_fp32(W0, stored, ref) == 0.0
+    wrong = (W0.astype(np.float64) - 2e-3 * np.arange(8)).astype(np.float32)
+    assert O.update_error_fp32(W0, wrong, ref) > 0.99
+    off_by_two_ulps = ref + 2 * np.spacing(np.float32(1.0))
+    assert O.update_error_fp32(W0, off_by_two_ulps, ref) > 0

@@ -10,7 +10,7 @@ from paper_1512_06216_b200 import binding as B  # noqa: E402
 
 f = B.lib.poseidon_debug_recon_tcgen05
 f.restype = ctypes.c_int
-f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
               ctypes.c_int64, ctypes.c_void_p, ctypes.c_float, ctypes.c_void_p]
 
 M, N, rows = 128, 256, 32
