@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""Poseidon-on-B200 benchmark (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
+    python bench.py --impl reference ...                     (fp64 CPU oracle arm)
+
+A step is one synchronous data-parallel training iteration of the config's CNN
+on synthetic data: forward, backward with DWBP (each layer's sync — SACP's SFB
+all-gather + tcgen05 reconstruct+SGD, or PS reduce-scatter + K2 + all-gather —
+launched by the library as soon as the layer's backward is done), and the
+next-forward barrier.  The optimiser step IS the sync (Alg. 1/3).  Metric
+(BASELINE.json): images/sec (whole job), plus exposed sync ms/iter and the
+roofline fraction of the dominant sync kernel.  Default config C3 (AlexNet,
+batch 256/GPU): the config the north-star target is stated on and the only
+one that exercises every hot-path step (SFB on FC + PS on conv + DWBP).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3", choices=["C2", "C3", "C4", "C5"])
+    ap.add_argument("--impl", default="poseidon", choices=["poseidon", "reference"])
+    ap.add_argument("--scheme", default=None, choices=[None, "auto", "ps", "sfb"])
+    ap.add_argument("--dwbp", default="on", choices=["on", "off"])
+    ap.add_argument("--recon", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layer-stats", action="store_true", help="print per-layer stats to stderr")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "source": "measured"}
+    # fallback stated in /opt/skills/guides/B200_PROFILING.md
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+TF32_OVER_BF16 = 1.1 / 2.25   # nominal dense ratio (B200_PROFILING.md table)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------- oracle arm ----
+def oracle_step_seconds(config: str, P: int, budget_s: float):
+    """Time the fp64 oracle's synchronous step (O4 for SFB layers, O6 for PS
+    layers) for one iteration of `config` at P workers on a bounded sample:
+    each SFB layer is timed on its first R output rows (R sized to the budget)
+    and scaled by M/R (each output row is independent work of equal size).
+    Returns (seconds per full iteration, sample description, threads)."""
+    import numpy as np
+
+    import oracle as O
+    import synthetic as S
+    from drivers.cnn import CONFIGS
+    import torch.nn as nn
+
+    cfg = CONFIGS[config]
+    K = cfg["batch"]
+    with_meta = __import__("torch").device("meta")
+    with with_meta:
+        model = cfg["model"]()
+    layers = []
+    for name, m in model.named_modules():
+        if isinstance(m, nn.Linear):
+            layers.append((name, O.LAYER_FC, m.out_features, m.in_features, True))
+        elif isinstance(m, nn.Conv2d):
+            layers.append((name, O.LAYER_CONV, m.out_channels, m.weight[0].numel(), m.bias is not None))
+    scheme_mode = cfg["scheme"]
+    total = 0.0
+    desc = []
+    flops_budget = 2.0e9 * budget_s  # ~2 GFLOP/s/thread-ish fp64 BLAS is conservative; refined below
+    for (name, kind, M, N, has_b) in layers:
+        sch = O.choose_scheme(kind, M, N, K, P)
+        if scheme_mode == "ps":
+            sch = O.SCHEME_PS
+        if sch == O.SCHEME_SFB:
+            rows = max(1, min(M, int(flops_budget / max(1.0, 2.0 * N * K * P))))
+            W = np.zeros((rows, N), np.float32)
+            b = np.zeros(rows, np.float32)
+            Us = [np.asarray(S.rng(p).standard_normal((K, rows)), np.float32) for p in range(P)]
+            Vs = [np.asarray(S.rng(100 + p).standard_normal((K, N)), np.float32) for p in range(P)]
+            t0 = time.perf_counter()
+            O.sync_step(W, b, Us, Vs, 0.01)
+            dt = time.perf_counter() - t0
+            total += dt * (M / rows)
+            desc.append(f"{name}:SFB O4 rows {rows}/{M}")
+        else:
+            n = M * N + (M if has_b else 0)
+            grads = [np.zeros(n, np.float32) for _ in range(P)]
+            w = np.zeros(n, np.float32)
+            t0 = time.perf_counter()
+            O.ps_step_flat(w, grads, 0.01)
+            total += time.perf_counter() - t0
+            desc.append(f"{name}:PS O6 n={n}")
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count() or 1
+    return total, "; ".join(desc), threads
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from drivers.cnn import CONFIGS
+    cfg = CONFIGS[args.config]
+    P = args.gpus
+    per_step_budget = max(0.5, 150.0 / max(1, args.steps + args.warmup))
+    times = []
+    desc, threads = "", 1
+    for i in range(args.warmup + args.steps):
+        sec, desc, threads = oracle_step_seconds(args.config, P, per_step_budget)
+        if i >= args.warmup:
+            times.append(sec)
+    sec = statistics.median(times)
+    value = P * cfg["batch"] / sec
+    line = {
+        "impl": "reference", "metric": "images/sec (sync step of one iteration, fp64 CPU oracle)",
+        "value": value, "unit": "images/s", "n_gpus": P, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} {cfg['name']} sync step", "global_batch": P * cfg["batch"],
+                   "per_gpu_batch": cfg["batch"], "parallelism": f"dp{P}"},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "oracle",
+                         "sample": "per step: " + desc + " (SFB rows scaled by M/R)"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------- poseidon arm ----
+def run_poseidon(args):
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+
+    import paper_1512_06216_b200 as pz
+    from paper_1512_06216_b200.dwbp import PoseidonSync
+    from drivers.cnn import CONFIGS
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    torch.backends.cudnn.benchmark = True
+    torch.backends.cudnn.allow_tf32 = True
+    torch.backends.cuda.matmul.allow_tf32 = True
+
+    cfg = CONFIGS[args.config]
+    K, hw, classes = cfg["batch"], cfg["hw"], cfg["classes"]
+    scheme = args.scheme or cfg["scheme"]
+
+    # NCCL unique id from rank 0 through torch.distributed (plumbing only)
+    nccl_id = None
+    if world > 1:
+        obj = [pz.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    flags = pz.FLAG_DWBP_OFF if args.dwbp == "off" else 0
+    ctx = pz.Context(rank=rank, world=world, device=local, nccl_id=nccl_id, flags=flags)
+
+    torch.manual_seed(6216)          # identical weights on every rank
+    model = cfg["model"]().to(dev)
+    recon = pz.RECON_TF32 if args.recon == "tf32" else pz.RECON_FP32
+    sync = PoseidonSync(model, ctx, K=K, lr=args.lr, scheme=scheme, recon=recon)
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(1512 + rank)
+    x = torch.rand((K, 3, hw, hw), device=dev, generator=g)
+    y = torch.randint(0, classes, (K,), device=dev, generator=g)
+
+    def step(xb, yb):
+        out = model(xb)
+        loss = F.cross_entropy(out, yb)
+        loss.backward()
+        sync.iteration_end()
+        return loss
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timed region ----
+    for _ in range(args.warmup):
+        step(x, y)
+    sync.wait_all()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.25)  # let the sampler start
+    l0 = pz.launch_count()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(x, y)
+    sync.wait_all()
+    ev1.record(stream)
+    ev1.synchronize()
+    launches = pz.launch_count() - l0
+    clk = clocks.stop()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    images = world * K * args.steps
+    value = images / (ms / 1e3)
+
+    # per-iteration sync statistics (device events kept by the library)
+    n_stats = min(args.steps, 7)
+    its = [ctx.iter_stats(a) for a in range(n_stats)]
+    exposed = statistics.mean(i["exposed_ms"] for i in its)
+    sync_total = statistics.mean(i["sync_total_ms"] for i in its)
+    nccl_sent = its[0]["nccl_bytes_sent"]
+    nccl_recv = its[0]["nccl_bytes_recv"]
+    if world > 1:
+        t = torch.tensor([exposed, sync_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        exposed, sync_total = float(t[0]), float(t[1])
+
+    # dominant sync kernel: the largest SFB layer's K1 (else the largest PS layer's K2)
+    sfb = [p for p in sync.plans if p.scheme == pz.SCHEME_SFB]
+    peaks = measured_peaks()
+    roof = None
+    if sfb:
+        top = max(sfb, key=lambda p: p.M * p.N)
+        kms = statistics.mean(ctx.layer_stats(top.layer_id, a)["kernel_ms"] for a in range(n_stats))
+        M, N, Kf, P = top.M, top.N, top.K, world
+        ldk = (Kf + 3) // 4 * 4
+        flops = 2.0 * M * N * Kf * P
+        byts = 8.0 * M * N + 4.0 * P * ldk * (M + N)
+        tf32_peak = peaks["bf16_tflops_sustained"] * TF32_OVER_BF16
+        ridge = tf32_peak * 1e12 / (peaks["hbm_gbs"] * 1e9)
+        if flops / byts >= ridge:
+            ach = flops / (kms / 1e3) / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
+                    "frac": ach / tf32_peak}
+        else:
+            ach = byts / (kms / 1e3) / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": ach / peaks["hbm_gbs"]}
+        roof.update({"kernel": f"K1 recon_tcgen05 ({top.name} {M}x{N}, P*K={P * Kf})" if args.recon == "tf32"
+                     else f"K1r recon_simt ({top.name})", "kernel_ms": kms,
+                     "algorithmic_flops": flops, "algorithmic_bytes": byts,
+                     "peak_source": f"{peaks['source']} (tf32 = bf16 sustained x 1.1/2.25)"})
+    else:
+        top = max(sync.plans, key=lambda p: p.n)
+        kms = statistics.mean(ctx.layer_stats(top.layer_id, a)["kernel_ms"] for a in range(n_stats))
+        b0, e0, _ = pz.shard_range(top.n, world, rank)
+        byts = 12.0 * (e0 - b0)
+        ach = byts / (kms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "kernel": f"K2 ps_shard_sgd ({top.name})", "kernel_ms": kms,
+                "algorithmic_bytes": byts, "peak_source": peaks["source"]}
+    roof["traffic"] = None
+    tr_path = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            with open(tr_path) as f:
+                tr = json.load(f)
+            key = f"{args.config}_P{world}"
+            if key in tr:
+                roof["traffic"] = tr[key]
+        except Exception:
+            pass
+
+    if args.layer_stats and rank == 0:
+        for p in sync.plans:
+            sys.stderr.write(json.dumps({"layer": p.name, **ctx.layer_stats(p.layer_id, 0)}) + "\n")
+
+    # ---- end to end: pinned host batch -> device each step, loss back to host ----
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        yh = y.cpu().pin_memory()
+        for _ in range(2):
+            step(xh.to(dev, non_blocking=True), yh.to(dev, non_blocking=True)).item()
+        sync.wait_all()
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            xb = xh.to(dev, non_blocking=True)
+            yb = yh.to(dev, non_blocking=True)
+            loss_val = step(xb, yb).item()
+        sync.wait_all()
+        ev1.record(stream)
+        ev1.synchronize()
+        ms_e = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms_e], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e = float(t.item())
+        e2e = {"value": images / (ms_e / 1e3), "unit": "images/s",
+               "h2d_bytes_per_step": int(xh.numel() * 4 + yh.numel() * 8), "d2h_bytes_per_step": 4,
+               "ms_per_step": ms_e / args.steps, "last_loss": loss_val}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sec, desc, threads = oracle_step_seconds(args.config, world, 12.0)
+        cpu = {"value": world * K / sec, "unit": "images/s", "cores": threads, "kind": "oracle",
+               "sample": f"fp64 oracle sync step of one {args.config} iteration at P={world}: {desc} "
+                         "(SFB layers timed on R rows, scaled by M/R)",
+               "seconds_per_iteration": sec}
+
+    if rank == 0:
+        line = {
+            "metric": "images/sec (exposed sync ms/iter and % of roofline alongside)",
+            "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "tf32" if args.recon == "tf32" else "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config} {cfg['name']} training step, Poseidon sync (SACP+DWBP)",
+                       "model": cfg["name"], "global_batch": world * K, "per_gpu_batch": K,
+                       "parallelism": f"dp{world}", "scheme": scheme, "dwbp": args.dwbp,
+                       "l2": "inputs larger than L2 (images 158 MB + weights 244 MB per step for C3)",
+                       "lr": args.lr},
+            "exposed_sync_ms": exposed, "sync_total_ms": sync_total,
+            "exposed_frac": (exposed / sync_total) if sync_total > 0 else None,
+            "nccl_bytes_sent_per_iter": nccl_sent, "nccl_bytes_recv_per_iter": nccl_recv,
+            "layers": [{k: d[k] for k in ("name", "scheme", "rule", "M", "N")} for d in sync.describe()],
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_poseidon(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

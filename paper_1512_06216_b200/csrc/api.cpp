@@ -183,11 +183,11 @@ poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float*
   else
     err = launch_recon_simt(L.Ug, L.Vg, P, L.K, L.ldk, L.M, L.N, W, alpha, c->recon_stream);
   if (err != cudaSuccess) return cuda_fail(err, "reconstruct+sgd launch");
+  CU_TRY(cudaEventRecord(e.kend, c->recon_stream));  // kernel_ms = K1/K1r alone
   if (bias) {
     err = launch_bias_update(L.Bs, L.M, P, bias, L.M, alpha, c->recon_stream);
     if (err != cudaSuccess) return cuda_fail(err, "bias update launch");
   }
-  CU_TRY(cudaEventRecord(e.kend, c->recon_stream));
   CU_TRY(cudaEventRecord(e.done, c->recon_stream));
   r.layers.push_back(id);
   return POSEIDON_OK;

@@ -1,0 +1,188 @@
+"""DWBP glue: drive libposeidon from PyTorch autograd (Alg. 2).
+
+Every parameterised layer of a model becomes a Poseidon layer:
+
+* FC layers (``nn.Linear``) that SACP assigns to SFB run through
+  ``SFBLinearFunction``: backward computes only E_i = dX (the error message the
+  layer below needs, Alg. 2 line 7) and hands the per-sample factors (grad_out,
+  input) to ``poseidon_sync_fc_sfb`` — the local dW is never formed (Eq. 5).
+* Other layers (conv, and FC layers the rule sends to PS) keep their
+  parameters as views into one padded flat buffer per layer (W row-major then
+  bias, ``poseidon_shard_range``), their ``.grad`` as views into a matching
+  gradient buffer, and fire ``poseidon_backprop_hook`` from a
+  post-accumulate-grad hook once all of the layer's gradients have landed.
+* A forward pre-hook makes the next forward of layer i wait for layer i's sync
+  (``poseidon_wait_layer``): the only synchronisation DWBP needs.
+
+All arithmetic of the sync happens in the library; this module only moves
+pointers and streams.  The optimiser step IS the sync (SGD applied by K1/K2),
+so there is no torch optimiser.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import torch
+import torch.nn as nn
+
+from . import binding as B
+
+
+@dataclass
+class LayerPlan:
+    layer_id: int
+    name: str
+    module: nn.Module
+    kind: int
+    M: int
+    N: int
+    K: int
+    scheme: int
+    rule_scheme: int
+    costs: tuple
+    n: int = 0
+    padded: int = 0
+    flat_w: Optional[torch.Tensor] = None
+    flat_g: Optional[torch.Tensor] = None
+    pending: int = 0
+    n_params: int = 0
+    hook_handles: List = field(default_factory=list)
+
+
+class SFBLinearFunction(torch.autograd.Function):
+    """y = x W^T + b; backward returns dX only and triggers the SFB sync."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias, plan, sync):
+        ctx.save_for_backward(x, weight)
+        ctx.plan = plan
+        ctx.sync = sync
+        ctx.bias = bias
+        if bias is not None:
+            return torch.addmm(bias, x, weight.t())
+        return x @ weight.t()
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        x, weight = ctx.saved_tensors
+        grad_out = grad_out.contiguous()
+        # E_i for the layer below (Alg. 2 line 7) BEFORE "Communicate" (line 9): the in-place
+        # update of W on the library's stream is ordered after this read by the ready event.
+        grad_x = grad_out @ weight if ctx.needs_input_grad[0] else None
+        ctx.sync.sfb_backward(ctx.plan, grad_out, x.contiguous(), weight, ctx.bias)
+        return grad_x, None, None, None, None
+
+
+class PoseidonSync:
+    """Registers a model's layers with a libposeidon context and installs the
+    DWBP hooks.  ``K`` is the per-GPU batch (number of sufficient-factor pairs
+    per worker per FC layer)."""
+
+    def __init__(self, model: nn.Module, ctx: B.Context, K: int, lr: float,
+                 scheme: str = "auto", recon: int = B.RECON_TF32, fc_flat_sfb_input: bool = True):
+        self.model = model
+        self.ctx = ctx
+        self.K = K
+        self.lr = float(lr)
+        self.plans: List[LayerPlan] = []
+        self.by_module: Dict[nn.Module, LayerPlan] = {}
+        ctx.set_lr(self.lr)
+        layer_id = 0
+        for name, mod in model.named_modules():
+            if isinstance(mod, (nn.Linear, nn.Conv2d)):
+                self._register(layer_id, name, mod, scheme, recon)
+                layer_id += 1
+
+    # ------------------------------------------------------------ setup ----
+    def _register(self, lid, name, mod, scheme, recon):
+        if isinstance(mod, nn.Linear):
+            kind, M, N = B.LAYER_FC, mod.out_features, mod.in_features
+        else:
+            kind = B.LAYER_CONV
+            M = mod.out_channels
+            N = mod.weight[0].numel()  # in_channels/groups * kh * kw
+        rule, costs = B.choose_scheme(kind, M, N, self.K, self.ctx.world)
+        override = -1
+        if scheme == "ps":
+            override = B.SCHEME_PS
+        elif scheme == "sfb" and kind == B.LAYER_FC:
+            override = B.SCHEME_SFB
+        has_bias = mod.bias is not None
+        chosen = self.ctx.register_layer(lid, kind, M, N, self.K, has_bias, override)
+        plan = LayerPlan(lid, name, mod, kind, M, N, self.K, chosen, rule, costs)
+        self.plans.append(plan)
+        self.by_module[mod] = plan
+        if chosen == B.SCHEME_SFB:
+            self.ctx.set_recon(recon, lid)
+            mod.weight.data = mod.weight.data.contiguous()
+            self.ctx.bind_sfb_params(lid, mod.weight, mod.bias)
+            self._wrap_linear(mod, plan)
+        else:
+            self._flatten_ps(mod, plan)
+        h = mod.register_forward_pre_hook(self._pre_forward(plan))
+        plan.hook_handles.append(h)
+
+    def _flatten_ps(self, mod, plan):
+        params = [mod.weight] + ([mod.bias] if mod.bias is not None else [])
+        n = sum(p.numel() for p in params)
+        _, _, padded = B.shard_range(n, self.ctx.world, self.ctx.rank)
+        dev = mod.weight.device
+        flat_w = torch.zeros(padded, device=dev, dtype=torch.float32)
+        flat_g = torch.zeros(padded, device=dev, dtype=torch.float32)
+        off = 0
+        for p in params:
+            k = p.numel()
+            flat_w[off:off + k].copy_(p.data.reshape(-1))
+            p.data = flat_w[off:off + k].view_as(p)
+            p.grad = flat_g[off:off + k].view_as(p)
+            off += k
+        plan.n, plan.padded, plan.flat_w, plan.flat_g = n, padded, flat_w, flat_g
+        plan.n_params = len(params)
+        self.ctx.bind_ps_buffers(plan.layer_id, flat_g, flat_w, n, B.PS_ZERO_GRAD)
+        for p in params:
+            plan.hook_handles.append(p.register_post_accumulate_grad_hook(self._post_accumulate(plan)))
+
+    def _wrap_linear(self, mod, plan):
+        sync = self
+
+        def forward(x):
+            return SFBLinearFunction.apply(x, mod.weight, mod.bias, plan, sync)
+
+        mod.forward = forward
+
+    # ------------------------------------------------------------ hooks ----
+    def _pre_forward(self, plan):
+        def hook(_mod, _inp):
+            self.ctx.wait_layer(plan.layer_id, torch.cuda.current_stream())
+        return hook
+
+    def _post_accumulate(self, plan):
+        def hook(_p):
+            plan.pending += 1
+            if plan.pending == plan.n_params:
+                plan.pending = 0
+                self.ctx.backprop_hook(plan.layer_id, torch.cuda.current_stream())
+        return hook
+
+    def sfb_backward(self, plan, grad_out, x, weight, bias):
+        self.ctx.sync_fc_sfb(plan.layer_id, grad_out, x, weight, bias, self.lr, torch.cuda.current_stream())
+
+    # ------------------------------------------------------------ driver ----
+    def iteration_end(self, stats: bool = False):
+        return self.ctx.iteration_end(torch.cuda.current_stream(), stats=stats)
+
+    def wait_all(self, stream=None):
+        s = stream or torch.cuda.current_stream()
+        for p in self.plans:
+            self.ctx.wait_layer(p.layer_id, s)
+
+    def describe(self):
+        out = []
+        for p in self.plans:
+            out.append({"id": p.layer_id, "name": p.name, "kind": "fc" if p.kind == B.LAYER_FC else "conv",
+                        "M": p.M, "N": p.N, "K": p.K,
+                        "scheme": "SFB" if p.scheme == B.SCHEME_SFB else "PS",
+                        "rule": "SFB" if p.rule_scheme == B.SCHEME_SFB else "PS",
+                        "cost_sfb": p.costs[0], "cost_sf_ps": p.costs[1], "cost_full_ps": p.costs[2]})
+        return out
