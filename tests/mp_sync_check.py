@@ -1,0 +1,186 @@
+"""Multi-GPU worker (torchrun, one process per GPU, NCCL through libposeidon).
+
+Checks, at world = P:
+  1. SFB sync of the C1 layer (M=128, N=256, K=8): integer variant bit-exact
+     vs the oracle O4 (TF32 and fp32 reconstruction), random factors within
+     the Z13 gate; every rank's W bit-identical.
+  2. PS sync of the same layer's flat buffer (RS -> K2 -> AG): integer variant
+     bit-exact vs O6, random within 1e-5; every rank bit-identical.
+  3. A layer with an empty shard (n=650 at P=8 has one) and odd sizes.
+  4. Two DWBP training steps of CIFAR-10 quick (C2 shapes, K=16/GPU, SACP
+     auto and forced PS, DWBP on and off): all ranks' parameters
+     bit-identical, DWBP on == off bitwise, and the step equals single-GPU SGD
+     on the concatenated P*K batch (torch fp32 reference, TF32 gate).
+Prints "MP_OK <rank>" on success; any failure raises.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.nn.functional as F
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle as O  # noqa: E402
+import synthetic as S  # noqa: E402
+import paper_1512_06216_b200 as pz  # noqa: E402
+from paper_1512_06216_b200.dwbp import PoseidonSync  # noqa: E402
+from drivers.cnn import CifarQuick  # noqa: E402
+
+
+def allsame(t):
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, t)
+    return all(torch.equal(parts[0], p) for p in parts[1:])
+
+
+def main():
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    obj = [pz.get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    P = world
+
+    def new_ctx(flags=0):
+        return pz.Context(rank=rank, world=world, device=local, nccl_id=obj[0], flags=flags)
+
+    ctx = new_ctx()
+    M, N, K = 128, 256, 8
+    assert ctx.register_layer(0, pz.LAYER_FC, M, N, K) == pz.SCHEME_SFB
+    assert ctx.register_layer(1, pz.LAYER_FC, M, N, K, scheme_override=pz.SCHEME_PS) == pz.SCHEME_PS
+
+    # ---- 1. SFB, integer variant, both reconstruction kernels ----
+    for recon in (pz.RECON_TF32, pz.RECON_FP32):
+        ctx.set_recon(recon, 0)
+        W, b, Us, Vs, lr = S.integer_factors(M, N, K, P, seed=3)
+        Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+        ctx.sync_fc_sfb(0, torch.from_numpy(Us[rank]).to(dev), torch.from_numpy(Vs[rank]).to(dev), Wd, bd, lr)
+        ctx.wait_layer(0)
+        st = ctx.iteration_end(stats=True)
+        torch.cuda.synchronize()
+        W1, b1 = O.sync_step(W, b, Us, Vs, lr)
+        assert np.array_equal(Wd.cpu().numpy().astype(np.float64), W1), f"SFB int mismatch recon={recon}"
+        assert np.array_equal(bd.cpu().numpy().astype(np.float64), b1)
+        assert allsame(Wd) and allsame(bd)
+        per = (M * 8 + N * 8 + M) * 4  # ldk = 8
+        assert st["nccl_bytes_sent"] == per and st["nccl_bytes_recv"] == per * (P - 1), st
+
+    # random factors (hidden-layer recipe), TF32 gate
+    ctx.set_recon(pz.RECON_TF32, 0)
+    W, b = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, P)
+    Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+    ctx.sync_fc_sfb(0, torch.from_numpy(Us[rank]).to(dev), torch.from_numpy(Vs[rank]).to(dev), Wd, bd, 0.5)
+    ctx.wait_layer(0)
+    ctx.iteration_end()
+    torch.cuda.synchronize()
+    W1, b1 = O.sync_step(W, b, Us, Vs, 0.5)
+    assert O.update_error_fp32(W, Wd.cpu().numpy(), W1) <= 2e-3
+    assert O.update_error_fp32(b, bd.cpu().numpy(), b1) <= 1e-5
+    assert allsame(Wd)
+
+    # ---- 2. PS of the same layer ----
+    for variant in ("int", "rand"):
+        if variant == "int":
+            W, b, Us, Vs, lr = S.integer_factors(M, N, K, P, seed=5)
+        else:
+            W, b = S.fc_weights_randbias(M, N)
+            Us, Vs = S.hidden_factors(M, N, K, P, seed=21)
+            lr = 0.5
+        n = M * N + M
+        _, _, padded = pz.shard_range(n, P, rank)
+        gflat = torch.zeros(padded, device=dev)
+        wflat = torch.zeros(padded, device=dev)
+        wflat[:n] = torch.from_numpy(O.flatten_params(W, b).astype(np.float32)).to(dev)
+        grads = [O.flatten_params(O.reconstruct(Us[p], Vs[p]), Us[p].astype(np.float64).sum(0)).astype(np.float32)
+                 for p in range(P)]
+        gflat[:n] = torch.from_numpy(grads[rank]).to(dev)
+        ctx.bind_ps_buffers(1, gflat, wflat, n, pz.PS_ZERO_GRAD)
+        ctx.sync_ps(1, gflat, wflat, n, lr)
+        ctx.wait_layer(1)
+        st = ctx.iteration_end(stats=True)
+        torch.cuda.synchronize()
+        ref = O.ps_step_flat(O.flatten_params(W, b), grads, lr)
+        out = wflat.cpu().numpy()[:n]
+        if variant == "int" and P in (1, 2, 4, 8):
+            assert np.array_equal(out.astype(np.float64), ref), "PS int mismatch"
+        else:
+            assert O.update_error_fp32(O.flatten_params(W, b), out, ref) <= 1e-5
+        assert allsame(wflat)
+        assert float(gflat.abs().sum()) == 0.0
+        S_ = padded // P
+        assert st["nccl_bytes_sent"] == 2 * S_ * 4 * (P - 1)
+
+    # ---- 3. odd sizes / empty shard ----
+    ctx.register_layer(2, pz.LAYER_FC, 10, 64, 4, 1, pz.SCHEME_PS)  # n = 650
+    n = 650
+    g0 = S.rng(9)
+    W = (g0.integers(-1023, 1024, size=n) * 2.0 ** -10).astype(np.float32)
+    grads = S.integer_grads(n, P, seed=10)
+    _, _, padded = pz.shard_range(n, P, rank)
+    gflat = torch.zeros(padded, device=dev)
+    gflat[:n] = torch.from_numpy(grads[rank]).to(dev)
+    wflat = torch.zeros(padded, device=dev)
+    wflat[:n] = torch.from_numpy(W).to(dev)
+    lr = 2.0 ** -7
+    ctx.sync_ps(2, gflat, wflat, n, lr)
+    ctx.wait_layer(2)
+    ctx.iteration_end()
+    torch.cuda.synchronize()
+    ref = O.ps_step_flat(W, grads, lr)
+    out = wflat.cpu().numpy()[:n].astype(np.float64)
+    if P in (1, 2, 4, 8):
+        assert np.array_equal(out, ref)
+    else:
+        assert O.update_error_fp32(W, out, ref) <= 1e-5
+    ctx.close()
+
+    # ---- 4. DWBP training steps of CIFAR-10 quick ----
+    Kc = 16
+    results = {}
+    for scheme in ("auto", "ps"):
+        for dwbp in ("on", "off"):
+            c2 = new_ctx(pz.FLAG_DWBP_OFF if dwbp == "off" else 0)
+            torch.manual_seed(1234)
+            model = CifarQuick().to(dev)
+            ref_model = CifarQuick().to(dev)
+            ref_model.load_state_dict(model.state_dict())
+            sync = PoseidonSync(model, c2, K=Kc, lr=0.05, scheme=scheme, recon=pz.RECON_TF32)
+            for it in range(2):
+                gen = torch.Generator().manual_seed(100 + it)
+                xall = torch.rand(P * Kc, 3, 32, 32, generator=gen).to(dev)
+                yall = torch.randint(0, 10, (P * Kc,), generator=gen).to(dev)
+                xb, yb = xall[rank * Kc:(rank + 1) * Kc], yall[rank * Kc:(rank + 1) * Kc]
+                loss = F.cross_entropy(model(xb), yb)
+                loss.backward()
+                sync.iteration_end()
+                # single-GPU SGD on the concatenated batch (the BSP equivalence of O7)
+                ref_model.zero_grad()
+                F.cross_entropy(ref_model(xall), yall).backward()
+                with torch.no_grad():
+                    for p in ref_model.parameters():
+                        p -= 0.05 * p.grad
+            sync.wait_all()
+            torch.cuda.synchronize()
+            flat = torch.cat([p.detach().reshape(-1) for p in model.parameters()])
+            assert allsame(flat), f"ranks differ ({scheme}, dwbp {dwbp})"
+            for (name, p), (_, q) in zip(model.named_parameters(), ref_model.named_parameters()):
+                w0 = q.detach().cpu().numpy()
+                err = np.max(np.abs(p.detach().cpu().numpy() - w0)) / max(1e-12, np.max(np.abs(w0)))
+                assert err < 2e-3, (name, err, scheme, dwbp)
+            results[(scheme, dwbp)] = flat.cpu()
+            c2.close()
+    for scheme in ("auto", "ps"):
+        assert torch.equal(results[(scheme, "on")], results[(scheme, "off")]), f"DWBP on/off differ ({scheme})"
+    dist.barrier()
+    print(f"MP_OK {rank}", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

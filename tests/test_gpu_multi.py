@@ -1,0 +1,26 @@
+"""Multi-GPU parity (NCCL over NVLink) — runs tests/mp_sync_check.py under
+torchrun on every visible GPU (needs >= 2; skipped otherwise)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("nproc", [2, 4, 8])
+def test_multi_gpu_sync(nproc):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29611 + nproc),
+           os.path.join(ROOT, "tests", "mp_sync_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    for rank in range(nproc):
+        assert f"MP_OK {rank}" in out, out[-4000:]
