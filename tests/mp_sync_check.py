@@ -42,11 +42,12 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    obj = [pz.get_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
     P = world
 
     def new_ctx(flags=0):
+        # an ncclUniqueId bootstraps exactly one communicator: fresh id per context
+        obj = [pz.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
         return pz.Context(rank=rank, world=world, device=local, nccl_id=obj[0], flags=flags)
 
     ctx = new_ctx()
