@@ -42,6 +42,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
+    # DWBP on/off must be bit-identical: only scheduling differs, so the driver's own
+    # convolutions must be deterministic too (cuDNN wgrad may otherwise use atomics)
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.benchmark = False
     P = world
 
     def new_ctx(flags=0):
