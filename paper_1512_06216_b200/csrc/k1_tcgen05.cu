@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "internal.h"
@@ -359,6 +360,249 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// ======================================================================
+// K1, 2-SM variant: a cluster of 2 CTAs (a TPC pair) computes a 256 x 256 tile
+// with tcgen05.mma.cta_group::2 (M=256, N=256, K=8).  Each CTA stages its own
+// 128 rows of A and its half (128 rows) of B per 32-k slab (32 KB / stage), so
+// the operand bytes per flop from L2 are 2/3 of the 1-SM 128x256 tile's — the
+// 1-SM kernel is L2-bandwidth bound (0.023 B/flop ~ 0.51 PFLOP/s at ~12 TB/s).
+// The leader CTA (rank 0) issues the MMAs; both CTAs' TMA loads complete on the
+// leader's "full" barrier; MMA completion is multicast to both CTAs' "empty" /
+// "tfull" barriers; each CTA's epilogue owns the 128 rows in its own TMEM and
+// reports "tempty" to the leader (remote mbarrier arrive).
+// ======================================================================
+namespace k2sm {
+constexpr int BM = 256;                 // tile rows (both CTAs)
+constexpr int BM_CTA = 128;             // rows per CTA (TMEM lanes)
+constexpr int BN = 256;                 // tile cols (UMMA N)
+constexpr int BN_CTA = 128;             // B rows staged per CTA
+constexpr int A_BYTES = BM_CTA * BK * 4;   // 16 KB
+constexpr int B_BYTES = BN_CTA * BK * 4;   // 16 KB
+constexpr int STAGE = A_BYTES + B_BYTES;   // 32 KB
+constexpr int STAGES = 4;
+constexpr int WSLOTS = 5;
+constexpr int SMEM = STAGES * STAGE + WSLOTS * W_CHUNK_BYTES + 1024 + 1024;
+
+__host__ __device__ constexpr uint32_t idesc() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+}  // namespace k2sm
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_2sm(const CUtensorMap* map, uint32_t bar_cluster, void* dst, int32_t x,
+                                                int32_t y, int32_t z, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(x), "r"(y), "r"(z), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+                   "r"(smem_u32(bar)),
+               "h"(mask)
+               : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    recon_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                             const __grid_constant__ CUtensorMap tmW, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_ops = smem;
+  uint8_t* smem_w = smem + k2sm::STAGES * k2sm::STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_w + k2sm::WSLOTS * W_CHUNK_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = full + k2sm::STAGES;
+  uint64_t* tfull = empty + k2sm::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* wfull = tempty + 2;
+  uint64_t* wempty = wfull + k2sm::WSLOTS;
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(wempty + k2sm::WSLOTS);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < k2sm::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+    for (int i = 0; i < k2sm::WSLOTS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_smem)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+
+  if (warp == 0) {
+    // ===================== operand TMA producer (both CTAs) =====================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_last();
+      uint32_t stage = 0, phase = 0;
+      for (int tile = pair; tile < p.num_tiles; tile += npairs) {
+        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+        const int a_row = mt * k2sm::BM + (int)rank * k2sm::BM_CTA;
+        const int b_row = nt * k2sm::BN + (int)rank * k2sm::BN_CTA;
+        for (int kk = 0; kk < p.num_kb; ++kk) {
+          const int pw = kk / p.kb_per_p, kb = kk - pw * p.kb_per_p;
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t full_leader = mapa_shared(smem_u32(&full[stage]), 0);
+          if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * k2sm::STAGE));
+          uint8_t* sa = smem_ops + stage * k2sm::STAGE;
+          uint8_t* sb = sa + k2sm::A_BYTES;
+          tma_load_3d_2sm(&tmA, full_leader, sa, kb * BK, a_row, pw, pol);
+          tma_load_3d_2sm(&tmB, full_leader, sb, kb * BK, b_row, pw, pol);
+          if (++stage == k2sm::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA, one thread) =====================
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t id = k2sm::idesc();
+      uint32_t stage = 0, phase = 0;
+      int it = 0;
+      for (int tile = pair; tile < p.num_tiles; tile += npairs, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * k2sm::BN);
+        for (int kk = 0; kk < p.num_kb; ++kk) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem_ops + stage * k2sm::STAGE);
+          const uint32_t sb = sa + k2sm::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k) {
+            const uint64_t ad = make_desc_k_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = make_desc_k_sw128(sb + k * 32, 16, 1024);
+            tc_mma_tf32_2sm(d_tmem, ad, bd, id, (kk | k) != 0 ? 1u : 0u);
+          }
+          tc_commit_2sm_mc(&empty[stage], 0x3);
+          if (++stage == k2sm::STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_2sm_mc(&tfull[acc], 0x3);
+      }
+    }
+  } else if (warp == 2) {
+    // ===================== W tile TMA producer (both CTAs, own rows) =====================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t g = 0;
+      for (int tile = pair; tile < p.num_tiles; tile += npairs) {
+        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+        const int n0 = nt * k2sm::BN, m0 = mt * k2sm::BM + (int)rank * k2sm::BM_CTA;
+        int nch = (p.N - n0 + W_CHUNK_COLS - 1) / W_CHUNK_COLS;
+        if (nch > CHUNKS_PER_TILE) nch = CHUNKS_PER_TILE;
+        if (m0 >= p.M) nch = 0;   // this CTA's half of the last tile is empty
+        for (int c = 0; c < nch; ++c, ++g) {
+          const uint32_t slot = g % k2sm::WSLOTS, ph = (g / k2sm::WSLOTS) & 1;
+          mbar_wait(&wempty[slot], ph ^ 1);
+          mbar_expect_tx(&wfull[slot], W_CHUNK_BYTES);
+          tma_load_2d(&tmW, &wfull[slot], smem_w + slot * W_CHUNK_BYTES, n0 + c * W_CHUNK_COLS, m0, pol);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue (128 threads per CTA, one W row each) =====================
+    const int q = warp - 4;
+    const int row = q * 32 + lane;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
+    uint32_t g = 0;
+    int it = 0;
+    for (int tile = pair; tile < p.num_tiles; tile += npairs, ++it) {
+      const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+      const int n0 = nt * k2sm::BN, m0 = mt * k2sm::BM + (int)rank * k2sm::BM_CTA;
+      int nch = (p.N - n0 + W_CHUNK_COLS - 1) / W_CHUNK_COLS;
+      if (nch > CHUNKS_PER_TILE) nch = CHUNKS_PER_TILE;
+      if (m0 >= p.M) nch = 0;
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      for (int c = 0; c < nch; ++c, ++g) {
+        const uint32_t slot = g % k2sm::WSLOTS, ph = (g / k2sm::WSLOTS) & 1;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * k2sm::BN + c * W_CHUNK_COLS), r);
+        tmem_ld_wait();
+        mbar_wait(&wfull[slot], ph);
+        uint8_t* wrow = smem_w + slot * W_CHUNK_BYTES + row * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4* p4 = reinterpret_cast<float4*>(wrow + ((j ^ (row & 7)) << 4));
+          float4 w = *p4;
+          w.x = fmaf(p.alpha, __uint_as_float(r[4 * j + 0]), w.x);
+          w.y = fmaf(p.alpha, __uint_as_float(r[4 * j + 1]), w.y);
+          w.z = fmaf(p.alpha, __uint_as_float(r[4 * j + 2]), w.z);
+          w.w = fmaf(p.alpha, __uint_as_float(r[4 * j + 3]), w.w);
+          *p4 = w;
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (q == 0 && lane == 0) {
+          tma_store_2d(&tmW, smem_w + slot * W_CHUNK_BYTES, n0 + c * W_CHUNK_COLS, m0);
+          bulk_commit();
+          bulk_wait_read<1>();
+          if (g > 0) mbar_arrive(&wempty[(g - 1) % k2sm::WSLOTS]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+    }
+    if (q == 0 && lane == 0) bulk_wait_all();
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
 // ------------------------------------------------------------- host side ----
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -431,6 +675,30 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   p.num_kb = p.kb_per_p * P;
   p.alpha = alpha;
   p.dbg = dbg;
+  static int variant = -1;  // 2 = cta_group::2 (default), 1 = single-CTA tiles
+  if (variant < 0) {
+    const char* v = getenv("POSEIDON_K1_VARIANT");
+    variant = (v && v[0] == '1') ? 1 : 2;
+  }
+  if (variant == 2 && dbg == nullptr) {
+    // re-encode the operand maps with 128-row boxes for B (each CTA stages half of the 256-wide N tile)
+    const uint32_t bB2[3] = {BK, (uint32_t)k2sm::BN_CTA, 1};
+    if (!encode(&tmB, Vg, 3, dB, sB, bB2)) return cudaErrorNotSupported;
+    p.m_tiles = (int32_t)((M + k2sm::BM - 1) / k2sm::BM);
+    p.n_tiles = (int32_t)((N + k2sm::BN - 1) / k2sm::BN);
+    p.num_tiles = p.m_tiles * p.n_tiles;
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaError_t e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           k2sm::SMEM);
+      if (e != cudaSuccess) return e;
+      attr2 = true;
+    }
+    const int pairs = std::min(p.num_tiles, sm_count_k1() / 2);
+    recon_tcgen05_2sm_kernel<<<2 * pairs, NUM_THREADS, k2sm::SMEM, s>>>(tmA, tmB, tmW, p);
+    g_launches.fetch_add(1);
+    return cudaGetLastError();
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(recon_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
