@@ -183,9 +183,20 @@ __host__ __device__ constexpr uint32_t make_idesc() {
 struct Params {
   int32_t M, N;
   int32_t m_tiles, n_tiles, num_tiles, num_kb, kb_per_p;
+  int32_t m_fast;  // raster: 1 -> consecutive tiles walk M (re-sweep the smaller operand Ug each wave)
   float alpha;
   float* dbg;  // debug dump (tile 0 of CTA 0): smem stage 0 of A|B, raw accumulator; NULL in production
 };
+
+__device__ __forceinline__ void tile_coords(const Params& p, int tile, int& mt, int& nt) {
+  if (p.m_fast) {
+    nt = tile / p.m_tiles;
+    mt = tile - nt * p.m_tiles;
+  } else {
+    mt = tile / p.n_tiles;
+    nt = tile - mt * p.n_tiles;
+  }
+}
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     recon_tcgen05_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -233,7 +244,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pol = policy_evict_last();
       uint32_t stage = 0, phase = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+        int mt, nt;
+        tile_coords(p, tile, mt, nt);
         for (int kk = 0; kk < p.num_kb; ++kk) {
           const int pw = kk / p.kb_per_p, kb = kk - pw * p.kb_per_p;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -285,7 +297,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pol = policy_evict_first();
       uint32_t g = 0;
       for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+        int mt, nt;
+        tile_coords(p, tile, mt, nt);
         const int n0 = nt * BN;
         int nch = (p.N - n0 + W_CHUNK_COLS - 1) / W_CHUNK_COLS;
         if (nch > CHUNKS_PER_TILE) nch = CHUNKS_PER_TILE;
@@ -304,7 +317,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t g = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
-      const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+      int mt, nt;
+        tile_coords(p, tile, mt, nt);
       const int n0 = nt * BN;
       int nch = (p.N - n0 + W_CHUNK_COLS - 1) / W_CHUNK_COLS;
       if (nch > CHUNKS_PER_TILE) nch = CHUNKS_PER_TILE;
@@ -379,9 +393,7 @@ constexpr int BN_CTA = 128;             // B rows staged per CTA
 constexpr int A_BYTES = BM_CTA * BK * 4;   // 16 KB
 constexpr int B_BYTES = BN_CTA * BK * 4;   // 16 KB
 constexpr int STAGE = A_BYTES + B_BYTES;   // 32 KB
-constexpr int STAGES = 4;
-constexpr int WSLOTS = 5;
-constexpr int SMEM = STAGES * STAGE + WSLOTS * W_CHUNK_BYTES + 1024 + 1024;
+constexpr int smem_bytes(int stages, int wslots) { return stages * STAGE + wslots * W_CHUNK_BYTES + 1024 + 1024; }
 
 __host__ __device__ constexpr uint32_t idesc() {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -430,30 +442,31 @@ __device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
                : "memory");
 }
 
+template <int NST, int NWS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     recon_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmW, const Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_ops = smem;
-  uint8_t* smem_w = smem + k2sm::STAGES * k2sm::STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_w + k2sm::WSLOTS * W_CHUNK_BYTES);
+  uint8_t* smem_w = smem + NST * k2sm::STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_w + NWS * W_CHUNK_BYTES);
   uint64_t* full = bars;
-  uint64_t* empty = full + k2sm::STAGES;
-  uint64_t* tfull = empty + k2sm::STAGES;
+  uint64_t* empty = full + NST;
+  uint64_t* tfull = empty + NST;
   uint64_t* tempty = tfull + 2;
   uint64_t* wfull = tempty + 2;
-  uint64_t* wempty = wfull + k2sm::WSLOTS;
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(wempty + k2sm::WSLOTS);
+  uint64_t* wempty = wfull + NWS;
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(wempty + NWS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < k2sm::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
-    for (int i = 0; i < k2sm::WSLOTS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
+    for (int i = 0; i < NWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -478,7 +491,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pol = policy_evict_last();
       uint32_t stage = 0, phase = 0;
       for (int tile = pair; tile < p.num_tiles; tile += npairs) {
-        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+        int mt, nt;
+        tile_coords(p, tile, mt, nt);
         const int a_row = mt * k2sm::BM + (int)rank * k2sm::BM_CTA;
         const int b_row = nt * k2sm::BN + (int)rank * k2sm::BN_CTA;
         for (int kk = 0; kk < p.num_kb; ++kk) {
@@ -490,7 +504,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           uint8_t* sb = sa + k2sm::A_BYTES;
           tma_load_3d_2sm(&tmA, full_leader, sa, kb * BK, a_row, pw, pol);
           tma_load_3d_2sm(&tmB, full_leader, sb, kb * BK, b_row, pw, pol);
-          if (++stage == k2sm::STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -518,7 +532,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             tc_mma_tf32_2sm(d_tmem, ad, bd, id, (kk | k) != 0 ? 1u : 0u);
           }
           tc_commit_2sm_mc(&empty[stage], 0x3);
-          if (++stage == k2sm::STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         tc_commit_2sm_mc(&tfull[acc], 0x3);
       }
@@ -529,13 +543,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pol = policy_evict_first();
       uint32_t g = 0;
       for (int tile = pair; tile < p.num_tiles; tile += npairs) {
-        const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+        int mt, nt;
+        tile_coords(p, tile, mt, nt);
         const int n0 = nt * k2sm::BN, m0 = mt * k2sm::BM + (int)rank * k2sm::BM_CTA;
         int nch = (p.N - n0 + W_CHUNK_COLS - 1) / W_CHUNK_COLS;
         if (nch > CHUNKS_PER_TILE) nch = CHUNKS_PER_TILE;
         if (m0 >= p.M) nch = 0;   // this CTA's half of the last tile is empty
         for (int c = 0; c < nch; ++c, ++g) {
-          const uint32_t slot = g % k2sm::WSLOTS, ph = (g / k2sm::WSLOTS) & 1;
+          const uint32_t slot = g % NWS, ph = (g / NWS) & 1;
           mbar_wait(&wempty[slot], ph ^ 1);
           mbar_expect_tx(&wfull[slot], W_CHUNK_BYTES);
           tma_load_2d(&tmW, &wfull[slot], smem_w + slot * W_CHUNK_BYTES, n0 + c * W_CHUNK_COLS, m0, pol);
@@ -551,7 +566,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint32_t g = 0;
     int it = 0;
     for (int tile = pair; tile < p.num_tiles; tile += npairs, ++it) {
-      const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+      int mt, nt;
+        tile_coords(p, tile, mt, nt);
       const int n0 = nt * k2sm::BN, m0 = mt * k2sm::BM + (int)rank * k2sm::BM_CTA;
       int nch = (p.N - n0 + W_CHUNK_COLS - 1) / W_CHUNK_COLS;
       if (nch > CHUNKS_PER_TILE) nch = CHUNKS_PER_TILE;
@@ -561,7 +577,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       for (int c = 0; c < nch; ++c, ++g) {
-        const uint32_t slot = g % k2sm::WSLOTS, ph = (g / k2sm::WSLOTS) & 1;
+        const uint32_t slot = g % NWS, ph = (g / NWS) & 1;
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * k2sm::BN + c * W_CHUNK_COLS), r);
         tmem_ld_wait();
@@ -583,7 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           tma_store_2d(&tmW, smem_w + slot * W_CHUNK_BYTES, n0 + c * W_CHUNK_COLS, m0);
           bulk_commit();
           bulk_wait_read<1>();
-          if (g > 0) mbar_arrive(&wempty[(g - 1) % k2sm::WSLOTS]);
+          if (g > 0) mbar_arrive(&wempty[(g - 1) % NWS]);
         }
       }
       tc_fence_before();
@@ -675,6 +691,7 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   p.num_kb = p.kb_per_p * P;
   p.alpha = alpha;
   p.dbg = dbg;
+  p.m_fast = (M <= N) ? 1 : 0;  // the operand swept once per wave is the smaller one
   static int variant = -1;  // 2 = cta_group::2 (default), 1 = single-CTA tiles
   if (variant < 0) {
     const char* v = getenv("POSEIDON_K1_VARIANT");
@@ -687,15 +704,29 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
     p.m_tiles = (int32_t)((M + k2sm::BM - 1) / k2sm::BM);
     p.n_tiles = (int32_t)((N + k2sm::BN - 1) / k2sm::BN);
     p.num_tiles = p.m_tiles * p.n_tiles;
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaError_t e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           k2sm::SMEM);
-      if (e != cudaSuccess) return e;
-      attr2 = true;
-    }
+    // Regime: with few factor rows per tile the kernel is bound by the W
+    // read-modify-write, so more W chunks in flight beat deeper operand staging.
+    const bool hbm_regime = p.num_kb <= 16;
+    static bool attr_a = false, attr_b = false;
     const int pairs = std::min(p.num_tiles, sm_count_k1() / 2);
-    recon_tcgen05_2sm_kernel<<<2 * pairs, NUM_THREADS, k2sm::SMEM, s>>>(tmA, tmB, tmW, p);
+    cudaError_t e = cudaSuccess;
+    if (hbm_regime) {
+      constexpr int SM_ = k2sm::smem_bytes(3, 8);
+      if (!attr_a) {
+        e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
+        if (e != cudaSuccess) return e;
+        attr_a = true;
+      }
+      recon_tcgen05_2sm_kernel<3, 8><<<2 * pairs, NUM_THREADS, SM_, s>>>(tmA, tmB, tmW, p);
+    } else {
+      constexpr int SM_ = k2sm::smem_bytes(4, 5);
+      if (!attr_b) {
+        e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
+        if (e != cudaSuccess) return e;
+        attr_b = true;
+      }
+      recon_tcgen05_2sm_kernel<4, 5><<<2 * pairs, NUM_THREADS, SM_, s>>>(tmA, tmB, tmW, p);
+    }
     g_launches.fetch_add(1);
     return cudaGetLastError();
   }
