@@ -692,6 +692,7 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   p.alpha = alpha;
   p.dbg = dbg;
   p.m_fast = (M <= N) ? 1 : 0;  // the operand swept once per wave is the smaller one
+  if (const char* r = getenv("POSEIDON_K1_RASTER")) p.m_fast = (r[0] == 'm');  // experiments only
   static int variant = -1;  // 2 = cta_group::2 (default), 1 = single-CTA tiles
   if (variant < 0) {
     const char* v = getenv("POSEIDON_K1_VARIANT");
@@ -706,7 +707,8 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
     p.num_tiles = p.m_tiles * p.n_tiles;
     // Regime: with few factor rows per tile the kernel is bound by the W
     // read-modify-write, so more W chunks in flight beat deeper operand staging.
-    const bool hbm_regime = p.num_kb <= 16;
+    bool hbm_regime = p.num_kb <= 16;
+    if (const char* c = getenv("POSEIDON_K1_CFG")) hbm_regime = (c[0] == 'a');  // experiments only
     static bool attr_a = false, attr_b = false;
     const int pairs = std::min(p.num_tiles, sm_count_k1() / 2);
     cudaError_t e = cudaSuccess;
