@@ -183,6 +183,7 @@ __host__ __device__ constexpr uint32_t make_idesc() {
 struct Params {
   int32_t M, N;
   int32_t m_tiles, n_tiles, num_tiles, num_kb, kb_per_p;
+  int32_t mode;    // experiments only: 1 = W streaming alone (no MMA), 0 = production
   int32_t m_fast;  // raster: 1 -> consecutive tiles walk M (re-sweep the smaller operand Ug each wave)
   float alpha;
   float* dbg;  // debug dump (tile 0 of CTA 0): smem stage 0 of A|B, raw accumulator; NULL in production
@@ -487,7 +488,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     // ===================== operand TMA producer (both CTAs) =====================
-    if (lane == 0) {
+    if (lane == 0 && p.mode == 0) {
       const uint64_t pol = policy_evict_last();
       uint32_t stage = 0, phase = 0;
       for (int tile = pair; tile < p.num_tiles; tile += npairs) {
@@ -510,7 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA, one thread) =====================
-    if (rank == 0 && lane == 0) {
+    if (rank == 0 && lane == 0 && p.mode == 0) {
       constexpr uint32_t id = k2sm::idesc();
       uint32_t stage = 0, phase = 0;
       int it = 0;
@@ -574,13 +575,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (m0 >= p.M) nch = 0;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
+      if (p.mode == 0) mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       for (int c = 0; c < nch; ++c, ++g) {
         const uint32_t slot = g % NWS, ph = (g / NWS) & 1;
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * k2sm::BN + c * W_CHUNK_COLS), r);
-        tmem_ld_wait();
+        if (p.mode == 0) {
+          tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * k2sm::BN + c * W_CHUNK_COLS), r);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = 0u;
+        }
         mbar_wait(&wfull[slot], ph);
         uint8_t* wrow = smem_w + slot * W_CHUNK_BYTES + row * 128;
 #pragma unroll
@@ -604,7 +610,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+      if (lane == 0 && p.mode == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
     }
     if (q == 0 && lane == 0) bulk_wait_all();
   }
@@ -693,6 +699,8 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   p.dbg = dbg;
   p.m_fast = (M <= N) ? 1 : 0;  // the operand swept once per wave is the smaller one
   if (const char* r = getenv("POSEIDON_K1_RASTER")) p.m_fast = (r[0] == 'm');  // experiments only
+  p.mode = 0;
+  if (const char* md = getenv("POSEIDON_K1_MODE")) p.mode = md[0] - '0';         // experiments only
   static int variant = -1;  // 2 = cta_group::2 (default), 1 = single-CTA tiles
   if (variant < 0) {
     const char* v = getenv("POSEIDON_K1_VARIANT");
