@@ -590,7 +590,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&wfull[slot], ph);
         uint8_t* wrow = smem_w + slot * W_CHUNK_BYTES + row * 128;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < (p.mode == 2 ? 0 : 8); ++j) {
           float4* p4 = reinterpret_cast<float4*>(wrow + ((j ^ (row & 7)) << 4));
           float4 w = *p4;
           w.x = fmaf(p.alpha, __uint_as_float(r[4 * j + 0]), w.x);
@@ -602,7 +602,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
         if (q == 0 && lane == 0) {
-          tma_store_2d(&tmW, smem_w + slot * W_CHUNK_BYTES, n0 + c * W_CHUNK_COLS, m0);
+          if (p.mode != 3) tma_store_2d(&tmW, smem_w + slot * W_CHUNK_BYTES, n0 + c * W_CHUNK_COLS, m0);
           bulk_commit();
           bulk_wait_read<1>();
           if (g > 0) mbar_arrive(&wempty[(g - 1) % NWS]);
