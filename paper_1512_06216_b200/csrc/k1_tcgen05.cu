@@ -52,6 +52,7 @@ constexpr int W_CHUNK_BYTES = BM * W_CHUNK_COLS * 4;     // 16 KB
 constexpr int CHUNKS_PER_TILE = BN / W_CHUNK_COLS;       // 8
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 256;
+constexpr int NUM_THREADS_2SM = 384;  // + a second epilogue warpgroup
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + WSLOTS * W_CHUNK_BYTES + 1024 /*barriers*/ + 1024 /*align*/;
 
 // ---------------------------------------------------------------- PTX ----
@@ -154,6 +155,14 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -444,7 +453,7 @@ __device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
 }
 
 template <int NST, int NWS>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     recon_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmW, const Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -466,7 +475,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 16); }
     for (int i = 0; i < NWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -559,16 +568,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue (128 threads per CTA, one W row each) =====================
-    const int q = warp - 4;
+    // ===================== epilogue: 2 groups x 4 warps, one W row per thread =====================
+    // Group e processes the chunks g with g % 2 == e (g = global chunk counter shared with the W
+    // loader), so two chunks are in flight per CTA; each group has its own named barrier and its
+    // own store-issuing thread, and releases a W slot once its store has been read out.
+    const int e = (warp - 4) >> 2;
+    const int q = (warp - 4) & 3;
     const int row = q * 32 + lane;
+    const bool store_thread = (q == 0 && lane == 0);
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
+    const uint32_t smem_w_u32 = smem_u32(smem_w);
     uint32_t g = 0;
     int it = 0;
+    int prev_g = -1;  // this group's previous chunk (its slot is released one chunk later)
     for (int tile = pair; tile < p.num_tiles; tile += npairs, ++it) {
       int mt, nt;
-        tile_coords(p, tile, mt, nt);
+      tile_coords(p, tile, mt, nt);
       const int n0 = nt * k2sm::BN, m0 = mt * k2sm::BM + (int)rank * k2sm::BM_CTA;
       int nch = (p.N - n0 + W_CHUNK_COLS - 1) / W_CHUNK_COLS;
       if (nch > CHUNKS_PER_TILE) nch = CHUNKS_PER_TILE;
@@ -578,6 +594,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (p.mode == 0) mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       for (int c = 0; c < nch; ++c, ++g) {
+        if ((int)(g & 1) != e) continue;
         const uint32_t slot = g % NWS, ph = (g / NWS) & 1;
         uint32_t r[32];
         if (p.mode == 0) {
@@ -588,31 +605,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           for (int j = 0; j < 32; ++j) r[j] = 0u;
         }
         mbar_wait(&wfull[slot], ph);
-        uint8_t* wrow = smem_w + slot * W_CHUNK_BYTES + row * 128;
+        const uint32_t wrow = smem_w_u32 + slot * W_CHUNK_BYTES + row * 128;
+        if (p.mode != 2) {
 #pragma unroll
-        for (int j = 0; j < (p.mode == 2 ? 0 : 8); ++j) {
-          float4* p4 = reinterpret_cast<float4*>(wrow + ((j ^ (row & 7)) << 4));
-          float4 w = *p4;
-          w.x = fmaf(p.alpha, __uint_as_float(r[4 * j + 0]), w.x);
-          w.y = fmaf(p.alpha, __uint_as_float(r[4 * j + 1]), w.y);
-          w.z = fmaf(p.alpha, __uint_as_float(r[4 * j + 2]), w.z);
-          w.w = fmaf(p.alpha, __uint_as_float(r[4 * j + 3]), w.w);
-          *p4 = w;
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t a4 = wrow + ((j ^ (row & 7)) << 4);
+            float4 w = lds128(a4);
+            w.x = fmaf(p.alpha, __uint_as_float(r[4 * j + 0]), w.x);
+            w.y = fmaf(p.alpha, __uint_as_float(r[4 * j + 1]), w.y);
+            w.z = fmaf(p.alpha, __uint_as_float(r[4 * j + 2]), w.z);
+            w.w = fmaf(p.alpha, __uint_as_float(r[4 * j + 3]), w.w);
+            sts128(a4, w);
+          }
         }
         fence_proxy_async_smem();
-        named_bar_sync(1, 128);
-        if (q == 0 && lane == 0) {
+        named_bar_sync(1 + e, 128);
+        if (store_thread) {
           if (p.mode != 3) tma_store_2d(&tmW, smem_w + slot * W_CHUNK_BYTES, n0 + c * W_CHUNK_COLS, m0);
           bulk_commit();
-          bulk_wait_read<1>();
-          if (g > 0) mbar_arrive(&wempty[(g - 1) % NWS]);
+          bulk_wait_read<1>();                       // this group's previous store has read its slot
+          if (prev_g >= 0) mbar_arrive(&wempty[prev_g % NWS]);
         }
+        prev_g = (int)g;
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0 && p.mode == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
     }
-    if (q == 0 && lane == 0) bulk_wait_all();
+    if (store_thread) {
+      bulk_wait_all();
+      if (prev_g >= 0) mbar_arrive(&wempty[prev_g % NWS]);
+    }
   }
 
   __syncwarp();
@@ -727,7 +750,7 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
         if (e != cudaSuccess) return e;
         attr_a = true;
       }
-      recon_tcgen05_2sm_kernel<3, 8><<<2 * pairs, NUM_THREADS, SM_, s>>>(tmA, tmB, tmW, p);
+      recon_tcgen05_2sm_kernel<3, 8><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, p);
     } else {
       constexpr int SM_ = k2sm::smem_bytes(4, 5);
       if (!attr_b) {
@@ -735,7 +758,7 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
         if (e != cudaSuccess) return e;
         attr_b = true;
       }
-      recon_tcgen05_2sm_kernel<4, 5><<<2 * pairs, NUM_THREADS, SM_, s>>>(tmA, tmB, tmW, p);
+      recon_tcgen05_2sm_kernel<4, 5><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, p);
     }
     g_launches.fetch_add(1);
     return cudaGetLastError();
