@@ -163,6 +163,11 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
 __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
+__device__ __forceinline__ void stg128_na(float* ptr, float4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -192,6 +197,7 @@ __host__ __device__ constexpr uint32_t make_idesc() {
 struct Params {
   int32_t M, N;
   int32_t m_tiles, n_tiles, num_tiles, num_kb, kb_per_p;
+  float* W;        // W base (row-major M x N) for the coalesced write-back of the 2-SM epilogue
   int32_t mode;    // experiments only: 1 = W streaming alone (no MMA), 0 = production
   int32_t m_fast;  // raster: 1 -> consecutive tiles walk M (re-sweep the smaller operand Ug each wave)
   float alpha;
@@ -568,20 +574,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue: 2 groups x 4 warps, one W row per thread =====================
+    // ===================== epilogue: 2 groups x 4 warps =====================
     // Group e processes the chunks g with g % 2 == e (g = global chunk counter shared with the W
-    // loader), so two chunks are in flight per CTA; each group has its own named barrier and its
-    // own store-issuing thread, and releases a W slot once its store has been read out.
+    // loader).  Per chunk: (1) thread-per-row: tcgen05.ld 32 accumulator columns of its TMEM lane,
+    // W = fmaf(alpha, acc, W) on the TMA-loaded W chunk in shared memory; (2) the group writes the
+    // chunk back with coalesced 128-bit stores (8 threads per 128-B row segment) and releases the
+    // slot right away — no bulk-store completion on the critical path.
     const int e = (warp - 4) >> 2;
     const int q = (warp - 4) & 3;
-    const int row = q * 32 + lane;
-    const bool store_thread = (q == 0 && lane == 0);
+    const int t = q * 32 + lane;           // 0..127 within the group
+    const int row = t;                     // TMEM lane / tile row owned in phase (1)
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
     const uint32_t smem_w_u32 = smem_u32(smem_w);
     uint32_t g = 0;
     int it = 0;
-    int prev_g = -1;  // this group's previous chunk (its slot is released one chunk later)
     for (int tile = pair; tile < p.num_tiles; tile += npairs, ++it) {
       int mt, nt;
       tile_coords(p, tile, mt, nt);
@@ -605,8 +612,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
           for (int j = 0; j < 32; ++j) r[j] = 0u;
         }
         mbar_wait(&wfull[slot], ph);
-        const uint32_t wrow = smem_w_u32 + slot * W_CHUNK_BYTES + row * 128;
+        const uint32_t sbase = smem_w_u32 + slot * W_CHUNK_BYTES;
         if (p.mode != 2) {
+          const uint32_t wrow = sbase + row * 128;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const uint32_t a4 = wrow + ((j ^ (row & 7)) << 4);
@@ -618,23 +626,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
             sts128(a4, w);
           }
         }
-        fence_proxy_async_smem();
         named_bar_sync(1 + e, 128);
-        if (store_thread) {
-          if (p.mode != 3) tma_store_2d(&tmW, smem_w + slot * W_CHUNK_BYTES, n0 + c * W_CHUNK_COLS, m0);
-          bulk_commit();
-          bulk_wait_read<1>();                       // this group's previous store has read its slot
-          if (prev_g >= 0) mbar_arrive(&wempty[prev_g % NWS]);
+        if (p.mode != 3) {
+          // coalesced write-back: 8 threads per 128-B row segment, 16 rows per pass
+          const int jj = t & 7;
+          const int col = n0 + c * W_CHUNK_COLS + jj * 4;
+          const bool col_ok = col < p.N;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = i * 16 + (t >> 3);
+            const float4 v = lds128(sbase + rr * 128 + ((jj ^ (rr & 7)) << 4));
+            if (col_ok && m0 + rr < p.M)
+              stg128_na(p.W + (size_t)(m0 + rr) * p.N + col, v);
+          }
         }
-        prev_g = (int)g;
+        named_bar_sync(1 + e, 128);
+        if (t == 0) mbar_arrive(&wempty[slot]);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0 && p.mode == 0) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
-    }
-    if (store_thread) {
-      bulk_wait_all();
-      if (prev_g >= 0) mbar_arrive(&wempty[prev_g % NWS]);
     }
   }
 
@@ -720,6 +731,7 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   p.num_kb = p.kb_per_p * P;
   p.alpha = alpha;
   p.dbg = dbg;
+  p.W = W;
   p.m_fast = (M <= N) ? 1 : 0;  // the operand swept once per wave is the smaller one
   if (const char* r = getenv("POSEIDON_K1_RASTER")) p.m_fast = (r[0] == 'm');  // experiments only
   p.mode = 0;
