@@ -732,7 +732,11 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   p.alpha = alpha;
   p.dbg = dbg;
   p.W = W;
-  p.m_fast = (M <= N) ? 1 : 0;  // the operand swept once per wave is the smaller one
+  // Raster (measured, tools/k1_sweep.sh): when both factor buffers fit comfortably in L2 the waves
+  // walk N so each wave's W tiles are whole row segments; otherwise consecutive tiles walk the
+  // dimension whose operand is smaller, so the operand re-swept every wave stays L2-resident.
+  const double operand_bytes = 4.0 * (double)P * (double)ldk * (double)(M + N);
+  p.m_fast = (operand_bytes <= 48e6) ? 0 : ((M <= N) ? 1 : 0);
   if (const char* r = getenv("POSEIDON_K1_RASTER")) p.m_fast = (r[0] == 'm');  // experiments only
   p.mode = 0;
   if (const char* md = getenv("POSEIDON_K1_MODE")) p.mode = md[0] - '0';         // experiments only
@@ -750,7 +754,7 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
     p.num_tiles = p.m_tiles * p.n_tiles;
     // Regime: with few factor rows per tile the kernel is bound by the W
     // read-modify-write, so more W chunks in flight beat deeper operand staging.
-    bool hbm_regime = p.num_kb <= 16;
+    bool hbm_regime = false;  // 4 stages + 5 W slots measured best in both regimes (tools/k1_sweep.sh)
     if (const char* c = getenv("POSEIDON_K1_CFG")) hbm_regime = (c[0] == 'a');  // experiments only
     static bool attr_a = false, attr_b = false;
     const int pairs = std::min(p.num_tiles, sm_count_k1() / 2);
