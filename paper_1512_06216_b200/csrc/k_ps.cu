@@ -57,46 +57,44 @@ __device__ __forceinline__ void warp_stats_flush(float sq, float bad, float* sta
   }
 }
 
+// One pass, no grid-stride loop: each thread owns 4 float4 (16 elements) spaced a block apart, all
+// loads issued before any use (8 x 16 B in flight per thread), grid = ceil(n / 4096).
 template <bool kStats>
 __global__ void __launch_bounds__(256) ps_shard_sgd_kernel(const float* __restrict__ g, float* __restrict__ W,
                                                             int64_t count, float alpha, float* stats) {
-  float sq = 0.f, bad = 0.f;
+  constexpr int U = 4;
   const int64_t n4 = count >> 2;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const float4* g4 = reinterpret_cast<const float4*>(g);
   float4* W4 = reinterpret_cast<float4*>(W);
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  // two independent float4 updates in flight per thread per iteration
-  for (; i + stride < n4; i += 2 * stride) {
-    float4 a0 = ld_stream(g4 + i), a1 = ld_stream(g4 + i + stride);
-    float4 w0 = W4[i], w1 = W4[i + stride];
-    w0.x = fmaf(alpha, a0.x, w0.x); w0.y = fmaf(alpha, a0.y, w0.y);
-    w0.z = fmaf(alpha, a0.z, w0.z); w0.w = fmaf(alpha, a0.w, w0.w);
-    w1.x = fmaf(alpha, a1.x, w1.x); w1.y = fmaf(alpha, a1.y, w1.y);
-    w1.z = fmaf(alpha, a1.z, w1.z); w1.w = fmaf(alpha, a1.w, w1.w);
-    W4[i] = w0; W4[i + stride] = w1;
-    if (kStats) {
-      const float u[8] = {alpha * a0.x, alpha * a0.y, alpha * a0.z, alpha * a0.w,
-                          alpha * a1.x, alpha * a1.y, alpha * a1.z, alpha * a1.w};
+  const int64_t base = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x;
+  float4 a[U], w[U];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) { sq = fmaf(u[j], u[j], sq); bad += isfinite(u[j]) ? 0.f : 1.f; }
+  for (int j = 0; j < U; ++j) {
+    const int64_t i = base + (int64_t)j * blockDim.x;
+    if (i < n4) {
+      a[j] = ld_stream(g4 + i);
+      w[j] = W4[i];
     }
   }
-  for (; i < n4; i += stride) {
-    float4 a0 = ld_stream(g4 + i);
-    float4 w0 = W4[i];
-    w0.x = fmaf(alpha, a0.x, w0.x); w0.y = fmaf(alpha, a0.y, w0.y);
-    w0.z = fmaf(alpha, a0.z, w0.z); w0.w = fmaf(alpha, a0.w, w0.w);
-    W4[i] = w0;
-    if (kStats) {
-      const float u[4] = {alpha * a0.x, alpha * a0.y, alpha * a0.z, alpha * a0.w};
+  float sq = 0.f, bad = 0.f;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) { sq = fmaf(u[j], u[j], sq); bad += isfinite(u[j]) ? 0.f : 1.f; }
+  for (int j = 0; j < U; ++j) {
+    const int64_t i = base + (int64_t)j * blockDim.x;
+    if (i < n4) {
+      float4 v = w[j];
+      v.x = fmaf(alpha, a[j].x, v.x); v.y = fmaf(alpha, a[j].y, v.y);
+      v.z = fmaf(alpha, a[j].z, v.z); v.w = fmaf(alpha, a[j].w, v.w);
+      W4[i] = v;
+      if (kStats) {
+        const float u[4] = {alpha * a[j].x, alpha * a[j].y, alpha * a[j].z, alpha * a[j].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { sq = fmaf(u[k], u[k], sq); bad += isfinite(u[k]) ? 0.f : 1.f; }
+      }
     }
   }
-  // scalar tail (count % 4)
-  const int64_t t = (n4 << 2) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < count) {
+  // scalar tail (count % 4), block 0
+  if (blockIdx.x == 0 && threadIdx.x < (count & 3)) {
+    const int64_t t = (n4 << 2) + threadIdx.x;
     const float u = alpha * g[t];
     W[t] = fmaf(alpha, g[t], W[t]);
     if (kStats) { sq = fmaf(u, u, sq); bad += isfinite(u) ? 0.f : 1.f; }
@@ -138,7 +136,9 @@ cudaError_t launch_ps_shard_update(const float* g, float* W, int64_t count, floa
     ps_shard_sgd_scalar<<<grid_for(count, threads), threads, 0, s>>>(g, W, count, alpha);
   } else {
     const int64_t n4 = count >> 2;
-    const int grid = grid_for(n4 > 0 ? (n4 + 1) / 2 : 1, threads);
+    const int64_t per_block = (int64_t)threads * 4;
+    const int64_t blocks = n4 > 0 ? (n4 + per_block - 1) / per_block : 1;
+    const dim3 grid((unsigned)blocks);
     if (stats)
       ps_shard_sgd_kernel<true><<<grid, threads, 0, s>>>(g, W, count, alpha, stats);
     else
