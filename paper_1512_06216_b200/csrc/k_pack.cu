@@ -16,6 +16,8 @@
 // M (N), the writes along K.  A block owns a 32-column strip and walks all K
 // rows, so the column sums are formed in a fixed order (bit-identical on
 // every rank).
+#include <algorithm>
+
 #include "internal.h"
 
 namespace poseidon {
@@ -39,12 +41,16 @@ __global__ void __launch_bounds__(256) pack_t_kernel(const float* __restrict__ s
   const int64_t c0 = (int64_t)blockIdx.x * 32;
   const int64_t c = c0 + tx;
   float acc = 0.f;
-  for (int64_t k0 = 0; k0 < K; k0 += 32) {
+  // without column sums the K range is split over gridDim.y (more blocks in flight)
+  const int64_t kspan = kColsum ? K : ((K + 31) / 32 + gridDim.y - 1) / gridDim.y * 32;
+  const int64_t kbeg = kColsum ? 0 : (int64_t)blockIdx.y * kspan;
+  const int64_t kend = kColsum ? K : (kbeg + kspan < K ? kbeg + kspan : K);
+  for (int64_t k0 = kbeg; k0 < kend; k0 += 32) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t k = k0 + ty + 8 * i;
       float v = 0.f;
-      if (k < K && c < cols) v = src[k * ld_src + c];
+      if (k < kend && c < cols) v = src[k * ld_src + c];
       if (kColsum) acc += v;
       tile[ty + 8 * i][tx] = v;
     }
@@ -53,7 +59,7 @@ __global__ void __launch_bounds__(256) pack_t_kernel(const float* __restrict__ s
     for (int i = 0; i < 4; ++i) {
       const int64_t cc = c0 + ty + 8 * i;
       const int64_t k = k0 + tx;
-      if (cc < cols && k < K) {
+      if (cc < cols && k < kend) {
         float v = tile[tx][ty + 8 * i];
         if (kRound) v = tf32_rn(v);
         dst[cc * ldk + k] = v;
@@ -87,7 +93,13 @@ __global__ void __launch_bounds__(256) bias_update_kernel(const float* __restric
 cudaError_t launch_pack_t(const float* src, int64_t ld_src, float* dst, int64_t ldk, int64_t K, int64_t cols,
                           bool round_tf32, float* colsum, cudaStream_t s) {
   if (K <= 0 || cols <= 0) return cudaSuccess;
-  const dim3 grid((unsigned)((cols + 31) / 32)), block(32, 8);
+  const int64_t cblocks = (cols + 31) / 32;
+  int64_t ksplit = 1;
+  if (!colsum) {  // aim for >= 4 blocks per SM
+    const int64_t want = (148 * 4 + cblocks - 1) / cblocks;
+    ksplit = std::max<int64_t>(1, std::min<int64_t>(want, (K + 31) / 32));
+  }
+  const dim3 grid((unsigned)cblocks, (unsigned)ksplit), block(32, 8);
   if (round_tf32) {
     if (colsum) pack_t_kernel<true, true><<<grid, block, 0, s>>>(src, ld_src, dst, ldk, K, cols, colsum);
     else pack_t_kernel<true, false><<<grid, block, 0, s>>>(src, ld_src, dst, ldk, K, cols, nullptr);

@@ -13,7 +13,7 @@ OURS = ("poseidon", "recon_tcgen05", "recon_simt", "ps_shard_sgd", "pack_t_kerne
 
 
 def short(name):
-    for key in ("recon_tcgen05_kernel", "recon_simt_kernel", "ps_shard_sgd_kernel", "ps_shard_sgd_scalar",
+    for key in ("recon_tcgen05_2sm_kernel", "recon_tcgen05_kernel", "recon_simt_kernel", "ps_shard_sgd_kernel", "ps_shard_sgd_scalar",
                 "pack_t_kernel", "bias_update_kernel", "ps_sim_kernel"):
         if key in name:
             return key + (" [libposeidon]")
