@@ -754,12 +754,12 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
     p.num_tiles = p.m_tiles * p.n_tiles;
     // Regime: with few factor rows per tile the kernel is bound by the W
     // read-modify-write, so more W chunks in flight beat deeper operand staging.
-    bool hbm_regime = false;  // 4 stages + 5 W slots measured best in both regimes (tools/k1_sweep.sh)
-    if (const char* c = getenv("POSEIDON_K1_CFG")) hbm_regime = (c[0] == 'a');  // experiments only
+    int cfg = 1;  // 0: <3,8>, 1: <4,5>, 2: <2,8>
+    if (const char* c = getenv("POSEIDON_K1_CFG")) cfg = (c[0] == 'a') ? 0 : (c[0] == 'c') ? 2 : 1;  // experiments
     static bool attr_a = false, attr_b = false;
     const int pairs = std::min(p.num_tiles, sm_count_k1() / 2);
     cudaError_t e = cudaSuccess;
-    if (hbm_regime) {
+    if (cfg == 0) {
       constexpr int SM_ = k2sm::smem_bytes(3, 8);
       if (!attr_a) {
         e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
@@ -767,6 +767,15 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
         attr_a = true;
       }
       recon_tcgen05_2sm_kernel<3, 8><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, p);
+    } else if (cfg == 2) {
+      constexpr int SM_ = k2sm::smem_bytes(2, 8);
+      static bool attr_c = false;
+      if (!attr_c) {
+        e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
+        if (e != cudaSuccess) return e;
+        attr_c = true;
+      }
+      recon_tcgen05_2sm_kernel<2, 8><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, p);
     } else {
       constexpr int SM_ = k2sm::smem_bytes(4, 5);
       if (!attr_b) {

@@ -36,7 +36,10 @@ __device__ __forceinline__ void tma2d(const CUtensorMap* m, uint64_t* bar, void*
 }
 
 constexpr int M = 4096, N = 9216, TM = 128, TN = 256;
-constexpr int SLOTS = 8, CH = 16384;
+#ifndef SLOTS_
+#define SLOTS_ 8
+#endif
+constexpr int SLOTS = SLOTS_, CH = 16384;
 
 template <int V>
 __global__ void __launch_bounds__(160, 1) probe(const __grid_constant__ CUtensorMap map, float* W) {
