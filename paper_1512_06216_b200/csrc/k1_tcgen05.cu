@@ -117,6 +117,11 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -199,6 +204,8 @@ struct Params {
   int32_t m_tiles, n_tiles, num_tiles, num_kb, kb_per_p;
   float* W;        // W base (row-major M x N) for the coalesced write-back of the 2-SM epilogue
   int32_t mode;    // experiments only: 1 = W streaming alone (no MMA), 0 = production
+  int32_t epi_groups;  // experiments only: 2 (production) or 1 epilogue warpgroups
+  int32_t w_policy;    // experiments only: 0 = evict_first (production), 1 = evict_normal
   int32_t m_fast;  // raster: 1 -> consecutive tiles walk M (re-sweep the smaller operand Ug each wave)
   float alpha;
   float* dbg;  // debug dump (tile 0 of CTA 0): smem stage 0 of A|B, raw accumulator; NULL in production
@@ -556,7 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
   } else if (warp == 2) {
     // ===================== W tile TMA producer (both CTAs, own rows) =====================
     if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
+      const uint64_t pol = p.w_policy ? policy_evict_normal() : policy_evict_first();
       uint32_t g = 0;
       for (int tile = pair; tile < p.num_tiles; tile += npairs) {
         int mt, nt;
@@ -601,7 +608,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
       if (p.mode == 0) mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       for (int c = 0; c < nch; ++c, ++g) {
-        if ((int)(g & 1) != e) continue;
+        if (p.epi_groups == 2 ? ((int)(g & 1) != e) : (e != 0)) continue;
         const uint32_t slot = g % NWS, ph = (g / NWS) & 1;
         uint32_t r[32];
         if (p.mode == 0) {
@@ -739,6 +746,10 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   p.m_fast = (operand_bytes <= 48e6) ? 0 : ((M <= N) ? 1 : 0);
   if (const char* r = getenv("POSEIDON_K1_RASTER")) p.m_fast = (r[0] == 'm');  // experiments only
   p.mode = 0;
+  p.epi_groups = 2;
+  p.w_policy = 0;
+  if (const char* eg = getenv("POSEIDON_K1_EPI")) p.epi_groups = eg[0] - '0';  // experiments only
+  if (const char* wp = getenv("POSEIDON_K1_WPOL")) p.w_policy = wp[0] - '0';   // experiments only
   if (const char* md = getenv("POSEIDON_K1_MODE")) p.mode = md[0] - '0';         // experiments only
   static int variant = -1;  // 2 = cta_group::2 (default), 1 = single-CTA tiles
   if (variant < 0) {
