@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--scheme", default=None, choices=[None, "auto", "ps", "sfb"])
     ap.add_argument("--dwbp", default="on", choices=["on", "off"])
     ap.add_argument("--recon", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--nvls", default="auto", choices=["auto", "on", "off"],
+                    help="fused one-kernel NVLink-SHARP PS sync (f1); auto = on when N > 1")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -240,12 +242,15 @@ def run_poseidon(args):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     flags = pz.FLAG_DWBP_OFF if args.dwbp == "off" else 0
+    use_nvls = world > 1 and args.nvls != "off"
+    if use_nvls:
+        flags |= pz.FLAG_NVLS_PS
     ctx = pz.Context(rank=rank, world=world, device=local, nccl_id=nccl_id, flags=flags)
 
     torch.manual_seed(6216)          # identical weights on every rank
     model = cfg["model"]().to(dev)
     recon = pz.RECON_TF32 if args.recon == "tf32" else pz.RECON_FP32
-    sync = PoseidonSync(model, ctx, K=K, lr=args.lr, scheme=scheme, recon=recon)
+    sync = PoseidonSync(model, ctx, K=K, lr=args.lr, scheme=scheme, recon=recon, arena=use_nvls)
 
     g = torch.Generator(device=dev)
     g.manual_seed(1512 + rank)
@@ -411,6 +416,9 @@ def run_poseidon(args):
             "config": {"workload": f"{args.config} {cfg['name']} training step, Poseidon sync (SACP+DWBP)",
                        "model": cfg["name"], "global_batch": world * K, "per_gpu_batch": K,
                        "parallelism": f"dp{world}", "scheme": scheme, "dwbp": args.dwbp,
+                       "ps_path": ("nvls-fused" if sync.nvls_active else
+                                   ("nccl rs/k2/ag" if world > 1 else "k2 (P=1)")),
+                       "nvls_status": ctx.nvls_status(),
                        "l2": "inputs larger than L2 (images 158 MB + weights 244 MB per step for C3)",
                        "lr": args.lr},
             "exposed_sync_ms": exposed, "sync_total_ms": sync_total,

@@ -77,6 +77,7 @@ typedef struct {
 
 #define POSEIDON_FLAG_DWBP_OFF 0x1u   /* ablation: sync starts only at iteration_end (Fig. dwbp (a)) */
 #define POSEIDON_FLAG_NO_PRIORITY 0x2u /* sync streams at default instead of highest priority */
+#define POSEIDON_FLAG_NVLS_PS 0x4u     /* PS layers in the arena sync with one fused NVLink-SHARP kernel */
 
 typedef struct poseidon_ctx* poseidon_ctx_t;
 
@@ -185,6 +186,23 @@ poseidon_status_t poseidon_bind_ps_buffers(poseidon_ctx_t ctx, int32_t layer_id,
                                            float* W, int64_t n, uint32_t flags);
 /* Bind an SFB layer's parameters (W: M x N, bias: M or NULL). */
 poseidon_status_t poseidon_bind_sfb_params(poseidon_ctx_t ctx, int32_t layer_id, float* W, float* bias);
+
+/* PS arena (collective over all ranks when world > 1): allocates ONE padded
+ * gradient buffer and ONE parameter buffer holding every registered PS layer
+ * (each layer's segment padded_n floats, 4 KB aligned), zero-filled, and binds
+ * each PS layer to its segments with POSEIDON_PS_ZERO_GRAD.  The caller copies
+ * its initial parameters in (poseidon_ps_layer_buffers) and makes its tensors
+ * views of them.  With POSEIDON_FLAG_NVLS_PS the arenas are NCCL symmetric
+ * windows (ncclMemAlloc + ncclCommWindowRegister) and each PS sync becomes ONE
+ * kernel: multimem.ld_reduce of the shard across all ranks (NVSwitch sum) ->
+ * SGD -> multimem.st of the updated shard to every rank -> zero the local
+ * gradient.  *nvls_active (nullable) = 1 if that path is active;
+ * otherwise the arena is plain device memory and the NCCL path is used. */
+poseidon_status_t poseidon_ps_arena(poseidon_ctx_t ctx, int32_t* nvls_active);
+poseidon_status_t poseidon_ps_layer_buffers(poseidon_ctx_t ctx, int32_t layer_id, float** grad, float** W,
+                                            int64_t* padded_n);
+/* Human-readable state of the fused NVLS path ("active", "not requested", or the NCCL error). */
+const char* poseidon_nvls_status(poseidon_ctx_t ctx);
 
 poseidon_status_t poseidon_set_lr(poseidon_ctx_t ctx, float lr);           /* lr used by backprop_hook */
 poseidon_status_t poseidon_set_recon(poseidon_ctx_t ctx, int32_t layer_id /* -1: all */, int32_t recon);

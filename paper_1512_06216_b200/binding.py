@@ -23,7 +23,7 @@ ERR_SHAPE, ERR_ALIGNMENT, ERR_UNSUPPORTED, ERR_STATE = -5, -6, -7, -8
 SCHEME_PS, SCHEME_SFB = 0, 1
 LAYER_CONV, LAYER_FC = 0, 1
 RECON_TF32, RECON_FP32 = 0, 1
-FLAG_DWBP_OFF, FLAG_NO_PRIORITY = 0x1, 0x2
+FLAG_DWBP_OFF, FLAG_NO_PRIORITY, FLAG_NVLS_PS = 0x1, 0x2, 0x4
 PS_ZERO_GRAD = 0x1
 
 _STATUS_NAMES = {0: "OK", -1: "INVALID_ARG", -2: "NOT_INITIALIZED", -3: "CUDA", -4: "NCCL",
@@ -92,6 +92,9 @@ _SIGS = {
     "poseidon_bind_ps_buffers": (_i32, [_vp, _i32, _vp, _vp, _i64, _u32]),
     "poseidon_bind_sfb_params": (_i32, [_vp, _i32, _vp, _vp]),
     "poseidon_set_lr": (_i32, [_vp, _f]),
+    "poseidon_ps_arena": (_i32, [_vp, _P(_i32)]),
+    "poseidon_ps_layer_buffers": (_i32, [_vp, _i32, _P(_vp), _P(_vp), _P(_i64)]),
+    "poseidon_nvls_status": (ctypes.c_char_p, [_vp]),
     "poseidon_set_recon": (_i32, [_vp, _i32, _i32]),
     "poseidon_wait_layer": (_i32, [_vp, _i32, _vp]),
     "poseidon_iteration_end": (_i32, [_vp, _vp, _P(IterStats)]),
@@ -219,6 +222,21 @@ class Context:
 
     def bind_sfb_params(self, layer_id, W, bias=None):
         _check(lib.poseidon_bind_sfb_params(self.h, layer_id, _ptr(W), _ptr(bias)))
+
+    def ps_arena(self) -> bool:
+        """Collective: allocate the PS arena; True if the fused NVLS path is active."""
+        act = _i32()
+        _check(lib.poseidon_ps_arena(self.h, ctypes.byref(act)))
+        return bool(act.value)
+
+    def ps_layer_buffers(self, layer_id):
+        g, w, n = _vp(), _vp(), _i64()
+        _check(lib.poseidon_ps_layer_buffers(self.h, layer_id, ctypes.byref(g), ctypes.byref(w), ctypes.byref(n)))
+        return g.value, w.value, n.value
+
+    def nvls_status(self) -> str:
+        m = lib.poseidon_nvls_status(self.h)
+        return m.decode() if m else ""
 
     def set_lr(self, lr):
         _check(lib.poseidon_set_lr(self.h, float(lr)))

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "nvls.h"
 
 namespace poseidon {
 
@@ -76,6 +77,8 @@ struct Layer {
   float *grad = nullptr, *Wps = nullptr;
   int64_t n = 0, S = 0, padded = 0, begin = 0, end = 0;
   uint32_t ps_flags = 0;
+  bool in_arena = false;     // PS buffers live in the library's (symmetric) arena
+  size_t arena_off = 0;      // byte offset of this layer in both arenas
   EvSet ev[RING];
   bool events_created = false;
   int64_t last_iter = -1;  // iteration of the latest sync
@@ -107,6 +110,15 @@ struct poseidon_ctx {
   int64_t iter = 0;  // current (open) iteration
   IterRecord rec[RING];
   std::vector<int32_t> pending_order;  // DWBP off: hook order of deferred syncs
+  // PS arena (poseidon_ps_arena): one gradient and one parameter buffer for all PS layers; NCCL
+  // symmetric windows + device communicator when the fused NVLS path is enabled and available
+  bool want_nvls = false;
+  float *arena_g = nullptr, *arena_w = nullptr;
+  size_t arena_bytes = 0;
+  bool arena_nccl_mem = false;
+  ncclWindow_t win_g = nullptr, win_w = nullptr;
+  NvlsState* nvls = nullptr;
+  std::string nvls_error;
 };
 
 namespace {
@@ -201,6 +213,24 @@ poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* 
   CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
   IterRecord& r = open_record(c);
+  if (P > 1 && c->nvls && L.in_arena) {
+    // fused one-kernel PS over NVLink SHARP (reduce-scatter + K2 + all-gather + zero-grad)
+    CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+    CU_TRY(cudaEventRecord(e.kstart, c->comm_stream));
+    cudaError_t err = launch_ps_nvls(c->nvls, c->win_g, c->win_w, L.arena_off, L.arena_off, L.begin, L.end,
+                                     L.padded, -lr / (float)P, (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0, 64,
+                                     c->comm_stream);
+    if (err != cudaSuccess) return cuda_fail(err, "fused NVLS PS launch");
+    CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
+    CU_TRY(cudaEventRecord(e.done, c->comm_stream));
+    // bytes through NVLink per rank: the switch reads this rank's gradient for the other P-1
+    // shards and writes the other ranks' updated shards here; this rank reads its reduced shard
+    // and writes its updated shard once into the switch
+    r.sent += (uint64_t)L.S * 4u * (uint64_t)P;
+    r.recv += (uint64_t)L.S * 4u * (uint64_t)P;
+    r.layers.push_back(id);
+    return POSEIDON_OK;
+  }
   if (P > 1) {
     NC_TRY(ncclReduceScatter(grad, grad + (size_t)c->rank * L.S, (size_t)L.S, ncclFloat32, ncclSum, c->comm,
                              c->comm_stream));
@@ -327,6 +357,7 @@ poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, 
   c->world = world;
   c->device = topo->device;
   c->flags = topo->flags;
+  c->want_nvls = (topo->flags & POSEIDON_FLAG_NVLS_PS) != 0 && world > 1;
   c->layers.resize(64);
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -362,6 +393,16 @@ poseidon_status_t poseidon_finalize(poseidon_ctx_t c) {
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->recon_stream) cudaStreamSynchronize(c->recon_stream);
   for (auto& L : c->layers) free_layer(L);
+  if (c->nvls) nvls_destroy(c->comm, c->nvls);
+  if (c->win_g) ncclCommWindowDeregister(c->comm, c->win_g);
+  if (c->win_w) ncclCommWindowDeregister(c->comm, c->win_w);
+  if (c->arena_nccl_mem) {
+    if (c->arena_g) ncclMemFree(c->arena_g);
+    if (c->arena_w) ncclMemFree(c->arena_w);
+  } else {
+    if (c->arena_g) cudaFree(c->arena_g);
+    if (c->arena_w) cudaFree(c->arena_w);
+  }
   for (auto& r : c->rec)
     if (r.bwd_end) cudaEventDestroy(r.bwd_end);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -469,6 +510,81 @@ poseidon_status_t poseidon_bind_sfb_params(poseidon_ctx_t c, int32_t id, float* 
   L->W = W;
   L->bias = bias;
   return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
+  poseidon_status_t st = check_ctx(c);
+  if (st) return st;
+  if (c->arena_g) return fail(POSEIDON_ERR_STATE, "PS arena already created");
+  cudaSetDevice(c->device);
+  size_t total = 0;
+  for (auto& L : c->layers) {
+    if (!L.registered || L.scheme != POSEIDON_SCHEME_PS) continue;
+    const int64_t n = L.M * L.N + (L.has_bias ? L.M : 0);
+    int64_t b, e, padded;
+    poseidon_shard_range(n, c->world, c->rank, &b, &e, &padded);
+    L.arena_off = total;
+    total += (size_t)round_up(padded * 4, 4096);
+  }
+  if (total == 0) total = 4096;
+  c->arena_bytes = total;
+  bool symmetric = false;
+  if (c->want_nvls && c->comm) {
+    void *g = nullptr, *w = nullptr;
+    ncclResult_t r1 = ncclMemAlloc(&g, total);
+    ncclResult_t r2 = (r1 == ncclSuccess) ? ncclMemAlloc(&w, total) : r1;
+    ncclResult_t r3 = (r2 == ncclSuccess) ? ncclCommWindowRegister(c->comm, g, total, &c->win_g, NCCL_WIN_COLL_SYMMETRIC) : r2;
+    ncclResult_t r4 = (r3 == ncclSuccess) ? ncclCommWindowRegister(c->comm, w, total, &c->win_w, NCCL_WIN_COLL_SYMMETRIC) : r3;
+    if (r4 == ncclSuccess) {
+      c->nvls = nvls_create(c->comm, 64, &c->nvls_error);
+      symmetric = true;
+      c->arena_nccl_mem = true;
+      c->arena_g = static_cast<float*>(g);
+      c->arena_w = static_cast<float*>(w);
+    } else {
+      c->nvls_error = std::string("symmetric window: ") + ncclGetErrorString(r4);
+      if (c->win_g) { ncclCommWindowDeregister(c->comm, c->win_g); c->win_g = nullptr; }
+      if (g) ncclMemFree(g);
+      if (w) ncclMemFree(w);
+    }
+  }
+  if (!symmetric) {
+    CU_TRY(cudaMalloc(&c->arena_g, total));
+    CU_TRY(cudaMalloc(&c->arena_w, total));
+  }
+  CU_TRY(cudaMemset(c->arena_g, 0, total));
+  CU_TRY(cudaMemset(c->arena_w, 0, total));
+  CU_TRY(cudaDeviceSynchronize());
+  for (int32_t id = 0; id < (int32_t)c->layers.size(); ++id) {
+    Layer& L = c->layers[id];
+    if (!L.registered || L.scheme != POSEIDON_SCHEME_PS) continue;
+    const int64_t n = L.M * L.N + (L.has_bias ? L.M : 0);
+    float* g = reinterpret_cast<float*>(reinterpret_cast<char*>(c->arena_g) + L.arena_off);
+    float* w = reinterpret_cast<float*>(reinterpret_cast<char*>(c->arena_w) + L.arena_off);
+    st = poseidon_bind_ps_buffers(c, id, g, w, n, POSEIDON_PS_ZERO_GRAD);
+    if (st) return st;
+    L.in_arena = true;
+  }
+  if (nvls_active) *nvls_active = c->nvls ? 1 : 0;
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_ps_layer_buffers(poseidon_ctx_t c, int32_t id, float** grad, float** W, int64_t* padded) {
+  Layer* L;
+  poseidon_status_t st = check_layer(c, id, &L);
+  if (st) return st;
+  if (!L->in_arena) return fail(POSEIDON_ERR_STATE, "layer has no arena buffers (call poseidon_ps_arena)");
+  if (grad) *grad = L->grad;
+  if (W) *W = L->Wps;
+  if (padded) *padded = L->padded;
+  return POSEIDON_OK;
+}
+
+const char* poseidon_nvls_status(poseidon_ctx_t c) {
+  if (!c) return "no context";
+  if (c->nvls) return "active";
+  if (!c->want_nvls) return "not requested";
+  return c->nvls_error.empty() ? "arena not created" : c->nvls_error.c_str();
 }
 
 poseidon_status_t poseidon_set_lr(poseidon_ctx_t c, float lr) {

@@ -1,0 +1,128 @@
+// K2n — fused one-kernel parameter-server sync over NVLink SHARP.
+//
+// Alg. 1's master ("Collect gradients ... Updates the part of model
+// parameters ... Push updated model parameters") and Alg. 3 lines 1-3 in ONE
+// kernel per layer, with the NVSwitch acting as the paper's "master node":
+//   1. LSA barrier: every rank's local gradient (accumulated by autograd into
+//      its symmetric-window copy) is complete and visible;
+//   2. for this rank's shard [b, e): g = multimem.ld_reduce.add(G_mc + i) —
+//      the switch reads and sums all P ranks' copies (the reduce-scatter);
+//      W' = fmaf(alpha, g, W_local) (K2's update); multimem.st(W_mc + i, W')
+//      — the switch writes the updated shard into every rank's W (the
+//      all-gather);
+//   3. LSA barrier: all ranks' stores landed and all reads of the local
+//      gradient are done; the local gradient buffer is then zeroed for the
+//      next iteration's accumulation.
+// Buffers live in NCCL symmetric windows (ncclMemAlloc +
+// ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC)); pointers come from the NCCL
+// device API (ncclGetLsaMultimemPointer / ncclGetLocalPointer).
+#include <nccl.h>
+#include <nccl_device.h>
+
+#include <cstring>
+
+#include "internal.h"
+#include "nvls.h"
+
+namespace poseidon {
+
+namespace {
+
+__device__ __forceinline__ float4 mm_ld_reduce_v4(const float* mc) {
+  float4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(mc)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float mm_ld_reduce(const float* mc) {
+  float v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(mc) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mm_st_v4(float* mc, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mm_st(float* mc, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "f"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(256) ps_nvls_kernel(const __grid_constant__ ncclDevComm comm, ncclWindow_t wg,
+                                                      ncclWindow_t ww, size_t off_g, size_t off_w, int64_t b,
+                                                      int64_t e, int64_t padded, float alpha, int zero_grad) {
+  ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamTagLsa(), blockIdx.x, /*multimem=*/true);
+  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+
+  const float* gmc = static_cast<const float*>(ncclGetLsaMultimemPointer(wg, off_g, comm));
+  float* wmc = static_cast<float*>(ncclGetLsaMultimemPointer(ww, off_w, comm));
+  const float* wloc = static_cast<const float*>(ncclGetLocalPointer(ww, off_w));
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n4 = (e - b) >> 2;  // b is 32-element aligned (shard map), so b + 4i is 16-B aligned
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const int64_t k = b + 4 * i;
+    const float4 g = mm_ld_reduce_v4(gmc + k);
+    float4 w = *reinterpret_cast<const float4*>(wloc + k);
+    w.x = fmaf(alpha, g.x, w.x);
+    w.y = fmaf(alpha, g.y, w.y);
+    w.z = fmaf(alpha, g.z, w.z);
+    w.w = fmaf(alpha, g.w, w.w);
+    mm_st_v4(wmc + k, w);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < ((e - b) & 3)) {
+    const int64_t k = b + 4 * n4 + threadIdx.x;
+    mm_st(wmc + k, fmaf(alpha, mm_ld_reduce(gmc + k), wloc[k]));
+  }
+
+  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  if (zero_grad) {
+    float4* gl = static_cast<float4*>(ncclGetLocalPointer(wg, off_g));
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (padded >> 2); i += stride) gl[i] = z;
+  }
+}
+
+}  // namespace
+
+struct NvlsState {
+  ncclDevComm dev{};
+  bool dev_ok = false;
+};
+
+cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww, size_t off_g, size_t off_w,
+                           int64_t b, int64_t e, int64_t padded, float alpha, bool zero_grad, int max_blocks,
+                           cudaStream_t s) {
+  const int64_t n4 = (e - b + 3) / 4;
+  int blocks = (int)((n4 + 255) / 256);
+  if (blocks < 1) blocks = 1;
+  if (blocks > max_blocks) blocks = max_blocks;
+  ps_nvls_kernel<<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, padded, alpha, zero_grad ? 1 : 0);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+NvlsState* nvls_create(ncclComm_t comm, int barriers, std::string* err) {
+  auto* st = new NvlsState();
+  ncclDevCommRequirements reqs;
+  memset(&reqs, 0, sizeof(reqs));
+  reqs.lsaMultimem = true;
+  reqs.lsaBarrierCount = barriers;
+  ncclResult_t r = ncclDevCommCreate(comm, &reqs, &st->dev);
+  if (r != ncclSuccess) {
+    *err = std::string("ncclDevCommCreate(lsaMultimem): ") + ncclGetErrorString(r);
+    delete st;
+    return nullptr;
+  }
+  st->dev_ok = true;
+  return st;
+}
+
+void nvls_destroy(ncclComm_t comm, NvlsState* st) {
+  if (!st) return;
+  if (st->dev_ok) ncclDevCommDestroy(comm, &st->dev);
+  delete st;
+}
+
+}  // namespace poseidon

@@ -80,7 +80,7 @@ class PoseidonSync:
     per worker per FC layer)."""
 
     def __init__(self, model: nn.Module, ctx: B.Context, K: int, lr: float,
-                 scheme: str = "auto", recon: int = B.RECON_TF32, fc_flat_sfb_input: bool = True):
+                 scheme: str = "auto", recon: int = B.RECON_TF32, arena: bool = False):
         self.model = model
         self.ctx = ctx
         self.K = K
@@ -88,11 +88,20 @@ class PoseidonSync:
         self.plans: List[LayerPlan] = []
         self.by_module: Dict[nn.Module, LayerPlan] = {}
         ctx.set_lr(self.lr)
+        self.arena = arena
+        self.nvls_active = False
         layer_id = 0
         for name, mod in model.named_modules():
             if isinstance(mod, (nn.Linear, nn.Conv2d)):
                 self._register(layer_id, name, mod, scheme, recon)
                 layer_id += 1
+        if arena:
+            # one library-owned gradient/parameter arena for all PS layers (symmetric NCCL windows
+            # with FLAG_NVLS_PS: each PS sync is then one fused multimem kernel)
+            self.nvls_active = ctx.ps_arena()
+            for plan in self.plans:
+                if plan.scheme == B.SCHEME_PS:
+                    self._bind_arena(plan)
 
     # ------------------------------------------------------------ setup ----
     def _register(self, lid, name, mod, scheme, recon):
@@ -123,9 +132,31 @@ class PoseidonSync:
         h = mod.register_forward_pre_hook(self._pre_forward(plan))
         plan.hook_handles.append(h)
 
+    def _bind_arena(self, plan):
+        mod = plan.module
+        params = [mod.weight] + ([mod.bias] if mod.bias is not None else [])
+        gptr, wptr, padded = self.ctx.ps_layer_buffers(plan.layer_id)
+        flat_g = B.device_view(gptr, (padded,))
+        flat_w = B.device_view(wptr, (padded,))
+        off = 0
+        for p in params:
+            k = p.numel()
+            flat_w[off:off + k].copy_(p.data.reshape(-1))
+            p.data = flat_w[off:off + k].view_as(p)
+            p.grad = flat_g[off:off + k].view_as(p)
+            off += k
+        torch.cuda.synchronize()
+        plan.flat_w, plan.flat_g, plan.padded = flat_w, flat_g, padded
+
     def _flatten_ps(self, mod, plan):
         params = [mod.weight] + ([mod.bias] if mod.bias is not None else [])
         n = sum(p.numel() for p in params)
+        plan.n = n
+        plan.n_params = len(params)
+        for p in params:
+            plan.hook_handles.append(p.register_post_accumulate_grad_hook(self._post_accumulate(plan)))
+        if self.arena:
+            return  # buffers come from the library arena after all layers are registered
         _, _, padded = B.shard_range(n, self.ctx.world, self.ctx.rank)
         dev = mod.weight.device
         flat_w = torch.zeros(padded, device=dev, dtype=torch.float32)
@@ -137,11 +168,8 @@ class PoseidonSync:
             p.data = flat_w[off:off + k].view_as(p)
             p.grad = flat_g[off:off + k].view_as(p)
             off += k
-        plan.n, plan.padded, plan.flat_w, plan.flat_g = n, padded, flat_w, flat_g
-        plan.n_params = len(params)
+        plan.padded, plan.flat_w, plan.flat_g = padded, flat_w, flat_g
         self.ctx.bind_ps_buffers(plan.layer_id, flat_g, flat_w, n, B.PS_ZERO_GRAD)
-        for p in params:
-            plan.hook_handles.append(p.register_post_accumulate_grad_hook(self._post_accumulate(plan)))
 
     def _wrap_linear(self, mod, plan):
         sync = self

@@ -145,17 +145,54 @@ def main():
         assert O.update_error_fp32(W, out, ref) <= 1e-5
     ctx.close()
 
+    # ---- 3b. fused NVLS PS (f1): arena in NCCL symmetric windows, one multimem kernel per layer ----
+    cn = new_ctx(pz.FLAG_NVLS_PS)
+    layers = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 96, 363, 2)]   # n = 32896, 650, 34944
+    for lid, M_, N_, K_ in layers:
+        cn.register_layer(lid, pz.LAYER_CONV, M_, N_, K_)
+    cn_lr = 2.0 ** -7
+    cn.set_lr(cn_lr)
+    active = cn.ps_arena()
+    status = cn.nvls_status()
+    if rank == 0:
+        print(f"NVLS {status}", flush=True)
+    for lid, M_, N_, K_ in layers:
+        n = M_ * N_ + M_
+        gp, wp, padded = cn.ps_layer_buffers(lid)
+        from paper_1512_06216_b200.binding import device_view
+        gv, wv = device_view(gp, (padded,)), device_view(wp, (padded,))
+        g0 = S.rng(lid + 40)
+        W = (g0.integers(-1023, 1024, size=n) * 2.0 ** -10).astype(np.float32)
+        grads = S.integer_grads(n, P, seed=lid + 50)
+        wv[:n].copy_(torch.from_numpy(W).to(dev))
+        gv[:n].copy_(torch.from_numpy(grads[rank]).to(dev))
+        torch.cuda.synchronize()
+        cn.backprop_hook(lid)
+        cn.wait_layer(lid)
+        st = cn.iteration_end(stats=True)
+        torch.cuda.synchronize()
+        ref = O.ps_step_flat(W, grads, cn_lr)
+        out = wv[:n].cpu().numpy().astype(np.float64)
+        if P in (1, 2, 4, 8):
+            assert np.array_equal(out, ref), f"NVLS PS mismatch layer {lid} ({status})"
+        else:
+            assert O.update_error_fp32(W, out, ref) <= 1e-5
+        assert allsame(wv[:n].clone())
+        assert float(gv.abs().sum()) == 0.0, "grad not zeroed"
+    cn.close()
+
     # ---- 4. DWBP training steps of CIFAR-10 quick ----
     Kc = 16
     results = {}
-    for scheme in ("auto", "ps"):
-        for dwbp in ("on", "off"):
-            c2 = new_ctx(pz.FLAG_DWBP_OFF if dwbp == "off" else 0)
+    variants = [(sc, dw, nv) for sc in ("auto", "ps") for dw in ("on", "off") for nv in (False, True)]
+    for scheme, dwbp, nv in variants:
+        if True:
+            c2 = new_ctx((pz.FLAG_DWBP_OFF if dwbp == "off" else 0) | (pz.FLAG_NVLS_PS if nv else 0))
             torch.manual_seed(1234)
             model = CifarQuick().to(dev)
             ref_model = CifarQuick().to(dev)
             ref_model.load_state_dict(model.state_dict())
-            sync = PoseidonSync(model, c2, K=Kc, lr=0.05, scheme=scheme, recon=pz.RECON_TF32)
+            sync = PoseidonSync(model, c2, K=Kc, lr=0.05, scheme=scheme, recon=pz.RECON_TF32, arena=nv)
             for it in range(2):
                 gen = torch.Generator().manual_seed(100 + it)
                 xall = torch.rand(P * Kc, 3, 32, 32, generator=gen).to(dev)
@@ -173,15 +210,17 @@ def main():
             sync.wait_all()
             torch.cuda.synchronize()
             flat = torch.cat([p.detach().reshape(-1) for p in model.parameters()])
-            assert allsame(flat), f"ranks differ ({scheme}, dwbp {dwbp})"
+            assert allsame(flat), f"ranks differ ({scheme}, dwbp {dwbp}, nvls {nv})"
             for (name, p), (_, q) in zip(model.named_parameters(), ref_model.named_parameters()):
                 w0 = q.detach().cpu().numpy()
                 err = np.max(np.abs(p.detach().cpu().numpy() - w0)) / max(1e-12, np.max(np.abs(w0)))
-                assert err < 2e-3, (name, err, scheme, dwbp)
-            results[(scheme, dwbp)] = flat.cpu()
+                assert err < 2e-3, (name, err, scheme, dwbp, nv)
+            results[(scheme, dwbp, nv)] = flat.cpu()
             c2.close()
     for scheme in ("auto", "ps"):
-        assert torch.equal(results[(scheme, "on")], results[(scheme, "off")]), f"DWBP on/off differ ({scheme})"
+        for nv in (False, True):
+            assert torch.equal(results[(scheme, "on", nv)], results[(scheme, "off", nv)]), \
+                f"DWBP on/off differ ({scheme}, nvls {nv})"
     dist.barrier()
     print(f"MP_OK {rank}", flush=True)
     dist.destroy_process_group()
