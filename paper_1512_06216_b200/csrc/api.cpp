@@ -219,7 +219,7 @@ poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* 
     CU_TRY(cudaEventRecord(e.kstart, c->comm_stream));
     cudaError_t err = launch_ps_nvls(c->nvls, c->win_g, c->win_w, L.arena_off, L.arena_off, L.begin, L.end,
                                      L.padded, -lr / (float)P, (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0, 64,
-                                     c->comm_stream);
+                                     L.S, c->comm_stream);
     if (err != cudaSuccess) return cuda_fail(err, "fused NVLS PS launch");
     CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
     CU_TRY(cudaEventRecord(e.done, c->comm_stream));

@@ -93,8 +93,11 @@ struct NvlsState {
 
 cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww, size_t off_g, size_t off_w,
                            int64_t b, int64_t e, int64_t padded, float alpha, bool zero_grad, int max_blocks,
-                           cudaStream_t s) {
-  const int64_t n4 = (e - b + 3) / 4;
+                           int64_t shard, cudaStream_t s) {
+  // The grid must be identical on every rank (block j of every rank meets at LSA barrier j), so it
+  // is sized from the shard size S, not from this rank's (possibly shorter or empty) range.
+  (void)e;
+  const int64_t n4 = (shard + 3) / 4;
   int blocks = (int)((n4 + 255) / 256);
   if (blocks < 1) blocks = 1;
   if (blocks > max_blocks) blocks = max_blocks;
