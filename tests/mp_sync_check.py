@@ -147,7 +147,9 @@ def main():
 
     # ---- 3b. fused NVLS PS (f1): arena in NCCL symmetric windows, one multimem kernel per layer ----
     cn = new_ctx(pz.FLAG_NVLS_PS)
-    layers = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 96, 363, 2)]   # n = 32896, 650, 34944
+    # n = 32896, 650, 34944, 2080 (at P=2 the last shard is 1024 floats vs S=1056: unequal local
+    # ranges must still launch identical grids on every rank)
+    layers = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 96, 363, 2), (3, 16, 129, 2)]
     for lid, M_, N_, K_ in layers:
         cn.register_layer(lid, pz.LAYER_CONV, M_, N_, K_)
     cn_lr = 2.0 ** -7
