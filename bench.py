@@ -44,6 +44,8 @@ def parse():
                     help="fused one-kernel NVLink-SHARP PS sync (f1); auto = on when N > 1")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--memory-format", default="channels_last", choices=["channels_last", "nchw"],
+                    help="driver CNN activation layout (cuDNN NHWC kernels avoid layout transposes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layer-stats", action="store_true", help="print per-layer stats to stderr")
     return ap.parse_args()
@@ -250,11 +252,15 @@ def run_poseidon(args):
     torch.manual_seed(6216)          # identical weights on every rank
     model = cfg["model"]().to(dev)
     recon = pz.RECON_TF32 if args.recon == "tf32" else pz.RECON_FP32
+    if args.memory_format == "channels_last":
+        model.to(memory_format=torch.channels_last)   # before PoseidonSync makes params buffer views
     sync = PoseidonSync(model, ctx, K=K, lr=args.lr, scheme=scheme, recon=recon, arena=use_nvls)
 
     g = torch.Generator(device=dev)
     g.manual_seed(1512 + rank)
     x = torch.rand((K, 3, hw, hw), device=dev, generator=g)
+    if args.memory_format == "channels_last":
+        x = x.contiguous(memory_format=torch.channels_last)
     y = torch.randint(0, classes, (K,), device=dev, generator=g)
 
     def step(xb, yb):
@@ -447,6 +453,7 @@ def run_poseidon(args):
                        "ps_path": ("nvls-fused" if sync.nvls_active else
                                    ("nccl rs/k2/ag" if world > 1 else "k2 (P=1)")),
                        "nvls_status": ctx.nvls_status(),
+                       "memory_format": args.memory_format,
                        "l2": "inputs larger than L2 (images 158 MB + weights 244 MB per step for C3)",
                        "lr": args.lr},
             "exposed_sync_ms": exposed, "sync_total_ms": sync_total,

@@ -50,6 +50,16 @@ class LayerPlan:
     hook_handles: List = field(default_factory=list)
 
 
+def _view_like(seg: torch.Tensor, p: torch.Tensor) -> torch.Tensor:
+    """View a flat buffer segment with p's shape AND memory format (a channels_last conv weight
+    keeps its NHWC strides, so cuDNN sees no layout change; the PS sync is elementwise over the
+    flat buffer and does not care about the element order)."""
+    if p.dim() == 4 and not p.is_contiguous() and p.is_contiguous(memory_format=torch.channels_last):
+        o, i, h, w = p.shape
+        return seg.view(o, h, w, i).permute(0, 3, 1, 2)
+    return seg.view_as(p)
+
+
 class SFBLinearFunction(torch.autograd.Function):
     """y = x W^T + b; backward returns dX only and triggers the SFB sync."""
 
@@ -141,9 +151,10 @@ class PoseidonSync:
         off = 0
         for p in params:
             k = p.numel()
-            flat_w[off:off + k].copy_(p.data.reshape(-1))
-            p.data = flat_w[off:off + k].view_as(p)
-            p.grad = flat_g[off:off + k].view_as(p)
+            wv = _view_like(flat_w[off:off + k], p)
+            wv.copy_(p.data)
+            p.data = wv
+            p.grad = _view_like(flat_g[off:off + k], p)
             off += k
         torch.cuda.synchronize()
         plan.flat_w, plan.flat_g, plan.padded = flat_w, flat_g, padded
@@ -164,9 +175,10 @@ class PoseidonSync:
         off = 0
         for p in params:
             k = p.numel()
-            flat_w[off:off + k].copy_(p.data.reshape(-1))
-            p.data = flat_w[off:off + k].view_as(p)
-            p.grad = flat_g[off:off + k].view_as(p)
+            wv = _view_like(flat_w[off:off + k], p)
+            wv.copy_(p.data)
+            p.data = wv
+            p.grad = _view_like(flat_g[off:off + k], p)
             off += k
         plan.padded, plan.flat_w, plan.flat_g = padded, flat_w, flat_g
         self.ctx.bind_ps_buffers(plan.layer_id, flat_g, flat_w, n, B.PS_ZERO_GRAD)
