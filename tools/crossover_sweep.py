@@ -86,8 +86,10 @@ def main():
             ctx.sync_ps(lid + 1, flat_g, flat_w, n, 0.01, s)
             ctx.wait_layer(lid + 1, s)
 
+        gview = flat_g[: M * N].view(M, N)
+
         def wgrad():
-            flat_g[: M * N].view(M, N).copy_(U.t() @ V)
+            torch.mm(U.t(), V, out=gview)
 
         t_sfb, t_ps, t_wg = timed(sfb), timed(ps), timed(wgrad)
         ctx.iteration_end(s)
