@@ -168,6 +168,24 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
 __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
+__device__ __forceinline__ float2 lds64(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void stg64_na(float* ptr, float2 v) {
+  asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1,%2};" ::"l"(ptr), "f"(v.x), "f"(v.y) : "memory");
+}
+// 16 lanes x 256 bit, 4 repetitions along columns: thread t gets rows t/4 and t/4+8 of the 16-lane
+// slab, columns 8j + 2(t%4) + {0,1} (r[4j+0..1] first row, r[4j+2..3] second row)
+__device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void stg128_na(float* ptr, float4 v) {
   asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w)
@@ -489,7 +507,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 16); }
-    for (int i = 0; i < NWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
+    for (int i = 0; i < NWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -583,14 +601,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
   } else if (warp >= 4) {
     // ===================== epilogue: 2 groups x 4 warps =====================
     // Group e processes the chunks g with g % 2 == e (g = global chunk counter shared with the W
-    // loader).  Per chunk: (1) thread-per-row: tcgen05.ld 32 accumulator columns of its TMEM lane,
-    // W = fmaf(alpha, acc, W) on the TMA-loaded W chunk in shared memory; (2) the group writes the
-    // chunk back with coalesced 128-bit stores (8 threads per 128-B row segment) and releases the
-    // slot right away — no bulk-store completion on the critical path.
+    // loader).  Each warp owns its 32 TMEM lanes (rows) and works alone: two tcgen05.ld.16x256b.x4
+    // (16 rows each; thread t holds rows t/4 and t/4+8, columns 8j + 2(t%4) + {0,1}, j = 0..3), the
+    // matching W pairs read straight from the TMA-swizzled smem chunk (conflict-free LDS.64),
+    // W' = fmaf(alpha, acc, W), and 8-byte stores that fill whole 32-B sectors of each row.  No
+    // smem write-back, no group barrier: the slot is released when the group's 4 warps have read it.
     const int e = (warp - 4) >> 2;
     const int q = (warp - 4) & 3;
-    const int t = q * 32 + lane;           // 0..127 within the group
-    const int row = t;                     // TMEM lane / tile row owned in phase (1)
+    const int t0 = lane & 3, tr = lane >> 2;   // column pair / row within a 16-lane slab
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
     const uint32_t smem_w_u32 = smem_u32(smem_w);
@@ -610,45 +628,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
       for (int c = 0; c < nch; ++c, ++g) {
         if (p.epi_groups == 2 ? ((int)(g & 1) != e) : (e != 0)) continue;
         const uint32_t slot = g % NWS, ph = (g / NWS) & 1;
-        uint32_t r[32];
-        if (p.mode == 0) {
-          tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * k2sm::BN + c * W_CHUNK_COLS), r);
-          tmem_ld_wait();
-        } else {
+        uint32_t r[2][16];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = 0u;
+        for (int h = 0; h < 2; ++h) {
+          if (p.mode == 0) {
+            tmem_ld_16x256b_x4(tmem_base + ((uint32_t)(q * 32 + h * 16) << 16) +
+                                   (uint32_t)(acc * k2sm::BN + c * W_CHUNK_COLS), r[h]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[h][j] = 0u;
+          }
         }
+        if (p.mode == 0) tmem_ld_wait();
         mbar_wait(&wfull[slot], ph);
         const uint32_t sbase = smem_w_u32 + slot * W_CHUNK_BYTES;
-        if (p.mode != 2) {
-          const uint32_t wrow = sbase + row * 128;
+        const int col_base = n0 + c * W_CHUNK_COLS;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint32_t a4 = wrow + ((j ^ (row & 7)) << 4);
-            float4 w = lds128(a4);
-            w.x = fmaf(p.alpha, __uint_as_float(r[4 * j + 0]), w.x);
-            w.y = fmaf(p.alpha, __uint_as_float(r[4 * j + 1]), w.y);
-            w.z = fmaf(p.alpha, __uint_as_float(r[4 * j + 2]), w.z);
-            w.w = fmaf(p.alpha, __uint_as_float(r[4 * j + 3]), w.w);
-            sts128(a4, w);
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int row = q * 32 + h * 16 + tr + 8 * k;     // row within this CTA's 128-row tile
+            const bool row_ok = m0 + row < p.M;
+            float* grow = p.W + (size_t)(m0 + row) * p.N;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int cl = 8 * j + 2 * t0;                 // column within the 32-column chunk
+              const uint32_t a8 = sbase + row * 128 + ((((cl >> 2) ^ (row & 7))) << 4) + ((cl & 3) << 2);
+              float2 w = lds64(a8);
+              if (p.mode != 2) {
+                w.x = fmaf(p.alpha, __uint_as_float(r[h][4 * j + 2 * k + 0]), w.x);
+                w.y = fmaf(p.alpha, __uint_as_float(r[h][4 * j + 2 * k + 1]), w.y);
+              }
+              if (p.mode != 3 && row_ok && col_base + cl < p.N) stg64_na(grow + col_base + cl, w);
+            }
           }
         }
-        named_bar_sync(1 + e, 128);
-        if (p.mode != 3) {
-          // coalesced write-back: 8 threads per 128-B row segment, 16 rows per pass
-          const int jj = t & 7;
-          const int col = n0 + c * W_CHUNK_COLS + jj * 4;
-          const bool col_ok = col < p.N;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int rr = i * 16 + (t >> 3);
-            const float4 v = lds128(sbase + rr * 128 + ((jj ^ (rr & 7)) << 4));
-            if (col_ok && m0 + rr < p.M)
-              stg128_na(p.W + (size_t)(m0 + rr) * p.N + col, v);
-          }
-        }
-        named_bar_sync(1 + e, 128);
-        if (t == 0) mbar_arrive(&wempty[slot]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&wempty[slot]);
       }
       tc_fence_before();
       __syncwarp();
