@@ -683,6 +683,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
 }
 
 // ------------------------------------------------------------- host side ----
+// Experiment knobs (tools/k1_sweep*.sh).  Read once; production runs never set them.
+//   POSEIDON_K1_VARIANT=1   single-CTA 128x256 kernel instead of the 2-SM kernel
+//   POSEIDON_K1_RASTER=m|n  force the tile raster;  POSEIDON_K1_CFG=a|b|c  stage/W-slot config
+//   POSEIDON_K1_EPI=1       one epilogue warpgroup;  POSEIDON_K1_WPOL=1  evict_normal W loads
+//   POSEIDON_K1_MODE=1|2|3  W streaming only / no update / loads only (no MMA in modes 1-3)
+struct K1Knobs {
+  int variant = 2, raster = -1, cfg = 1, epi = 2, wpol = 0, mode = 0;
+  K1Knobs() {
+    if (const char* v = getenv("POSEIDON_K1_VARIANT")) variant = (v[0] == '1') ? 1 : 2;
+    if (const char* r = getenv("POSEIDON_K1_RASTER")) raster = (r[0] == 'm') ? 1 : 0;
+    if (const char* c = getenv("POSEIDON_K1_CFG")) cfg = (c[0] == 'a') ? 0 : (c[0] == 'c') ? 2 : 1;
+    if (const char* e = getenv("POSEIDON_K1_EPI")) epi = (e[0] == '1') ? 1 : 2;
+    if (const char* w = getenv("POSEIDON_K1_WPOL")) wpol = w[0] - '0';
+    if (const char* m = getenv("POSEIDON_K1_MODE")) mode = m[0] - '0';
+  }
+};
+const K1Knobs& knobs() {
+  static const K1Knobs k;
+  return k;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -760,18 +781,14 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   // dimension whose operand is smaller, so the operand re-swept every wave stays L2-resident.
   const double operand_bytes = 4.0 * (double)P * (double)ldk * (double)(M + N);
   p.m_fast = (operand_bytes <= 48e6) ? 0 : ((M <= N) ? 1 : 0);
-  if (const char* r = getenv("POSEIDON_K1_RASTER")) p.m_fast = (r[0] == 'm');  // experiments only
+  if (knobs().raster >= 0) p.m_fast = knobs().raster;
   p.mode = 0;
   p.epi_groups = 2;
   p.w_policy = 0;
-  if (const char* eg = getenv("POSEIDON_K1_EPI")) p.epi_groups = eg[0] - '0';  // experiments only
-  if (const char* wp = getenv("POSEIDON_K1_WPOL")) p.w_policy = wp[0] - '0';   // experiments only
-  if (const char* md = getenv("POSEIDON_K1_MODE")) p.mode = md[0] - '0';         // experiments only
-  static int variant = -1;  // 2 = cta_group::2 (default), 1 = single-CTA tiles
-  if (variant < 0) {
-    const char* v = getenv("POSEIDON_K1_VARIANT");
-    variant = (v && v[0] == '1') ? 1 : 2;
-  }
+  p.epi_groups = knobs().epi;
+  p.w_policy = knobs().wpol;
+  p.mode = knobs().mode;
+  const int variant = knobs().variant;
   if (variant == 2 && dbg == nullptr) {
     // re-encode the operand maps with 128-row boxes for B (each CTA stages half of the 256-wide N tile)
     const uint32_t bB2[3] = {BK, (uint32_t)k2sm::BN_CTA, 1};
@@ -781,8 +798,7 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
     p.num_tiles = p.m_tiles * p.n_tiles;
     // Regime: with few factor rows per tile the kernel is bound by the W
     // read-modify-write, so more W chunks in flight beat deeper operand staging.
-    int cfg = 1;  // 0: <3,8>, 1: <4,5>, 2: <2,8>
-    if (const char* c = getenv("POSEIDON_K1_CFG")) cfg = (c[0] == 'a') ? 0 : (c[0] == 'c') ? 2 : 1;  // experiments
+    const int cfg = knobs().cfg;  // 0: <3,8>, 1: <4,5> (production), 2: <2,8>
     static bool attr_a = false, attr_b = false;
     const int pairs = std::min(p.num_tiles, sm_count_k1() / 2);
     cudaError_t e = cudaSuccess;
