@@ -71,6 +71,16 @@ def measured_peaks():
 
 
 TF32_OVER_BF16 = 1.1 / 2.25   # nominal dense ratio (B200_PROFILING.md table)
+METRIC = "images/sec (exposed sync ms/iter and % of roofline alongside)"
+
+
+def workload_config(args, cfg, world):
+    """The `config` object both arms print (identical for the driver's ratio)."""
+    return {"workload": f"{args.config} {cfg['name']} data-parallel training step with Poseidon sync "
+                        f"(SACP + DWBP), synthetic data",
+            "model": cfg["name"], "global_batch": world * cfg["batch"], "per_gpu_batch": cfg["batch"],
+            "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2 (C3: images 158 MB + weights 244 MB per step)"}
 
 
 class ClockSampler:
@@ -197,12 +207,13 @@ def run_reference(args):
     sec = statistics.median(times)
     value = P * cfg["batch"] / sec
     line = {
-        "impl": "reference", "metric": "images/sec (sync step of one iteration, fp64 CPU oracle)",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "images/s", "n_gpus": P, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} {cfg['name']} sync step", "global_batch": P * cfg["batch"],
-                   "per_gpu_batch": cfg["batch"], "parallelism": f"dp{P}"},
+        "config": workload_config(args, cfg, P),
+        "reference_note": "the fp64 CPU oracle's synchronous step (O4/O6) for one iteration, images/s = "
+                          "P * batch / oracle seconds; the CNN forward/backward is not part of the oracle",
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "oracle",
                          "sample": "per step: " + desc + " (SFB rows scaled by M/R)"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -443,19 +454,16 @@ def run_poseidon(args):
 
     if rank == 0:
         line = {
-            "metric": "images/sec (exposed sync ms/iter and % of roofline alongside)",
+            "metric": METRIC,
             "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "tf32" if args.recon == "tf32" else "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config} {cfg['name']} training step, Poseidon sync (SACP+DWBP)",
-                       "model": cfg["name"], "global_batch": world * K, "per_gpu_batch": K,
-                       "parallelism": f"dp{world}", "scheme": scheme, "dwbp": args.dwbp,
-                       "ps_path": ("nvls-fused" if sync.nvls_active else
-                                   ("nccl rs/k2/ag" if world > 1 else "k2 (P=1)")),
-                       "nvls_status": ctx.nvls_status(),
-                       "memory_format": args.memory_format,
-                       "l2": "inputs larger than L2 (images 158 MB + weights 244 MB per step for C3)",
-                       "lr": args.lr},
+            "config": workload_config(args, cfg, world),
+            "details": {"scheme": scheme, "dwbp": args.dwbp, "recon": args.recon, "lr": args.lr,
+                        "memory_format": args.memory_format,
+                        "ps_path": ("nvls-fused" if sync.nvls_active else
+                                    ("nccl rs/k2/ag" if world > 1 else "k2 (P=1)")),
+                        "nvls_status": ctx.nvls_status()},
             "exposed_sync_ms": exposed, "sync_total_ms": sync_total,
             "exposed_frac": (exposed / sync_total) if sync_total > 0 else None,
             "nccl_bytes_sent_per_iter": nccl_sent, "nccl_bytes_recv_per_iter": nccl_recv,
