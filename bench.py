@@ -78,7 +78,7 @@ def workload_config(args, cfg, world):
     """The `config` object both arms print (identical for the driver's ratio)."""
     return {"workload": f"{args.config} {cfg['name']} data-parallel training step with Poseidon sync "
                         f"(SACP + DWBP), synthetic data",
-            "model": cfg["name"], "global_batch": world * cfg["batch"], "per_gpu_batch": cfg["batch"],
+            "global_batch": world * cfg["batch"], "per_gpu_batch": cfg["batch"],
             "parallelism": f"dp{world}",
             "l2": "inputs larger than L2 (C3: images 158 MB + weights 244 MB per step)"}
 
