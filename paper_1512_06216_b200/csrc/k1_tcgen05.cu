@@ -670,7 +670,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&wempty[slot]);
+        // the slot's LDS results were consumed above (data dependence), so a relaxed arrive suffices
+        // and does not wait for this warp's W stores
+        if (lane == 0) mbar_arrive_relaxed(&wempty[slot]);
       }
       tc_fence_before();
       __syncwarp();
