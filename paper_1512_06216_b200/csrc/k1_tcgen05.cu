@@ -702,7 +702,7 @@ struct K1Knobs {
   K1Knobs() {
     if (const char* v = getenv("POSEIDON_K1_VARIANT")) variant = (v[0] == '1') ? 1 : 2;
     if (const char* r = getenv("POSEIDON_K1_RASTER")) raster = (r[0] == 'm') ? 1 : 0;
-    if (const char* c = getenv("POSEIDON_K1_CFG")) cfg = (c[0] == 'a') ? 0 : (c[0] == 'c') ? 2 : 1;
+    if (const char* c = getenv("POSEIDON_K1_CFG")) cfg = (c[0] == 'a') ? 0 : (c[0] == 'c') ? 2 : (c[0] == 'd') ? 3 : 1;
     if (const char* e = getenv("POSEIDON_K1_EPI")) epi = (e[0] == '1') ? 1 : 2;
     if (const char* w = getenv("POSEIDON_K1_WPOL")) wpol = w[0] - '0';
     if (const char* m = getenv("POSEIDON_K1_MODE")) mode = m[0] - '0';
@@ -819,6 +819,15 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
         attr_a = true;
       }
       recon_tcgen05_2sm_kernel<3, 8><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, p);
+    } else if (cfg == 3) {
+      constexpr int SM_ = k2sm::smem_bytes(5, 4);
+      static bool attr_d = false;
+      if (!attr_d) {
+        e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<5, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
+        if (e != cudaSuccess) return e;
+        attr_d = true;
+      }
+      recon_tcgen05_2sm_kernel<5, 4><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, p);
     } else if (cfg == 2) {
       constexpr int SM_ = k2sm::smem_bytes(2, 8);
       static bool attr_c = false;
