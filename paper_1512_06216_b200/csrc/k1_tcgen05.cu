@@ -698,7 +698,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
 //   POSEIDON_K1_MODE=1|2|3  W streaming only / no update / loads only (no MMA in modes 1-3)
 //   POSEIDON_K1_MODE=5|6    TMEM loads without MMA / MMA + accumulator handshake without TMEM loads
 struct K1Knobs {
-  int variant = 2, raster = -1, cfg = 1, epi = 2, wpol = 0, mode = 0;
+  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0;
   K1Knobs() {
     if (const char* v = getenv("POSEIDON_K1_VARIANT")) variant = (v[0] == '1') ? 1 : 2;
     if (const char* r = getenv("POSEIDON_K1_RASTER")) raster = (r[0] == 'm') ? 1 : 0;
@@ -807,7 +807,10 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
     p.num_tiles = p.m_tiles * p.n_tiles;
     // Regime: with few factor rows per tile the kernel is bound by the W
     // read-modify-write, so more W chunks in flight beat deeper operand staging.
-    const int cfg = knobs().cfg;  // 0: <3,8>, 1: <4,5> (production), 2: <2,8>
+    // Stage / W-slot split (tools/k1_sweep*.sh): with <= 8 factor slabs per tile the W stream
+    // dominates and <4 stages, 5 W slots> wins; with more slabs deeper operand staging <5, 4> wins
+    // (fc6 P*K=2048: 686 -> 743 TFLOP/s).  0: <3,8>, 1: <4,5>, 2: <2,8>, 3: <5,4>.
+    const int cfg = knobs().cfg >= 0 ? knobs().cfg : (p.num_kb <= 8 ? 1 : 3);
     static bool attr_a = false, attr_b = false;
     const int pairs = std::min(p.num_tiles, sm_count_k1() / 2);
     cudaError_t e = cudaSuccess;
