@@ -224,6 +224,7 @@ struct Params {
   int32_t mode;    // experiments only: 1 = W streaming alone (no MMA), 0 = production
   int32_t epi_groups;  // experiments only: 2 (production) or 1 epilogue warpgroups
   int32_t w_policy;    // experiments only: 0 = evict_first (production), 1 = evict_normal
+  int32_t release_arrive;  // experiments only: 1 = release-semantics epilogue arrives
   int32_t m_fast;  // raster: 1 -> consecutive tiles walk M (re-sweep the smaller operand Ug each wave)
   float alpha;
   float* dbg;  // debug dump (tile 0 of CTA 0): smem stage 0 of A|B, raw accumulator; NULL in production
@@ -460,6 +461,9 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cluster_release(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
   asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -672,11 +676,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
         __syncwarp();
         // the slot's LDS results were consumed above (data dependence), so a relaxed arrive suffices
         // and does not wait for this warp's W stores
-        if (lane == 0) mbar_arrive_relaxed(&wempty[slot]);
+        if (lane == 0) {
+          if (p.release_arrive) mbar_arrive(&wempty[slot]);
+          else mbar_arrive_relaxed(&wempty[slot]);
+        }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0 && (p.mode == 0 || p.mode == 6)) mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+      if (lane == 0 && (p.mode == 0 || p.mode == 6)) {
+        if (p.release_arrive) mbar_arrive_cluster_release(acc == 0 ? tempty_leader0 : tempty_leader1);
+        else mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+      }
     }
   }
 
@@ -698,7 +708,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
 //   POSEIDON_K1_MODE=1|2|3  W streaming only / no update / loads only (no MMA in modes 1-3)
 //   POSEIDON_K1_MODE=5|6    TMEM loads without MMA / MMA + accumulator handshake without TMEM loads
 struct K1Knobs {
-  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0;
+  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0, release = 0;
   K1Knobs() {
     if (const char* v = getenv("POSEIDON_K1_VARIANT")) variant = (v[0] == '1') ? 1 : 2;
     if (const char* r = getenv("POSEIDON_K1_RASTER")) raster = (r[0] == 'm') ? 1 : 0;
@@ -706,6 +716,7 @@ struct K1Knobs {
     if (const char* e = getenv("POSEIDON_K1_EPI")) epi = (e[0] == '1') ? 1 : 2;
     if (const char* w = getenv("POSEIDON_K1_WPOL")) wpol = w[0] - '0';
     if (const char* m = getenv("POSEIDON_K1_MODE")) mode = m[0] - '0';
+    if (const char* r = getenv("POSEIDON_K1_RELEASE")) release = r[0] - '0';
   }
 };
 const K1Knobs& knobs() {
@@ -797,6 +808,7 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   p.epi_groups = knobs().epi;
   p.w_policy = knobs().wpol;
   p.mode = knobs().mode;
+  p.release_arrive = knobs().release;
   const int variant = knobs().variant;
   if (variant == 2 && dbg == nullptr) {
     // re-encode the operand maps with 128-row boxes for B (each CTA stages half of the 256-wide N tile)
