@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -34,6 +35,22 @@ poseidon_status_t fail(poseidon_status_t code, const std::string& msg) {
 }
 poseidon_status_t cuda_fail(cudaError_t e, const char* what) {
   return fail(POSEIDON_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// POSEIDON_DEBUG_SYNC=1: synchronise the library stream after every kernel launch and report the
+// kernel that faulted (debugging aid for asynchronous launch failures; off in production).
+bool debug_sync_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("POSEIDON_DEBUG_SYNC");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+cudaError_t debug_sync(cudaStream_t s, const char* what) {
+  if (!debug_sync_enabled()) return cudaSuccess;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) fprintf(stderr, "[poseidon] %s faulted: %s\n", what, cudaGetErrorString(e));
+  return e;
 }
 
 }  // namespace poseidon
@@ -195,10 +212,12 @@ poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float*
   else
     err = launch_recon_simt(L.Ug, L.Vg, P, L.K, L.ldk, L.M, L.N, W, alpha, c->recon_stream);
   if (err != cudaSuccess) return cuda_fail(err, "reconstruct+sgd launch");
+  if ((err = debug_sync(c->recon_stream, "K1/K1r reconstruct+sgd")) != cudaSuccess) return cuda_fail(err, "K1");
   CU_TRY(cudaEventRecord(e.kend, c->recon_stream));  // kernel_ms = K1/K1r alone
   if (bias) {
     err = launch_bias_update(L.Bs, L.M, P, bias, L.M, alpha, c->recon_stream);
     if (err != cudaSuccess) return cuda_fail(err, "bias update launch");
+    if ((err = debug_sync(c->recon_stream, "bias update")) != cudaSuccess) return cuda_fail(err, "bias");
   }
   CU_TRY(cudaEventRecord(e.done, c->recon_stream));
   r.layers.push_back(id);
@@ -243,6 +262,7 @@ poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* 
   cudaError_t err = launch_ps_shard_update(grad + L.begin, W + L.begin, L.end - L.begin, alpha, nullptr,
                                            c->comm_stream);
   if (err != cudaSuccess) return cuda_fail(err, "ps shard update launch");
+  if ((err = debug_sync(c->comm_stream, "K2 ps shard update")) != cudaSuccess) return cuda_fail(err, "K2");
   CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
   if (P > 1) {
     NC_TRY(ncclAllGather(W + (size_t)c->rank * L.S, W, (size_t)L.S, ncclFloat32, c->comm, c->comm_stream));
@@ -282,6 +302,7 @@ poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t l
   if (err != cudaSuccess) return cuda_fail(err, "pack U launch");
   err = launch_pack_t(V, ldV, v_slot, L.ldk, L.K, L.N, round, nullptr, producer);
   if (err != cudaSuccess) return cuda_fail(err, "pack V launch");
+  if ((err = debug_sync(producer, "K3 pack")) != cudaSuccess) return cuda_fail(err, "K3");
   return POSEIDON_OK;
 }
 
