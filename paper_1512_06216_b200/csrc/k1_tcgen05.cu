@@ -299,6 +299,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
+      for (int i = 0; i < STAGES; ++i) {  // tail: all MMA-commit arrivals have landed
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread) =====================
@@ -332,6 +336,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         tc_commit(&tfull[acc]);
       }
+      for (int j = it; j < it + 2; ++j) mbar_wait(&tempty[j & 1], ((j >> 1) & 1) ^ 1);  // tail
     }
   } else if (warp == 2) {
     // ===================== W tile TMA producer =====================
@@ -558,6 +563,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
+      // Producer tail: the leader's MMA commits arrive on THIS CTA's empty barriers
+      // asynchronously (multicast); wait until every stage has been released so that no arrival
+      // is still in flight when the CTA exits (exiting first faults the launch intermittently).
+      for (int i = 0; i < NST; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == NST) { stage = 0; phase ^= 1; }
+      }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA, one thread) =====================
@@ -587,6 +599,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
         }
         tc_commit_2sm_mc(&tfull[acc], 0x3);
       }
+      // MMA tail: the epilogues of both CTAs (one of them remote) arrive on tempty after their
+      // last tiles; wait for those arrivals before this CTA can exit.
+      for (int j = it; j < it + 2; ++j) mbar_wait(&tempty[j & 1], ((j >> 1) & 1) ^ 1);
     }
   } else if (warp == 2) {
     // ===================== W tile TMA producer (both CTAs, own rows) =====================
