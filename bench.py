@@ -48,6 +48,7 @@ def parse():
                     help="driver CNN activation layout (cuDNN NHWC kernels avoid layout transposes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layer-stats", action="store_true", help="print per-layer stats to stderr")
+    ap.add_argument("--cudnn-benchmark", default="on", choices=["on", "off"])
     return ap.parse_args()
 
 
@@ -240,7 +241,7 @@ def run_poseidon(args):
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
-    torch.backends.cudnn.benchmark = True
+    torch.backends.cudnn.benchmark = args.cudnn_benchmark == "on"
     torch.backends.cudnn.allow_tf32 = True
     torch.backends.cuda.matmul.allow_tf32 = True
 
