@@ -513,7 +513,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* wfull = tempty + 2;
   uint64_t* wempty = wfull + NWS;
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(wempty + NWS);
+  uint64_t* tempty_local = wempty + NWS;   // [2]: this CTA's 8 epilogue warps -> relay thread
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty_local + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -521,7 +522,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 16); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2);        // one relay arrival per CTA
+      mbar_init(&tempty_local[i], 8);  // one arrival per local epilogue warp
+    }
     for (int i = 0; i < NWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -623,6 +628,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
         }
       }
     }
+  } else if (warp == 3) {
+    // ===================== accumulator-free relay =====================
+    // The 8 local epilogue warps arrive on tempty_local (CTA scope); this thread forwards ONE
+    // release.cluster arrival to the leader's tempty.  It issues no global stores, so the
+    // cluster-scope release does not make anybody wait for outstanding W stores.
+    if (lane == 0 && (p.mode == 0 || p.mode == 6)) {
+      const uint32_t tl0 = mapa_shared(smem_u32(&tempty[0]), 0);
+      const uint32_t tl1 = mapa_shared(smem_u32(&tempty[1]), 0);
+      int it = 0;
+      for (int tile = pair; tile < p.num_tiles; tile += npairs, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty_local[acc], (it >> 1) & 1);
+        mbar_arrive_cluster_release(acc == 0 ? tl0 : tl1);
+      }
+    }
   } else if (warp >= 4) {
     // ===================== epilogue: 2 groups x 4 warps =====================
     // Group e processes the chunks g with g % 2 == e (g = global chunk counter shared with the W
@@ -634,8 +654,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     const int e = (warp - 4) >> 2;
     const int q = (warp - 4) & 3;
     const int t0 = lane & 3, tr = lane >> 2;   // column pair / row within a 16-lane slab
-    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
-    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
     const uint32_t smem_w_u32 = smem_u32(smem_w);
     uint32_t g = 0;
     int it = 0;
@@ -691,17 +709,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
         __syncwarp();
         // the slot's LDS results were consumed above (data dependence), so a relaxed arrive suffices
         // and does not wait for this warp's W stores
-        if (lane == 0) {
-          if (p.release_arrive) mbar_arrive(&wempty[slot]);
-          else mbar_arrive_relaxed(&wempty[slot]);
-        }
+        if (lane == 0) mbar_arrive(&wempty[slot]);
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0 && (p.mode == 0 || p.mode == 6)) {
-        if (p.release_arrive) mbar_arrive_cluster_release(acc == 0 ? tempty_leader0 : tempty_leader1);
-        else mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
-      }
+      if (lane == 0 && (p.mode == 0 || p.mode == 6)) mbar_arrive(&tempty_local[acc]);
     }
   }
 
