@@ -224,7 +224,6 @@ struct Params {
   int32_t mode;    // experiments only: 1 = W streaming alone (no MMA), 0 = production
   int32_t epi_groups;  // experiments only: 2 (production) or 1 epilogue warpgroups
   int32_t w_policy;    // experiments only: 0 = evict_first (production), 1 = evict_normal
-  int32_t release_arrive;  // experiments only: 1 = release-semantics epilogue arrives
   int32_t m_fast;  // raster: 1 -> consecutive tiles walk M (re-sweep the smaller operand Ug each wave)
   float alpha;
   float* dbg;  // debug dump (tile 0 of CTA 0): smem stage 0 of A|B, raw accumulator; NULL in production
@@ -460,17 +459,10 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// Accumulator-free signal to the leader CTA.  Relaxed: it only orders the tcgen05.ld reads (via
-// tcgen05.fence::before_thread_sync), not this warp's global stores — a release at cluster scope
-// would make every warp wait for its outstanding W stores at the end of each tile.
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
+// Remote arrive on the leader CTA's barrier (release at cluster scope: only issued by the relay
+// thread, which has no outstanding global stores to drain).
 __device__ __forceinline__ void mbar_arrive_cluster_release(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void tma_load_3d_2sm(const CUtensorMap* map, uint32_t bar_cluster, void* dst, int32_t x,
                                                 int32_t y, int32_t z, uint64_t policy) {
@@ -735,7 +727,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
 //   POSEIDON_K1_MODE=1|2|3  W streaming only / no update / loads only (no MMA in modes 1-3)
 //   POSEIDON_K1_MODE=5|6    TMEM loads without MMA / MMA + accumulator handshake without TMEM loads
 struct K1Knobs {
-  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0, release = 0;
+  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0;
   K1Knobs() {
     if (const char* v = getenv("POSEIDON_K1_VARIANT")) variant = (v[0] == '1') ? 1 : 2;
     if (const char* r = getenv("POSEIDON_K1_RASTER")) raster = (r[0] == 'm') ? 1 : 0;
@@ -743,7 +735,6 @@ struct K1Knobs {
     if (const char* e = getenv("POSEIDON_K1_EPI")) epi = (e[0] == '1') ? 1 : 2;
     if (const char* w = getenv("POSEIDON_K1_WPOL")) wpol = w[0] - '0';
     if (const char* m = getenv("POSEIDON_K1_MODE")) mode = m[0] - '0';
-    if (const char* r = getenv("POSEIDON_K1_RELEASE")) release = r[0] - '0';
   }
 };
 const K1Knobs& knobs() {
@@ -835,7 +826,6 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   p.epi_groups = knobs().epi;
   p.w_policy = knobs().wpol;
   p.mode = knobs().mode;
-  p.release_arrive = knobs().release;
   const int variant = knobs().variant;
   if (variant == 2 && dbg == nullptr) {
     // re-encode the operand maps with 128-row boxes for B (each CTA stages half of the 256-wide N tile)
