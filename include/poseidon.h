@@ -152,6 +152,22 @@ poseidon_status_t poseidon_sync_ps(poseidon_ctx_t ctx, int32_t layer_id, float* 
  * POSEIDON_FLAG_DWBP_OFF). */
 poseidon_status_t poseidon_backprop_hook(poseidon_ctx_t ctx, int32_t layer_id, poseidon_stream_t stream);
 
+/* Hardware figures for the measured-cost model (GB/s, TFLOP/s, microseconds). */
+typedef struct {
+  double nvlink_gbps;           /* per-direction peer bandwidth, e.g. 770 (measured peer copy) */
+  double hbm_gbps;              /* e.g. 6543.7 (MEASURED_PEAKS.json) */
+  double tensor_tflops;         /* TF32 dense, e.g. 669.6 (sustained) */
+  double collective_latency_us; /* per collective launch + sync, e.g. 10 */
+} poseidon_hw_t;
+
+/* Measured-cost SACP variant, reported BESIDE the paper's rule, never used by it:
+ * predicted per-rank times of the SFB execution (pack + all-gather + K1) and of the PS execution
+ * (local dW GEMM + reduce-scatter + K2 + all-gather) from an alpha-beta NVLink model and the
+ * HBM / tensor rooflines; returns the faster scheme (non-FC -> PS) or a negative status.
+ * Pure host code.  t_sfb_us / t_ps_us may be NULL. */
+int32_t poseidon_choose_scheme_model(int32_t kind, int64_t M, int64_t N, int64_t K, int32_t P,
+                                     const poseidon_hw_t* hw, double* t_sfb_us, double* t_ps_us);
+
 /* ================================ helpers ================================= */
 
 /* ncclGetUniqueId into out[128] (call on rank 0 only). */

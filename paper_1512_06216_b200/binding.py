@@ -40,6 +40,11 @@ class Costs(ctypes.Structure):
     _fields_ = [("sfb", ctypes.c_uint64), ("sf_ps", ctypes.c_uint64), ("full_ps", ctypes.c_uint64)]
 
 
+class Hardware(ctypes.Structure):
+    _fields_ = [("nvlink_gbps", ctypes.c_double), ("hbm_gbps", ctypes.c_double),
+                ("tensor_tflops", ctypes.c_double), ("collective_latency_us", ctypes.c_double)]
+
+
 class Topology(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("nccl_id", ctypes.c_uint8 * 128), ("flags", ctypes.c_uint32)]
@@ -69,7 +74,7 @@ class LayerStats(ctypes.Structure):
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_1512_06216_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_1512_06216_b200/build.py` "
             "(there is no CPU fallback)")
     return ctypes.CDLL(LIB_PATH)
 
@@ -82,6 +87,8 @@ _P = ctypes.POINTER
 _SIGS = {
     "poseidon_init": (_i32, [_i32, _P(Topology), _P(_vp)]),
     "poseidon_choose_scheme": (_i32, [_i32, _i64, _i64, _i64, _i32, _P(Costs)]),
+    "poseidon_choose_scheme_model": (_i32, [_i32, _i64, _i64, _i64, _i32, _P(Hardware),
+                                            _P(ctypes.c_double), _P(ctypes.c_double)]),
     "poseidon_sync_fc_sfb": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _f, _vp]),
     "poseidon_sync_ps": (_i32, [_vp, _i32, _vp, _vp, _i64, _f, _vp]),
     "poseidon_backprop_hook": (_i32, [_vp, _i32, _vp]),
@@ -159,6 +166,19 @@ def choose_scheme(kind: int, M: int, N: int, K: int, P: int) -> Tuple[int, Tuple
     if r < 0:
         raise PoseidonError(r, last_error())
     return r, (c.sfb, c.sf_ps, c.full_ps)
+
+
+B200_HW = dict(nvlink_gbps=770.0, hbm_gbps=6543.7, tensor_tflops=669.6, collective_latency_us=10.0)
+
+
+def choose_scheme_model(kind: int, M: int, N: int, K: int, P: int, hw: Optional[dict] = None):
+    """Measured-cost model pick (scheme, t_sfb_us, t_ps_us); reported beside the paper's rule."""
+    h = Hardware(**(hw or B200_HW))
+    ts, tp = ctypes.c_double(), ctypes.c_double()
+    r = lib.poseidon_choose_scheme_model(kind, M, N, K, P, ctypes.byref(h), ctypes.byref(ts), ctypes.byref(tp))
+    if r < 0:
+        raise PoseidonError(r, last_error())
+    return r, ts.value, tp.value
 
 
 def shard_range(n: int, P: int, rank: int) -> Tuple[int, int, int]:

@@ -1,7 +1,8 @@
 """Build libposeidon.so in-tree with nvcc for sm_100a (no torch extension
 machinery: the product is a plain C-ABI shared library).
 
-    python -m paper_1512_06216_b200.build [--force]
+    python paper_1512_06216_b200/build.py [--force]
+(run it as a file, not with -m: importing the package loads the library it is about to rebuild)
 """
 from __future__ import annotations
 

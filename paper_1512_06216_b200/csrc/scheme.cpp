@@ -1,5 +1,6 @@
 // SACP cost rule (Alg. 3; costs P:L333 and P:L335) and the shard
 // map of a PS layer (reading Z11).  Pure host integer code: no context, no GPU.
+#include <algorithm>
 #include <limits>
 
 #include "internal.h"
@@ -54,4 +55,36 @@ extern "C" poseidon_status_t poseidon_shard_range(int64_t n, int32_t P, int32_t 
   if (end) *end = e;
   if (padded_n) *padded_n = S * P;
   return POSEIDON_OK;
+}
+
+// Measured-cost SACP variant: the paper's rule counts floats on Ethernet, where
+// reconstruction is "often negligible compared to communication".  On NVLink it is not, so
+// this alpha-beta + roofline model of the two B200 executions is reported BESIDE the paper's rule
+// (the rule stays the default and is bit-exact); see profiles/c5_crossover_r1.md for measurements.
+extern "C" int32_t poseidon_choose_scheme_model(int32_t kind, int64_t M, int64_t N, int64_t K, int32_t P,
+                                                const poseidon_hw_t* hw, double* t_sfb_us, double* t_ps_us) {
+  using namespace poseidon;
+  if (M < 0 || N < 0 || K < 0 || P < 1 || !hw || hw->nvlink_gbps <= 0 || hw->hbm_gbps <= 0 ||
+      hw->tensor_tflops <= 0) {
+    fail(POSEIDON_ERR_INVALID_ARG, "choose_scheme_model: bad arguments");
+    return POSEIDON_ERR_INVALID_ARG;
+  }
+  const double m = (double)M, n = (double)N, k = (double)K, p = (double)P;
+  const double nvl = hw->nvlink_gbps * 1e9, hbm = hw->hbm_gbps * 1e9, tc = hw->tensor_tflops * 1e12;
+  const double alpha = hw->collective_latency_us * 1e-6;
+  const double ldk = 4.0 * ((K + 3) / 4);
+  // SFB: pack (read + write both factors) + all-gather of everyone's factors + K1
+  const double t_pack = 8.0 * k * (m + n) / hbm;
+  const double t_ag = (P > 1) ? ((p - 1.0) * ldk * (m + n) * 4.0 / nvl + alpha) : 0.0;
+  const double t_k1 = std::max(2.0 * m * n * p * k / tc, (8.0 * m * n + 4.0 * p * ldk * (m + n)) / hbm);
+  const double t_sfb = t_pack + t_ag + t_k1;
+  // PS: local dW GEMM (which SFB skips) + reduce-scatter + K2 + all-gather
+  const double t_wgrad = std::max(2.0 * m * n * k / tc, (4.0 * k * (m + n) + 4.0 * m * n) / hbm);
+  const double t_rsag = (P > 1) ? (2.0 * (p - 1.0) / p * 4.0 * m * n / nvl + 2.0 * alpha) : 0.0;
+  const double t_k2 = 12.0 * m * n / p / hbm;
+  const double t_ps = t_wgrad + t_rsag + t_k2;
+  if (t_sfb_us) *t_sfb_us = t_sfb * 1e6;
+  if (t_ps_us) *t_ps_us = t_ps * 1e6;
+  if (kind != POSEIDON_LAYER_FC) return POSEIDON_SCHEME_PS;
+  return t_sfb <= t_ps ? POSEIDON_SCHEME_SFB : POSEIDON_SCHEME_PS;
 }

@@ -77,3 +77,22 @@ def test_struct_layouts_match_header():
     import ctypes
     assert ctypes.sizeof(B.Topology) == 4 * 3 + 128 + 4
     assert ctypes.sizeof(B.Costs) == 24
+
+
+def test_measured_cost_model_properties():
+    """The measured-cost model (reported beside the paper's rule) on the measured crossover points
+    of profiles/c5_crossover_r1.md, and basic properties."""
+    from paper_1512_06216_b200 import binding as Bn
+    # measured winners (sync + wgrad) at 4 GPUs: fc6 K=256 -> SFB, fc6 K=1024 -> PS, K=2048 -> PS
+    assert Bn.choose_scheme_model(1, 4096, 9216, 256, 4)[0] == pz.SCHEME_SFB
+    assert Bn.choose_scheme_model(1, 4096, 9216, 1024, 4)[0] == pz.SCHEME_PS
+    assert Bn.choose_scheme_model(1, 4096, 9216, 2048, 4)[0] == pz.SCHEME_PS
+    # C5 softmax layer at 4 GPUs, K=256: SFB (measured 0.52 ms vs PS 1.1 ms + wgrad)
+    assert Bn.choose_scheme_model(1, 21841, 4096, 256, 4)[0] == pz.SCHEME_SFB
+    # conv layers are always PS; times are positive and SFB time grows with K faster than PS time
+    assert Bn.choose_scheme_model(0, 96, 363, 256, 8)[0] == pz.SCHEME_PS
+    _, s1, p1 = Bn.choose_scheme_model(1, 4096, 4096, 128, 8)
+    _, s2, p2 = Bn.choose_scheme_model(1, 4096, 4096, 256, 8)
+    assert 0 < s1 < s2 and 0 < p1 <= p2 and (s2 - s1) > (p2 - p1)
+    with pytest.raises(pz.PoseidonError):
+        Bn.choose_scheme_model(1, 10, 10, 10, 0)
