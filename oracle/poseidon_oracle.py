@@ -326,3 +326,48 @@ def sync_step_rows(W_rows, b_rows, Us, Vs, lr, rows):
     W1 = np.asarray(W_rows, np.float64) - lr * (1.0 / P) * G
     b1 = None if b_rows is None else np.asarray(b_rows, np.float64) - lr * (1.0 / P) * gb
     return W1, b1
+
+
+# --------------------------------------------------------------------------
+# O4m — the synchronous step with Lambda = momentum + weight decay (Eq. 3 / Eq. 4
+# "Lambda(A^{t-1}) contains regularization and momentums"; Alg. 3 line 8
+# "A_i <- A_i + sum_j u v^T + Lambda(A_i)"; reading Z4b: applied once at the
+# aggregation point; Caffe's SGD solver semantics, decay on every parameter)
+# --------------------------------------------------------------------------
+def sync_step_momentum(W, b, VW, Vb, Us, Vs, lr: float, mu: float, wd: float):
+    """g = (1/P) sum_p G_p;  V' = mu V + lr (g + wd W);  W' = W - V'   (same for the bias).
+    Returns (W', b', VW', Vb')."""
+    P = len(Us)
+    W = np.asarray(W, np.float64)
+    G = np.zeros_like(W)
+    gb = np.zeros(W.shape[0], dtype=np.float64)
+    for p in range(P):
+        G += reconstruct(Us[p], Vs[p])
+        gb += np.asarray(Us[p], dtype=np.float64).sum(axis=0)
+    G /= P
+    gb /= P
+    VW1 = mu * np.asarray(VW, np.float64) + lr * (G + wd * W)
+    W1 = W - VW1
+    if b is None:
+        return W1, None, VW1, None
+    b = np.asarray(b, np.float64)
+    Vb1 = mu * np.asarray(Vb, np.float64) + lr * (gb + wd * b)
+    return W1, b - Vb1, VW1, Vb1
+
+
+def ps_step_flat_momentum(w, v, grads: Sequence[np.ndarray], lr: float, mu: float, wd: float):
+    """Parameter-server step with momentum/decay on a flat buffer: each shard owner keeps the
+    velocity of its own shard only.  Returns (w', v')."""
+    P = len(grads)
+    w = np.asarray(w, np.float64)
+    v = np.asarray(v, np.float64)
+    w1 = np.empty_like(w)
+    v1 = np.empty_like(v)
+    for r in range(P):
+        lo, hi, _ = shard_range(w.shape[0], P, r)
+        s = np.zeros(hi - lo)
+        for p in range(P):
+            s += np.asarray(grads[p], np.float64)[lo:hi]
+        v1[lo:hi] = mu * v[lo:hi] + lr * (s / P + wd * w[lo:hi])
+        w1[lo:hi] = w[lo:hi] - v1[lo:hi]
+    return w1, v1

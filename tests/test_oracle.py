@@ -324,3 +324,51 @@ def test_update_error_fp32_excuses_only_storage_rounding():
     assert O.update_error_fp32(W0, wrong, ref) > 0.99
     off_by_two_ulps = ref + 2 * np.spacing(np.float32(1.0))
     assert O.update_error_fp32(W0, off_by_two_ulps, ref) > 0
+
+
+# --------------------------------------------------------------- O4m ----
+def test_o4m_reduces_to_o4_without_momentum_and_decay():
+    W, b = S.fc_weights_randbias(12, 9)
+    Us, Vs = S.hidden_factors(12, 9, 4, 3)
+    z = np.zeros_like(W, dtype=np.float64)
+    W1, b1, VW, Vb = O.sync_step_momentum(W, b, z, np.zeros(12), Us, Vs, 0.1, 0.0, 0.0)
+    W4, b4 = O.sync_step(W, b, Us, Vs, 0.1)
+    assert np.max(np.abs(W1 - W4)) < 1e-14 and np.max(np.abs(b1 - b4)) < 1e-14
+    assert np.allclose(VW, W.astype(np.float64) - W4, rtol=0, atol=1e-14)
+
+
+def test_o4m_geometric_series_closed_form():
+    """Constant gradient, no decay: after t steps W_t = W_0 - lr g sum_{s=1..t} (1 - mu^s)/(1 - mu)."""
+    W, b = S.fc_weights_randbias(6, 5)
+    Us, Vs = S.hidden_factors(6, 5, 3, 2)
+    g = sum(O.reconstruct(u, v) for u, v in zip(Us, Vs)) / 2
+    lr, mu, T = 0.05, 0.9, 6
+    Wt, bt = W.astype(np.float64), b.astype(np.float64)
+    VW, Vb = np.zeros_like(Wt), np.zeros_like(bt)
+    for _ in range(T):
+        Wt, bt, VW, Vb = O.sync_step_momentum(Wt, bt, VW, Vb, Us, Vs, lr, mu, 0.0)
+    coeff = sum((1 - mu ** s) / (1 - mu) for s in range(1, T + 1))
+    assert np.max(np.abs(Wt - (W.astype(np.float64) - lr * g * coeff))) < 1e-12
+
+
+def test_o4m_pure_decay_closed_form():
+    """Zero gradient, mu = 0: one step is W (1 - lr wd)."""
+    W, b = S.fc_weights_randbias(5, 4)
+    Us = [np.zeros((2, 5), np.float32)]
+    Vs = [np.zeros((2, 4), np.float32)]
+    W1, b1, _, _ = O.sync_step_momentum(W, b, np.zeros((5, 4)), np.zeros(5), Us, Vs, 0.1, 0.0, 0.01)
+    assert np.allclose(W1, W.astype(np.float64) * (1 - 0.1 * 0.01), rtol=0, atol=1e-15)
+    assert np.allclose(b1, b.astype(np.float64) * (1 - 0.1 * 0.01), rtol=0, atol=1e-15)
+
+
+def test_o4m_ps_equals_definition():
+    M, N, K, P = 7, 5, 3, 3
+    W, b = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, P)
+    g = S.rng(3)
+    VW0, Vb0 = g.standard_normal((M, N)) * 1e-3, g.standard_normal(M) * 1e-3
+    W1, b1, VW1, Vb1 = O.sync_step_momentum(W, b, VW0, Vb0, Us, Vs, 0.2, 0.8, 0.05)
+    grads = [O.flatten_params(O.reconstruct(u, v), np.asarray(u, np.float64).sum(0)) for u, v in zip(Us, Vs)]
+    w1, v1 = O.ps_step_flat_momentum(O.flatten_params(W, b), O.flatten_params(VW0, Vb0), grads, 0.2, 0.8, 0.05)
+    assert np.max(np.abs(w1 - O.flatten_params(W1, b1))) < 1e-13
+    assert np.max(np.abs(v1 - O.flatten_params(VW1, Vb1))) < 1e-13
