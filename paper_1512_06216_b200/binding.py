@@ -99,6 +99,7 @@ _SIGS = {
     "poseidon_bind_ps_buffers": (_i32, [_vp, _i32, _vp, _vp, _i64, _u32]),
     "poseidon_bind_sfb_params": (_i32, [_vp, _i32, _vp, _vp]),
     "poseidon_set_lr": (_i32, [_vp, _f]),
+    "poseidon_set_momentum": (_i32, [_vp, _i32, _f, _f]),
     "poseidon_ps_arena": (_i32, [_vp, _P(_i32)]),
     "poseidon_ps_layer_buffers": (_i32, [_vp, _i32, _P(_vp), _P(_vp), _P(_i64)]),
     "poseidon_nvls_status": (ctypes.c_char_p, [_vp]),
@@ -257,6 +258,9 @@ class Context:
     def nvls_status(self) -> str:
         m = lib.poseidon_nvls_status(self.h)
         return m.decode() if m else ""
+
+    def set_momentum(self, mu, weight_decay=0.0, layer_id=-1):
+        _check(lib.poseidon_set_momentum(self.h, layer_id, float(mu), float(weight_decay)))
 
     def set_lr(self, lr):
         _check(lib.poseidon_set_lr(self.h, float(lr)))

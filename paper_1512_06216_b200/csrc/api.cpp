@@ -95,6 +95,10 @@ struct Layer {
   int64_t n = 0, S = 0, padded = 0, begin = 0, end = 0;
   uint32_t ps_flags = 0;
   bool in_arena = false;     // PS buffers live in the library's (symmetric) arena
+  // f4 momentum / weight decay (oracle O4m): velocity of W (SFB: M x N, replicated; PS: this
+  // rank's shard only) and of the bias (SFB)
+  float mu = 0.f, wd = 0.f;
+  float *vel = nullptr, *vel_b = nullptr;
   size_t arena_off = 0;      // byte offset of this layer in both arenas
   EvSet ev[RING];
   bool events_created = false;
@@ -207,15 +211,25 @@ poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float*
   CU_TRY(cudaEventRecord(e.kstart, c->recon_stream));
   const float alpha = -lr / (float)P;
   cudaError_t err;
-  if (L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(L.Ug, L.Vg, L.ldk, L.M, L.N, W))
-    err = launch_recon_tcgen05(L.Ug, L.Vg, P, L.K, L.ldk, L.M, L.N, W, alpha, c->recon_stream);
+  const bool mom = (L.vel != nullptr);
+  // plain SGD: W = fmaf(-lr/P, acc, W).  Momentum (f4): the velocity is the target,
+  // v_partial = fmaf(lr/P, acc, mu * v), then momentum_apply: v += lr*wd*w, w -= v.
+  float* target = mom ? L.vel : W;
+  const float a1 = mom ? (lr / (float)P) : alpha, b1 = mom ? L.mu : 1.0f;
+  if (L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(L.Ug, L.Vg, L.ldk, L.M, L.N, target))
+    err = launch_recon_tcgen05(L.Ug, L.Vg, P, L.K, L.ldk, L.M, L.N, target, a1, b1, c->recon_stream);
   else
-    err = launch_recon_simt(L.Ug, L.Vg, P, L.K, L.ldk, L.M, L.N, W, alpha, c->recon_stream);
+    err = launch_recon_simt(L.Ug, L.Vg, P, L.K, L.ldk, L.M, L.N, target, a1, b1, c->recon_stream);
   if (err != cudaSuccess) return cuda_fail(err, "reconstruct+sgd launch");
+  if (mom) {
+    err = launch_momentum_apply(W, L.vel, L.M * L.N, lr * L.wd, c->recon_stream);
+    if (err != cudaSuccess) return cuda_fail(err, "momentum apply launch");
+  }
   if ((err = debug_sync(c->recon_stream, "K1/K1r reconstruct+sgd")) != cudaSuccess) return cuda_fail(err, "K1");
   CU_TRY(cudaEventRecord(e.kend, c->recon_stream));  // kernel_ms = K1/K1r alone
   if (bias) {
-    err = launch_bias_update(L.Bs, L.M, P, bias, L.M, alpha, c->recon_stream);
+    err = mom ? launch_bias_momentum(L.Bs, L.M, P, bias, L.vel_b, L.M, lr, L.mu, L.wd, c->recon_stream)
+              : launch_bias_update(L.Bs, L.M, P, bias, L.M, alpha, c->recon_stream);
     if (err != cudaSuccess) return cuda_fail(err, "bias update launch");
     if ((err = debug_sync(c->recon_stream, "bias update")) != cudaSuccess) return cuda_fail(err, "bias");
   }
@@ -238,7 +252,7 @@ poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* 
     CU_TRY(cudaEventRecord(e.kstart, c->comm_stream));
     cudaError_t err = launch_ps_nvls(c->nvls, c->win_g, c->win_w, L.arena_off, L.arena_off, L.begin, L.end,
                                      L.padded, -lr / (float)P, (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0, 64,
-                                     L.S, c->comm_stream);
+                                     L.S, L.vel, 1.0f / (float)P, lr, L.mu, L.wd, c->comm_stream);
     if (err != cudaSuccess) return cuda_fail(err, "fused NVLS PS launch");
     CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
     CU_TRY(cudaEventRecord(e.done, c->comm_stream));
@@ -259,8 +273,10 @@ poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* 
   CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
   CU_TRY(cudaEventRecord(e.kstart, c->comm_stream));
   const float alpha = -lr / (float)P;
-  cudaError_t err = launch_ps_shard_update(grad + L.begin, W + L.begin, L.end - L.begin, alpha, nullptr,
-                                           c->comm_stream);
+  cudaError_t err = L.vel ? launch_ps_momentum(grad + L.begin, W + L.begin, L.vel, L.end - L.begin,
+                                                 1.0f / (float)P, lr, L.mu, L.wd, c->comm_stream)
+                          : launch_ps_shard_update(grad + L.begin, W + L.begin, L.end - L.begin, alpha, nullptr,
+                                                   c->comm_stream);
   if (err != cudaSuccess) return cuda_fail(err, "ps shard update launch");
   if ((err = debug_sync(c->comm_stream, "K2 ps shard update")) != cudaSuccess) return cuda_fail(err, "K2");
   CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
@@ -312,7 +328,9 @@ void free_layer(Layer& L) {
   if (L.Bs) cudaFree(L.Bs);
   if (L.stU) cudaFree(L.stU);
   if (L.stV) cudaFree(L.stV);
-  L.Ug = L.Vg = L.Bs = L.stU = L.stV = nullptr;
+  if (L.vel) cudaFree(L.vel);
+  if (L.vel_b) cudaFree(L.vel_b);
+  L.Ug = L.Vg = L.Bs = L.stU = L.stV = L.vel = L.vel_b = nullptr;
   if (L.events_created) {
     for (int i = 0; i < RING; ++i) {
       EvSet& e = L.ev[i];
@@ -608,6 +626,51 @@ const char* poseidon_nvls_status(poseidon_ctx_t c) {
   return c->nvls_error.empty() ? "arena not created" : c->nvls_error.c_str();
 }
 
+static poseidon_status_t set_momentum_one(poseidon_ctx_t c, Layer& L, float mu, float wd) {
+  L.mu = mu;
+  L.wd = wd;
+  if (mu == 0.f && wd == 0.f) {
+    if (L.vel) cudaFree(L.vel);
+    if (L.vel_b) cudaFree(L.vel_b);
+    L.vel = L.vel_b = nullptr;
+    return POSEIDON_OK;
+  }
+  if (L.vel) return POSEIDON_OK;  // keep the existing velocity
+  cudaSetDevice(c->device);
+  size_t count;
+  if (L.scheme == POSEIDON_SCHEME_SFB) {
+    count = (size_t)(L.M * L.N);
+    if (L.has_bias) {
+      CU_TRY(cudaMalloc(&L.vel_b, (size_t)L.M * 4));
+      CU_TRY(cudaMemset(L.vel_b, 0, (size_t)L.M * 4));
+    }
+  } else {
+    int64_t b, e, padded;
+    const int64_t n = L.M * L.N + (L.has_bias ? L.M : 0);
+    poseidon_shard_range(n, c->world, c->rank, &b, &e, &padded);
+    count = (size_t)(padded / c->world);  // this rank's shard only
+  }
+  CU_TRY(cudaMalloc(&L.vel, count * 4));
+  CU_TRY(cudaMemset(L.vel, 0, count * 4));
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_set_momentum(poseidon_ctx_t c, int32_t id, float mu, float weight_decay) {
+  poseidon_status_t st = check_ctx(c);
+  if (st) return st;
+  if (!(mu >= 0.f && mu < 1.f) || !(weight_decay >= 0.f))
+    return fail(POSEIDON_ERR_INVALID_ARG, "need 0 <= mu < 1 and weight_decay >= 0");
+  if (id == -1) {
+    for (auto& L : c->layers)
+      if (L.registered && (st = set_momentum_one(c, L, mu, weight_decay)) != POSEIDON_OK) return st;
+    return POSEIDON_OK;
+  }
+  Layer* L;
+  st = check_layer(c, id, &L);
+  if (st) return st;
+  return set_momentum_one(c, *L, mu, weight_decay);
+}
+
 poseidon_status_t poseidon_set_lr(poseidon_ctx_t c, float lr) {
   poseidon_status_t st = check_ctx(c);
   if (st) return st;
@@ -833,9 +896,9 @@ poseidon_status_t poseidon_sfb_simulated(const float* U_all, const float* V_all,
   const float alpha = -lr / (float)P;
   if (err == cudaSuccess) {
     if (round && recon_tcgen05_supported(Ug, Vg, ldk, M, N, W))
-      err = launch_recon_tcgen05(Ug, Vg, P, K, ldk, M, N, W, alpha, s);
+      err = launch_recon_tcgen05(Ug, Vg, P, K, ldk, M, N, W, alpha, 1.0f, s);
     else
-      err = launch_recon_simt(Ug, Vg, P, K, ldk, M, N, W, alpha, s);
+      err = launch_recon_simt(Ug, Vg, P, K, ldk, M, N, W, alpha, 1.0f, s);
   }
   if (err == cudaSuccess && bias) err = launch_bias_update(Bs, M, P, bias, M, alpha, s);
   cudaFreeAsync(Ug, s);
@@ -878,9 +941,9 @@ poseidon_status_t poseidon_reconstruct_sgd(const float* Ug, const float* Vg, int
   if (recon == POSEIDON_RECON_TF32) {
     if (!recon_tcgen05_supported(Ug, Vg, ldk, M, N, W))
       return fail(POSEIDON_ERR_ALIGNMENT, "tcgen05 path needs 16-B aligned buffers and ldk, N multiples of 4");
-    err = launch_recon_tcgen05(Ug, Vg, P, K, ldk, M, N, W, alpha, s);
+    err = launch_recon_tcgen05(Ug, Vg, P, K, ldk, M, N, W, alpha, 1.0f, s);
   } else if (recon == POSEIDON_RECON_FP32) {
-    err = launch_recon_simt(Ug, Vg, P, K, ldk, M, N, W, alpha, s);
+    err = launch_recon_simt(Ug, Vg, P, K, ldk, M, N, W, alpha, 1.0f, s);
   } else {
     return fail(POSEIDON_ERR_INVALID_ARG, "bad recon");
   }

@@ -35,18 +35,27 @@ cudaError_t launch_ps_sim_update(const float* g, int64_t ld, int32_t P, float* W
 // also writes colsum[c] = sum_k src[k][c] (fp32, fixed order, UNROUNDED values).
 cudaError_t launch_pack_t(const float* src, int64_t ld_src, float* dst, int64_t ldk, int64_t K, int64_t cols,
                           bool round_tf32, float* colsum, cudaStream_t s);
+// Momentum / weight decay (f4, oracle O4m):  v = mu v + lr (g + wd w);  w -= v.
+// PS shard: g = gsum * inv_p.   SFB: K1 already left v_partial = mu v + lr/P * acc in V, so
+// momentum_apply does v += lr*wd*w; w -= v.   Bias: g = inv_p * sum_p bs[p][m].
+cudaError_t launch_ps_momentum(const float* gsum, float* W, float* V, int64_t count, float inv_p, float lr,
+                               float mu, float wd, cudaStream_t s);
+cudaError_t launch_momentum_apply(float* W, float* V, int64_t count, float lr_wd, cudaStream_t s);
+cudaError_t launch_bias_momentum(const float* bs, int64_t ld, int32_t P, float* bias, float* vb, int64_t M,
+                                 float lr, float mu, float wd, cudaStream_t s);
 // bias[m] = fmaf(alpha, sum_p bs[p*ld + m], bias[m]) for m in [0, M), p in worker order.
 cudaError_t launch_bias_update(const float* bs, int64_t ld, int32_t P, float* bias, int64_t M, float alpha,
                                cudaStream_t s);
 
 // K1r: W[M x N] += alpha * sum_p sum_k Ug[p][m][k] Vg[p][n][k] on CUDA cores (fp32 FMA).
 cudaError_t launch_recon_simt(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
-                              int64_t N, float* W, float alpha, cudaStream_t s);
+                              int64_t N, float* W, float alpha, float beta, cudaStream_t s);
 
 // K1: the same on tcgen05 (TF32 operands, fp32 TMEM accumulators).  Returns cudaErrorNotSupported
 // when TMA cannot describe the buffers.  Tensor maps are encoded per call (host only, ~us).
+// Both compute W' = fmaf(alpha, acc, beta * W) (beta = 1: SGD; beta = mu: velocity update, f4).
 cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
-                                 int64_t N, float* W, float alpha, cudaStream_t s, float* dbg = nullptr);
+                                 int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg = nullptr);
 bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int64_t M, int64_t N, const float* W);
 
 }  // namespace poseidon

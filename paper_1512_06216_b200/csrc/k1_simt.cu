@@ -7,7 +7,8 @@
 //
 // The 1e-5 path (fp32 FMA, no TF32 rounding).  64 x 64 output tile per
 // 256-thread block, 4 x 4 outputs per thread, 16-k slabs of Ug/Vg staged in
-// shared memory (loads coalesced along k), fused epilogue W = fmaf(alpha, acc, W).
+// shared memory (loads coalesced along k), fused epilogue W = fmaf(alpha, acc, beta * W)
+// (beta = 1 for SGD; the momentum coefficient when the target is a velocity buffer).
 #include "internal.h"
 
 namespace poseidon {
@@ -18,7 +19,7 @@ constexpr int TM = 64, TN = 64, TK = 16;
 
 __global__ void __launch_bounds__(256) recon_simt_kernel(const float* __restrict__ Ug, const float* __restrict__ Vg,
                                                          int P, int64_t K, int64_t ldk, int64_t M, int64_t N,
-                                                         float* __restrict__ W, float alpha) {
+                                                         float* __restrict__ W, float alpha, float beta) {
   __shared__ float As[TK][TM + 1];
   __shared__ float Bs[TK][TN + 1];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(256) recon_simt_kernel(const float* __restrict
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t n = n0 + tx * 4 + j;
-      if (n < N) W[m * N + n] = fmaf(alpha, acc[i][j], W[m * N + n]);
+      if (n < N) W[m * N + n] = fmaf(alpha, acc[i][j], beta * W[m * N + n]);
     }
   }
 }
@@ -68,10 +69,10 @@ __global__ void __launch_bounds__(256) recon_simt_kernel(const float* __restrict
 }  // namespace
 
 cudaError_t launch_recon_simt(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
-                              int64_t N, float* W, float alpha, cudaStream_t s) {
+                              int64_t N, float* W, float alpha, float beta, cudaStream_t s) {
   if (M <= 0 || N <= 0 || K <= 0 || P <= 0) return cudaSuccess;
   const dim3 grid((unsigned)((N + TN - 1) / TN), (unsigned)((M + TM - 1) / TM));
-  recon_simt_kernel<<<grid, 256, 0, s>>>(Ug, Vg, P, K, ldk, M, N, W, alpha);
+  recon_simt_kernel<<<grid, 256, 0, s>>>(Ug, Vg, P, K, ldk, M, N, W, alpha, beta);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }

@@ -226,6 +226,7 @@ struct Params {
   int32_t w_policy;    // experiments only: 0 = evict_first (production), 1 = evict_normal
   int32_t m_fast;  // raster: 1 -> consecutive tiles walk M (re-sweep the smaller operand Ug each wave)
   float alpha;
+  float beta;   // W' = fmaf(alpha, acc, beta * W): 1 for SGD; mu when the target is a velocity (f4)
   float* dbg;  // debug dump (tile 0 of CTA 0): smem stage 0 of A|B, raw accumulator; NULL in production
 };
 
@@ -387,10 +388,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int j = 0; j < 8; ++j) {
           float4* p4 = reinterpret_cast<float4*>(wrow + ((j ^ (row & 7)) << 4));
           float4 w = *p4;
-          w.x = fmaf(p.alpha, __uint_as_float(r[4 * j + 0]), w.x);
-          w.y = fmaf(p.alpha, __uint_as_float(r[4 * j + 1]), w.y);
-          w.z = fmaf(p.alpha, __uint_as_float(r[4 * j + 2]), w.z);
-          w.w = fmaf(p.alpha, __uint_as_float(r[4 * j + 3]), w.w);
+          w.x = fmaf(p.alpha, __uint_as_float(r[4 * j + 0]), p.beta * w.x);
+          w.y = fmaf(p.alpha, __uint_as_float(r[4 * j + 1]), p.beta * w.y);
+          w.z = fmaf(p.alpha, __uint_as_float(r[4 * j + 2]), p.beta * w.z);
+          w.w = fmaf(p.alpha, __uint_as_float(r[4 * j + 3]), p.beta * w.w);
           *p4 = w;
         }
         fence_proxy_async_smem();
@@ -691,8 +692,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
               const uint32_t a8 = sbase + row * 128 + ((((cl >> 2) ^ (row & 7))) << 4) + ((cl & 3) << 2);
               float2 w = lds64(a8);
               if (p.mode != 2) {
-                w.x = fmaf(p.alpha, __uint_as_float(r[h][4 * j + 2 * k + 0]), w.x);
-                w.y = fmaf(p.alpha, __uint_as_float(r[h][4 * j + 2 * k + 1]), w.y);
+                w.x = fmaf(p.alpha, __uint_as_float(r[h][4 * j + 2 * k + 0]), p.beta * w.x);
+                w.y = fmaf(p.alpha, __uint_as_float(r[h][4 * j + 2 * k + 1]), p.beta * w.y);
               }
               if (p.mode != 3 && row_ok && col_base + cl < p.N) stg64_na(grow + col_base + cl, w);
             }
@@ -788,7 +789,7 @@ bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int6
 }
 
 cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
-                                 int64_t N, float* W, float alpha, cudaStream_t s, float* dbg) {
+                                 int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg) {
   if (M <= 0 || N <= 0 || K <= 0 || P <= 0) return cudaSuccess;
   if (!recon_tcgen05_supported(Ug, Vg, ldk, M, N, W) || ldk < K) return cudaErrorNotSupported;
   CUtensorMap tmA, tmB, tmW;
@@ -812,6 +813,7 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   p.kb_per_p = (int32_t)((K + BK - 1) / BK);  // k columns >= K of a block are zero (padding / TMA OOB)
   p.num_kb = p.kb_per_p * P;
   p.alpha = alpha;
+  p.beta = beta;
   p.dbg = dbg;
   p.W = W;
   // Raster (measured, tools/k1_sweep.sh): when both factor buffers fit comfortably in L2 the waves
@@ -899,7 +901,7 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
 // accumulator into dbg (STAGE_BYTES/4 + 128*256 floats).
 extern "C" int poseidon_debug_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk,
                                             int64_t M, int64_t N, float* W, float alpha, float* dbg) {
-  cudaError_t e = poseidon::launch_recon_tcgen05(Ug, Vg, P, K, ldk, M, N, W, alpha, 0, dbg);
+  cudaError_t e = poseidon::launch_recon_tcgen05(Ug, Vg, P, K, ldk, M, N, W, alpha, 1.0f, 0, dbg);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   return (int)e;
 }

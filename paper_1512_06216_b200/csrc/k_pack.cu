@@ -88,7 +88,28 @@ __global__ void __launch_bounds__(256) bias_update_kernel(const float* __restric
   bias[m] = fmaf(alpha, s, bias[m]);
 }
 
+__global__ void __launch_bounds__(256) bias_momentum_kernel(const float* __restrict__ bs, int64_t ld, int P,
+                                                            float* __restrict__ bias, float* __restrict__ vb,
+                                                            int64_t M, float lr, float mu, float wd) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  float s = 0.f;
+  for (int p = 0; p < P; ++p) s += bs[(int64_t)p * ld + m];
+  const float b = bias[m];
+  const float v = fmaf(mu, vb[m], lr * fmaf(wd, b, s * (1.0f / (float)P)));
+  vb[m] = v;
+  bias[m] = b - v;
+}
+
 }  // namespace
+
+cudaError_t launch_bias_momentum(const float* bs, int64_t ld, int32_t P, float* bias, float* vb, int64_t M,
+                                 float lr, float mu, float wd, cudaStream_t s) {
+  if (M <= 0 || bias == nullptr) return cudaSuccess;
+  bias_momentum_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(bs, ld, P, bias, vb, M, lr, mu, wd);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_pack_t(const float* src, int64_t ld_src, float* dst, int64_t ldk, int64_t K, int64_t cols,
                           bool round_tf32, float* colsum, cudaStream_t s) {

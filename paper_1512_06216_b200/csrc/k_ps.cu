@@ -121,6 +121,30 @@ __global__ void __launch_bounds__(256) ps_sim_kernel(const float* __restrict__ g
   }
 }
 
+// f4: v = mu v + lr (g * inv_p + wd w); w -= v   (float4 where aligned, fp32 FMA chain of O4m)
+__global__ void __launch_bounds__(256) ps_momentum_kernel(const float* __restrict__ g, float* __restrict__ W,
+                                                          float* __restrict__ V, int64_t count, float inv_p,
+                                                          float lr, float mu, float wd) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float w = W[i];
+    const float v = fmaf(mu, V[i], lr * fmaf(wd, w, g[i] * inv_p));
+    V[i] = v;
+    W[i] = w - v;
+  }
+}
+
+__global__ void __launch_bounds__(256) momentum_apply_kernel(float* __restrict__ W, float* __restrict__ V,
+                                                             int64_t count, float lr_wd) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float w = W[i];
+    const float v = fmaf(lr_wd, w, V[i]);
+    V[i] = v;
+    W[i] = w - v;
+  }
+}
+
 int grid_for(int64_t work_items, int threads) {
   const int64_t blocks = (work_items + threads - 1) / threads;
   const int64_t cap = (int64_t)sm_count() * 8;  // 8 x 256 threads resident per SM
@@ -145,6 +169,21 @@ cudaError_t launch_ps_shard_update(const float* g, float* W, int64_t count, floa
     else
       ps_shard_sgd_kernel<false><<<grid, threads, 0, s>>>(g, W, count, alpha, nullptr);
   }
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ps_momentum(const float* gsum, float* W, float* V, int64_t count, float inv_p, float lr,
+                               float mu, float wd, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  ps_momentum_kernel<<<grid_for(count, 256), 256, 0, s>>>(gsum, W, V, count, inv_p, lr, mu, wd);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_momentum_apply(float* W, float* V, int64_t count, float lr_wd, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  momentum_apply_kernel<<<grid_for(count, 256), 256, 0, s>>>(W, V, count, lr_wd);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }

@@ -50,9 +50,22 @@ __device__ __forceinline__ void mm_st(float* mc, float v) {
   asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "f"(v) : "memory");
 }
 
+struct NvlsMomentum {
+  float* v;     // velocity of this rank's shard (index k - b), NULL -> plain SGD
+  float inv_p, lr, mu, wd;
+};
+
+__device__ __forceinline__ float nvls_update(float w, float g, float alpha, const NvlsMomentum& m, int64_t j) {
+  if (m.v == nullptr) return fmaf(alpha, g, w);
+  const float v = fmaf(m.mu, m.v[j], m.lr * fmaf(m.wd, w, g * m.inv_p));
+  m.v[j] = v;
+  return w - v;
+}
+
 __global__ void __launch_bounds__(256) ps_nvls_kernel(const __grid_constant__ ncclDevComm comm, ncclWindow_t wg,
                                                       ncclWindow_t ww, size_t off_g, size_t off_w, int64_t b,
-                                                      int64_t e, int64_t padded, float alpha, int zero_grad) {
+                                                      int64_t e, int64_t padded, float alpha, int zero_grad,
+                                                      NvlsMomentum mom) {
   ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamTagLsa(), blockIdx.x, /*multimem=*/true);
   bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
 
@@ -65,15 +78,16 @@ __global__ void __launch_bounds__(256) ps_nvls_kernel(const __grid_constant__ nc
     const int64_t k = b + 4 * i;
     const float4 g = mm_ld_reduce_v4(gmc + k);
     float4 w = *reinterpret_cast<const float4*>(wloc + k);
-    w.x = fmaf(alpha, g.x, w.x);
-    w.y = fmaf(alpha, g.y, w.y);
-    w.z = fmaf(alpha, g.z, w.z);
-    w.w = fmaf(alpha, g.w, w.w);
+    const int64_t j = k - b;
+    w.x = nvls_update(w.x, g.x, alpha, mom, j + 0);
+    w.y = nvls_update(w.y, g.y, alpha, mom, j + 1);
+    w.z = nvls_update(w.z, g.z, alpha, mom, j + 2);
+    w.w = nvls_update(w.w, g.w, alpha, mom, j + 3);
     mm_st_v4(wmc + k, w);
   }
   if (blockIdx.x == 0 && threadIdx.x < ((e - b) & 3)) {
     const int64_t k = b + 4 * n4 + threadIdx.x;
-    mm_st(wmc + k, fmaf(alpha, mm_ld_reduce(gmc + k), wloc[k]));
+    mm_st(wmc + k, nvls_update(wloc[k], mm_ld_reduce(gmc + k), alpha, mom, k - b));
   }
 
   bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
@@ -93,7 +107,7 @@ struct NvlsState {
 
 cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww, size_t off_g, size_t off_w,
                            int64_t b, int64_t e, int64_t padded, float alpha, bool zero_grad, int max_blocks,
-                           int64_t shard, cudaStream_t s) {
+                           int64_t shard, float* vel, float inv_p, float lr, float mu, float wd, cudaStream_t s) {
   // The grid must be identical on every rank (block j of every rank meets at LSA barrier j), so it
   // is sized from the shard size S, not from this rank's (possibly shorter or empty) range.
   (void)e;
@@ -101,7 +115,8 @@ cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww
   int blocks = (int)((n4 + 255) / 256);
   if (blocks < 1) blocks = 1;
   if (blocks > max_blocks) blocks = max_blocks;
-  ps_nvls_kernel<<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, padded, alpha, zero_grad ? 1 : 0);
+  NvlsMomentum mom{vel, inv_p, lr, mu, wd};
+  ps_nvls_kernel<<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, padded, alpha, zero_grad ? 1 : 0, mom);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }

@@ -183,6 +183,50 @@ def main():
         assert float(gv.abs().sum()) == 0.0, "grad not zeroed"
     cn.close()
 
+    # ---- 3c. momentum + weight decay (f4) on SFB, NCCL PS and fused NVLS PS, two steps ----
+    for nv in (False, True):
+        cm = new_ctx(pz.FLAG_NVLS_PS if nv else 0)
+        M_, N_, K_, lr_m, mu_m, wd_m = 96, 130, 8, 0.2, 0.9, 1e-2
+        cm.register_layer(0, pz.LAYER_FC, M_, N_, K_)                         # SFB
+        cm.register_layer(1, pz.LAYER_FC, M_, N_, K_, True, pz.SCHEME_PS)     # PS
+        cm.set_lr(lr_m)
+        cm.set_momentum(mu_m, wd_m)
+        n = M_ * N_ + M_
+        if nv:
+            cm.ps_arena()
+            from paper_1512_06216_b200.binding import device_view
+            gp, wp, padded = cm.ps_layer_buffers(1)
+            gflat, wflat = device_view(gp, (padded,)), device_view(wp, (padded,))
+        else:
+            _, _, padded = pz.shard_range(n, P, rank)
+            gflat, wflat = torch.zeros(padded, device=dev), torch.zeros(padded, device=dev)
+            cm.bind_ps_buffers(1, gflat, wflat, n, pz.PS_ZERO_GRAD)
+        W, b = S.fc_weights_randbias(M_, N_)
+        Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+        wflat[:n].copy_(torch.from_numpy(O.flatten_params(W, b).astype(np.float32)).to(dev))
+        Wr, br = W.astype(np.float64), b.astype(np.float64)
+        VW, Vb = np.zeros_like(Wr), np.zeros_like(br)
+        wr, vr = O.flatten_params(W, b), np.zeros(n)
+        for t in range(2):
+            Us, Vs = S.hidden_factors(M_, N_, K_, P, seed=300 + 10 * t)
+            cm.sync_fc_sfb(0, torch.from_numpy(Us[rank]).to(dev), torch.from_numpy(Vs[rank]).to(dev), Wd, bd, lr_m)
+            grads = [O.flatten_params(O.reconstruct(Us[p], Vs[p]), Us[p].astype(np.float64).sum(0)).astype(np.float32)
+                     for p in range(P)]
+            gflat[:n].copy_(torch.from_numpy(grads[rank]).to(dev))
+            cm.backprop_hook(1)
+            cm.wait_layer(0)
+            cm.wait_layer(1)
+            cm.iteration_end()
+            torch.cuda.synchronize()
+            Wr, br, VW, Vb = O.sync_step_momentum(Wr, br, VW, Vb, Us, Vs, lr_m, mu_m, wd_m)
+            wr, vr = O.ps_step_flat_momentum(wr, vr, grads, lr_m, mu_m, wd_m)
+        assert O.update_error_fp32(W, Wd.cpu().numpy(), Wr) <= 2e-3, "SFB momentum"
+        assert O.update_error_fp32(b, bd.cpu().numpy(), br) <= 1e-5, "SFB bias momentum"
+        assert O.update_error_fp32(O.flatten_params(W, b), wflat[:n].cpu().numpy(), wr) <= 1e-5, \
+            f"PS momentum (nvls {nv})"
+        assert allsame(Wd) and allsame(wflat[:n].clone())
+        cm.close()
+
     # ---- 4. DWBP training steps of CIFAR-10 quick ----
     Kc = 16
     results = {}
