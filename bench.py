@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--nvls", default="auto", choices=["auto", "on", "off"],
                     help="fused one-kernel NVLink-SHARP PS sync (f1); auto = on when N > 1")
     ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--momentum", type=float, default=0.0, help="f4: Lambda momentum (0 = plain SGD hot path)")
+    ap.add_argument("--weight-decay", type=float, default=0.0, help="f4: Lambda weight decay")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--memory-format", default="channels_last", choices=["channels_last", "nchw"],
                     help="driver CNN activation layout (cuDNN NHWC kernels avoid layout transposes)")
@@ -267,6 +269,8 @@ def run_poseidon(args):
     if args.memory_format == "channels_last":
         model.to(memory_format=torch.channels_last)   # before PoseidonSync makes params buffer views
     sync = PoseidonSync(model, ctx, K=K, lr=args.lr, scheme=scheme, recon=recon, arena=use_nvls)
+    if args.momentum or args.weight_decay:
+        ctx.set_momentum(args.momentum, args.weight_decay)
 
     g = torch.Generator(device=dev)
     g.manual_seed(1512 + rank)
@@ -461,6 +465,7 @@ def run_poseidon(args):
             "dtype": "tf32" if args.recon == "tf32" else "f32", "data": "synthetic",
             "config": workload_config(args, cfg, world),
             "details": {"scheme": scheme, "dwbp": args.dwbp, "recon": args.recon, "lr": args.lr,
+                        "momentum": args.momentum, "weight_decay": args.weight_decay,
                         "memory_format": args.memory_format,
                         "ps_path": ("nvls-fused" if sync.nvls_active else
                                     ("nccl rs/k2/ag" if world > 1 else "k2 (P=1)")),
