@@ -60,6 +60,7 @@ using namespace poseidon;
 namespace {
 
 constexpr int RING = 8;           // iterations of events kept for statistics
+constexpr int kNvlsBlocks = 128;  // max grid of the fused NVLS PS kernel = LSA barriers requested
 constexpr int MAX_LAYERS = 4096;
 
 #define CU_TRY(expr)                                      \
@@ -251,7 +252,7 @@ poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* 
     CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
     CU_TRY(cudaEventRecord(e.kstart, c->comm_stream));
     cudaError_t err = launch_ps_nvls(c->nvls, c->win_g, c->win_w, L.arena_off, L.arena_off, L.begin, L.end,
-                                     L.padded, -lr / (float)P, (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0, 64,
+                                     L.padded, -lr / (float)P, (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0, kNvlsBlocks,
                                      L.S, L.vel, 1.0f / (float)P, lr, L.mu, L.wd, c->comm_stream);
     if (err != cudaSuccess) return cuda_fail(err, "fused NVLS PS launch");
     CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
@@ -575,7 +576,7 @@ poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
     ncclResult_t r3 = (r2 == ncclSuccess) ? ncclCommWindowRegister(c->comm, g, total, &c->win_g, NCCL_WIN_COLL_SYMMETRIC) : r2;
     ncclResult_t r4 = (r3 == ncclSuccess) ? ncclCommWindowRegister(c->comm, w, total, &c->win_w, NCCL_WIN_COLL_SYMMETRIC) : r3;
     if (r4 == ncclSuccess) {
-      c->nvls = nvls_create(c->comm, 64, &c->nvls_error);
+      c->nvls = nvls_create(c->comm, kNvlsBlocks, &c->nvls_error);
       symmetric = true;
       c->arena_nccl_mem = true;
       c->arena_g = static_cast<float*>(g);

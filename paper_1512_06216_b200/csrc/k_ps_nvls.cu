@@ -74,16 +74,31 @@ __global__ void __launch_bounds__(256) ps_nvls_kernel(const __grid_constant__ nc
   const float* wloc = static_cast<const float*>(ncclGetLocalPointer(ww, off_w));
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t n4 = (e - b) >> 2;  // b is 32-element aligned (shard map), so b + 4i is 16-B aligned
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
-    const int64_t k = b + 4 * i;
-    const float4 g = mm_ld_reduce_v4(gmc + k);
-    float4 w = *reinterpret_cast<const float4*>(wloc + k);
-    const int64_t j = k - b;
-    w.x = nvls_update(w.x, g.x, alpha, mom, j + 0);
-    w.y = nvls_update(w.y, g.y, alpha, mom, j + 1);
-    w.z = nvls_update(w.z, g.z, alpha, mom, j + 2);
-    w.w = nvls_update(w.w, g.w, alpha, mom, j + 3);
-    mm_st_v4(wmc + k, w);
+  // 4 independent switch reductions in flight per thread (each is a round trip through the NVSwitch)
+  constexpr int U = 4;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+    float4 g[U], w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n4) {
+        g[u] = mm_ld_reduce_v4(gmc + b + 4 * i);
+        w[u] = *reinterpret_cast<const float4*>(wloc + b + 4 * i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n4) {
+        const int64_t j = 4 * i;
+        float4 v = w[u];
+        v.x = nvls_update(v.x, g[u].x, alpha, mom, j + 0);
+        v.y = nvls_update(v.y, g[u].y, alpha, mom, j + 1);
+        v.z = nvls_update(v.z, g[u].z, alpha, mom, j + 2);
+        v.w = nvls_update(v.w, g[u].w, alpha, mom, j + 3);
+        mm_st_v4(wmc + b + j, v);
+      }
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x < ((e - b) & 3)) {
     const int64_t k = b + 4 * n4 + threadIdx.x;
