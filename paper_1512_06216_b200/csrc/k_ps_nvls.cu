@@ -19,6 +19,7 @@
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -62,6 +63,7 @@ __device__ __forceinline__ float nvls_update(float w, float g, float alpha, cons
   return w - v;
 }
 
+template <int U>
 __global__ void __launch_bounds__(256) ps_nvls_kernel(const __grid_constant__ ncclDevComm comm, ncclWindow_t wg,
                                                       ncclWindow_t ww, size_t off_g, size_t off_w, int64_t b,
                                                       int64_t e, int64_t padded, float alpha, int zero_grad,
@@ -74,8 +76,7 @@ __global__ void __launch_bounds__(256) ps_nvls_kernel(const __grid_constant__ nc
   const float* wloc = static_cast<const float*>(ncclGetLocalPointer(ww, off_w));
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t n4 = (e - b) >> 2;  // b is 32-element aligned (shard map), so b + 4i is 16-B aligned
-  // 4 independent switch reductions in flight per thread (each is a round trip through the NVSwitch)
-  constexpr int U = 4;
+  // U independent switch reductions in flight per thread (each is a round trip through the NVSwitch)
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
     float4 g[U], w[U];
 #pragma unroll
@@ -127,11 +128,25 @@ cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww
   // is sized from the shard size S, not from this rank's (possibly shorter or empty) range.
   (void)e;
   const int64_t n4 = (shard + 3) / 4;
+  static const int env_grid = [] {
+    const char* v = getenv("POSEIDON_NVLS_GRID");
+    return v ? atoi(v) : 0;
+  }();
+  static const int env_u = [] {
+    const char* v = getenv("POSEIDON_NVLS_U");
+    return v ? atoi(v) : 4;
+  }();
+  if (env_grid > 0 && env_grid < max_blocks) max_blocks = env_grid;
   int blocks = (int)((n4 + 255) / 256);
   if (blocks < 1) blocks = 1;
   if (blocks > max_blocks) blocks = max_blocks;
   NvlsMomentum mom{vel, inv_p, lr, mu, wd};
-  ps_nvls_kernel<<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, padded, alpha, zero_grad ? 1 : 0, mom);
+  if (env_u == 8)
+    ps_nvls_kernel<8><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, padded, alpha, zero_grad ? 1 : 0, mom);
+  else if (env_u == 2)
+    ps_nvls_kernel<2><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, padded, alpha, zero_grad ? 1 : 0, mom);
+  else
+    ps_nvls_kernel<4><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, padded, alpha, zero_grad ? 1 : 0, mom);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }

@@ -1,6 +1,6 @@
 """Collective bus bandwidth on NVLink 5 (nccl-tests conventions: busbw = algbw * (P-1)/P).
 
-    torchrun --nproc-per-node P tools/collective_bench.py
+    torchrun --nproc-per-node P tools/collective_bench.py [--ps-only]
 
 (a) raw NCCL all-gather / reduce-scatter through torch.distributed (the same libnccl.so.2 the
     library links), message sizes per rank 1 MB .. 512 MB;
@@ -47,7 +47,8 @@ def main():
         if rank == 0:
             print(json.dumps(d), flush=True)
 
-    for mb in (1, 4, 16, 64, 256, 512):
+    only_ps = "--ps-only" in sys.argv
+    for mb in (() if only_ps else (1, 4, 16, 64, 256, 512)):
         n = mb * (1 << 20) // 4
         x = torch.randn(n, device=dev)
         y = torch.empty(n * P, device=dev)
@@ -68,7 +69,8 @@ def main():
 
     # (b1) SFB factor all-gather inside poseidon_sync_fc_sfb
     ctx = new_ctx(0)
-    for lid, (name, M, N) in enumerate((("fc6", 4096, 9216), ("fc7", 4096, 4096), ("i22k_fc8", 21841, 4096))):
+    sfb_layers = () if only_ps else (("fc6", 4096, 9216), ("fc7", 4096, 4096), ("i22k_fc8", 21841, 4096))
+    for lid, (name, M, N) in enumerate(sfb_layers):
         K = 256
         ctx.register_layer(lid, pz.LAYER_FC, M, N, K)
         U = torch.randn(K, M, device=dev) / K
@@ -95,7 +97,7 @@ def main():
     # (b2) PS of a 37.7M-parameter layer: NCCL path vs fused NVLS kernel
     M, N = 4096, 9216
     n = M * N
-    for nv in (False, True):
+    for nv in ((True,) if only_ps else (False, True)):
         c = new_ctx(pz.FLAG_NVLS_PS if nv else 0)
         c.register_layer(0, pz.LAYER_FC, M, N, 256, False, pz.SCHEME_PS)
         if nv:
@@ -125,7 +127,8 @@ def main():
         bus = 2.0 * (P - 1) / P * 4.0 * padded / (t / 1e3) / 1e9
         out({"what": "poseidon PS sync 37.7M params (" + ("fused NVLS kernel" if active else "NCCL RS + K2 + AG") + ")",
              "P": P, "MB": round(4 * n / 2**20, 1), "ms": round(t, 4), "busbw_GBps(RS+AG equiv)": round(bus, 1),
-             "nvls": c.nvls_status()})
+             "nvls": c.nvls_status(), "grid": os.environ.get("POSEIDON_NVLS_GRID", "auto"),
+             "U": os.environ.get("POSEIDON_NVLS_U", "4")})
         c.close()
     dist.destroy_process_group()
 
