@@ -78,6 +78,10 @@ constexpr int MAX_LAYERS = 4096;
 struct EvSet {
   cudaEvent_t ready = nullptr, start = nullptr, gathered = nullptr, kstart = nullptr, kend = nullptr,
               done = nullptr;
+  // The events the statistics read for "collective done", "kernel start" and "kernel end".  An event
+  // record costs ~1 us of stream time, so a sync records only the events whose time differs from
+  // one already recorded (e.g. the fused NVLS kernel: ready, start, done) and aliases the rest.
+  cudaEvent_t g_eff = nullptr, ks_eff = nullptr, ke_eff = nullptr;
 };
 
 struct Layer {
@@ -196,6 +200,7 @@ poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float*
   CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
   IterRecord& r = open_record(c);
+  e.g_eff = e.start;
   if (P > 1) {
     const size_t ucount = (size_t)(L.M * L.ldk), vcount = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
     NC_TRY(ncclGroupStart());
@@ -206,10 +211,13 @@ poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float*
     const uint64_t per = (uint64_t)(ucount + vcount + bcount) * 4u;
     r.sent += per;  // handed to NCCL once; NCCL forwards it to P-1 peers
     r.recv += per * (uint64_t)(P - 1);
+    CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+    e.g_eff = e.gathered;
   }
-  CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
-  CU_TRY(cudaStreamWaitEvent(c->recon_stream, e.gathered, 0));
+  CU_TRY(cudaStreamWaitEvent(c->recon_stream, e.g_eff, 0));
   CU_TRY(cudaEventRecord(e.kstart, c->recon_stream));
+  e.ks_eff = e.kstart;
+  e.ke_eff = e.kend;
   const float alpha = -lr / (float)P;
   cudaError_t err;
   const bool mom = (L.vel != nullptr);
@@ -249,13 +257,12 @@ poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* 
   IterRecord& r = open_record(c);
   if (P > 1 && c->nvls && L.in_arena) {
     // fused one-kernel PS over NVLink SHARP (reduce-scatter + K2 + all-gather + zero-grad)
-    CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
-    CU_TRY(cudaEventRecord(e.kstart, c->comm_stream));
+    e.g_eff = e.ks_eff = e.start;
+    e.ke_eff = e.done;
     cudaError_t err = launch_ps_nvls(c->nvls, c->win_g, c->win_w, L.arena_off, L.arena_off, L.begin, L.end,
                                      L.padded, -lr / (float)P, (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0, kNvlsBlocks,
                                      L.S, L.vel, 1.0f / (float)P, lr, L.mu, L.wd, c->comm_stream);
     if (err != cudaSuccess) return cuda_fail(err, "fused NVLS PS launch");
-    CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
     CU_TRY(cudaEventRecord(e.done, c->comm_stream));
     // bytes through NVLink per rank: the switch reads this rank's gradient for the other P-1
     // shards and writes the other ranks' updated shards here; this rank reads its reduced shard
@@ -265,28 +272,46 @@ poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* 
     r.layers.push_back(id);
     return POSEIDON_OK;
   }
+  e.g_eff = e.ks_eff = e.start;
   if (P > 1) {
     NC_TRY(ncclReduceScatter(grad, grad + (size_t)c->rank * L.S, (size_t)L.S, ncclFloat32, ncclSum, c->comm,
                              c->comm_stream));
     r.sent += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
     r.recv += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
+    CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+    e.g_eff = e.ks_eff = e.gathered;
   }
-  CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
-  CU_TRY(cudaEventRecord(e.kstart, c->comm_stream));
   const float alpha = -lr / (float)P;
-  cudaError_t err = L.vel ? launch_ps_momentum(grad + L.begin, W + L.begin, L.vel, L.end - L.begin,
-                                                 1.0f / (float)P, lr, L.mu, L.wd, c->comm_stream)
-                          : launch_ps_shard_update(grad + L.begin, W + L.begin, L.end - L.begin, alpha, nullptr,
-                                                   c->comm_stream);
+  const bool zero = (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0;
+  // K2 with the gradient clear fused in (one launch) unless momentum or an unaligned buffer needs the
+  // separate paths
+  const bool fused_zero = zero && !L.vel && ps_shard_update_zero_supported(grad, W, L.begin);
+  cudaError_t err;
+  if (fused_zero)
+    err = launch_ps_shard_update_zero(grad, W, L.begin, L.end, L.padded, alpha, c->comm_stream);
+  else if (L.vel)
+    err = launch_ps_momentum(grad + L.begin, W + L.begin, L.vel, L.end - L.begin, 1.0f / (float)P, lr, L.mu, L.wd,
+                             c->comm_stream);
+  else
+    err = launch_ps_shard_update(grad + L.begin, W + L.begin, L.end - L.begin, alpha, nullptr, c->comm_stream);
   if (err != cudaSuccess) return cuda_fail(err, "ps shard update launch");
   if ((err = debug_sync(c->comm_stream, "K2 ps shard update")) != cudaSuccess) return cuda_fail(err, "K2");
-  CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
   if (P > 1) {
+    CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
+    e.ke_eff = e.kend;
     NC_TRY(ncclAllGather(W + (size_t)c->rank * L.S, W, (size_t)L.S, ncclFloat32, c->comm, c->comm_stream));
     r.sent += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
     r.recv += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
+  } else {
+    e.ke_eff = e.done;
   }
-  if (L.ps_flags & POSEIDON_PS_ZERO_GRAD) CU_TRY(cudaMemsetAsync(grad, 0, (size_t)L.padded * 4u, c->comm_stream));
+  if (zero && !fused_zero) {
+    if (P == 1) {  // kernel_ms must not include the memset
+      CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
+      e.ke_eff = e.kend;
+    }
+    CU_TRY(cudaMemsetAsync(grad, 0, (size_t)L.padded * 4u, c->comm_stream));
+  }
   CU_TRY(cudaEventRecord(e.done, c->comm_stream));
   r.layers.push_back(id);
   return POSEIDON_OK;
@@ -823,9 +848,9 @@ poseidon_status_t poseidon_get_iter_stats(poseidon_ctx_t c, int32_t ago, poseido
     out->sync_total_ms += elapsed(e.start, e.done);
     out->queue_ms += elapsed(e.ready, e.start);
     if (L.scheme == POSEIDON_SCHEME_SFB)
-      out->recon_ms += elapsed(e.kstart, e.kend);
+      out->recon_ms += elapsed(e.ks_eff, e.ke_eff);
     else
-      out->ps_update_ms += elapsed(e.kstart, e.kend);
+      out->ps_update_ms += elapsed(e.ks_eff, e.ke_eff);
   }
   out->exposed_ms = exposed;
   out->first_ready_to_bwd_end_ms = first_ready;
@@ -859,8 +884,8 @@ poseidon_status_t poseidon_get_layer_stats(poseidon_ctx_t c, int32_t ago, int32_
   CU_TRY(cudaEventSynchronize(r.bwd_end));
   out->launched = 1;
   out->ready_to_start_ms = elapsed(e.ready, e.start);
-  out->comm_ms = elapsed(e.start, e.gathered);
-  out->kernel_ms = elapsed(e.kstart, e.kend);
+  out->comm_ms = elapsed(e.start, e.g_eff);
+  out->kernel_ms = elapsed(e.ks_eff, e.ke_eff);
   out->start_to_done_ms = elapsed(e.start, e.done);
   out->done_after_bwd_end_ms = elapsed(r.bwd_end, e.done);
   return POSEIDON_OK;

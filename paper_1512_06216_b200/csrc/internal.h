@@ -24,6 +24,10 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 // ---- kernels (each returns the launch error) ----
 
 // K2: W[i] = fmaf(alpha, g[i], W[i]), i in [0, count). stats: optional 2 floats.
+// K2 with the PS_ZERO_GRAD clear fused in: update W[b, e) from g[b, e), then zero g[0, padded).
+bool ps_shard_update_zero_supported(const float* gbase, const float* Wbase, int64_t b);
+cudaError_t launch_ps_shard_update_zero(float* gbase, float* Wbase, int64_t b, int64_t e, int64_t padded,
+                                        float alpha, cudaStream_t s);
 cudaError_t launch_ps_shard_update(const float* g, float* W, int64_t count, float alpha, float* stats,
                                    cudaStream_t s);
 // PS with P simulated workers: W[i] = fmaf(alpha, sum_p g[p*ld + i], W[i]), i in [0,count).

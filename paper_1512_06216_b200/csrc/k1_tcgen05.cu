@@ -541,7 +541,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
 
   if (warp == 0) {
     // ===================== operand TMA producer (both CTAs) =====================
-    if (lane == 0 && (p.mode == 0 || p.mode == 6)) {
+    if (lane == 0 && (p.mode == 0 || p.mode == 6 || p.mode == 7)) {
       const uint64_t pol = policy_evict_last();
       uint32_t stage = 0, phase = 0;
       for (int tile = pair; tile < p.num_tiles; tile += npairs) {
@@ -571,7 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA, one thread) =====================
-    if (rank == 0 && lane == 0 && (p.mode == 0 || p.mode == 6)) {
+    if (rank == 0 && lane == 0 && (p.mode == 0 || p.mode == 6 || p.mode == 7)) {
       constexpr uint32_t id = k2sm::idesc();
       uint32_t stage = 0, phase = 0;
       int it = 0;
@@ -603,7 +603,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     }
   } else if (warp == 2) {
     // ===================== W tile TMA producer (both CTAs, own rows) =====================
-    if (lane == 0) {
+    if (lane == 0 && p.mode != 7) {
       const uint64_t pol = p.w_policy ? policy_evict_normal() : policy_evict_first();
       uint32_t g = 0;
       for (int tile = pair; tile < p.num_tiles; tile += npairs) {
@@ -626,7 +626,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     // The 8 local epilogue warps arrive on tempty_local (CTA scope); this thread forwards ONE
     // release.cluster arrival to the leader's tempty.  It issues no global stores, so the
     // cluster-scope release does not make anybody wait for outstanding W stores.
-    if (lane == 0 && (p.mode == 0 || p.mode == 6)) {
+    if (lane == 0 && (p.mode == 0 || p.mode == 6 || p.mode == 7)) {
       const uint32_t tl0 = mapa_shared(smem_u32(&tempty[0]), 0);
       const uint32_t tl1 = mapa_shared(smem_u32(&tempty[1]), 0);
       int it = 0;
@@ -659,7 +659,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
       if (m0 >= p.M) nch = 0;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      if (p.mode == 0 || p.mode == 6) mbar_wait(&tfull[acc], acc_phase);
+      if (p.mode == 0 || p.mode == 6 || p.mode == 7) mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       for (int c = 0; c < nch; ++c, ++g) {
         if (p.epi_groups == 2 ? ((int)(g & 1) != e) : (e != 0)) continue;
@@ -667,7 +667,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
         uint32_t r[2][16];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          if (p.mode == 0 || p.mode == 5) {
+          if (p.mode == 0 || p.mode == 5 || p.mode == 7) {
             tmem_ld_16x256b_x4(tmem_base + ((uint32_t)(q * 32 + h * 16) << 16) +
                                    (uint32_t)(acc * k2sm::BN + c * W_CHUNK_COLS), r[h]);
           } else {
@@ -675,7 +675,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
             for (int j = 0; j < 16; ++j) r[h][j] = 0u;
           }
         }
-        if (p.mode == 0 || p.mode == 5) tmem_ld_wait();
+        if (p.mode == 0 || p.mode == 5 || p.mode == 7) tmem_ld_wait();
+        if (p.mode == 7) {   // operands + MMA + TMEM loads only: no W traffic
+          float acc_sum = 0.f;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc_sum += __uint_as_float(r[0][j]) + __uint_as_float(r[1][j]);
+          if (acc_sum == 12345.678f) p.W[0] = acc_sum;   // keeps the loads live
+          continue;
+        }
         mbar_wait(&wfull[slot], ph);
         const uint32_t sbase = smem_w_u32 + slot * W_CHUNK_BYTES;
         const int col_base = n0 + c * W_CHUNK_COLS;
@@ -706,7 +713,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0 && (p.mode == 0 || p.mode == 6)) mbar_arrive(&tempty_local[acc]);
+      if (lane == 0 && (p.mode == 0 || p.mode == 6 || p.mode == 7)) mbar_arrive(&tempty_local[acc]);
     }
   }
 
@@ -727,6 +734,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
 //   POSEIDON_K1_EPI=1       one epilogue warpgroup;  POSEIDON_K1_WPOL=1  evict_normal W loads
 //   POSEIDON_K1_MODE=1|2|3  W streaming only / no update / loads only (no MMA in modes 1-3)
 //   POSEIDON_K1_MODE=5|6    TMEM loads without MMA / MMA + accumulator handshake without TMEM loads
+//   POSEIDON_K1_MODE=7      operands + MMA + TMEM loads, no W traffic
 struct K1Knobs {
   int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0;
   K1Knobs() {

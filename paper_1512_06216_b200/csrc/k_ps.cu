@@ -60,9 +60,13 @@ __device__ __forceinline__ void warp_stats_flush(float sq, float bad, float* sta
 
 // One pass, no grid-stride loop: each thread owns 4 float4 (16 elements) spaced a block apart, all
 // loads issued before any use (8 x 16 B in flight per thread), grid = ceil(n / 4096).
-template <bool kStats>
+// kZero (PS_ZERO_GRAD): the kernel also clears the layer's whole padded gradient buffer zbase[0, zpad)
+// for the next iteration's accumulation — each thread zeroes the shard elements it has read, and the
+// grid-strided rest covers [0, zb) and [ze, zpad) — which saves the separate memset launch.
+template <bool kStats, bool kZero>
 __global__ void __launch_bounds__(256) ps_shard_sgd_kernel(const float* __restrict__ g, float* __restrict__ W,
-                                                            int64_t count, float alpha, float* stats) {
+                                                            int64_t count, float alpha, float* stats,
+                                                            float* zbase, int64_t zb, int64_t ze, int64_t zpad) {
   constexpr int U = 4;
   const int64_t n4 = count >> 2;
   const float4* g4 = reinterpret_cast<const float4*>(g);
@@ -75,6 +79,14 @@ __global__ void __launch_bounds__(256) ps_shard_sgd_kernel(const float* __restri
     if (i < n4) {
       a[j] = ld_stream(g4 + i);
       w[j] = W4[i];
+    }
+  }
+  if (kZero) {
+    float4* gz4 = reinterpret_cast<float4*>(zbase + zb);
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t i = base + (int64_t)j * blockDim.x;
+      if (i < n4) gz4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
   float sq = 0.f, bad = 0.f;
@@ -96,9 +108,22 @@ __global__ void __launch_bounds__(256) ps_shard_sgd_kernel(const float* __restri
   // scalar tail (count % 4), block 0
   if (blockIdx.x == 0 && threadIdx.x < (count & 3)) {
     const int64_t t = (n4 << 2) + threadIdx.x;
-    const float u = alpha * g[t];
-    W[t] = fmaf(alpha, g[t], W[t]);
+    const float gt = g[t];
+    const float u = alpha * gt;
+    W[t] = fmaf(alpha, gt, W[t]);
+    if (kZero) zbase[zb + t] = 0.f;
     if (kStats) { sq = fmaf(u, u, sq); bad += isfinite(u) ? 0.f : 1.f; }
+  }
+  if (kZero) {
+    // the rest of the padded buffer: [0, zb) (zb is a multiple of 32) and [ze, zpad) (zpad = P*S,
+    // a multiple of 32; ze arbitrary -> scalar up to the next multiple of 4)
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    float4* z4 = reinterpret_cast<float4*>(zbase);
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = tid; i < (zb >> 2); i += nth) z4[i] = z;
+    const int64_t ze4 = (ze + 3) & ~int64_t(3);
+    if (tid < ze4 - ze && ze + tid < zpad) zbase[ze + tid] = 0.f;
+    for (int64_t i = (ze4 >> 2) + tid; i < (zpad >> 2); i += nth) z4[i] = z;
   }
   if (kStats) warp_stats_flush(sq, bad, stats);
 }
@@ -165,10 +190,30 @@ cudaError_t launch_ps_shard_update(const float* g, float* W, int64_t count, floa
     const int64_t blocks = n4 > 0 ? (n4 + per_block - 1) / per_block : 1;
     const dim3 grid((unsigned)blocks);
     if (stats)
-      ps_shard_sgd_kernel<true><<<grid, threads, 0, s>>>(g, W, count, alpha, stats);
+      ps_shard_sgd_kernel<true, false><<<grid, threads, 0, s>>>(g, W, count, alpha, stats, nullptr, 0, 0, 0);
     else
-      ps_shard_sgd_kernel<false><<<grid, threads, 0, s>>>(g, W, count, alpha, nullptr);
+      ps_shard_sgd_kernel<false, false><<<grid, threads, 0, s>>>(g, W, count, alpha, nullptr, nullptr, 0, 0, 0);
   }
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+bool ps_shard_update_zero_supported(const float* gbase, const float* Wbase, int64_t b) {
+  return aligned16(gbase) && aligned16(Wbase) && (b & 3) == 0;
+}
+
+cudaError_t launch_ps_shard_update_zero(float* gbase, float* Wbase, int64_t b, int64_t e, int64_t padded,
+                                        float alpha, cudaStream_t s) {
+  const int threads = 256;
+  const int64_t count = e > b ? e - b : 0;
+  const int64_t n4 = count >> 2;
+  const int64_t per_block = (int64_t)threads * 4;
+  int64_t blocks = (n4 + per_block - 1) / per_block;
+  const int64_t zero_blocks = ((padded - count) / 4 + per_block * 4 - 1) / (per_block * 4);  // ~16 float4 / thread
+  if (blocks < zero_blocks) blocks = zero_blocks;
+  if (blocks < 1) blocks = 1;
+  ps_shard_sgd_kernel<false, true><<<(unsigned)blocks, threads, 0, s>>>(gbase + b, Wbase + b, count, alpha, nullptr,
+                                                                       gbase, b, b + count, padded);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }

@@ -1,0 +1,73 @@
+"""Render tools/layer_roofline.py JSON lines (one file per P) as the markdown tables in profiles/.
+
+    python tools/layer_roofline_md.py out.md P1.jsonl P2.jsonl P4.jsonl
+
+Two bounds per layer:
+  bandwidth roof  SFB: (P-1)K(M+N)4/BW_nvl + max(2MNPK/TC, (8MN + 4PK(M+N) + 8M)/BW_hbm)
+                  PS:  2(P-1)/P 4n/BW_nvl + 12n/P/BW_hbm
+  effective roof  each term raised to its latency floor: a collective costs at least alpha (SFB: one
+                  all-gather; PS: reduce-scatter + all-gather = 2 alpha), a kernel at least T_LAUNCH.
+alpha = the 8-byte NCCL all-gather measured in the same run; T_LAUNCH = 2 us.
+"""
+import json
+import sys
+
+TC_TF32, BW_HBM, BW_NVL, T_LAUNCH = 794e12, 6543.7e9, 900e9, 2e-6
+
+
+def bounds(d, P, alpha):
+    M, N, K, n = d["M"], d["N"], d["K"], d["n"]
+    if d["scheme"] == "sfb":
+        comm = (P - 1) * K * (M + N) * 4 / BW_NVL
+        kern = max(2.0 * M * N * P * K / TC_TF32, (8.0 * M * N + 4.0 * P * K * (M + N) + 8.0 * M) / BW_HBM)
+        comm_eff = max(comm, alpha) if P > 1 else 0.0
+    else:
+        comm = 2.0 * (P - 1) / P * 4 * n / BW_NVL
+        kern = 12.0 * n / P / BW_HBM
+        comm_eff = max(comm, 2 * alpha) if P > 1 else 0.0
+    return (comm + kern) * 1e6, (comm_eff + max(kern, T_LAUNCH)) * 1e6
+
+
+def main():
+    out, files = sys.argv[1], sys.argv[2:]
+    lines = ["# Per-layer sync vs its roofline, each layer in isolation (round 1)", "",
+             "`tools/layer_roofline.py` under torchrun, rendered by `tools/layer_roofline_md.py` (median of 50",
+             "syncs per layer, max over ranks; a ~100 us device spin precedes each sync so all of its launches are",
+             "queued; time = the library's device events start -> done).  `bw roof`: SURVEY §8(d) bandwidth",
+             "roofline (NVLink 5 900 GB/s, TF32 794 TFLOP/s, HBM 6543.7 GB/s).  `eff roof`: the same with every",
+             "collective raised to the measured 8-byte NCCL latency alpha (PS: 2 alpha) and every kernel to 2 us.",
+             "ps_nccl = NCCL reduce-scatter + K2 + all-gather; ps_nvls = the fused multimem kernel; sfb = NCCL",
+             "all-gather of the factors + K1.", ""]
+    for f in files:
+        L = [json.loads(l) for l in open(f) if l.startswith("{")]
+        head = [d for d in L if "alpha_us" in d][0]
+        P, alpha = head["P"], head["alpha_us"] * 1e-6
+        lines.append(f"## P = {P}  (alpha = {head['alpha_us']} us; NCCL all-gather busbw at 256 MB = "
+                     f"{head['bw_nvl_measured_GBps']} GB/s)")
+        lines.append("")
+        lines.append("| layer | M x N | path | measured us | bw roof us | frac | eff roof us | frac of eff |")
+        lines.append("|---|---|---|---:|---:|---:|---:|---:|")
+        c4 = {}
+        for d in L:
+            if "layer" not in d:
+                continue
+            bw, eff = bounds(d, P, alpha)
+            t = d["measured_us"]
+            if d["layer"].startswith("C4"):
+                a = c4.setdefault(d["scheme"], [0, 0.0, 0.0, 0.0])
+                a[0] += 1
+                a[1] += t
+                a[2] += bw
+                a[3] += eff
+                continue
+            lines.append(f"| {d['layer']} | {d['M']} x {d['N']} | {d['scheme']} | {t:.1f} | {bw:.1f} | {bw / t:.3f} | "
+                         f"{eff:.1f} | {eff / t:.3f} |")
+        for sch, (cnt, t, bw, eff) in sorted(c4.items()):
+            lines.append(f"| C4 GoogLeNet ({cnt} layers, summed) | - | {sch} | {t:.1f} | {bw:.1f} | {bw / t:.3f} | "
+                         f"{eff:.1f} | {eff / t:.3f} |")
+        lines.append("")
+    open(out, "w").write("\n".join(lines) + "\n")
+
+
+if __name__ == "__main__":
+    main()
