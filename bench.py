@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--recon", default="tf32", choices=["tf32", "fp32"])
     ap.add_argument("--nvls", default="auto", choices=["auto", "on", "off"],
                     help="fused one-kernel NVLink-SHARP PS sync (f1); auto = on when N > 1")
+    ap.add_argument("--sfb-wire", default="auto", choices=["auto", "nccl", "symm", "nvls"],
+                    help="SFB factor broadcast: NCCL all-gather on plain buffers, on NCCL symmetric windows, "
+                         "or the library's NVLS multicast kernel; auto = symm when N > 1")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--momentum", type=float, default=0.0, help="f4: Lambda momentum (0 = plain SGD hot path)")
     ap.add_argument("--weight-decay", type=float, default=0.0, help="f4: Lambda weight decay")
@@ -261,6 +264,8 @@ def run_poseidon(args):
     use_nvls = world > 1 and args.nvls != "off"
     if use_nvls:
         flags |= pz.FLAG_NVLS_PS
+    sfb_wire = ("symm" if args.sfb_wire == "auto" else args.sfb_wire) if world > 1 else "none (P=1)"
+    flags |= {"symm": pz.FLAG_SYMM_SFB, "nvls": pz.FLAG_NVLS_SFB}.get(sfb_wire, 0)
     ctx = pz.Context(rank=rank, world=world, device=local, nccl_id=nccl_id, flags=flags)
 
     torch.manual_seed(6216)          # identical weights on every rank
@@ -469,7 +474,10 @@ def run_poseidon(args):
                         "memory_format": args.memory_format,
                         "ps_path": ("nvls-fused" if sync.nvls_active else
                                     ("nccl rs/k2/ag" if world > 1 else "k2 (P=1)")),
-                        "nvls_status": ctx.nvls_status()},
+                        "nvls_status": ctx.nvls_status(),
+                        "sfb_wire": sfb_wire,
+                        "sfb_paths": sorted({ctx.sfb_path(d["id"]) for d in sync.describe()
+                                             if d["scheme"] == "SFB"}) if world > 1 else []},
             "exposed_sync_ms": exposed, "sync_total_ms": sync_total,
             "exposed_frac": (exposed / sync_total) if sync_total > 0 else None,
             "nccl_bytes_sent_per_iter": nccl_sent, "nccl_bytes_recv_per_iter": nccl_recv,

@@ -78,6 +78,12 @@ typedef struct {
 #define POSEIDON_FLAG_DWBP_OFF 0x1u   /* ablation: sync starts only at iteration_end (Fig. dwbp (a)) */
 #define POSEIDON_FLAG_NO_PRIORITY 0x2u /* sync streams at default instead of highest priority */
 #define POSEIDON_FLAG_NVLS_PS 0x4u     /* PS layers in the arena sync with one fused NVLink-SHARP kernel */
+#define POSEIDON_FLAG_SYMM_SFB 0x8u    /* SFB gather buffers in NCCL symmetric windows (NCCL's symmetric-memory
+                                         all-gather kernels); registration is collective, so every rank must
+                                         register the same layers in the same order */
+#define POSEIDON_FLAG_NVLS_SFB 0x10u   /* SFB factor "broadcast" as one NVLink-SHARP multicast store per
+                                         rank into symmetric gather buffers, instead of an NCCL all-gather
+                                         (implies POSEIDON_FLAG_SYMM_SFB) */
 
 typedef struct poseidon_ctx* poseidon_ctx_t;
 
@@ -217,7 +223,11 @@ poseidon_status_t poseidon_bind_sfb_params(poseidon_ctx_t ctx, int32_t layer_id,
 poseidon_status_t poseidon_ps_arena(poseidon_ctx_t ctx, int32_t* nvls_active);
 poseidon_status_t poseidon_ps_layer_buffers(poseidon_ctx_t ctx, int32_t layer_id, float** grad, float** W,
                                             int64_t* padded_n);
-/* Human-readable state of the fused NVLS path ("active", "not requested", or the NCCL error). */
+/* How SFB layer `layer_id` moves its factors at world > 1: 0 = NCCL all-gather on plain device
+ * buffers, 1 = NCCL all-gather on symmetric-window buffers (FLAG_SYMM_SFB), 2 = NVLS multicast
+ * broadcast (FLAG_NVLS_SFB).  Negative status for a bad id or a PS layer. */
+int32_t poseidon_sfb_path(poseidon_ctx_t ctx, int32_t layer_id);
+/* Human-readable state of the fused NVLS PS path ("active", "not requested", or the NCCL error). */
 const char* poseidon_nvls_status(poseidon_ctx_t ctx);
 
 poseidon_status_t poseidon_set_lr(poseidon_ctx_t ctx, float lr);           /* lr used by backprop_hook */

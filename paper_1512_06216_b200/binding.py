@@ -23,7 +23,8 @@ ERR_SHAPE, ERR_ALIGNMENT, ERR_UNSUPPORTED, ERR_STATE = -5, -6, -7, -8
 SCHEME_PS, SCHEME_SFB = 0, 1
 LAYER_CONV, LAYER_FC = 0, 1
 RECON_TF32, RECON_FP32 = 0, 1
-FLAG_DWBP_OFF, FLAG_NO_PRIORITY, FLAG_NVLS_PS = 0x1, 0x2, 0x4
+FLAG_DWBP_OFF, FLAG_NO_PRIORITY, FLAG_NVLS_PS, FLAG_SYMM_SFB, FLAG_NVLS_SFB = 0x1, 0x2, 0x4, 0x8, 0x10
+SFB_PATH_NCCL, SFB_PATH_NCCL_SYMM, SFB_PATH_NVLS = 0, 1, 2
 PS_ZERO_GRAD = 0x1
 
 _STATUS_NAMES = {0: "OK", -1: "INVALID_ARG", -2: "NOT_INITIALIZED", -3: "CUDA", -4: "NCCL",
@@ -103,6 +104,7 @@ _SIGS = {
     "poseidon_ps_arena": (_i32, [_vp, _P(_i32)]),
     "poseidon_ps_layer_buffers": (_i32, [_vp, _i32, _P(_vp), _P(_vp), _P(_i64)]),
     "poseidon_nvls_status": (ctypes.c_char_p, [_vp]),
+    "poseidon_sfb_path": (_i32, [_vp, _i32]),
     "poseidon_set_recon": (_i32, [_vp, _i32, _i32]),
     "poseidon_wait_layer": (_i32, [_vp, _i32, _vp]),
     "poseidon_iteration_end": (_i32, [_vp, _vp, _P(IterStats)]),
@@ -254,6 +256,11 @@ class Context:
         g, w, n = _vp(), _vp(), _i64()
         _check(lib.poseidon_ps_layer_buffers(self.h, layer_id, ctypes.byref(g), ctypes.byref(w), ctypes.byref(n)))
         return g.value, w.value, n.value
+
+    def sfb_path(self, layer_id) -> int:
+        r = lib.poseidon_sfb_path(self.h, layer_id)
+        _check(min(r, 0))
+        return r
 
     def nvls_status(self) -> str:
         m = lib.poseidon_nvls_status(self.h)

@@ -93,6 +93,11 @@ struct Layer {
   // Vg [P][N][ldk], Bs [P][M] (per-worker column sums of U); optional staging [K][M], [K][N]
   int64_t ldk = 0;
   float *Ug = nullptr, *Vg = nullptr, *Bs = nullptr;
+  // POSEIDON_FLAG_SYMM_SFB: Ug|Vg|Bs are one ncclMemAlloc buffer registered as a symmetric window
+  void* symm = nullptr;
+  ncclWindow_t win = nullptr;
+  ncclComm_t win_comm = nullptr;
+  bool bcast = false;   // POSEIDON_FLAG_NVLS_SFB: factors broadcast by the multicast kernel
   float *stU = nullptr, *stV = nullptr;
   float *W = nullptr, *bias = nullptr;  // bound SFB params
   // PS: caller-owned padded flat buffers
@@ -138,7 +143,10 @@ struct poseidon_ctx {
   std::vector<int32_t> pending_order;  // DWBP off: hook order of deferred syncs
   // PS arena (poseidon_ps_arena): one gradient and one parameter buffer for all PS layers; NCCL
   // symmetric windows + device communicator when the fused NVLS path is enabled and available
-  bool want_nvls = false;
+  bool want_nvls = false;      // FLAG_NVLS_PS
+  bool want_nvls_sfb = false;  // FLAG_NVLS_SFB
+  bool ps_nvls = false;        // PS arena is symmetric and the device communicator exists
+  std::string devcomm_error;
   float *arena_g = nullptr, *arena_w = nullptr;
   size_t arena_bytes = 0;
   bool arena_nccl_mem = false;
@@ -185,6 +193,16 @@ IterRecord& open_record(poseidon_ctx_t c) {
   return r;
 }
 
+// The NCCL device communicator (LSA multicast team + barriers) shared by the fused NVLS PS kernel and
+// the NVLS factor broadcast.  ncclDevCommCreate is collective: it is reached at the same point of the
+// registration sequence on every rank (first NVLS SFB layer or the PS arena, whichever comes first).
+bool ensure_devcomm(poseidon_ctx_t c) {
+  if (c->nvls) return true;
+  if (!c->devcomm_error.empty() || !c->comm) return false;
+  c->nvls = nvls_create(c->comm, kNvlsBlocks, &c->devcomm_error);
+  return c->nvls != nullptr;
+}
+
 // Producer-side prologue shared by both schemes: the previous sync of this
 // layer must be finished before its buffers are rewritten.
 poseidon_status_t producer_guard(poseidon_ctx_t c, Layer& L, cudaStream_t producer) {
@@ -201,7 +219,22 @@ poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float*
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
   IterRecord& r = open_record(c);
   e.g_eff = e.start;
-  if (P > 1) {
+  if (P > 1 && L.bcast) {
+    // the paper's "broadcast" done by the NVSwitch: one multicast store of this rank's slots lands in
+    // every rank's gather buffers (barrier, multimem.st, barrier; k_ps_nvls.cu)
+    const size_t ucount = (size_t)(L.M * L.ldk), vcount = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
+    const size_t vbase = (size_t)((char*)L.Vg - (char*)L.symm), bbase = (size_t)((char*)L.Bs - (char*)L.symm);
+    cudaError_t err = launch_sfb_bcast_nvls(c->nvls, L.win, (size_t)c->rank * ucount * 4, (int64_t)ucount,
+                                            vbase + (size_t)c->rank * vcount * 4, (int64_t)vcount,
+                                            bbase + (size_t)c->rank * bcount * 4, (int64_t)bcount, kNvlsBlocks,
+                                            c->comm_stream);
+    if (err != cudaSuccess) return cuda_fail(err, "NVLS factor broadcast launch");
+    const uint64_t per = (uint64_t)(ucount + vcount + bcount) * 4u;
+    r.sent += per;  // one copy into the switch
+    r.recv += per * (uint64_t)(P - 1);
+    CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+    e.g_eff = e.gathered;
+  } else if (P > 1) {
     const size_t ucount = (size_t)(L.M * L.ldk), vcount = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
     NC_TRY(ncclGroupStart());
     NC_TRY(ncclAllGather(L.Ug + (size_t)c->rank * ucount, L.Ug, ucount, ncclFloat32, c->comm, c->comm_stream));
@@ -255,7 +288,7 @@ poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* 
   CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
   IterRecord& r = open_record(c);
-  if (P > 1 && c->nvls && L.in_arena) {
+  if (P > 1 && c->ps_nvls && L.in_arena) {
     // fused one-kernel PS over NVLink SHARP (reduce-scatter + K2 + all-gather + zero-grad)
     e.g_eff = e.ks_eff = e.start;
     e.ke_eff = e.done;
@@ -349,9 +382,16 @@ poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t l
 }
 
 void free_layer(Layer& L) {
-  if (L.Ug) cudaFree(L.Ug);
-  if (L.Vg) cudaFree(L.Vg);
-  if (L.Bs) cudaFree(L.Bs);
+  if (L.symm) {
+    if (L.win) ncclCommWindowDeregister(L.win_comm, L.win);  // collective: every rank frees the layer
+    ncclMemFree(L.symm);
+    L.symm = nullptr;
+    L.win = nullptr;
+  } else {
+    if (L.Ug) cudaFree(L.Ug);
+    if (L.Vg) cudaFree(L.Vg);
+    if (L.Bs) cudaFree(L.Bs);
+  }
   if (L.stU) cudaFree(L.stU);
   if (L.stV) cudaFree(L.stV);
   if (L.vel) cudaFree(L.vel);
@@ -423,6 +463,7 @@ poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, 
   c->device = topo->device;
   c->flags = topo->flags;
   c->want_nvls = (topo->flags & POSEIDON_FLAG_NVLS_PS) != 0 && world > 1;
+  c->want_nvls_sfb = (topo->flags & POSEIDON_FLAG_NVLS_SFB) != 0 && world > 1;
   c->layers.resize(64);
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -510,9 +551,34 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
     L.ldk = round_up(K, 4);
     const size_t P = (size_t)c->world;
     const size_t ub = P * (size_t)(M * L.ldk) * 4, vb = P * (size_t)(N * L.ldk) * 4, bb = P * (size_t)M * 4;
-    CU_TRY(cudaMalloc(&L.Ug, ub));
-    CU_TRY(cudaMalloc(&L.Vg, vb));
-    CU_TRY(cudaMalloc(&L.Bs, bb));
+    bool placed = false;
+    if (c->world > 1 && (c->flags & (POSEIDON_FLAG_SYMM_SFB | POSEIDON_FLAG_NVLS_SFB))) {
+      // one symmetric window for the layer's three gather buffers: NCCL then runs the factor
+      // all-gather with its symmetric-memory kernels (collective call: all ranks register alike)
+      const size_t ua = round_up((int64_t)ub, 4096), va = round_up((int64_t)vb, 4096);
+      const size_t total = ua + va + round_up((int64_t)bb, 4096);
+      void* base = nullptr;
+      if (ncclMemAlloc(&base, total) == ncclSuccess) {
+        ncclWindow_t w = nullptr;
+        if (ncclCommWindowRegister(c->comm, base, total, &w, NCCL_WIN_COLL_SYMMETRIC) == ncclSuccess) {
+          L.symm = base;
+          L.win = w;
+          L.win_comm = c->comm;
+          L.Ug = static_cast<float*>(base);
+          L.Vg = reinterpret_cast<float*>(static_cast<char*>(base) + ua);
+          L.Bs = reinterpret_cast<float*>(static_cast<char*>(base) + ua + va);
+          placed = true;
+          L.bcast = c->want_nvls_sfb && ensure_devcomm(c);
+        } else {
+          ncclMemFree(base);
+        }
+      }
+    }
+    if (!placed) {
+      CU_TRY(cudaMalloc(&L.Ug, ub));
+      CU_TRY(cudaMalloc(&L.Vg, vb));
+      CU_TRY(cudaMalloc(&L.Bs, bb));
+    }
     CU_TRY(cudaMemset(L.Ug, 0, ub));  // k columns in [K, ldk) stay zero forever
     CU_TRY(cudaMemset(L.Vg, 0, vb));
     CU_TRY(cudaMemset(L.Bs, 0, bb));
@@ -601,7 +667,8 @@ poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
     ncclResult_t r3 = (r2 == ncclSuccess) ? ncclCommWindowRegister(c->comm, g, total, &c->win_g, NCCL_WIN_COLL_SYMMETRIC) : r2;
     ncclResult_t r4 = (r3 == ncclSuccess) ? ncclCommWindowRegister(c->comm, w, total, &c->win_w, NCCL_WIN_COLL_SYMMETRIC) : r3;
     if (r4 == ncclSuccess) {
-      c->nvls = nvls_create(c->comm, kNvlsBlocks, &c->nvls_error);
+      c->ps_nvls = ensure_devcomm(c);
+      if (!c->ps_nvls) c->nvls_error = c->devcomm_error;
       symmetric = true;
       c->arena_nccl_mem = true;
       c->arena_g = static_cast<float*>(g);
@@ -630,7 +697,7 @@ poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
     if (st) return st;
     L.in_arena = true;
   }
-  if (nvls_active) *nvls_active = c->nvls ? 1 : 0;
+  if (nvls_active) *nvls_active = c->ps_nvls ? 1 : 0;
   return POSEIDON_OK;
 }
 
@@ -645,9 +712,17 @@ poseidon_status_t poseidon_ps_layer_buffers(poseidon_ctx_t c, int32_t id, float*
   return POSEIDON_OK;
 }
 
+int32_t poseidon_sfb_path(poseidon_ctx_t c, int32_t id) {
+  Layer* L;
+  poseidon_status_t st = check_layer(c, id, &L);
+  if (st) return st;
+  if (L->scheme != POSEIDON_SCHEME_SFB) return fail(POSEIDON_ERR_STATE, "layer is not an SFB layer");
+  return L->bcast ? 2 : (L->symm ? 1 : 0);
+}
+
 const char* poseidon_nvls_status(poseidon_ctx_t c) {
   if (!c) return "no context";
-  if (c->nvls) return "active";
+  if (c->ps_nvls) return "active";
   if (!c->want_nvls) return "not requested";
   return c->nvls_error.empty() ? "arena not created" : c->nvls_error.c_str();
 }

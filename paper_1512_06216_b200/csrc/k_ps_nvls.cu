@@ -114,6 +114,52 @@ __global__ void __launch_bounds__(256) ps_nvls_kernel(const __grid_constant__ nc
   }
 }
 
+struct BcastSeg {
+  size_t off;   // byte offset of this rank's slot within the layer's window
+  int64_t n;    // floats
+};
+
+// SFB step 2 ("Broadcast ... to all other workers") done by the NVSwitch: each rank stores its
+// own factor slots once into the multicast address and the switch writes them into every rank's
+// gather buffers.  Barrier first (every rank has packed its slots and finished reading the previous
+// iteration's gather buffers), barrier last (every rank's stores have landed before K1 reads them).
+template <int U>
+__global__ void __launch_bounds__(256) sfb_bcast_kernel(const __grid_constant__ ncclDevComm comm, ncclWindow_t win,
+                                                        BcastSeg s0, BcastSeg s1, BcastSeg s2) {
+  ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamTagLsa(), blockIdx.x, /*multimem=*/true);
+  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const BcastSeg segs[3] = {s0, s1, s2};
+#pragma unroll 1
+  for (int sgi = 0; sgi < 3; ++sgi) {
+    const BcastSeg sg = segs[sgi];
+    // slots of odd length (the bias sums, M floats) start off 16-B alignment on ranks > 0: scalar head
+    const int64_t head = sg.n < ((4 - ((int64_t)(sg.off >> 2) & 3)) & 3) ? sg.n : ((4 - ((int64_t)(sg.off >> 2) & 3)) & 3);
+    const float* src0 = static_cast<const float*>(ncclGetLocalPointer(win, sg.off));
+    float* dst0 = static_cast<float*>(ncclGetLsaMultimemPointer(win, sg.off, comm));
+    if (blockIdx.x == 0 && threadIdx.x < head) mm_st(dst0 + threadIdx.x, src0[threadIdx.x]);
+    const float* src = src0 + head;
+    float* dst = dst0 + head;
+    const int64_t nb = sg.n - head;
+    const int64_t n4 = nb >> 2;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i < n4) v[u] = *reinterpret_cast<const float4*>(src + 4 * i);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i < n4) mm_st_v4(dst + 4 * i, v[u]);
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (nb & 3)) mm_st(dst + 4 * n4 + threadIdx.x, src[4 * n4 + threadIdx.x]);
+  }
+  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
 }  // namespace
 
 struct NvlsState {
@@ -147,6 +193,19 @@ cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww
     ps_nvls_kernel<2><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, padded, alpha, zero_grad ? 1 : 0, mom);
   else
     ps_nvls_kernel<4><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, padded, alpha, zero_grad ? 1 : 0, mom);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sfb_bcast_nvls(const NvlsState* st, ncclWindow_t win, size_t off_u, int64_t n_u, size_t off_v,
+                                  int64_t n_v, size_t off_b, int64_t n_b, int max_blocks, cudaStream_t s) {
+  // identical grid on every rank (the slot sizes are the same everywhere)
+  const int64_t n4 = (n_u + n_v + n_b) / 4;
+  int blocks = (int)((n4 + 1023) / 1024);
+  if (blocks < 1) blocks = 1;
+  if (blocks > max_blocks) blocks = max_blocks;
+  sfb_bcast_kernel<4><<<blocks, 256, 0, s>>>(st->dev, win, BcastSeg{off_u, n_u}, BcastSeg{off_v, n_v},
+                                            BcastSeg{off_b, n_b});
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }

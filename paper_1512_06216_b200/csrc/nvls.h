@@ -15,4 +15,9 @@ cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww
                            int64_t b, int64_t e, int64_t padded, float alpha, bool zero_grad, int max_blocks,
                            int64_t shard, float* vel, float inv_p, float lr, float mu, float wd, cudaStream_t s);
 
+// NVLS factor broadcast (SFB step 2 done by the switch): barrier; multimem.st of this rank's three
+// slots (byte offsets within the layer's window, float counts); barrier.
+cudaError_t launch_sfb_bcast_nvls(const NvlsState* st, ncclWindow_t win, size_t off_u, int64_t n_u, size_t off_v,
+                                  int64_t n_v, size_t off_b, int64_t n_b, int max_blocks, cudaStream_t s);
+
 }  // namespace poseidon

@@ -6,6 +6,8 @@ Checks, at world = P:
      the Z13 gate; every rank's W bit-identical.
   2. PS sync of the same layer's flat buffer (RS -> K2 -> AG): integer variant
      bit-exact vs O6, random within 1e-5; every rank bit-identical.
+  1b. SFB on NCCL symmetric windows and over the NVLS multicast broadcast: integer variant
+     bit-exact vs O4 for three shapes (odd M, K not a multiple of 4) over three iterations.
   3. A layer with an empty shard (n=650 at P=8 has one) and odd sizes.
   4. Two DWBP training steps of CIFAR-10 quick (C2 shapes, K=16/GPU, SACP
      auto and forced PS, DWBP on and off): all ranks' parameters
@@ -89,6 +91,35 @@ def main():
     assert O.update_error_fp32(b, bd.cpu().numpy(), b1) <= 1e-5
     assert allsame(Wd)
 
+    # ---- 1b. SFB on symmetric buffers: NCCL all-gather (SYMM_SFB) and the NVLS multicast broadcast
+    #          (NVLS_SFB); odd M (bias slot not a multiple of 4), ldk padding, 3 iterations in a row
+    #          (the broadcast's entry barrier guards the gather buffers the previous K1 read) ----
+    for flags in (pz.FLAG_SYMM_SFB, pz.FLAG_NVLS_SFB):
+        cs = new_ctx(flags)
+        shapes = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 1000, 4096, 33)]
+        for lid, M_, N_, K_ in shapes:
+            assert cs.register_layer(lid, pz.LAYER_FC, M_, N_, K_) == pz.SCHEME_SFB
+        path = cs.sfb_path(0)
+        assert path >= pz.SFB_PATH_NCCL_SYMM, path
+        if rank == 0:
+            print(f"SFB path flags={flags}: {path}", flush=True)
+        for it in range(3):
+            for lid, M_, N_, K_ in shapes:
+                W, b, Us, Vs, lr = S.integer_factors(M_, N_, K_, P, seed=100 * it + lid)
+                Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+                cs.sync_fc_sfb(lid, torch.from_numpy(Us[rank]).to(dev), torch.from_numpy(Vs[rank]).to(dev), Wd, bd, lr)
+                cs.wait_layer(lid)
+                W1, b1 = O.sync_step(W, b, Us, Vs, lr)
+                torch.cuda.synchronize()
+                assert np.array_equal(Wd.cpu().numpy().astype(np.float64), W1), f"SFB flags={flags} it={it} lid={lid}"
+                assert np.array_equal(bd.cpu().numpy().astype(np.float64), b1)
+                assert allsame(Wd) and allsame(bd)
+            st = cs.iteration_end(stats=True)
+            ldks = [(K_ + 3) // 4 * 4 for _, _, _, K_ in shapes]
+            per = sum((M_ * l + N_ * l + M_) * 4 for (_, M_, N_, _), l in zip(shapes, ldks))
+            assert st["nccl_bytes_recv"] == per * (P - 1), st
+        cs.close()
+
     # ---- 2. PS of the same layer ----
     for variant in ("int", "rand"):
         if variant == "int":
@@ -128,11 +159,12 @@ def main():
     W = (g0.integers(-1023, 1024, size=n) * 2.0 ** -10).astype(np.float32)
     grads = S.integer_grads(n, P, seed=10)
     _, _, padded = pz.shard_range(n, P, rank)
-    gflat = torch.zeros(padded, device=dev)
+    gflat = torch.full((padded,), 7.0, device=dev)   # padding holds garbage: it must be cleared too
     gflat[:n] = torch.from_numpy(grads[rank]).to(dev)
     wflat = torch.zeros(padded, device=dev)
     wflat[:n] = torch.from_numpy(W).to(dev)
     lr = 2.0 ** -7
+    ctx.bind_ps_buffers(2, gflat, wflat, n, pz.PS_ZERO_GRAD)   # K2 clears the gradient in-kernel
     ctx.sync_ps(2, gflat, wflat, n, lr)
     ctx.wait_layer(2)
     ctx.iteration_end()
@@ -143,6 +175,7 @@ def main():
         assert np.array_equal(out, ref)
     else:
         assert O.update_error_fp32(W, out, ref) <= 1e-5
+    assert float(gflat.abs().sum()) == 0.0, "odd-size PS gradient not cleared"
     ctx.close()
 
     # ---- 3b. fused NVLS PS (f1): arena in NCCL symmetric windows, one multimem kernel per layer ----

@@ -2,12 +2,15 @@
 symbol include/poseidon.h declares, and its pure host functions (SACP rule,
 shard map) agree bit-exactly with the oracle.  No GPU compute is called."""
 import itertools
+import os
 
 import pytest
 
 import oracle as O
 import paper_1512_06216_b200 as pz
 from paper_1512_06216_b200 import binding as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_library_exports_every_header_symbol():
@@ -96,3 +99,14 @@ def test_measured_cost_model_properties():
     assert 0 < s1 < s2 and 0 < p1 <= p2 and (s2 - s1) > (p2 - p1)
     with pytest.raises(pz.PoseidonError):
         Bn.choose_scheme_model(1, 10, 10, 10, 0)
+
+
+def test_flag_values_match_header():
+    """Every POSEIDON_FLAG_* / POSEIDON_PS_* define in include/poseidon.h has the same value in the binding."""
+    import re
+    import paper_1512_06216_b200.binding as B
+    text = open(os.path.join(ROOT, "include", "poseidon.h")).read()
+    defs = dict(re.findall(r"#define POSEIDON_((?:FLAG|PS)_[A-Z_]+)\s+(0x[0-9a-fA-F]+)u", text))
+    assert "FLAG_NVLS_SFB" in defs and "FLAG_SYMM_SFB" in defs
+    for name, val in defs.items():
+        assert getattr(B, name) == int(val, 16), name

@@ -104,3 +104,29 @@ def test_context_errors(pz):
     with pytest.raises(pz.PoseidonError):
         ctx.bind_ps_buffers(7, g, g, 12345)  # wrong n
     ctx.close()
+
+
+@pytest.mark.parametrize("n", [1, 3, 5, 650, 4097, 100003])
+def test_ps_zero_grad_odd_sizes(pz, n):
+    """K2 with the fused gradient clear at P = 1: exact update of W[0, n), W padding untouched,
+    the whole padded gradient buffer (garbage padding included) zero afterwards."""
+    ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device())
+    ctx.register_layer(0, pz.LAYER_CONV, 1, n, 1, False)
+    _, _, padded = pz.shard_range(n, 1, 0)
+    g = S.integer_grads(n, 1, seed=n)[0]
+    w0 = (S.rng(n + 1).integers(-1023, 1024, size=n) * 2.0 ** -10).astype(np.float32)
+    gflat = torch.full((padded,), 5.0, device="cuda")
+    gflat[:n] = dev(g)
+    wflat = torch.full((padded,), -3.0, device="cuda")
+    wflat[:n] = dev(w0)
+    ctx.bind_ps_buffers(0, gflat, wflat, n, pz.PS_ZERO_GRAD)
+    lr = 2.0 ** -7
+    ctx.sync_ps(0, gflat, wflat, n, lr)
+    ctx.wait_layer(0)
+    ctx.iteration_end()
+    torch.cuda.synchronize()
+    out = host(wflat)
+    assert np.array_equal(out[:n].astype(np.float64), O.ps_step_flat(w0, [g], lr))
+    assert np.all(out[n:] == -3.0)
+    assert np.all(host(gflat) == 0)
+    ctx.close()

@@ -67,32 +67,37 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         return pz.Context(rank=rank, world=world, device=local, nccl_id=obj[0], flags=flags)
 
-    # (b1) SFB factor all-gather inside poseidon_sync_fc_sfb
-    ctx = new_ctx(0)
+    # (b1) SFB factor all-gather inside poseidon_sync_fc_sfb: plain cudaMalloc gather buffers vs NCCL
+    #      symmetric windows (FLAG_SYMM_SFB)
     sfb_layers = () if only_ps else (("fc6", 4096, 9216), ("fc7", 4096, 4096), ("i22k_fc8", 21841, 4096))
-    for lid, (name, M, N) in enumerate(sfb_layers):
-        K = 256
-        ctx.register_layer(lid, pz.LAYER_FC, M, N, K)
-        U = torch.randn(K, M, device=dev) / K
-        V = torch.randn(K, N, device=dev).relu()
-        W = torch.zeros(M, N, device=dev)
-        comm = []
-        for _ in range(6):
-            dist.barrier()
-            ctx.sync_fc_sfb(lid, U, V, W, None, 0.0, s)
-            ctx.wait_layer(lid, s)
-            ctx.iteration_end(s)
-            torch.cuda.synchronize()
-            comm.append(ctx.layer_stats(lid)["comm_ms"])
-        t = sorted(comm[1:])[len(comm[1:]) // 2]
-        tt = torch.tensor([t], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt.item())
-        per_rank = K * (M + N + M // K + 1) * 4  # U + V slot (+ bias column sums) per rank
-        alg = per_rank * P / (t / 1e3) / 1e9
-        out({"what": f"poseidon SFB all-gather ({name}, K=256)", "P": P, "MB_per_rank": round(per_rank / 2**20, 2),
-             "ms": round(t, 4), "busbw_GBps": round(alg * (P - 1) / P, 1)})
-    ctx.close()
+    for flags, tag in ((0, "cudaMalloc"), (pz.FLAG_SYMM_SFB, "symmetric window"),
+                       (pz.FLAG_NVLS_SFB, "NVLS multicast broadcast")):
+        ctx = new_ctx(flags)
+        for lid, (name, M, N) in enumerate(sfb_layers):
+            K = 256
+            ctx.register_layer(lid, pz.LAYER_FC, M, N, K)
+            U = torch.randn(K, M, device=dev) / K
+            V = torch.randn(K, N, device=dev).relu()
+            W = torch.zeros(M, N, device=dev)
+            comm = []
+            for _ in range(8):
+                dist.barrier()
+                torch.cuda._sleep(200_000)   # queue the whole sync before it runs (device time only)
+                ctx.sync_fc_sfb(lid, U, V, W, None, 0.0, s)
+                ctx.wait_layer(lid, s)
+                ctx.iteration_end(s)
+                torch.cuda.synchronize()
+                comm.append(ctx.layer_stats(lid)["comm_ms"])
+            t = sorted(comm[2:])[len(comm[2:]) // 2]
+            tt = torch.tensor([t], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+            per_rank = K * (M + N + M // K + 1) * 4  # U + V slot (+ bias column sums) per rank
+            alg = per_rank * P / (t / 1e3) / 1e9
+            out({"what": f"poseidon SFB all-gather ({name}, K=256, {tag})", "P": P, "path": ctx.sfb_path(lid),
+                 "MB_per_rank": round(per_rank / 2**20, 2), "ms": round(t, 4),
+                 "busbw_GBps": round(alg * (P - 1) / P, 1)})
+        ctx.close()
 
     # (b2) PS of a 37.7M-parameter layer: NCCL path vs fused NVLS kernel
     M, N = 4096, 9216
