@@ -183,7 +183,10 @@ cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww
     return v ? atoi(v) : 4;
   }();
   if (env_grid > 0 && env_grid < max_blocks) max_blocks = env_grid;
-  int blocks = (int)((n4 + 255) / 256);
+  // one pass of U float4 per thread: small layers get few CTAs (a CTA waiting at the entry barrier for
+  // a slower rank occupies an SM slot the backward could use)
+  const int64_t per_block = 256 * (int64_t)(env_u == 8 ? 8 : env_u == 2 ? 2 : 4);
+  int blocks = (int)((n4 + per_block - 1) / per_block);
   if (blocks < 1) blocks = 1;
   if (blocks > max_blocks) blocks = max_blocks;
   NvlsMomentum mom{vel, inv_p, lr, mu, wd};

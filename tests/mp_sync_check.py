@@ -13,6 +13,8 @@ Checks, at world = P:
      auto and forced PS, DWBP on and off): all ranks' parameters
      bit-identical, DWBP on == off bitwise, and the step equals single-GPU SGD
      on the concatenated P*K batch (torch fp32 reference, TF32 gate).
+  5. Full size in bench.py's N > 1 configuration: C3 fc6 SFB on symmetric windows (sampled rows vs O4)
+     and a 37.7M-parameter PS layer through the fused NVLS kernel (sampled elements vs O6).
 Prints "MP_OK <rank>" on success; any failure raises.
 """
 import os
@@ -300,6 +302,52 @@ def main():
         for nv in (False, True):
             assert torch.equal(results[(scheme, "on", nv)], results[(scheme, "off", nv)]), \
                 f"DWBP on/off differ ({scheme}, nvls {nv})"
+    # ---- 5. full size in bench.py's N > 1 launch configuration (SYMM_SFB | NVLS_PS): C3 fc6 as SFB
+    #          (4096 x 9216, K = 256) and a 37.7M-parameter PS layer in the NVLS arena, sampled against
+    #          the oracle (O4 rows / O6 elements) ----
+    cf = new_ctx(pz.FLAG_SYMM_SFB | pz.FLAG_NVLS_PS)
+    M, N, K = 4096, 9216, 256
+    assert cf.register_layer(0, pz.LAYER_FC, M, N, K) == pz.SCHEME_SFB
+    cf.register_layer(1, pz.LAYER_CONV, M, N, 1, True, pz.SCHEME_PS)
+    cf.ps_arena()
+    W, b = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, P, seed=500)
+    Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+    cf.sync_fc_sfb(0, torch.from_numpy(Us[rank]).to(dev), torch.from_numpy(Vs[rank]).to(dev), Wd, bd, 0.5)
+    cf.wait_layer(0)
+    n = M * N + M
+    gp, wp, padded = cf.ps_layer_buffers(1)
+    from paper_1512_06216_b200.binding import device_view
+    gv, wv = device_view(gp, (padded,)), device_view(wp, (padded,))
+    grads = S.dense_grads(n, P, seed=600)
+    w0 = S.rng(601).standard_normal(n).astype(np.float32)
+    wv[:n] = torch.from_numpy(w0).to(dev)
+    gv[:n] = torch.from_numpy(grads[rank]).to(dev)
+    torch.cuda.synchronize()
+    dist.barrier()
+    cf.set_lr(0.05)
+    cf.backprop_hook(1, torch.cuda.current_stream())
+    cf.wait_layer(1)
+    cf.iteration_end()
+    torch.cuda.synchronize()
+    rows = np.unique(np.concatenate([[0, 1, 255, 256, M - 1], S.rng(502).integers(0, M, 43)]))
+    Wr, br = O.sync_step_rows(W[rows], b[rows], Us, Vs, 0.5, rows)
+    Wout = Wd.cpu().numpy()
+    assert O.update_error(W[rows], Wout[rows], Wr) <= 2e-3, "full-size SFB (symmetric wire) off the TF32 gate"
+    assert O.update_error_fp32(b[rows], bd.cpu().numpy()[rows], br) <= 1e-5
+    assert allsame(Wd) and allsame(bd)
+    idx = np.unique(np.concatenate([[0, n - 1, n // P, padded // P - 1], S.rng(603).integers(0, n, 4093)]))
+    idx = idx[idx < n]
+    ref = O.ps_step_flat(w0[idx], [g[idx] for g in grads], 0.05)
+    out = wv[:n].cpu().numpy()[idx]
+    assert O.update_error_fp32(w0[idx], out, ref) <= 1e-5, "full-size NVLS PS off the 1e-5 gate"
+    assert allsame(wv[:n].contiguous())
+    assert float(gv.abs().sum()) == 0.0
+    if rank == 0:
+        print(f"full-size: SFB path {cf.sfb_path(0)}, PS {cf.nvls_status()}", flush=True)
+    del grads
+    cf.close()
+
     dist.barrier()
     print(f"MP_OK {rank}", flush=True)
     dist.destroy_process_group()
