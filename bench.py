@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--sfb-wire", default="auto", choices=["auto", "nccl", "symm", "nvls"],
                     help="SFB factor broadcast: NCCL all-gather on plain buffers, on NCCL symmetric windows, "
                          "or the library's NVLS multicast kernel; auto = symm when N > 1")
+    ap.add_argument("--ssp", type=int, default=0, choices=[0, 1],
+                    help="staleness s of the SSP consistency model (P:L399-402, E11); 0 = BSP (the paper's "
+                         "headline setting)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--momentum", type=float, default=0.0, help="f4: Lambda momentum (0 = plain SGD hot path)")
     ap.add_argument("--weight-decay", type=float, default=0.0, help="f4: Lambda weight decay")
@@ -82,8 +85,9 @@ METRIC = "images/sec (exposed sync ms/iter and % of roofline alongside)"
 
 def workload_config(args, cfg, world):
     """The `config` object both arms print (identical for the driver's ratio)."""
+    consistency = "" if not getattr(args, "ssp", 0) else ", SSP staleness 1"
     return {"workload": f"{args.config} {cfg['name']} data-parallel training step with Poseidon sync "
-                        f"(SACP + DWBP), synthetic data",
+                        f"(SACP + DWBP{consistency}), synthetic data",
             "global_batch": world * cfg["batch"], "per_gpu_batch": cfg["batch"],
             "parallelism": f"dp{world}",
             "l2": "inputs larger than L2 (C3: images 158 MB + weights 244 MB per step)"}
@@ -266,6 +270,8 @@ def run_poseidon(args):
         flags |= pz.FLAG_NVLS_PS
     sfb_wire = ("symm" if args.sfb_wire == "auto" else args.sfb_wire) if world > 1 else "none (P=1)"
     flags |= {"symm": pz.FLAG_SYMM_SFB, "nvls": pz.FLAG_NVLS_SFB}.get(sfb_wire, 0)
+    if args.ssp:
+        flags |= pz.FLAG_SSP1
     ctx = pz.Context(rank=rank, world=world, device=local, nccl_id=nccl_id, flags=flags)
 
     torch.manual_seed(6216)          # identical weights on every rank
@@ -273,7 +279,7 @@ def run_poseidon(args):
     recon = pz.RECON_TF32 if args.recon == "tf32" else pz.RECON_FP32
     if args.memory_format == "channels_last":
         model.to(memory_format=torch.channels_last)   # before PoseidonSync makes params buffer views
-    sync = PoseidonSync(model, ctx, K=K, lr=args.lr, scheme=scheme, recon=recon, arena=use_nvls)
+    sync = PoseidonSync(model, ctx, K=K, lr=args.lr, scheme=scheme, recon=recon, arena=use_nvls or bool(args.ssp))
     if args.momentum or args.weight_decay:
         ctx.set_momentum(args.momentum, args.weight_decay)
 
@@ -475,7 +481,7 @@ def run_poseidon(args):
                         "ps_path": ("nvls-fused" if sync.nvls_active else
                                     ("nccl rs/k2/ag" if world > 1 else "k2 (P=1)")),
                         "nvls_status": ctx.nvls_status(),
-                        "sfb_wire": sfb_wire,
+                        "sfb_wire": sfb_wire, "ssp": args.ssp,
                         "sfb_paths": sorted({ctx.sfb_path(d["id"]) for d in sync.describe()
                                              if d["scheme"] == "SFB"}) if world > 1 else []},
             "exposed_sync_ms": exposed, "sync_total_ms": sync_total,

@@ -84,6 +84,12 @@ typedef struct {
 #define POSEIDON_FLAG_NVLS_SFB 0x10u   /* SFB factor "broadcast" as one NVLink-SHARP multicast store per
                                          rank into symmetric gather buffers, instead of an NCCL all-gather
                                          (implies POSEIDON_FLAG_SYMM_SFB) */
+#define POSEIDON_FLAG_SSP1 0x20u       /* stale synchronous parallel with staleness s = 1 (
+                                         reading Z19): the update of a layer's sync t is applied at the
+                                         layer's hook of iteration t+1, after that backward has read W, so
+                                         forward t+1 reads every update of iterations <= t-1.  Gradient and
+                                         factor buffers are double-buffered; PS layers need the arena.
+                                         Incompatible with POSEIDON_FLAG_DWBP_OFF. */
 
 typedef struct poseidon_ctx* poseidon_ctx_t;
 
@@ -221,6 +227,9 @@ poseidon_status_t poseidon_bind_sfb_params(poseidon_ctx_t ctx, int32_t layer_id,
  * gradient.  *nvls_active (nullable) = 1 if that path is active;
  * otherwise the arena is plain device memory and the NCCL path is used. */
 poseidon_status_t poseidon_ps_arena(poseidon_ctx_t ctx, int32_t* nvls_active);
+/* A PS layer's arena segments: *grad = the gradient buffer the layer's NEXT sync reduces (with
+ * POSEIDON_FLAG_SSP1 two buffers alternate: re-point the parameters' gradients after every
+ * iteration), *W = its parameters, *padded_n = segment length in floats. */
 poseidon_status_t poseidon_ps_layer_buffers(poseidon_ctx_t ctx, int32_t layer_id, float** grad, float** W,
                                             int64_t* padded_n);
 /* How SFB layer `layer_id` moves its factors at world > 1: 0 = NCCL all-gather on plain device
@@ -241,6 +250,11 @@ poseidon_status_t poseidon_set_lr(poseidon_ctx_t ctx, float lr);           /* lr
  * layer; mu = weight_decay = 0 returns the layer to plain SGD.  0 <= mu < 1, weight_decay >= 0. */
 poseidon_status_t poseidon_set_momentum(poseidon_ctx_t ctx, int32_t layer_id, float mu, float weight_decay);
 poseidon_status_t poseidon_set_recon(poseidon_ctx_t ctx, int32_t layer_id /* -1: all */, int32_t recon);
+
+/* SSP (POSEIDON_FLAG_SSP1): apply every layer's deferred update now (in layer-id order, identical on
+ * every rank: collective).  Call it on all ranks after the last iteration (and before reading the
+ * parameters); afterwards poseidon_wait_layer orders a consumer after the updates.  No-op without SSP. */
+poseidon_status_t poseidon_flush(poseidon_ctx_t ctx, poseidon_stream_t stream);
 
 /* Next-forward barrier: `consumer` waits until layer_id's latest sync is done
  * (under DWBP_OFF: until every layer's sync of the last iteration is done). */

@@ -371,3 +371,22 @@ def ps_step_flat_momentum(w, v, grads: Sequence[np.ndarray], lr: float, mu: floa
         v1[lo:hi] = mu * v[lo:hi] + lr * (s / P + wd * w[lo:hi])
         w1[lo:hi] = w[lo:hi] - v1[lo:hi]
     return w1, v1
+
+
+# --------------------------------------------------------------------------
+# O10 — stale synchronous parallel with staleness s ("if a worker reads from server at
+# iteration t, it is guaranteed to receive all updates from all workers computed at and before
+# iteration t-s-1"), read at the staleness bound (reading Z19): the parameters a
+# worker's forward of iteration t uses contain exactly the updates of iterations <= t-s-1.
+# --------------------------------------------------------------------------
+def ssp_visible_weights(W0, b0, steps, lr: float, s: int = 1):
+    """steps[t] = (Us, Vs): the sufficient factors every worker produces at iteration t (fixed
+    inputs, independent of the parameters).  Returns vis with vis[t] = (W, b) the forward of
+    iteration t reads, for t = 0 .. len(steps) + s (the last entries are what remains after all
+    updates have been applied, i.e. after a flush)."""
+    applied = [(np.asarray(W0, np.float64), None if b0 is None else np.asarray(b0, np.float64))]
+    for Us, Vs in steps:                      # applied[k] = parameters after the updates of 0..k-1
+        W, b = applied[-1]
+        applied.append(sync_step(W, b, Us, Vs, lr))
+    T = len(steps)
+    return [applied[min(max(0, t - s), T)] for t in range(T + s + 1)]

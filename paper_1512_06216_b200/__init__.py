@@ -6,7 +6,7 @@ the DWBP glue that drives it from PyTorch autograd (``dwbp``).
 """
 from .binding import (  # noqa: F401
     LAYER_CONV, LAYER_FC, SCHEME_PS, SCHEME_SFB, RECON_TF32, RECON_FP32, FLAG_DWBP_OFF,
-    FLAG_NO_PRIORITY, FLAG_NVLS_PS, FLAG_SYMM_SFB, FLAG_NVLS_SFB, SFB_PATH_NCCL, SFB_PATH_NCCL_SYMM, SFB_PATH_NVLS,
+    FLAG_NO_PRIORITY, FLAG_NVLS_PS, FLAG_SYMM_SFB, FLAG_NVLS_SFB, FLAG_SSP1, SFB_PATH_NCCL, SFB_PATH_NCCL_SYMM, SFB_PATH_NVLS,
     PS_ZERO_GRAD, Context, PoseidonError, choose_scheme, shard_range,
     get_unique_id, launch_count, sfb_simulated, ps_simulated, ps_shard_update, reconstruct_sgd,
 )

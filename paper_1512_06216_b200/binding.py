@@ -23,7 +23,7 @@ ERR_SHAPE, ERR_ALIGNMENT, ERR_UNSUPPORTED, ERR_STATE = -5, -6, -7, -8
 SCHEME_PS, SCHEME_SFB = 0, 1
 LAYER_CONV, LAYER_FC = 0, 1
 RECON_TF32, RECON_FP32 = 0, 1
-FLAG_DWBP_OFF, FLAG_NO_PRIORITY, FLAG_NVLS_PS, FLAG_SYMM_SFB, FLAG_NVLS_SFB = 0x1, 0x2, 0x4, 0x8, 0x10
+FLAG_DWBP_OFF, FLAG_NO_PRIORITY, FLAG_NVLS_PS, FLAG_SYMM_SFB, FLAG_NVLS_SFB, FLAG_SSP1 = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 SFB_PATH_NCCL, SFB_PATH_NCCL_SYMM, SFB_PATH_NVLS = 0, 1, 2
 PS_ZERO_GRAD = 0x1
 
@@ -105,6 +105,7 @@ _SIGS = {
     "poseidon_ps_layer_buffers": (_i32, [_vp, _i32, _P(_vp), _P(_vp), _P(_i64)]),
     "poseidon_nvls_status": (ctypes.c_char_p, [_vp]),
     "poseidon_sfb_path": (_i32, [_vp, _i32]),
+    "poseidon_flush": (_i32, [_vp, _vp]),
     "poseidon_set_recon": (_i32, [_vp, _i32, _i32]),
     "poseidon_wait_layer": (_i32, [_vp, _i32, _vp]),
     "poseidon_iteration_end": (_i32, [_vp, _vp, _P(IterStats)]),
@@ -215,7 +216,7 @@ class Context:
         h = _vp()
         _check(lib.poseidon_init(world, ctypes.byref(topo), ctypes.byref(h)))
         self.h = h
-        self.rank, self.world, self.device = rank, world, device
+        self.rank, self.world, self.device, self.flags = rank, world, device, flags
 
     def close(self):
         if getattr(self, "h", None):
@@ -256,6 +257,10 @@ class Context:
         g, w, n = _vp(), _vp(), _i64()
         _check(lib.poseidon_ps_layer_buffers(self.h, layer_id, ctypes.byref(g), ctypes.byref(w), ctypes.byref(n)))
         return g.value, w.value, n.value
+
+    def flush(self, stream=None):
+        """SSP: apply every layer's deferred update (collective; no-op without FLAG_SSP1)."""
+        _check(lib.poseidon_flush(self.h, _stream(stream)))
 
     def sfb_path(self, layer_id) -> int:
         r = lib.poseidon_sfb_path(self.h, layer_id)

@@ -93,6 +93,9 @@ struct Layer {
   // Vg [P][N][ldk], Bs [P][M] (per-worker column sums of U); optional staging [K][M], [K][N]
   int64_t ldk = 0;
   float *Ug = nullptr, *Vg = nullptr, *Bs = nullptr;
+  // POSEIDON_FLAG_SSP1: a second gather set (sync t packs/gathers into set t % 2 while the deferred
+  // update of sync t-1 still reads set (t-1) % 2)
+  float *Ug2 = nullptr, *Vg2 = nullptr, *Bs2 = nullptr;
   // POSEIDON_FLAG_SYMM_SFB: Ug|Vg|Bs are one ncclMemAlloc buffer registered as a symmetric window
   void* symm = nullptr;
   ncclWindow_t win = nullptr;
@@ -110,6 +113,14 @@ struct Layer {
   float mu = 0.f, wd = 0.f;
   float *vel = nullptr, *vel_b = nullptr;
   size_t arena_off = 0;      // byte offset of this layer in both arenas
+  float* gsets[2] = {nullptr, nullptr};  // arena gradient buffers (SSP: two, alternating per sync)
+  int64_t nsync = 0;         // syncs issued so far (SSP set parity)
+  // SSP (s = 1): the sync whose update is deferred to this layer's next hook (or poseidon_flush)
+  bool ssp_pend = false;
+  int64_t pend_iter = -1;
+  int pend_set = 0;
+  float pend_lr = 0.f;
+  float *pend_W2 = nullptr, *pend_bias2 = nullptr, *pend_grad2 = nullptr;
   EvSet ev[RING];
   bool events_created = false;
   int64_t last_iter = -1;  // iteration of the latest sync
@@ -148,9 +159,11 @@ struct poseidon_ctx {
   bool ps_nvls = false;        // PS arena is symmetric and the device communicator exists
   std::string devcomm_error;
   float *arena_g = nullptr, *arena_w = nullptr;
+  float* arena_g2 = nullptr;  // SSP: second gradient arena
   size_t arena_bytes = 0;
   bool arena_nccl_mem = false;
-  ncclWindow_t win_g = nullptr, win_w = nullptr;
+  ncclWindow_t win_g = nullptr, win_w = nullptr, win_g2 = nullptr;
+  bool ssp = false;           // FLAG_SSP1
   NvlsState* nvls = nullptr;
   std::string nvls_error;
 };
@@ -210,47 +223,63 @@ poseidon_status_t producer_guard(poseidon_ctx_t c, Layer& L, cudaStream_t produc
   return POSEIDON_OK;
 }
 
-// Comm + update part of an SFB sync (steps 2 and 3 of P:L330-331).
-poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* W, float* bias, float lr,
-                                  cudaEvent_t wait_ev) {
-  EvSet& e = L.ev[c->iter % RING];
+struct GatherSet {
+  float *U, *V, *B;
+};
+GatherSet gather_set(const Layer& L, int set) {
+  return set ? GatherSet{L.Ug2, L.Vg2, L.Bs2} : GatherSet{L.Ug, L.Vg, L.Bs};
+}
+// the gather set the next sync of this layer packs into (always 0 without SSP)
+int next_set(poseidon_ctx_t c, const Layer& L) { return c->ssp ? (int)(L.nsync & 1) : 0; }
+
+// SFB step 2: broadcast every worker's factors = all-gather of gather set `set`, on the
+// comm stream after `wait_ev`.  Records e.start and e.gathered.
+poseidon_status_t sfb_comm(poseidon_ctx_t c, Layer& L, int set, EvSet& e, cudaEvent_t wait_ev, IterRecord& r) {
   const int P = c->world;
+  const GatherSet g = gather_set(L, set);
   CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
-  IterRecord& r = open_record(c);
   e.g_eff = e.start;
-  if (P > 1 && L.bcast) {
+  if (P <= 1) return POSEIDON_OK;
+  const size_t ucount = (size_t)(L.M * L.ldk), vcount = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
+  const uint64_t per = (uint64_t)(ucount + vcount + bcount) * 4u;
+  if (L.bcast) {
     // the paper's "broadcast" done by the NVSwitch: one multicast store of this rank's slots lands in
     // every rank's gather buffers (barrier, multimem.st, barrier; k_ps_nvls.cu)
-    const size_t ucount = (size_t)(L.M * L.ldk), vcount = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
-    const size_t vbase = (size_t)((char*)L.Vg - (char*)L.symm), bbase = (size_t)((char*)L.Bs - (char*)L.symm);
-    cudaError_t err = launch_sfb_bcast_nvls(c->nvls, L.win, (size_t)c->rank * ucount * 4, (int64_t)ucount,
-                                            vbase + (size_t)c->rank * vcount * 4, (int64_t)vcount,
-                                            bbase + (size_t)c->rank * bcount * 4, (int64_t)bcount, kNvlsBlocks,
+    const size_t ub = (size_t)((char*)g.U - (char*)L.symm), vb = (size_t)((char*)g.V - (char*)L.symm),
+                 bb = (size_t)((char*)g.B - (char*)L.symm);
+    cudaError_t err = launch_sfb_bcast_nvls(c->nvls, L.win, ub + (size_t)c->rank * ucount * 4, (int64_t)ucount,
+                                            vb + (size_t)c->rank * vcount * 4, (int64_t)vcount,
+                                            bb + (size_t)c->rank * bcount * 4, (int64_t)bcount, kNvlsBlocks,
                                             c->comm_stream);
     if (err != cudaSuccess) return cuda_fail(err, "NVLS factor broadcast launch");
-    const uint64_t per = (uint64_t)(ucount + vcount + bcount) * 4u;
     r.sent += per;  // one copy into the switch
-    r.recv += per * (uint64_t)(P - 1);
-    CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
-    e.g_eff = e.gathered;
-  } else if (P > 1) {
-    const size_t ucount = (size_t)(L.M * L.ldk), vcount = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
+  } else {
     NC_TRY(ncclGroupStart());
-    NC_TRY(ncclAllGather(L.Ug + (size_t)c->rank * ucount, L.Ug, ucount, ncclFloat32, c->comm, c->comm_stream));
-    NC_TRY(ncclAllGather(L.Vg + (size_t)c->rank * vcount, L.Vg, vcount, ncclFloat32, c->comm, c->comm_stream));
-    NC_TRY(ncclAllGather(L.Bs + (size_t)c->rank * bcount, L.Bs, bcount, ncclFloat32, c->comm, c->comm_stream));
+    NC_TRY(ncclAllGather(g.U + (size_t)c->rank * ucount, g.U, ucount, ncclFloat32, c->comm, c->comm_stream));
+    NC_TRY(ncclAllGather(g.V + (size_t)c->rank * vcount, g.V, vcount, ncclFloat32, c->comm, c->comm_stream));
+    NC_TRY(ncclAllGather(g.B + (size_t)c->rank * bcount, g.B, bcount, ncclFloat32, c->comm, c->comm_stream));
     NC_TRY(ncclGroupEnd());
-    const uint64_t per = (uint64_t)(ucount + vcount + bcount) * 4u;
     r.sent += per;  // handed to NCCL once; NCCL forwards it to P-1 peers
-    r.recv += per * (uint64_t)(P - 1);
-    CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
-    e.g_eff = e.gathered;
   }
-  CU_TRY(cudaStreamWaitEvent(c->recon_stream, e.g_eff, 0));
-  CU_TRY(cudaEventRecord(e.kstart, c->recon_stream));
-  e.ks_eff = e.kstart;
-  e.ke_eff = e.kend;
+  r.recv += per * (uint64_t)(P - 1);
+  CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+  e.g_eff = e.gathered;
+  return POSEIDON_OK;
+}
+
+// SFB step 3: reconstruct from gather set `set` and apply the update, on the recon stream
+// after `src_g` (the set's all-gather) and `extra` (SSP: this layer's current backward is done with
+// W).  Records dst.kstart / kend / done.
+poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, float* bias, float lr, cudaEvent_t src_g,
+                             cudaEvent_t extra, EvSet& dst) {
+  const int P = c->world;
+  const GatherSet g = gather_set(L, set);
+  CU_TRY(cudaStreamWaitEvent(c->recon_stream, src_g, 0));
+  if (extra) CU_TRY(cudaStreamWaitEvent(c->recon_stream, extra, 0));
+  CU_TRY(cudaEventRecord(dst.kstart, c->recon_stream));
+  dst.ks_eff = dst.kstart;
+  dst.ke_eff = dst.kend;
   const float alpha = -lr / (float)P;
   cudaError_t err;
   const bool mom = (L.vel != nullptr);
@@ -258,61 +287,84 @@ poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float*
   // v_partial = fmaf(lr/P, acc, mu * v), then momentum_apply: v += lr*wd*w, w -= v.
   float* target = mom ? L.vel : W;
   const float a1 = mom ? (lr / (float)P) : alpha, b1 = mom ? L.mu : 1.0f;
-  if (L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(L.Ug, L.Vg, L.ldk, L.M, L.N, target))
-    err = launch_recon_tcgen05(L.Ug, L.Vg, P, L.K, L.ldk, L.M, L.N, target, a1, b1, c->recon_stream);
+  if (L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(g.U, g.V, L.ldk, L.M, L.N, target))
+    err = launch_recon_tcgen05(g.U, g.V, P, L.K, L.ldk, L.M, L.N, target, a1, b1, c->recon_stream);
   else
-    err = launch_recon_simt(L.Ug, L.Vg, P, L.K, L.ldk, L.M, L.N, target, a1, b1, c->recon_stream);
+    err = launch_recon_simt(g.U, g.V, P, L.K, L.ldk, L.M, L.N, target, a1, b1, c->recon_stream);
   if (err != cudaSuccess) return cuda_fail(err, "reconstruct+sgd launch");
   if (mom) {
     err = launch_momentum_apply(W, L.vel, L.M * L.N, lr * L.wd, c->recon_stream);
     if (err != cudaSuccess) return cuda_fail(err, "momentum apply launch");
   }
   if ((err = debug_sync(c->recon_stream, "K1/K1r reconstruct+sgd")) != cudaSuccess) return cuda_fail(err, "K1");
-  CU_TRY(cudaEventRecord(e.kend, c->recon_stream));  // kernel_ms = K1/K1r alone
+  CU_TRY(cudaEventRecord(dst.kend, c->recon_stream));  // kernel_ms = K1/K1r alone
   if (bias) {
-    err = mom ? launch_bias_momentum(L.Bs, L.M, P, bias, L.vel_b, L.M, lr, L.mu, L.wd, c->recon_stream)
-              : launch_bias_update(L.Bs, L.M, P, bias, L.M, alpha, c->recon_stream);
+    err = mom ? launch_bias_momentum(g.B, L.M, P, bias, L.vel_b, L.M, lr, L.mu, L.wd, c->recon_stream)
+              : launch_bias_update(g.B, L.M, P, bias, L.M, alpha, c->recon_stream);
     if (err != cudaSuccess) return cuda_fail(err, "bias update launch");
     if ((err = debug_sync(c->recon_stream, "bias update")) != cudaSuccess) return cuda_fail(err, "bias");
   }
-  CU_TRY(cudaEventRecord(e.done, c->recon_stream));
+  CU_TRY(cudaEventRecord(dst.done, c->recon_stream));
+  return POSEIDON_OK;
+}
+
+// BSP SFB sync (steps 2 and 3 of P:L330-331) of the current iteration.
+poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* W, float* bias, float lr,
+                                  cudaEvent_t wait_ev) {
+  EvSet& e = L.ev[c->iter % RING];
+  IterRecord& r = open_record(c);
+  poseidon_status_t st = sfb_comm(c, L, 0, e, wait_ev, r);
+  if (st) return st;
+  st = sfb_update(c, L, 0, W, bias, lr, e.g_eff, nullptr, e);
+  if (st) return st;
   r.layers.push_back(id);
   return POSEIDON_OK;
 }
 
-// PS sync (Alg. 3 lines 1-3 / Alg. 1 master): RS -> K2 -> AG, all on comm_stream.
-poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* grad, float* W, float lr,
-                                 cudaEvent_t wait_ev) {
-  EvSet& e = L.ev[c->iter % RING];
+bool ps_fused(poseidon_ctx_t c, const Layer& L) { return c->world > 1 && c->ps_nvls && L.in_arena; }
+
+// PS reduce-scatter leg (Alg. 3 line 1-2 / Alg. 1 "Collect gradients") of gradient buffer `grad` on
+// the comm stream after `wait_ev`.  On the fused NVLS path the reduction happens inside the update
+// kernel, so nothing is launched here.  Records e.start (and e.gathered).
+poseidon_status_t ps_comm(poseidon_ctx_t c, Layer& L, float* grad, EvSet& e, cudaEvent_t wait_ev, IterRecord& r) {
   const int P = c->world;
   CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
-  IterRecord& r = open_record(c);
-  if (P > 1 && c->ps_nvls && L.in_arena) {
+  e.g_eff = e.ks_eff = e.start;
+  if (ps_fused(c, L) || P <= 1) return POSEIDON_OK;
+  NC_TRY(ncclReduceScatter(grad, grad + (size_t)c->rank * L.S, (size_t)L.S, ncclFloat32, ncclSum, c->comm,
+                           c->comm_stream));
+  r.sent += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
+  r.recv += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
+  CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+  e.g_eff = e.ks_eff = e.gathered;
+  return POSEIDON_OK;
+}
+
+// PS update + all-gather legs (K2 "Updates the part of model parameters", Alg. 1) of the
+// gradient buffer `grad` (gradient set `set` of the arena on the fused path), then the gradient clear.
+// `mark_kstart` records dst.kstart first (SSP: the update is not adjacent to its reduce-scatter).
+poseidon_status_t ps_update(poseidon_ctx_t c, Layer& L, float* grad, int set, float* W, float lr, EvSet& dst,
+                            IterRecord& r, bool mark_kstart) {
+  const int P = c->world;
+  if (mark_kstart) {
+    CU_TRY(cudaEventRecord(dst.kstart, c->comm_stream));
+    dst.ks_eff = dst.kstart;
+  }
+  if (ps_fused(c, L)) {
     // fused one-kernel PS over NVLink SHARP (reduce-scatter + K2 + all-gather + zero-grad)
-    e.g_eff = e.ks_eff = e.start;
-    e.ke_eff = e.done;
-    cudaError_t err = launch_ps_nvls(c->nvls, c->win_g, c->win_w, L.arena_off, L.arena_off, L.begin, L.end,
-                                     L.padded, -lr / (float)P, (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0, kNvlsBlocks,
-                                     L.S, L.vel, 1.0f / (float)P, lr, L.mu, L.wd, c->comm_stream);
+    dst.ke_eff = dst.done;
+    cudaError_t err = launch_ps_nvls(c->nvls, set ? c->win_g2 : c->win_g, c->win_w, L.arena_off, L.arena_off, L.begin,
+                                     L.end, L.padded, -lr / (float)P, (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0,
+                                     kNvlsBlocks, L.S, L.vel, 1.0f / (float)P, lr, L.mu, L.wd, c->comm_stream);
     if (err != cudaSuccess) return cuda_fail(err, "fused NVLS PS launch");
-    CU_TRY(cudaEventRecord(e.done, c->comm_stream));
+    CU_TRY(cudaEventRecord(dst.done, c->comm_stream));
     // bytes through NVLink per rank: the switch reads this rank's gradient for the other P-1
     // shards and writes the other ranks' updated shards here; this rank reads its reduced shard
     // and writes its updated shard once into the switch
     r.sent += (uint64_t)L.S * 4u * (uint64_t)P;
     r.recv += (uint64_t)L.S * 4u * (uint64_t)P;
-    r.layers.push_back(id);
     return POSEIDON_OK;
-  }
-  e.g_eff = e.ks_eff = e.start;
-  if (P > 1) {
-    NC_TRY(ncclReduceScatter(grad, grad + (size_t)c->rank * L.S, (size_t)L.S, ncclFloat32, ncclSum, c->comm,
-                             c->comm_stream));
-    r.sent += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
-    r.recv += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
-    CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
-    e.g_eff = e.ks_eff = e.gathered;
   }
   const float alpha = -lr / (float)P;
   const bool zero = (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0;
@@ -330,22 +382,67 @@ poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* 
   if (err != cudaSuccess) return cuda_fail(err, "ps shard update launch");
   if ((err = debug_sync(c->comm_stream, "K2 ps shard update")) != cudaSuccess) return cuda_fail(err, "K2");
   if (P > 1) {
-    CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
-    e.ke_eff = e.kend;
+    CU_TRY(cudaEventRecord(dst.kend, c->comm_stream));
+    dst.ke_eff = dst.kend;
     NC_TRY(ncclAllGather(W + (size_t)c->rank * L.S, W, (size_t)L.S, ncclFloat32, c->comm, c->comm_stream));
     r.sent += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
     r.recv += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
   } else {
-    e.ke_eff = e.done;
+    dst.ke_eff = dst.done;
   }
   if (zero && !fused_zero) {
     if (P == 1) {  // kernel_ms must not include the memset
-      CU_TRY(cudaEventRecord(e.kend, c->comm_stream));
-      e.ke_eff = e.kend;
+      CU_TRY(cudaEventRecord(dst.kend, c->comm_stream));
+      dst.ke_eff = dst.kend;
     }
     CU_TRY(cudaMemsetAsync(grad, 0, (size_t)L.padded * 4u, c->comm_stream));
   }
-  CU_TRY(cudaEventRecord(e.done, c->comm_stream));
+  CU_TRY(cudaEventRecord(dst.done, c->comm_stream));
+  return POSEIDON_OK;
+}
+
+// BSP PS sync (Alg. 3 lines 1-3 / Alg. 1 master): RS -> K2 -> AG (or the fused NVLS kernel), all on
+// the comm stream.
+poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* grad, float* W, float lr,
+                                 cudaEvent_t wait_ev) {
+  EvSet& e = L.ev[c->iter % RING];
+  IterRecord& r = open_record(c);
+  poseidon_status_t st = ps_comm(c, L, grad, e, wait_ev, r);
+  if (st) return st;
+  st = ps_update(c, L, grad, 0, W, lr, e, r, false);
+  if (st) return st;
+  r.layers.push_back(id);
+  return POSEIDON_OK;
+}
+
+// SSP s = 1 (reading Z19): this hook issues sync t's communication and applies the update of sync
+// t-1 — after this layer's backward t has finished reading W (e.ready) — so the forward of t+1 reads
+// W with every update of iterations <= t-1 (P:L123 with s = 1, at the staleness bound).
+poseidon_status_t ssp_hook(poseidon_ctx_t c, int32_t id, Layer& L, float* W, float* bias, float* grad, float lr) {
+  EvSet& e = L.ev[c->iter % RING];
+  IterRecord& r = open_record(c);
+  const int set = next_set(c, L);
+  poseidon_status_t st = (L.scheme == POSEIDON_SCHEME_SFB) ? sfb_comm(c, L, set, e, e.ready, r)
+                                                           : ps_comm(c, L, grad, e, e.ready, r);
+  if (st) return st;
+  if (L.ssp_pend) {
+    const EvSet& src = L.ev[L.pend_iter % RING];
+    st = (L.scheme == POSEIDON_SCHEME_SFB)
+             ? sfb_update(c, L, L.pend_set, L.pend_W2, L.pend_bias2, L.pend_lr, src.g_eff, e.ready, e)
+             : ps_update(c, L, L.pend_grad2, L.pend_set, L.Wps, L.pend_lr, e, r, true);
+    if (st) return st;
+  } else {
+    CU_TRY(cudaEventRecord(e.done, c->comm_stream));  // first sync: nothing to apply yet
+    e.ks_eff = e.ke_eff = e.done;
+  }
+  L.ssp_pend = true;
+  L.pend_iter = c->iter;
+  L.pend_set = set;
+  L.pend_lr = lr;
+  L.pend_W2 = W;
+  L.pend_bias2 = bias;
+  L.pend_grad2 = grad;
+  L.nsync += 1;
   r.layers.push_back(id);
   return POSEIDON_OK;
 }
@@ -355,6 +452,7 @@ poseidon_status_t sfb_after_pack(poseidon_ctx_t c, int32_t id, Layer& L, float* 
   EvSet& e = L.ev[c->iter % RING];
   CU_TRY(cudaEventRecord(e.ready, producer));
   L.last_iter = c->iter;
+  if (c->ssp) return ssp_hook(c, id, L, W, bias, nullptr, lr);
   if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
     L.pending = true;
     L.pending_lr = lr;
@@ -370,9 +468,10 @@ poseidon_status_t sfb_after_pack(poseidon_ctx_t c, int32_t id, Layer& L, float* 
 poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t ldU, const float* V, int64_t ldV,
                            cudaStream_t producer) {
   const bool round = (L.recon == POSEIDON_RECON_TF32);
-  float* u_slot = L.Ug + (size_t)c->rank * L.M * L.ldk;
-  float* v_slot = L.Vg + (size_t)c->rank * L.N * L.ldk;
-  float* b_slot = L.Bs + (size_t)c->rank * L.M;
+  const GatherSet g = gather_set(L, next_set(c, L));
+  float* u_slot = g.U + (size_t)c->rank * L.M * L.ldk;
+  float* v_slot = g.V + (size_t)c->rank * L.N * L.ldk;
+  float* b_slot = g.B + (size_t)c->rank * L.M;
   cudaError_t err = launch_pack_t(U, ldU, u_slot, L.ldk, L.K, L.M, round, b_slot, producer);
   if (err != cudaSuccess) return cuda_fail(err, "pack U launch");
   err = launch_pack_t(V, ldV, v_slot, L.ldk, L.K, L.N, round, nullptr, producer);
@@ -388,10 +487,10 @@ void free_layer(Layer& L) {
     L.symm = nullptr;
     L.win = nullptr;
   } else {
-    if (L.Ug) cudaFree(L.Ug);
-    if (L.Vg) cudaFree(L.Vg);
-    if (L.Bs) cudaFree(L.Bs);
+    for (float* q : {L.Ug, L.Vg, L.Bs, L.Ug2, L.Vg2, L.Bs2})
+      if (q) cudaFree(q);
   }
+  L.Ug2 = L.Vg2 = L.Bs2 = nullptr;
   if (L.stU) cudaFree(L.stU);
   if (L.stV) cudaFree(L.stV);
   if (L.vel) cudaFree(L.vel);
@@ -457,6 +556,8 @@ poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, 
       if (!ok) return fail(POSEIDON_ERR_UNSUPPORTED, "GPUs are not all-pairs peer connected");
     }
   }
+  if ((topo->flags & POSEIDON_FLAG_SSP1) && (topo->flags & POSEIDON_FLAG_DWBP_OFF))
+    return fail(POSEIDON_ERR_INVALID_ARG, "FLAG_SSP1 needs DWBP (the stale update is applied at the next hook)");
   auto* c = new poseidon_ctx();
   c->rank = topo->rank;
   c->world = world;
@@ -464,6 +565,7 @@ poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, 
   c->flags = topo->flags;
   c->want_nvls = (topo->flags & POSEIDON_FLAG_NVLS_PS) != 0 && world > 1;
   c->want_nvls_sfb = (topo->flags & POSEIDON_FLAG_NVLS_SFB) != 0 && world > 1;
+  c->ssp = (topo->flags & POSEIDON_FLAG_SSP1) != 0;
   c->layers.resize(64);
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -501,14 +603,13 @@ poseidon_status_t poseidon_finalize(poseidon_ctx_t c) {
   for (auto& L : c->layers) free_layer(L);
   if (c->nvls) nvls_destroy(c->comm, c->nvls);
   if (c->win_g) ncclCommWindowDeregister(c->comm, c->win_g);
+  if (c->win_g2) ncclCommWindowDeregister(c->comm, c->win_g2);
   if (c->win_w) ncclCommWindowDeregister(c->comm, c->win_w);
-  if (c->arena_nccl_mem) {
-    if (c->arena_g) ncclMemFree(c->arena_g);
-    if (c->arena_w) ncclMemFree(c->arena_w);
-  } else {
-    if (c->arena_g) cudaFree(c->arena_g);
-    if (c->arena_w) cudaFree(c->arena_w);
-  }
+  for (float* q : {c->arena_g, c->arena_g2, c->arena_w})
+    if (q) {
+      if (c->arena_nccl_mem) ncclMemFree(q);
+      else cudaFree(q);
+    }
   for (auto& r : c->rec)
     if (r.bwd_end) cudaEventDestroy(r.bwd_end);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -551,12 +652,14 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
     L.ldk = round_up(K, 4);
     const size_t P = (size_t)c->world;
     const size_t ub = P * (size_t)(M * L.ldk) * 4, vb = P * (size_t)(N * L.ldk) * 4, bb = P * (size_t)M * 4;
+    const int nsets = c->ssp ? 2 : 1;
     bool placed = false;
     if (c->world > 1 && (c->flags & (POSEIDON_FLAG_SYMM_SFB | POSEIDON_FLAG_NVLS_SFB))) {
-      // one symmetric window for the layer's three gather buffers: NCCL then runs the factor
-      // all-gather with its symmetric-memory kernels (collective call: all ranks register alike)
+      // one symmetric window for the layer's gather buffers: NCCL then runs the factor all-gather
+      // with its symmetric-memory kernels (collective call: all ranks register alike)
       const size_t ua = round_up((int64_t)ub, 4096), va = round_up((int64_t)vb, 4096);
-      const size_t total = ua + va + round_up((int64_t)bb, 4096);
+      const size_t one = ua + va + round_up((int64_t)bb, 4096);
+      const size_t total = one * (size_t)nsets;
       void* base = nullptr;
       if (ncclMemAlloc(&base, total) == ncclSuccess) {
         ncclWindow_t w = nullptr;
@@ -564,9 +667,15 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
           L.symm = base;
           L.win = w;
           L.win_comm = c->comm;
-          L.Ug = static_cast<float*>(base);
-          L.Vg = reinterpret_cast<float*>(static_cast<char*>(base) + ua);
-          L.Bs = reinterpret_cast<float*>(static_cast<char*>(base) + ua + va);
+          char* b0 = static_cast<char*>(base);
+          L.Ug = reinterpret_cast<float*>(b0);
+          L.Vg = reinterpret_cast<float*>(b0 + ua);
+          L.Bs = reinterpret_cast<float*>(b0 + ua + va);
+          if (nsets == 2) {
+            L.Ug2 = reinterpret_cast<float*>(b0 + one);
+            L.Vg2 = reinterpret_cast<float*>(b0 + one + ua);
+            L.Bs2 = reinterpret_cast<float*>(b0 + one + ua + va);
+          }
           placed = true;
           L.bcast = c->want_nvls_sfb && ensure_devcomm(c);
         } else {
@@ -578,6 +687,16 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
       CU_TRY(cudaMalloc(&L.Ug, ub));
       CU_TRY(cudaMalloc(&L.Vg, vb));
       CU_TRY(cudaMalloc(&L.Bs, bb));
+      if (nsets == 2) {
+        CU_TRY(cudaMalloc(&L.Ug2, ub));
+        CU_TRY(cudaMalloc(&L.Vg2, vb));
+        CU_TRY(cudaMalloc(&L.Bs2, bb));
+      }
+    }
+    if (nsets == 2) {
+      CU_TRY(cudaMemset(L.Ug2, 0, ub));
+      CU_TRY(cudaMemset(L.Vg2, 0, vb));
+      CU_TRY(cudaMemset(L.Bs2, 0, bb));
     }
     CU_TRY(cudaMemset(L.Ug, 0, ub));  // k columns in [K, ldk) stay zero forever
     CU_TRY(cudaMemset(L.Vg, 0, vb));
@@ -661,31 +780,37 @@ poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
   c->arena_bytes = total;
   bool symmetric = false;
   if (c->want_nvls && c->comm) {
-    void *g = nullptr, *w = nullptr;
-    ncclResult_t r1 = ncclMemAlloc(&g, total);
-    ncclResult_t r2 = (r1 == ncclSuccess) ? ncclMemAlloc(&w, total) : r1;
-    ncclResult_t r3 = (r2 == ncclSuccess) ? ncclCommWindowRegister(c->comm, g, total, &c->win_g, NCCL_WIN_COLL_SYMMETRIC) : r2;
-    ncclResult_t r4 = (r3 == ncclSuccess) ? ncclCommWindowRegister(c->comm, w, total, &c->win_w, NCCL_WIN_COLL_SYMMETRIC) : r3;
-    if (r4 == ncclSuccess) {
+    void *g = nullptr, *w = nullptr, *g2 = nullptr;
+    ncclResult_t r = ncclMemAlloc(&g, total);
+    if (r == ncclSuccess) r = ncclMemAlloc(&w, total);
+    if (r == ncclSuccess && c->ssp) r = ncclMemAlloc(&g2, total);
+    if (r == ncclSuccess) r = ncclCommWindowRegister(c->comm, g, total, &c->win_g, NCCL_WIN_COLL_SYMMETRIC);
+    if (r == ncclSuccess) r = ncclCommWindowRegister(c->comm, w, total, &c->win_w, NCCL_WIN_COLL_SYMMETRIC);
+    if (r == ncclSuccess && c->ssp) r = ncclCommWindowRegister(c->comm, g2, total, &c->win_g2, NCCL_WIN_COLL_SYMMETRIC);
+    if (r == ncclSuccess) {
       c->ps_nvls = ensure_devcomm(c);
       if (!c->ps_nvls) c->nvls_error = c->devcomm_error;
       symmetric = true;
       c->arena_nccl_mem = true;
       c->arena_g = static_cast<float*>(g);
       c->arena_w = static_cast<float*>(w);
+      c->arena_g2 = static_cast<float*>(g2);
     } else {
-      c->nvls_error = std::string("symmetric window: ") + ncclGetErrorString(r4);
+      c->nvls_error = std::string("symmetric window: ") + ncclGetErrorString(r);
       if (c->win_g) { ncclCommWindowDeregister(c->comm, c->win_g); c->win_g = nullptr; }
-      if (g) ncclMemFree(g);
-      if (w) ncclMemFree(w);
+      if (c->win_w) { ncclCommWindowDeregister(c->comm, c->win_w); c->win_w = nullptr; }
+      for (void* q : {g, w, g2})
+        if (q) ncclMemFree(q);
     }
   }
   if (!symmetric) {
     CU_TRY(cudaMalloc(&c->arena_g, total));
     CU_TRY(cudaMalloc(&c->arena_w, total));
+    if (c->ssp) CU_TRY(cudaMalloc(&c->arena_g2, total));
   }
   CU_TRY(cudaMemset(c->arena_g, 0, total));
   CU_TRY(cudaMemset(c->arena_w, 0, total));
+  if (c->arena_g2) CU_TRY(cudaMemset(c->arena_g2, 0, total));
   CU_TRY(cudaDeviceSynchronize());
   for (int32_t id = 0; id < (int32_t)c->layers.size(); ++id) {
     Layer& L = c->layers[id];
@@ -696,6 +821,8 @@ poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
     st = poseidon_bind_ps_buffers(c, id, g, w, n, POSEIDON_PS_ZERO_GRAD);
     if (st) return st;
     L.in_arena = true;
+    L.gsets[0] = g;
+    L.gsets[1] = c->arena_g2 ? reinterpret_cast<float*>(reinterpret_cast<char*>(c->arena_g2) + L.arena_off) : nullptr;
   }
   if (nvls_active) *nvls_active = c->ps_nvls ? 1 : 0;
   return POSEIDON_OK;
@@ -706,7 +833,8 @@ poseidon_status_t poseidon_ps_layer_buffers(poseidon_ctx_t c, int32_t id, float*
   poseidon_status_t st = check_layer(c, id, &L);
   if (st) return st;
   if (!L->in_arena) return fail(POSEIDON_ERR_STATE, "layer has no arena buffers (call poseidon_ps_arena)");
-  if (grad) *grad = L->grad;
+  // the gradient buffer the layer's NEXT sync reduces (SSP alternates two)
+  if (grad) *grad = (c->ssp && L->gsets[1]) ? L->gsets[next_set(c, *L)] : L->grad;
   if (W) *W = L->Wps;
   if (padded) *padded = L->padded;
   return POSEIDON_OK;
@@ -833,6 +961,10 @@ poseidon_status_t poseidon_sync_ps(poseidon_ctx_t c, int32_t id, float* grad, fl
   EvSet& e = L->ev[c->iter % RING];
   CU_TRY(cudaEventRecord(e.ready, ps));
   L->last_iter = c->iter;
+  if (c->ssp) {
+    float* g = (L->in_arena && L->gsets[1]) ? L->gsets[next_set(c, *L)] : L->grad;
+    return ssp_hook(c, id, *L, L->Wps, nullptr, g, lr);
+  }
   if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
     L->pending = true;
     L->pending_lr = lr;
@@ -859,6 +991,32 @@ poseidon_status_t poseidon_backprop_hook(poseidon_ctx_t c, int32_t id, poseidon_
   st = pack_sfb(c, *L, L->stU, L->M, L->stV, L->N, ps);
   if (st) return st;
   return sfb_after_pack(c, id, *L, L->W, L->bias, c->lr, ps);
+}
+
+poseidon_status_t poseidon_flush(poseidon_ctx_t c, poseidon_stream_t stream) {
+  poseidon_status_t st = check_ctx(c);
+  if (st) return st;
+  if (!c->ssp) return POSEIDON_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  IterRecord& r = open_record(c);
+  for (int32_t id = 0; id < (int32_t)c->layers.size(); ++id) {   // same order on every rank
+    Layer& L = c->layers[id];
+    if (!L.registered || !L.ssp_pend) continue;
+    EvSet& e = L.ev[c->iter % RING];
+    CU_TRY(cudaEventRecord(e.ready, s));
+    CU_TRY(cudaStreamWaitEvent(c->comm_stream, e.ready, 0));
+    CU_TRY(cudaEventRecord(e.start, c->comm_stream));
+    e.g_eff = e.ks_eff = e.start;
+    const EvSet& src = L.ev[L.pend_iter % RING];
+    st = (L.scheme == POSEIDON_SCHEME_SFB)
+             ? sfb_update(c, L, L.pend_set, L.pend_W2, L.pend_bias2, L.pend_lr, src.g_eff, e.ready, e)
+             : ps_update(c, L, L.pend_grad2, L.pend_set, L.Wps, L.pend_lr, e, r, true);
+    if (st) return st;
+    L.ssp_pend = false;
+    L.last_iter = c->iter;
+    r.layers.push_back(id);
+  }
+  return POSEIDON_OK;
 }
 
 poseidon_status_t poseidon_wait_layer(poseidon_ctx_t c, int32_t id, poseidon_stream_t consumer) {

@@ -13,6 +13,10 @@ Every parameterised layer of a model becomes a Poseidon layer:
   post-accumulate-grad hook once all of the layer's gradients have landed.
 * A forward pre-hook makes the next forward of layer i wait for layer i's sync
   (``poseidon_wait_layer``): the only synchronisation DWBP needs.
+* With ``FLAG_SSP1`` (staleness 1) the library applies a layer's update one hook
+  later; PS gradients then alternate between two arena buffers, so the
+  parameters' ``.grad`` views are re-pointed after every iteration, and
+  ``flush()`` applies the last deferred updates.
 
 All arithmetic of the sync happens in the library; this module only moves
 pointers and streams.  The optimiser step IS the sync (SGD applied by K1/K2),
@@ -98,6 +102,9 @@ class PoseidonSync:
         self.plans: List[LayerPlan] = []
         self.by_module: Dict[nn.Module, LayerPlan] = {}
         ctx.set_lr(self.lr)
+        self.ssp = bool(getattr(ctx, "flags", 0) & B.FLAG_SSP1)
+        if self.ssp and not arena:
+            raise ValueError("FLAG_SSP1 needs the library arena (arena=True): PS gradients are double-buffered")
         self.arena = arena
         self.nvls_active = False
         layer_id = 0
@@ -141,6 +148,18 @@ class PoseidonSync:
             self._flatten_ps(mod, plan)
         h = mod.register_forward_pre_hook(self._pre_forward(plan))
         plan.hook_handles.append(h)
+
+    def _point_grads(self, plan, gptr):
+        """Make the layer's parameter gradients views of the arena gradient buffer at gptr."""
+        mod = plan.module
+        params = [mod.weight] + ([mod.bias] if mod.bias is not None else [])
+        flat_g = B.device_view(gptr, (plan.padded,))
+        off = 0
+        for p in params:
+            k = p.numel()
+            p.grad = _view_like(flat_g[off:off + k], p)
+            off += k
+        plan.flat_g = flat_g
 
     def _bind_arena(self, plan):
         mod = plan.module
@@ -210,7 +229,23 @@ class PoseidonSync:
 
     # ------------------------------------------------------------ driver ----
     def iteration_end(self, stats: bool = False):
-        return self.ctx.iteration_end(torch.cuda.current_stream(), stats=stats)
+        out = self.ctx.iteration_end(torch.cuda.current_stream(), stats=stats)
+        if self.ssp:
+            # the next backward accumulates into the other gradient buffer (zeroed by the library
+            # before the next forward of the layer may start: poseidon_wait_layer orders it)
+            for plan in self.plans:
+                if plan.scheme == B.SCHEME_PS:
+                    gptr = self.ctx.ps_layer_buffers(plan.layer_id)[0]
+                    if gptr != plan.flat_g.data_ptr():
+                        self._point_grads(plan, gptr)
+        return out
+
+    def flush(self, stream=None):
+        """SSP: apply the deferred updates of the last iteration on every rank, then order the
+        stream after them (no-op for BSP)."""
+        s = stream or torch.cuda.current_stream()
+        self.ctx.flush(s)
+        self.wait_all(s)
 
     def wait_all(self, stream=None):
         s = stream or torch.cuda.current_stream()

@@ -13,6 +13,8 @@ Checks, at world = P:
      auto and forced PS, DWBP on and off): all ranks' parameters
      bit-identical, DWBP on == off bitwise, and the step equals single-GPU SGD
      on the concatenated P*K batch (torch fp32 reference, TF32 gate).
+  6. SSP, staleness 1: SFB + PS over 4 iterations and a flush, integer variant bit-exact vs O10 on
+     the NCCL and the NVLS paths.
   5. Full size in bench.py's N > 1 configuration: C3 fc6 SFB on symmetric windows (sampled rows vs O4)
      and a 37.7M-parameter PS layer through the fused NVLS kernel (sampled elements vs O6).
 Prints "MP_OK <rank>" on success; any failure raises.
@@ -302,6 +304,55 @@ def main():
         for nv in (False, True):
             assert torch.equal(results[(scheme, "on", nv)], results[(scheme, "off", nv)]), \
                 f"DWBP on/off differ ({scheme}, nvls {nv})"
+    # ---- 6. SSP with staleness 1 (FLAG_SSP1, reading Z19): SFB + PS (arena) over 4 iterations and a
+    #          flush, integer variant bit-exact vs O10, on the NCCL paths and on the NVLS paths ----
+    from paper_1512_06216_b200.binding import device_view
+    for flags in (pz.FLAG_SSP1 | pz.FLAG_SYMM_SFB, pz.FLAG_SSP1 | pz.FLAG_NVLS_PS | pz.FLAG_NVLS_SFB):
+        cs = new_ctx(flags)
+        M, N, K, T = 40, 72, 4, 4
+        cs.register_layer(0, pz.LAYER_FC, M, N, K)
+        cs.register_layer(1, pz.LAYER_CONV, M, N, K, True, pz.SCHEME_PS)
+        cs.ps_arena()
+        W, b, _, _, lr = S.integer_factors(M, N, K, P, seed=70)
+        steps = []
+        for t in range(T):
+            _, _, Us, Vs, _ = S.integer_factors(M, N, K, P, seed=80 + t)
+            steps.append((Us, Vs))
+        vis = O.ssp_visible_weights(W, b, steps, lr, s=1)
+        Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+        n = M * N + M
+        _, wp, padded = cs.ps_layer_buffers(1)
+        wflat = device_view(wp, (padded,))
+        wflat[:n] = torch.from_numpy(O.flatten_params(W, b).astype(np.float32)).to(dev)
+        cs.set_lr(lr)
+        torch.cuda.synchronize()
+        for t, (Us, Vs) in enumerate(steps):
+            cs.sync_fc_sfb(0, torch.from_numpy(Us[rank]).to(dev), torch.from_numpy(Vs[rank]).to(dev), Wd, bd, lr)
+            gflat = device_view(cs.ps_layer_buffers(1)[0], (padded,))
+            g = O.flatten_params(O.reconstruct(Us[rank], Vs[rank]), Us[rank].astype(np.float64).sum(0))
+            gflat[:n] = torch.from_numpy(g.astype(np.float32)).to(dev)
+            cs.backprop_hook(1, torch.cuda.current_stream())
+            cs.wait_layer(0)
+            cs.wait_layer(1)
+            cs.iteration_end()
+            torch.cuda.synchronize()
+            Wv, bv = vis[t + 1]
+            assert np.array_equal(Wd.cpu().numpy().astype(np.float64), Wv), f"SSP SFB flags={flags} t={t}"
+            assert np.array_equal(bd.cpu().numpy().astype(np.float64), bv)
+            assert np.array_equal(wflat[:n].cpu().numpy().astype(np.float64), O.flatten_params(Wv, bv)), \
+                f"SSP PS flags={flags} t={t}"
+        cs.flush()
+        cs.wait_layer(0)
+        cs.wait_layer(1)
+        torch.cuda.synchronize()
+        Wf, bf = vis[T + 1]
+        assert np.array_equal(Wd.cpu().numpy().astype(np.float64), Wf)
+        assert np.array_equal(wflat[:n].cpu().numpy().astype(np.float64), O.flatten_params(Wf, bf))
+        assert allsame(Wd) and allsame(wflat)
+        if rank == 0:
+            print(f"SSP flags={flags}: PS {cs.nvls_status()}, SFB path {cs.sfb_path(0)}", flush=True)
+        cs.close()
+
     # ---- 5. full size in bench.py's N > 1 launch configuration (SYMM_SFB | NVLS_PS): C3 fc6 as SFB
     #          (4096 x 9216, K = 256) and a 37.7M-parameter PS layer in the NVLS arena, sampled against
     #          the oracle (O4 rows / O6 elements) ----

@@ -372,3 +372,44 @@ def test_o4m_ps_equals_definition():
     w1, v1 = O.ps_step_flat_momentum(O.flatten_params(W, b), O.flatten_params(VW0, Vb0), grads, 0.2, 0.8, 0.05)
     assert np.max(np.abs(w1 - O.flatten_params(W1, b1))) < 1e-13
     assert np.max(np.abs(v1 - O.flatten_params(VW1, Vb1))) < 1e-13
+
+
+
+# ---------------------------------------------------------------- O10 SSP ----
+def _ssp_steps(M, N, K, P, T, seed):
+    out = []
+    for t in range(T):
+        _, _, Us, Vs, _ = S.integer_factors(M, N, K, P, seed=seed + t)
+        out.append((Us, Vs))
+    return out
+
+
+def test_ssp_zero_staleness_is_bsp():
+    """s = 0 is bulk synchronous: iteration t reads every update of iterations <= t-1."""
+    W, b, _, _, lr = S.integer_factors(12, 20, 3, 2, seed=1)
+    steps = _ssp_steps(12, 20, 3, 2, 4, seed=10)
+    vis = O.ssp_visible_weights(W, b, steps, lr, s=0)
+    Wt, bt = W.astype(np.float64), b.astype(np.float64)
+    for t, (Us, Vs) in enumerate(steps):
+        assert np.array_equal(vis[t][0], Wt) and np.array_equal(vis[t][1], bt)
+        Wt, bt = O.sync_step(Wt, bt, Us, Vs, lr)
+    assert np.array_equal(vis[len(steps)][0], Wt)
+
+
+def test_ssp_one_reads_exactly_updates_up_to_t_minus_2():
+    """s = 1 at the bound (P:L123 with s = 1): the forward of iteration t sees the updates of
+    iterations 0..t-2 and none of t-1: W_t = W_0 + sum_{tau <= t-2} dW_tau, with each dW_tau
+    computed independently of the others from its own factors (closed form, not the recursion)."""
+    M, N, K, P, T = 9, 14, 2, 4, 5
+    W, b, _, _, lr = S.integer_factors(M, N, K, P, seed=2)
+    steps = _ssp_steps(M, N, K, P, T, seed=20)
+    vis = O.ssp_visible_weights(W, b, steps, lr, s=1)
+    assert len(vis) == T + 2
+    dW = [(-lr / P) * sum(np.asarray(U, np.float64).T @ np.asarray(V, np.float64) for U, V in zip(Us, Vs))
+          for Us, Vs in steps]
+    for t in range(T + 2):
+        ref = W.astype(np.float64) + sum((dW[k] for k in range(0, max(0, t - 1))), np.zeros((M, N)))
+        assert np.array_equal(vis[t][0], ref), t
+    # iterations 0 and 1 both read the initial parameters; the flushed end state equals BSP's
+    assert np.array_equal(vis[0][0], vis[1][0])
+    assert np.array_equal(vis[-1][0], O.ssp_visible_weights(W, b, steps, lr, s=0)[-1][0])
