@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--ssp", type=int, default=0, choices=[0, 1],
                     help="staleness s of the SSP consistency model (P:L399-402, E11); 0 = BSP (the paper's "
                          "headline setting)")
+    ap.add_argument("--straggle-us", type=float, default=0.0,
+                    help="ablation only: every step one rank (a fixed pseudo-random sequence) is delayed by this "
+                         "many microseconds on its GPU before the forward (a straggler, P:L568)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--momentum", type=float, default=0.0, help="f4: Lambda momentum (0 = plain SGD hot path)")
     ap.add_argument("--weight-decay", type=float, default=0.0, help="f4: Lambda weight decay")
@@ -290,7 +293,14 @@ def run_poseidon(args):
         x = x.contiguous(memory_format=torch.channels_last)
     y = torch.randint(0, classes, (K,), device=dev, generator=g)
 
+    step_no = [0]
+    straggle_cycles = int(args.straggle_us * 1965)   # ~1965 MHz SM clock under load
+
     def step(xb, yb):
+        if straggle_cycles and world > 1:
+            if (step_no[0] * 2654435761 + 12345) % 1000003 % world == rank:
+                torch.cuda._sleep(straggle_cycles)
+        step_no[0] += 1
         out = model(xb)
         loss = F.cross_entropy(out, yb)
         loss.backward()
@@ -481,7 +491,7 @@ def run_poseidon(args):
                         "ps_path": ("nvls-fused" if sync.nvls_active else
                                     ("nccl rs/k2/ag" if world > 1 else "k2 (P=1)")),
                         "nvls_status": ctx.nvls_status(),
-                        "sfb_wire": sfb_wire, "ssp": args.ssp,
+                        "sfb_wire": sfb_wire, "ssp": args.ssp, "straggle_us": args.straggle_us,
                         "sfb_paths": sorted({ctx.sfb_path(d["id"]) for d in sync.describe()
                                              if d["scheme"] == "SFB"}) if world > 1 else []},
             "exposed_sync_ms": exposed, "sync_total_ms": sync_total,

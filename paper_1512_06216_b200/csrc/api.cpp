@@ -342,19 +342,13 @@ poseidon_status_t ps_comm(poseidon_ctx_t c, Layer& L, float* grad, EvSet& e, cud
 }
 
 // PS update + all-gather legs (K2 "Updates the part of model parameters", Alg. 1) of the
-// gradient buffer `grad` (gradient set `set` of the arena on the fused path), then the gradient clear.
-// `mark_kstart` records dst.kstart first (SSP: the update is not adjacent to its reduce-scatter).
-poseidon_status_t ps_update(poseidon_ctx_t c, Layer& L, float* grad, int set, float* W, float lr, EvSet& dst,
-                            IterRecord& r, bool mark_kstart) {
+// gradient buffer `grad`, then the gradient clear (the fused NVLS kernel does all of it).
+poseidon_status_t ps_update(poseidon_ctx_t c, Layer& L, float* grad, float* W, float lr, EvSet& dst, IterRecord& r) {
   const int P = c->world;
-  if (mark_kstart) {
-    CU_TRY(cudaEventRecord(dst.kstart, c->comm_stream));
-    dst.ks_eff = dst.kstart;
-  }
   if (ps_fused(c, L)) {
     // fused one-kernel PS over NVLink SHARP (reduce-scatter + K2 + all-gather + zero-grad)
     dst.ke_eff = dst.done;
-    cudaError_t err = launch_ps_nvls(c->nvls, set ? c->win_g2 : c->win_g, c->win_w, L.arena_off, L.arena_off, L.begin,
+    cudaError_t err = launch_ps_nvls(c->nvls, c->win_g, c->win_w, L.arena_off, L.arena_off, L.begin,
                                      L.end, L.padded, -lr / (float)P, (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0,
                                      kNvlsBlocks, L.S, L.vel, 1.0f / (float)P, lr, L.mu, L.wd, c->comm_stream);
     if (err != cudaSuccess) return cuda_fail(err, "fused NVLS PS launch");
@@ -409,30 +403,79 @@ poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* 
   IterRecord& r = open_record(c);
   poseidon_status_t st = ps_comm(c, L, grad, e, wait_ev, r);
   if (st) return st;
-  st = ps_update(c, L, grad, 0, W, lr, e, r, false);
+  st = ps_update(c, L, grad, W, lr, e, r);
   if (st) return st;
   r.layers.push_back(id);
   return POSEIDON_OK;
 }
 
+// SSP, PS layers: the communication of sync t is ONE all-reduce of the gradient (the reduce-scatter
+// and all-gather legs of a PS sync, applied to the gradient instead of the updated shard), so the
+// deferred update is local and the next forward depends on the previous iteration's collective only.
+poseidon_status_t ps_comm_allreduce(poseidon_ctx_t c, Layer& L, float* grad, EvSet& e, cudaEvent_t wait_ev,
+                                    IterRecord& r) {
+  const int P = c->world;
+  CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
+  CU_TRY(cudaEventRecord(e.start, c->comm_stream));
+  e.g_eff = e.start;
+  if (P <= 1) return POSEIDON_OK;
+  NC_TRY(ncclAllReduce(grad, grad, (size_t)L.padded, ncclFloat32, ncclSum, c->comm, c->comm_stream));
+  const uint64_t wire = 2u * (uint64_t)L.S * 4u * (uint64_t)(P - 1);
+  r.sent += wire;
+  r.recv += wire;
+  CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+  e.g_eff = e.gathered;
+  return POSEIDON_OK;
+}
+
+// SSP, PS layers: W[0, n) = fmaf(-lr/P, gsum, W) on every rank (the same fp32 operation K2 applies to
+// the shard, so every rank stays bit-identical), then the gradient buffer is cleared; on the recon
+// stream after the all-reduce `src_g` and `extra` (this layer's current backward is done with W).
+poseidon_status_t ps_update_local(poseidon_ctx_t c, Layer& L, float* grad, float* W, float lr, cudaEvent_t src_g,
+                                  cudaEvent_t extra, EvSet& dst) {
+  const int P = c->world;
+  CU_TRY(cudaStreamWaitEvent(c->recon_stream, src_g, 0));
+  if (extra) CU_TRY(cudaStreamWaitEvent(c->recon_stream, extra, 0));
+  CU_TRY(cudaEventRecord(dst.kstart, c->recon_stream));
+  dst.ks_eff = dst.kstart;
+  dst.ke_eff = dst.done;
+  const bool zero = (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0;
+  cudaError_t err;
+  if (!L.vel && zero && ps_shard_update_zero_supported(grad, W, 0)) {
+    err = launch_ps_shard_update_zero(grad, W, 0, L.n, L.padded, -lr / (float)P, c->recon_stream);
+  } else {
+    err = L.vel ? launch_ps_momentum(grad, W, L.vel, L.n, 1.0f / (float)P, lr, L.mu, L.wd, c->recon_stream)
+                : launch_ps_shard_update(grad, W, L.n, -lr / (float)P, nullptr, c->recon_stream);
+    if (err == cudaSuccess && zero) err = cudaMemsetAsync(grad, 0, (size_t)L.padded * 4u, c->recon_stream);
+  }
+  if (err != cudaSuccess) return cuda_fail(err, "SSP PS local update launch");
+  if ((err = debug_sync(c->recon_stream, "SSP PS update")) != cudaSuccess) return cuda_fail(err, "SSP PS update");
+  CU_TRY(cudaEventRecord(dst.done, c->recon_stream));
+  return POSEIDON_OK;
+}
+
 // SSP s = 1 (reading Z19): this hook issues sync t's communication and applies the update of sync
 // t-1 — after this layer's backward t has finished reading W (e.ready) — so the forward of t+1 reads
-// W with every update of iterations <= t-1 (P:L123 with s = 1, at the staleness bound).
+// W with every update of iterations <= t-1 (P:L123 with s = 1, at the staleness bound).  The update
+// is local (SFB: K1 on the gathered factors; PS: the all-reduced gradient), so a rank's next forward
+// waits for the other ranks' hook t-1, not hook t: one iteration of slack.
 poseidon_status_t ssp_hook(poseidon_ctx_t c, int32_t id, Layer& L, float* W, float* bias, float* grad, float lr) {
   EvSet& e = L.ev[c->iter % RING];
   IterRecord& r = open_record(c);
   const int set = next_set(c, L);
   poseidon_status_t st = (L.scheme == POSEIDON_SCHEME_SFB) ? sfb_comm(c, L, set, e, e.ready, r)
-                                                           : ps_comm(c, L, grad, e, e.ready, r);
+                                                           : ps_comm_allreduce(c, L, grad, e, e.ready, r);
   if (st) return st;
   if (L.ssp_pend) {
     const EvSet& src = L.ev[L.pend_iter % RING];
     st = (L.scheme == POSEIDON_SCHEME_SFB)
              ? sfb_update(c, L, L.pend_set, L.pend_W2, L.pend_bias2, L.pend_lr, src.g_eff, e.ready, e)
-             : ps_update(c, L, L.pend_grad2, L.pend_set, L.Wps, L.pend_lr, e, r, true);
+             : ps_update_local(c, L, L.pend_grad2, L.Wps, L.pend_lr, src.g_eff, e.ready, e);
     if (st) return st;
   } else {
-    CU_TRY(cudaEventRecord(e.done, c->comm_stream));  // first sync: nothing to apply yet
+    // first sync: nothing to apply yet; done only orders after this backward
+    CU_TRY(cudaStreamWaitEvent(c->recon_stream, e.ready, 0));
+    CU_TRY(cudaEventRecord(e.done, c->recon_stream));
     e.ks_eff = e.ke_eff = e.done;
   }
   L.ssp_pend = true;
@@ -877,7 +920,8 @@ static poseidon_status_t set_momentum_one(poseidon_ctx_t c, Layer& L, float mu, 
     int64_t b, e, padded;
     const int64_t n = L.M * L.N + (L.has_bias ? L.M : 0);
     poseidon_shard_range(n, c->world, c->rank, &b, &e, &padded);
-    count = (size_t)(padded / c->world);  // this rank's shard only
+    // BSP: this rank's shard only; SSP: the whole layer (every rank applies the all-reduced gradient)
+    count = c->ssp ? (size_t)n : (size_t)(padded / c->world);
   }
   CU_TRY(cudaMalloc(&L.vel, count * 4));
   CU_TRY(cudaMemset(L.vel, 0, count * 4));
@@ -1010,7 +1054,7 @@ poseidon_status_t poseidon_flush(poseidon_ctx_t c, poseidon_stream_t stream) {
     const EvSet& src = L.ev[L.pend_iter % RING];
     st = (L.scheme == POSEIDON_SCHEME_SFB)
              ? sfb_update(c, L, L.pend_set, L.pend_W2, L.pend_bias2, L.pend_lr, src.g_eff, e.ready, e)
-             : ps_update(c, L, L.pend_grad2, L.pend_set, L.Wps, L.pend_lr, e, r, true);
+             : ps_update_local(c, L, L.pend_grad2, L.Wps, L.pend_lr, src.g_eff, e.ready, e);
     if (st) return st;
     L.ssp_pend = false;
     L.last_iter = c->iter;
