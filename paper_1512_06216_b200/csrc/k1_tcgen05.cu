@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "internal.h"
 
@@ -791,6 +792,43 @@ int sm_count_k1() {
 
 }  // namespace
 
+namespace {
+struct MapKey {
+  const void *u, *v, *w;
+  int64_t P, K, ldk, M, N;
+  bool operator==(const MapKey& o) const {
+    return u == o.u && v == o.v && w == o.w && P == o.P && K == o.K && ldk == o.ldk && M == o.M && N == o.N;
+  }
+};
+struct MapEntry {
+  MapKey key;
+  CUtensorMap a, b, w, b2;
+};
+std::mutex g_map_mu;
+std::vector<MapEntry> g_maps;   // small FIFO: one entry per SFB layer (and per gather set)
+constexpr size_t kMapCap = 256;
+bool map_cache_get(const MapKey& k, CUtensorMap* a, CUtensorMap* b, CUtensorMap* w, CUtensorMap* b2) {
+  std::lock_guard<std::mutex> lock(g_map_mu);
+  for (const auto& e : g_maps)
+    if (e.key == k) {
+      *a = e.a;
+      *b = e.b;
+      *w = e.w;
+      *b2 = e.b2;
+      return true;
+    }
+  return false;
+}
+void map_cache_put(const MapKey& k, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& w,
+                   const CUtensorMap& b2) {
+  std::lock_guard<std::mutex> lock(g_map_mu);
+  if (g_maps.size() >= kMapCap) g_maps.erase(g_maps.begin());
+  g_maps.push_back(MapEntry{k, a, b, w, b2});
+}
+}  // namespace
+
+// A freed and reallocated buffer can come back at the same address with the same shape: its cached
+// maps are then still exact (a tensor map holds only address, shape and strides).
 bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int64_t M, int64_t N, const float* W) {
   return aligned16(Ug) && aligned16(Vg) && aligned16(W) && ldk % 4 == 0 && N % 4 == 0 && M < (1 << 30) &&
          N < (1 << 30) && ldk < (1 << 30);
@@ -800,7 +838,13 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
                                  int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg) {
   if (M <= 0 || N <= 0 || K <= 0 || P <= 0) return cudaSuccess;
   if (!recon_tcgen05_supported(Ug, Vg, ldk, M, N, W) || ldk < K) return cudaErrorNotSupported;
-  CUtensorMap tmA, tmB, tmW;
+  CUtensorMap tmA, tmB, tmW, tmB2;
+  const int variant = knobs().variant;
+  // Tensor maps are cached per (buffers, shape): encoding four of them costs ~10 us of host time per
+  // launch, which lands on the step whenever the GPU is not far behind the host (small layers).
+  const MapKey key{Ug, Vg, W, P, K, ldk, M, N};
+  if (dbg == nullptr && map_cache_get(key, &tmA, &tmB, &tmW, &tmB2)) goto have_maps;
+  {
   const uint64_t dA[3] = {(uint64_t)ldk, (uint64_t)M, (uint64_t)P};
   const uint64_t sA[2] = {(uint64_t)ldk * 4, (uint64_t)ldk * 4 * (uint64_t)M};
   const uint32_t bA[3] = {BK, BM, 1};
@@ -812,6 +856,12 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   const uint32_t bW[2] = {W_CHUNK_COLS, BM};
   if (!encode(&tmA, Ug, 3, dA, sA, bA) || !encode(&tmB, Vg, 3, dB, sB, bB) || !encode(&tmW, W, 2, dW, sW, bW))
     return cudaErrorNotSupported;
+  // the 2-SM kernel stages 128 rows of B per CTA (half of the 256-wide N tile)
+  const uint32_t bB2[3] = {BK, (uint32_t)k2sm::BN_CTA, 1};
+  if (!encode(&tmB2, Vg, 3, dB, sB, bB2)) return cudaErrorNotSupported;
+  if (dbg == nullptr) map_cache_put(key, tmA, tmB, tmW, tmB2);
+  }
+have_maps:
   Params p;
   p.M = (int32_t)M;
   p.N = (int32_t)N;
@@ -836,11 +886,8 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   p.epi_groups = knobs().epi;
   p.w_policy = knobs().wpol;
   p.mode = knobs().mode;
-  const int variant = knobs().variant;
   if (variant == 2 && dbg == nullptr) {
-    // re-encode the operand maps with 128-row boxes for B (each CTA stages half of the 256-wide N tile)
-    const uint32_t bB2[3] = {BK, (uint32_t)k2sm::BN_CTA, 1};
-    if (!encode(&tmB, Vg, 3, dB, sB, bB2)) return cudaErrorNotSupported;
+    tmB = tmB2;
     p.m_tiles = (int32_t)((M + k2sm::BM - 1) / k2sm::BM);
     p.n_tiles = (int32_t)((N + k2sm::BN - 1) / k2sm::BN);
     p.num_tiles = p.m_tiles * p.n_tiles;

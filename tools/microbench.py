@@ -16,6 +16,7 @@ def timeit(fn, iters=20, warm=3):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ts = []
     for _ in range(iters):
+        torch.cuda._sleep(200_000)  # queue the launch before the GPU reaches s (device time, not host latency)
         s.record(); fn(); e.record(); e.synchronize()
         ts.append(s.elapsed_time(e))
     ts.sort()
