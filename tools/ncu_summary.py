@@ -61,7 +61,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__data_pipe_tc_wavefronts_mem_shared.sum", "launch__grid_size", "launch__block_size",
         "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "sm__cycles_elapsed.avg",
         "smsp__cycles_active.avg", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "gpc__cycles_elapsed.max", "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active"]
+        "gpc__cycles_elapsed.max", "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_sectors.sum.pct_of_peak_sustained_elapsed", "lts__d_sectors.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__m_xbar2l1tex_read_bytes.sum"]
 
 
 def full(path):
