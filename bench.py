@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--straggle-us", type=float, default=0.0,
                     help="ablation only: every step one rank (a fixed pseudo-random sequence) is delayed by this "
                          "many microseconds on its GPU before the forward (a straggler, P:L568)")
+    ap.add_argument("--bucket-kb", type=int, default=0,
+                    help="sync runs of small PS layers as one bucket of at most this many KB (f1; needs the arena)")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--momentum", type=float, default=0.0, help="f4: Lambda momentum (0 = plain SGD hot path)")
     ap.add_argument("--weight-decay", type=float, default=0.0, help="f4: Lambda weight decay")
@@ -282,7 +284,8 @@ def run_poseidon(args):
     recon = pz.RECON_TF32 if args.recon == "tf32" else pz.RECON_FP32
     if args.memory_format == "channels_last":
         model.to(memory_format=torch.channels_last)   # before PoseidonSync makes params buffer views
-    sync = PoseidonSync(model, ctx, K=K, lr=args.lr, scheme=scheme, recon=recon, arena=use_nvls or bool(args.ssp))
+    sync = PoseidonSync(model, ctx, K=K, lr=args.lr, scheme=scheme, recon=recon, arena=use_nvls or bool(args.ssp) or bool(args.bucket_kb),
+                        bucket_bytes=args.bucket_kb * 1024)
     if args.momentum or args.weight_decay:
         ctx.set_momentum(args.momentum, args.weight_decay)
 
@@ -492,6 +495,7 @@ def run_poseidon(args):
                                     ("nccl rs/k2/ag" if world > 1 else "k2 (P=1)")),
                         "nvls_status": ctx.nvls_status(),
                         "sfb_wire": sfb_wire, "ssp": args.ssp, "straggle_us": args.straggle_us,
+                        "bucket_kb": args.bucket_kb,
                         "sfb_paths": sorted({ctx.sfb_path(d["id"]) for d in sync.describe()
                                              if d["scheme"] == "SFB"}) if world > 1 else []},
             "exposed_sync_ms": exposed, "sync_total_ms": sync_total,

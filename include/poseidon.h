@@ -227,6 +227,12 @@ poseidon_status_t poseidon_bind_sfb_params(poseidon_ctx_t ctx, int32_t layer_id,
  * gradient.  *nvls_active (nullable) = 1 if that path is active;
  * otherwise the arena is plain device memory and the NCCL path is used. */
 poseidon_status_t poseidon_ps_arena(poseidon_ctx_t ctx, int32_t* nvls_active);
+/* PS layer bucketing (BSP only): call before poseidon_ps_arena, identically on every rank.
+ * Runs of consecutive PS layers (layer-id order) whose 128-B aligned sizes add up to at most
+ * bucket_bytes share one contiguous arena span and sync as ONE flat buffer (one fused NVLS kernel, or
+ * one reduce-scatter / K2 / all-gather) once the last member's hook has fired; a run of one layer
+ * stays unbucketed.  Members' stats report the bucket's sync.  0 (default) disables bucketing. */
+poseidon_status_t poseidon_set_ps_buckets(poseidon_ctx_t ctx, int64_t bucket_bytes);
 /* A PS layer's arena segments: *grad = the gradient buffer the layer's NEXT sync reduces (with
  * POSEIDON_FLAG_SSP1 two buffers alternate: re-point the parameters' gradients after every
  * iteration), *W = its parameters, *padded_n = segment length in floats. */

@@ -106,6 +106,7 @@ _SIGS = {
     "poseidon_nvls_status": (ctypes.c_char_p, [_vp]),
     "poseidon_sfb_path": (_i32, [_vp, _i32]),
     "poseidon_flush": (_i32, [_vp, _vp]),
+    "poseidon_set_ps_buckets": (_i32, [_vp, _i64]),
     "poseidon_set_recon": (_i32, [_vp, _i32, _i32]),
     "poseidon_wait_layer": (_i32, [_vp, _i32, _vp]),
     "poseidon_iteration_end": (_i32, [_vp, _vp, _P(IterStats)]),
@@ -257,6 +258,10 @@ class Context:
         g, w, n = _vp(), _vp(), _i64()
         _check(lib.poseidon_ps_layer_buffers(self.h, layer_id, ctypes.byref(g), ctypes.byref(w), ctypes.byref(n)))
         return g.value, w.value, n.value
+
+    def set_ps_buckets(self, bucket_bytes: int):
+        """Sync runs of small PS layers as one flat buffer (call before ps_arena, same on every rank)."""
+        _check(lib.poseidon_set_ps_buckets(self.h, int(bucket_bytes)))
 
     def flush(self, stream=None):
         """SSP: apply every layer's deferred update (collective; no-op without FLAG_SSP1)."""

@@ -114,6 +114,11 @@ struct Layer {
   float *vel = nullptr, *vel_b = nullptr;
   size_t arena_off = 0;      // byte offset of this layer in both arenas
   float* gsets[2] = {nullptr, nullptr};  // arena gradient buffers (SSP: two, alternating per sync)
+  // PS bucketing (poseidon_set_ps_buckets): a member layer points at its bucket; a bucket is a hidden
+  // pseudo-layer over the members' contiguous arena span, synced once all members are ready
+  int32_t bucket = -1;
+  std::vector<int32_t> members;
+  size_t members_ready = 0;
   int64_t nsync = 0;         // syncs issued so far (SSP set parity)
   // SSP (s = 1): the sync whose update is deferred to this layer's next hook (or poseidon_flush)
   bool ssp_pend = false;
@@ -164,6 +169,8 @@ struct poseidon_ctx {
   bool arena_nccl_mem = false;
   ncclWindow_t win_g = nullptr, win_w = nullptr, win_g2 = nullptr;
   bool ssp = false;           // FLAG_SSP1
+  int64_t bucket_bytes = 0;   // poseidon_set_ps_buckets
+  std::vector<Layer> buckets; // pseudo-layers, addressed as MAX_LAYERS + index in records
   NvlsState* nvls = nullptr;
   std::string nvls_error;
 };
@@ -182,6 +189,11 @@ poseidon_status_t check_layer(poseidon_ctx_t c, int32_t id, Layer** out) {
     return fail(POSEIDON_ERR_STATE, "layer " + std::to_string(id) + " is not registered");
   *out = &c->layers[id];
   return POSEIDON_OK;
+}
+
+// a record entry is a layer id or MAX_LAYERS + bucket index
+Layer& resolve(poseidon_ctx_t c, int32_t id) {
+  return id >= MAX_LAYERS ? c->buckets[(size_t)(id - MAX_LAYERS)] : c->layers[(size_t)id];
 }
 
 poseidon_status_t ensure_events(Layer& L) {
@@ -644,6 +656,10 @@ poseidon_status_t poseidon_finalize(poseidon_ctx_t c) {
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->recon_stream) cudaStreamSynchronize(c->recon_stream);
   for (auto& L : c->layers) free_layer(L);
+  for (auto& B : c->buckets) {
+    B.grad = B.Wps = nullptr;   // views into the arena
+    free_layer(B);
+  }
   if (c->nvls) nvls_destroy(c->comm, c->nvls);
   if (c->win_g) ncclCommWindowDeregister(c->comm, c->win_g);
   if (c->win_g2) ncclCommWindowDeregister(c->comm, c->win_g2);
@@ -805,18 +821,81 @@ poseidon_status_t poseidon_bind_sfb_params(poseidon_ctx_t c, int32_t id, float* 
   return POSEIDON_OK;
 }
 
+static poseidon_status_t set_momentum_one(poseidon_ctx_t c, Layer& L, float mu, float wd);
+
+poseidon_status_t poseidon_set_ps_buckets(poseidon_ctx_t c, int64_t bucket_bytes) {
+  poseidon_status_t st = check_ctx(c);
+  if (st) return st;
+  if (bucket_bytes < 0) return fail(POSEIDON_ERR_INVALID_ARG, "bucket_bytes must be >= 0");
+  if (c->arena_g) return fail(POSEIDON_ERR_STATE, "set buckets before poseidon_ps_arena");
+  if (c->ssp && bucket_bytes > 0) return fail(POSEIDON_ERR_INVALID_ARG, "PS buckets are not supported with FLAG_SSP1");
+  c->bucket_bytes = bucket_bytes;
+  return POSEIDON_OK;
+}
+
 poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
   poseidon_status_t st = check_ctx(c);
   if (st) return st;
   if (c->arena_g) return fail(POSEIDON_ERR_STATE, "PS arena already created");
   cudaSetDevice(c->device);
   size_t total = 0;
-  for (auto& L : c->layers) {
-    if (!L.registered || L.scheme != POSEIDON_SCHEME_PS) continue;
-    const int64_t n = L.M * L.N + (L.has_bias ? L.M : 0);
+  // Buckets (poseidon_set_ps_buckets): runs of consecutive PS layers (id order) whose 128-B aligned
+  // spans add up to at most bucket_bytes share one contiguous arena span and sync as one flat buffer
+  // with its own shard map; a run of one stays a plain layer.
+  c->buckets.clear();
+  std::vector<std::vector<int32_t>> groups;
+  {
+    std::vector<int32_t> cur;
+    size_t cur_bytes = 0;
+    auto close = [&]() {
+      if (!cur.empty()) groups.push_back(cur);
+      cur.clear();
+      cur_bytes = 0;
+    };
+    for (int32_t id = 0; id < (int32_t)c->layers.size(); ++id) {
+      Layer& L = c->layers[(size_t)id];
+      if (!L.registered || L.scheme != POSEIDON_SCHEME_PS) continue;
+      const size_t seg = (size_t)round_up((L.M * L.N + (L.has_bias ? L.M : 0)) * 4, 128);
+      if (c->bucket_bytes <= 0 || seg > (size_t)c->bucket_bytes) {
+        close();
+        groups.push_back({id});
+        continue;
+      }
+      if (cur_bytes + seg > (size_t)c->bucket_bytes) close();
+      cur.push_back(id);
+      cur_bytes += seg;
+    }
+    close();
+  }
+  for (auto& g : groups) {
+    if (g.size() == 1) {
+      Layer& L = c->layers[(size_t)g[0]];
+      const int64_t n = L.M * L.N + (L.has_bias ? L.M : 0);
+      int64_t b, e, padded;
+      poseidon_shard_range(n, c->world, c->rank, &b, &e, &padded);
+      L.arena_off = total;
+      L.bucket = -1;
+      total += (size_t)round_up(padded * 4, 4096);
+      continue;
+    }
+    c->buckets.emplace_back();
+    Layer& B = c->buckets.back();
+    B.registered = true;
+    B.kind = POSEIDON_LAYER_CONV;
+    B.scheme = POSEIDON_SCHEME_PS;
+    B.members = g;
+    B.arena_off = total;
+    size_t off = 0;
+    for (int32_t m : g) {
+      Layer& L = c->layers[(size_t)m];
+      L.bucket = (int32_t)c->buckets.size() - 1;
+      L.arena_off = total + off;
+      off += (size_t)round_up((L.M * L.N + (L.has_bias ? L.M : 0)) * 4, 128);
+    }
+    B.M = 1;
+    B.N = (int64_t)(off / 4);  // flat length of the bucket (n of the pseudo-layer)
     int64_t b, e, padded;
-    poseidon_shard_range(n, c->world, c->rank, &b, &e, &padded);
-    L.arena_off = total;
+    poseidon_shard_range(B.N, c->world, c->rank, &b, &e, &padded);
     total += (size_t)round_up(padded * 4, 4096);
   }
   if (total == 0) total = 4096;
@@ -855,17 +934,50 @@ poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
   CU_TRY(cudaMemset(c->arena_w, 0, total));
   if (c->arena_g2) CU_TRY(cudaMemset(c->arena_g2, 0, total));
   CU_TRY(cudaDeviceSynchronize());
+  auto at = [](float* base, size_t off) {
+    return base ? reinterpret_cast<float*>(reinterpret_cast<char*>(base) + off) : nullptr;
+  };
   for (int32_t id = 0; id < (int32_t)c->layers.size(); ++id) {
     Layer& L = c->layers[id];
     if (!L.registered || L.scheme != POSEIDON_SCHEME_PS) continue;
     const int64_t n = L.M * L.N + (L.has_bias ? L.M : 0);
-    float* g = reinterpret_cast<float*>(reinterpret_cast<char*>(c->arena_g) + L.arena_off);
-    float* w = reinterpret_cast<float*>(reinterpret_cast<char*>(c->arena_w) + L.arena_off);
-    st = poseidon_bind_ps_buffers(c, id, g, w, n, POSEIDON_PS_ZERO_GRAD);
-    if (st) return st;
+    float* g = at(c->arena_g, L.arena_off);
+    float* w = at(c->arena_w, L.arena_off);
+    if (L.bucket >= 0) {
+      // a member: its own views only (the bucket pseudo-layer holds the shard map)
+      L.grad = g;
+      L.Wps = w;
+      L.n = n;
+      L.padded = round_up(n * 4, 128) / 4;
+      L.ps_flags = POSEIDON_PS_ZERO_GRAD;
+    } else {
+      st = poseidon_bind_ps_buffers(c, id, g, w, n, POSEIDON_PS_ZERO_GRAD);
+      if (st) return st;
+    }
     L.in_arena = true;
     L.gsets[0] = g;
-    L.gsets[1] = c->arena_g2 ? reinterpret_cast<float*>(reinterpret_cast<char*>(c->arena_g2) + L.arena_off) : nullptr;
+    L.gsets[1] = at(c->arena_g2, L.arena_off);
+  }
+  for (auto& B : c->buckets) {
+    B.grad = at(c->arena_g, B.arena_off);
+    B.Wps = at(c->arena_w, B.arena_off);
+    B.n = B.N;
+    int64_t b, e, padded;
+    poseidon_shard_range(B.n, c->world, c->rank, &b, &e, &padded);
+    B.begin = b;
+    B.end = e;
+    B.padded = padded;
+    B.S = padded / c->world;
+    B.ps_flags = POSEIDON_PS_ZERO_GRAD;
+    B.in_arena = true;
+    st = ensure_events(B);
+    if (st) return st;
+    // momentum already set on the members carries over to the bucket (all members share mu, wd)
+    const Layer& M0 = c->layers[(size_t)B.members[0]];
+    if (M0.vel) {
+      st = set_momentum_one(c, B, M0.mu, M0.wd);
+      if (st) return st;
+    }
   }
   if (nvls_active) *nvls_active = c->ps_nvls ? 1 : 0;
   return POSEIDON_OK;
@@ -936,11 +1048,15 @@ poseidon_status_t poseidon_set_momentum(poseidon_ctx_t c, int32_t id, float mu, 
   if (id == -1) {
     for (auto& L : c->layers)
       if (L.registered && (st = set_momentum_one(c, L, mu, weight_decay)) != POSEIDON_OK) return st;
+    for (auto& B : c->buckets)
+      if ((st = set_momentum_one(c, B, mu, weight_decay)) != POSEIDON_OK) return st;
     return POSEIDON_OK;
   }
   Layer* L;
   st = check_layer(c, id, &L);
   if (st) return st;
+  if (L->bucket >= 0)
+    return fail(POSEIDON_ERR_STATE, "bucketed PS layers share their bucket's velocity: use layer_id -1");
   return set_momentum_one(c, *L, mu, weight_decay);
 }
 
@@ -992,6 +1108,9 @@ poseidon_status_t poseidon_sync_ps(poseidon_ctx_t c, int32_t id, float* grad, fl
   poseidon_status_t st = check_layer(c, id, &L);
   if (st) return st;
   if (L->scheme != POSEIDON_SCHEME_PS) return fail(POSEIDON_ERR_STATE, "layer is not a PS layer");
+  if (L->bucket >= 0 && (grad != nullptr && grad != L->grad))
+    return fail(POSEIDON_ERR_STATE, "a bucketed PS layer syncs its arena buffers (pass NULL buffers)");
+  if (L->bucket >= 0) grad = W = nullptr;
   if (grad || W) {
     if (!grad || !W) return fail(POSEIDON_ERR_INVALID_ARG, "pass both grad and W, or neither");
     if (grad != L->grad || W != L->Wps || n != L->n) {
@@ -1008,6 +1127,28 @@ poseidon_status_t poseidon_sync_ps(poseidon_ctx_t c, int32_t id, float* grad, fl
   if (c->ssp) {
     float* g = (L->in_arena && L->gsets[1]) ? L->gsets[next_set(c, *L)] : L->grad;
     return ssp_hook(c, id, *L, L->Wps, nullptr, g, lr);
+  }
+  if (L->bucket >= 0) {
+    // bucketed: the bucket syncs once every member's gradient is ready (hooks fire in the same order
+    // on every rank, so the bucket's collectives are issued at the same point everywhere)
+    Layer& B = c->buckets[(size_t)L->bucket];
+    if (++B.members_ready < B.members.size()) return POSEIDON_OK;
+    B.members_ready = 0;
+    const int32_t bid = MAX_LAYERS + L->bucket;
+    for (int32_t m : B.members)
+      if (m != id) CU_TRY(cudaStreamWaitEvent(c->comm_stream, c->layers[(size_t)m].ev[c->iter % RING].ready, 0));
+    CU_TRY(cudaEventRecord(B.ev[c->iter % RING].ready, ps));
+    B.last_iter = c->iter;
+    if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
+      B.pending = true;
+      B.pending_lr = lr;
+      B.pending_grad = B.grad;
+      B.pending_W = B.Wps;
+      c->pending_order.push_back(bid);
+      open_record(c);
+      return POSEIDON_OK;
+    }
+    return launch_ps_comm(c, bid, B, B.grad, B.Wps, lr, B.ev[c->iter % RING].ready);
   }
   if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
     L->pending = true;
@@ -1072,10 +1213,11 @@ poseidon_status_t poseidon_wait_layer(poseidon_ctx_t c, int32_t id, poseidon_str
     // traditional BP (Fig. dwbp (a)): the next iteration waits for every layer
     const IterRecord& r = c->rec[(c->iter + RING - 1) % RING];
     if (r.iter == c->iter - 1)
-      for (int32_t lid : r.layers) CU_TRY(cudaStreamWaitEvent(cs, c->layers[lid].ev[r.iter % RING].done, 0));
+      for (int32_t lid : r.layers) CU_TRY(cudaStreamWaitEvent(cs, resolve(c, lid).ev[r.iter % RING].done, 0));
     return POSEIDON_OK;
   }
-  if (L->last_iter >= 0) CU_TRY(cudaStreamWaitEvent(cs, L->ev[L->last_iter % RING].done, 0));
+  const Layer& D = (L->bucket >= 0) ? c->buckets[(size_t)L->bucket] : *L;
+  if (D.last_iter >= 0) CU_TRY(cudaStreamWaitEvent(cs, D.ev[D.last_iter % RING].done, 0));
   return POSEIDON_OK;
 }
 
@@ -1088,7 +1230,7 @@ poseidon_status_t poseidon_iteration_end(poseidon_ctx_t c, poseidon_stream_t com
   if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
     // deferred syncs in the order the hooks fired, all after the whole backward
     for (int32_t id : c->pending_order) {
-      Layer& L = c->layers[id];
+      Layer& L = resolve(c, id);
       if (!L.pending) continue;
       L.pending = false;
       st = (L.scheme == POSEIDON_SCHEME_SFB)
@@ -1117,7 +1259,7 @@ poseidon_status_t poseidon_get_iter_stats(poseidon_ctx_t c, int32_t ago, poseido
   CU_TRY(cudaEventSynchronize(r.bwd_end));
   float exposed = 0.f, first_ready = 0.f;
   for (int32_t id : r.layers) {
-    Layer& L = c->layers[id];
+    Layer& L = resolve(c, id);
     EvSet& e = L.ev[it % RING];
     CU_TRY(cudaEventSynchronize(e.done));
     exposed = std::max(exposed, elapsed(r.bwd_end, e.done));
@@ -1153,10 +1295,13 @@ poseidon_status_t poseidon_get_layer_stats(poseidon_ctx_t c, int32_t ago, int32_
   if (r.iter != it || !r.closed) return fail(POSEIDON_ERR_STATE, "iteration record overwritten");
   memset(out, 0, sizeof(*out));
   out->scheme = L->scheme;
+  // a bucketed layer reports its bucket's sync (the same numbers for every member)
+  const int32_t rid = (L->bucket >= 0) ? MAX_LAYERS + L->bucket : id;
+  Layer* D = (L->bucket >= 0) ? &c->buckets[(size_t)L->bucket] : L;
   bool found = false;
-  for (int32_t lid : r.layers) found |= (lid == id);
+  for (int32_t lid : r.layers) found |= (lid == rid);
   if (!found) return POSEIDON_OK;
-  EvSet& e = L->ev[it % RING];
+  EvSet& e = D->ev[it % RING];
   CU_TRY(cudaEventSynchronize(e.done));
   CU_TRY(cudaEventSynchronize(r.bwd_end));
   out->launched = 1;

@@ -94,7 +94,7 @@ class PoseidonSync:
     per worker per FC layer)."""
 
     def __init__(self, model: nn.Module, ctx: B.Context, K: int, lr: float,
-                 scheme: str = "auto", recon: int = B.RECON_TF32, arena: bool = False):
+                 scheme: str = "auto", recon: int = B.RECON_TF32, arena: bool = False, bucket_bytes: int = 0):
         self.model = model
         self.ctx = ctx
         self.K = K
@@ -114,7 +114,10 @@ class PoseidonSync:
                 layer_id += 1
         if arena:
             # one library-owned gradient/parameter arena for all PS layers (symmetric NCCL windows
-            # with FLAG_NVLS_PS: each PS sync is then one fused multimem kernel)
+            # with FLAG_NVLS_PS: each PS sync is then one fused multimem kernel); optionally runs of
+            # small PS layers sync as one bucket
+            if bucket_bytes:
+                ctx.set_ps_buckets(bucket_bytes)
             self.nvls_active = ctx.ps_arena()
             for plan in self.plans:
                 if plan.scheme == B.SCHEME_PS:

@@ -15,6 +15,7 @@ Checks, at world = P:
      on the concatenated P*K batch (torch fp32 reference, TF32 gate).
   6. SSP, staleness 1: SFB + PS over 4 iterations and a flush, integer variant bit-exact vs O10 on
      the NCCL and the NVLS paths.
+  7. PS buckets: six layers of mixed sizes, NCCL and fused NVLS paths, integer bit-exact per layer.
   5. Full size in bench.py's N > 1 configuration: C3 fc6 SFB on symmetric windows (sampled rows vs O4)
      and a 37.7M-parameter PS layer through the fused NVLS kernel (sampled elements vs O6).
 Prints "MP_OK <rank>" on success; any failure raises.
@@ -352,6 +353,50 @@ def main():
         if rank == 0:
             print(f"SSP flags={flags}: PS {cs.nvls_status()}, SFB path {cs.sfb_path(0)}", flush=True)
         cs.close()
+
+    # ---- 7. PS buckets (f1): small PS layers synced as one flat buffer, NCCL and fused NVLS paths;
+    #          integer variant bit-exact vs O6 per layer, gradients cleared, ranks identical ----
+    shapes = [(10, 65), (32, 64), (3, 1), (96, 363), (16, 129), (500, 400)]
+    for flags in (0, pz.FLAG_NVLS_PS):
+        cb = new_ctx(flags)
+        for lid, (M_, N_) in enumerate(shapes):
+            cb.register_layer(lid, pz.LAYER_CONV, M_, N_, 1, True, pz.SCHEME_PS)
+        cb.set_ps_buckets(256 * 1024)
+        cb.ps_arena()
+        lr = 2.0 ** -7
+        cb.set_lr(lr)
+        refs, views = [], []
+        for lid, (M_, N_) in enumerate(shapes):
+            n = M_ * N_ + M_
+            gp, wp, padded = cb.ps_layer_buffers(lid)
+            grads = S.integer_grads(n, P, seed=200 + lid)
+            w0 = (S.rng(300 + lid).integers(-1023, 1024, size=n) * 2.0 ** -10).astype(np.float32)
+            wv, gv = device_view(wp, (padded,)), device_view(gp, (padded,))
+            wv[:n] = torch.from_numpy(w0).to(dev)
+            gv[:n] = torch.from_numpy(grads[rank]).to(dev)
+            refs.append(O.ps_step_flat(w0, grads, lr))
+            views.append((wv, gv, n))
+        torch.cuda.synchronize()
+        dist.barrier()
+        for lid in reversed(range(len(shapes))):
+            cb.backprop_hook(lid, torch.cuda.current_stream())
+        for lid in range(len(shapes)):
+            cb.wait_layer(lid)
+        st = cb.iteration_end(stats=True)
+        torch.cuda.synchronize()
+        for (wv, gv, n), ref in zip(views, refs):
+            out = wv[:n].cpu().numpy().astype(np.float64)
+            if P in (1, 2, 4, 8):
+                assert np.array_equal(out, ref), f"bucket PS flags={flags}"
+            else:
+                assert O.update_error_fp32(ref, out, ref) <= 1e-5
+            assert float(gv[:n].abs().sum()) == 0.0
+            assert allsame(wv[:n].contiguous())
+        assert st["n_layers"] < len(shapes), st
+        if rank == 0:
+            print(f"buckets flags={flags}: {st['n_layers']} syncs for {len(shapes)} layers, PS {cb.nvls_status()}",
+                  flush=True)
+        cb.close()
 
     # ---- 5. full size in bench.py's N > 1 launch configuration (SYMM_SFB | NVLS_PS): C3 fc6 as SFB
     #          (4096 x 9216, K = 256) and a 37.7M-parameter PS layer in the NVLS arena, sampled against

@@ -130,3 +130,46 @@ def test_ps_zero_grad_odd_sizes(pz, n):
     assert np.all(out[n:] == -3.0)
     assert np.all(host(gflat) == 0)
     ctx.close()
+
+
+@pytest.mark.parametrize("bucket_kb", [0, 16, 256])
+def test_ps_buckets_world1(pz, bucket_kb):
+    """PS layers in buckets (one flat sync per bucket) give exactly O6 per layer, clear every gradient,
+    and report the bucket's stats for each member."""
+    from paper_1512_06216_b200.binding import device_view
+    shapes = [(10, 65), (32, 64), (3, 1), (96, 363), (64, 1025), (500, 400)]   # n = M*N + M
+    ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device())
+    for lid, (M, N) in enumerate(shapes):
+        ctx.register_layer(lid, pz.LAYER_CONV, M, N, 1, True, pz.SCHEME_PS)
+    ctx.set_ps_buckets(bucket_kb * 1024)
+    ctx.ps_arena()
+    lr = 2.0 ** -7
+    ctx.set_lr(lr)
+    refs, views = [], []
+    for lid, (M, N) in enumerate(shapes):
+        n = M * N + M
+        gp, wp, padded = ctx.ps_layer_buffers(lid)
+        g = S.integer_grads(n, 1, seed=lid)[0]
+        w0 = (S.rng(100 + lid).integers(-1023, 1024, size=n) * 2.0 ** -10).astype(np.float32)
+        wv, gv = device_view(wp, (padded,)), device_view(gp, (padded,))
+        wv[:n] = dev(w0)
+        gv[:n] = dev(g)
+        refs.append(O.ps_step_flat(w0, [g], lr))
+        views.append((wv, gv, n))
+    torch.cuda.synchronize()
+    for lid in reversed(range(len(shapes))):          # backward order
+        ctx.backprop_hook(lid, torch.cuda.current_stream())
+    for lid in range(len(shapes)):
+        ctx.wait_layer(lid)
+    st = ctx.iteration_end(stats=True)
+    torch.cuda.synchronize()
+    for (wv, gv, n), ref in zip(views, refs):
+        assert np.array_equal(host(wv)[:n].astype(np.float64), ref)
+        assert np.all(host(gv)[:n] == 0)
+    if bucket_kb == 0:
+        assert st["n_layers"] == len(shapes)
+    else:
+        assert st["n_layers"] < len(shapes)            # buckets count once
+    for lid in range(len(shapes)):
+        assert ctx.layer_stats(lid)["launched"] == 1
+    ctx.close()
