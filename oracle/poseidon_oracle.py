@@ -238,6 +238,58 @@ def ps_simulated(W, b, Us, Vs, lr):
 
 
 # --------------------------------------------------------------------------
+# O11 — SF-via-PS, the literal else-branch of Alg. 3 ("Send u, v
+# to the master node; Synchronize A_i from the master node"; Adam-style,
+# P:L335), with the master sharded by rows (reading Z20): worker r is the
+# master of the output rows [lo_r, hi_r) = O2's shard_range(M, P, r).
+# --------------------------------------------------------------------------
+def row_shard_range(M: int, P: int, rank: int) -> Tuple[int, int]:
+    """Output rows mastered by ``rank``: O2's shard map applied to the M rows."""
+    lo, hi, _ = shard_range(M, P, rank)
+    return lo, hi
+
+
+def sf_ps_simulated(W, b, Us, Vs, lr):
+    """Every worker p sends its sufficient factors to the masters: to master r
+    the entries of its error messages for r's rows (columns [lo_r, hi_r) of
+    U_p) and all of its inputs V_p.  Master r reconstructs its rows of
+    sum_p U_p^T V_p, applies W[lo_r:hi_r] += (-lr/P) * (.) (and the bias rows),
+    and every worker synchronises A_i from the masters (the row blocks,
+    concatenated).  Each row must be mastered exactly once.
+
+    Returns (W', b', floats) where ``floats`` counts the floats that cross
+    between distinct workers (factor messages + the pushed row blocks)."""
+    P = len(Us)
+    W = np.asarray(W, np.float64)
+    M, N = W.shape
+    W1 = np.empty_like(W)
+    b1 = None if b is None else np.empty(M, dtype=np.float64)
+    owned = np.zeros(M, dtype=np.int64)
+    floats = 0
+    for r in range(P):
+        lo, hi = row_shard_range(M, P, r)
+        G = np.zeros((hi - lo, N), dtype=np.float64)
+        gb = np.zeros(hi - lo, dtype=np.float64)
+        for p in range(P):
+            u = np.asarray(Us[p], np.float64)[:, lo:hi]      # message p -> r: K x (hi-lo)
+            v = np.asarray(Vs[p], np.float64)                # and K x N
+            if p != r:
+                floats += u.size + v.size
+            for k in range(u.shape[0]):                      # Eq. 5: sum of outer products
+                G += np.outer(u[k], v[k])
+            gb += u.sum(axis=0)
+        W1[lo:hi] = W[lo:hi] + (-lr / P) * G
+        if b1 is not None:
+            b1[lo:hi] = np.asarray(b, np.float64)[lo:hi] + (-lr / P) * gb
+        # "synchronize A_i": the updated rows (and bias entries) go to the P-1 others
+        floats += (P - 1) * (hi - lo) * (N + (0 if b is None else 1))
+        owned[lo:hi] += 1
+    if not np.all(owned == 1):
+        raise AssertionError("row shards do not cover [0, M) exactly once")
+    return W1, b1, floats
+
+
+# --------------------------------------------------------------------------
 # O7 — one SGD step of single-worker softmax regression on the concatenated
 # batch (P:L24 "converges to the same objective value as a single machine")
 # --------------------------------------------------------------------------

@@ -260,6 +260,48 @@ def test_o4_invariants():
     assert np.allclose(W1w, W3w, rtol=0, atol=1e-14) and np.allclose(b1w, b3w, rtol=0, atol=1e-14)
 
 
+@pytest.mark.parametrize("M,N,K,P", [(7, 5, 3, 1), (16, 9, 4, 2), (33, 17, 5, 3), (70, 40, 8, 8),
+                                     (10, 6, 3, 8)])
+def test_o11_sf_ps_equals_definition(M, N, K, P):
+    """Sharded SF-via-PS (Alg. 3 else-branch) computes the same step as O4 (pure
+    reassociation); (10, 6, 3, 8) has masters with no rows (empty shards)."""
+    W, b = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, P)
+    W4, b4 = O.sync_step(W, b, Us, Vs, 0.05)
+    W11, b11, _ = O.sf_ps_simulated(W, b, Us, Vs, 0.05)
+    assert np.max(np.abs(W11 - W4)) < 1e-12 and np.max(np.abs(b11 - b4)) < 1e-12
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_o11_sf_ps_against_exact_rationals(P):
+    """Integer variant, P a power of two: every operation is exact, so equality is exact."""
+    W, b, Us, Vs, lr = S.integer_factors(37, 6, 3, P, seed=10 + P)
+    W11, b11, _ = O.sf_ps_simulated(W, b, Us, Vs, lr)
+    We, be = _exact_sync(W, b, Us, Vs, lr)
+    for m in range(37):
+        assert b11[m] == float(be[m])
+        for n in range(6):
+            assert W11[m, n] == float(We[m][n])
+
+
+def test_o11_row_masters_and_message_count():
+    """Row masters follow O2 (32-row shards, empty trailing masters legal), and the floats that
+    cross between workers add up, by a hand count of the messages, to
+    (P-1) (K M + P K N + M (N+1)): each worker's U columns go to the P-1 other masters once
+    (K M in total per worker), its V to every other master (K N each), and every row block
+    (with its bias entry) to the P-1 other workers."""
+    assert [O.row_shard_range(1000, 8, r) for r in range(8)] == \
+        [(0, 128), (128, 256), (256, 384), (384, 512), (512, 640), (640, 768), (768, 896), (896, 1000)]
+    assert O.row_shard_range(10, 8, 0) == (0, 10) and O.row_shard_range(10, 8, 1) == (10, 10)
+    for M, N, K, P in [(70, 9, 3, 3), (10, 6, 3, 8), (33, 5, 2, 1)]:
+        W, b = S.fc_weights_randbias(M, N)
+        Us, Vs = S.hidden_factors(M, N, K, P)
+        _, _, floats = O.sf_ps_simulated(W, b, Us, Vs, 0.1)
+        assert floats == (P - 1) * (K * M + P * K * N + M * (N + 1))
+        _, _, floats_nb = O.sf_ps_simulated(W, None, Us, Vs, 0.1)
+        assert floats_nb == (P - 1) * (K * M + P * K * N + M * N)
+
+
 def test_o6_shard_cover_failure_is_detected():
     """ps_step_flat checks coverage; an inconsistent P/grad list still works
     only when the map covers [0,n) — sanity that the check exists."""
