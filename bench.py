@@ -37,7 +37,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C3", choices=["C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="poseidon", choices=["poseidon", "reference"])
-    ap.add_argument("--scheme", default=None, choices=[None, "auto", "ps", "sfb"])
+    ap.add_argument("--scheme", default=None, choices=[None, "auto", "ps", "sfb", "sfps"])
+    ap.add_argument("--else-branch", default="ps", choices=["ps", "sfps"],
+                    help="how FC layers the SACP rule sends to the server execute: full-gradient PS (reading Z7) "
+                         "or the literal sharded SF-PS of Alg. 3 (reading Z20, POSEIDON_FLAG_SFPS)")
     ap.add_argument("--dwbp", default="on", choices=["on", "off"])
     ap.add_argument("--recon", default="tf32", choices=["tf32", "fp32"])
     ap.add_argument("--nvls", default="auto", choices=["auto", "on", "off"],
@@ -277,6 +280,8 @@ def run_poseidon(args):
     flags |= {"symm": pz.FLAG_SYMM_SFB, "nvls": pz.FLAG_NVLS_SFB}.get(sfb_wire, 0)
     if args.ssp:
         flags |= pz.FLAG_SSP1
+    if args.else_branch == "sfps":
+        flags |= pz.FLAG_SFPS
     ctx = pz.Context(rank=rank, world=world, device=local, nccl_id=nccl_id, flags=flags)
 
     torch.manual_seed(6216)          # identical weights on every rank
@@ -488,7 +493,7 @@ def run_poseidon(args):
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "tf32" if args.recon == "tf32" else "f32", "data": "synthetic",
             "config": workload_config(args, cfg, world),
-            "details": {"scheme": scheme, "dwbp": args.dwbp, "recon": args.recon, "lr": args.lr,
+            "details": {"scheme": scheme, "else_branch": args.else_branch, "dwbp": args.dwbp, "recon": args.recon, "lr": args.lr,
                         "momentum": args.momentum, "weight_decay": args.weight_decay,
                         "memory_format": args.memory_format,
                         "ps_path": ("nvls-fused" if sync.nvls_active else

@@ -50,7 +50,14 @@ typedef enum {
   POSEIDON_ERR_STATE = -8
 } poseidon_status_t;
 
-typedef enum { POSEIDON_SCHEME_PS = 0, POSEIDON_SCHEME_SFB = 1 } poseidon_scheme_t;
+/* PS: full-gradient parameter server (Alg. 3 lines 1-3; also the rule's else-branch, reading Z7).
+ * SFB: sufficient-factor broadcasting (Alg. 3 lines 6-8).
+ * SFPS: the rule's else-branch executed literally (Alg. 3 lines 9-11, Adam-style
+ *       P:L335): factors go to the master of each row block (rank q masters the output rows
+ *       poseidon_shard_range(M, P, q)), the master reconstructs and updates its rows only, and the
+ *       workers synchronise A_i from the masters (reading Z20).  Never returned by
+ *       poseidon_choose_scheme; selected by scheme_override = 2 or POSEIDON_FLAG_SFPS. */
+typedef enum { POSEIDON_SCHEME_PS = 0, POSEIDON_SCHEME_SFB = 1, POSEIDON_SCHEME_SFPS = 2 } poseidon_scheme_t;
 typedef enum { POSEIDON_LAYER_CONV = 0, POSEIDON_LAYER_FC = 1 } poseidon_layer_kind_t;
 
 /* Reconstruction kernel of the SFB path (step 3 of P:L331).
@@ -90,6 +97,9 @@ typedef struct {
                                          forward t+1 reads every update of iterations <= t-1.  Gradient and
                                          factor buffers are double-buffered; PS layers need the arena.
                                          Incompatible with POSEIDON_FLAG_DWBP_OFF. */
+#define POSEIDON_FLAG_SFPS 0x40u       /* FC layers the rule sends to the server (Alg. 3 else-branch) run as
+                                         sharded SF-PS (POSEIDON_SCHEME_SFPS) instead of full-gradient PS.
+                                         Not combined with POSEIDON_FLAG_SSP1. */
 
 typedef struct poseidon_ctx* poseidon_ctx_t;
 
@@ -141,7 +151,13 @@ int32_t poseidon_choose_scheme(int32_t kind, int64_t M, int64_t N, int64_t K, in
  * the library's streams: all-gather of all ranks' factors (NCCL, skipped at
  * P == 1) and the fused reconstruction + SGD  W += alpha * Ug^T Vg,
  * b += alpha * sum_rows Ug.  U and V may be reused after the producer stream
- * passes this point.  K must equal the registered K. */
+ * passes this point.  K must equal the registered K.
+ * SF-PS layers (POSEIDON_SCHEME_SFPS) take the same call: after the pack, each
+ * rank sends its U rows of master q's block to q (NCCL send/recv) and all-gathers
+ * V and the bias sums; master r runs K1 on its rows [rb, re) only
+ * (W[rb:re] += alpha * sum_p U_p[:, rb:re]^T V_p); every master then broadcasts
+ * its updated rows (ncclBroadcast, root q, in place) and every rank applies the
+ * same bias update.  W must be the same-shaped replica on every rank. */
 poseidon_status_t poseidon_sync_fc_sfb(poseidon_ctx_t ctx, int32_t layer_id, const float* U,
                                        const float* V, float* W, float* bias, float lr,
                                        poseidon_stream_t producer);
@@ -192,7 +208,9 @@ poseidon_status_t poseidon_shard_range(int64_t n, int32_t P, int32_t rank, int64
 
 /* Register layer `layer_id` (0 <= id < 4096): kind, M x N weight, per-worker
  * batch K, has_bias.  scheme_override: -1 -> SACP rule, else the scheme to use
- * (C2 forces PS).  chosen_scheme may be NULL.  SFB layers get library-owned
+ * (C2 forces PS; 2 = SF-PS, FC only).  chosen_scheme may be NULL.  With
+ * POSEIDON_FLAG_SFPS an FC layer the rule sends to PS is registered as SF-PS.
+ * SFB and SF-PS layers get library-owned
  * gather buffers, rank-major with K-major blocks (the tensor cores consume
  * TF32 operands K-major): Ug [P][M][ldk], Vg [P][N][ldk], Bs [P][M] (per-worker
  * column sums of U for the bias), ldk = roundup(K,4), padding zero.
@@ -201,7 +219,7 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t ctx, int32_t layer_id, 
                                           int64_t M, int64_t N, int64_t K, int32_t has_bias,
                                           int32_t scheme_override, int32_t* chosen_scheme);
 
-/* Staging slot of an SFB layer for poseidon_backprop_hook: library-owned
+/* Staging slot of an SFB / SF-PS layer for poseidon_backprop_hook: library-owned
  * device buffers U [K x M] (*ld_u = M) and V [K x N] (*ld_v = N), row-major,
  * allocated on first call.  The caller writes the factors there (ordered
  * before the hook's stream), then calls poseidon_backprop_hook. */
@@ -212,7 +230,7 @@ poseidon_status_t poseidon_sfb_slot(poseidon_ctx_t ctx, int32_t layer_id, float*
 /* Bind a PS layer's padded flat buffers (caller-owned, padded_n floats each). */
 poseidon_status_t poseidon_bind_ps_buffers(poseidon_ctx_t ctx, int32_t layer_id, float* grad,
                                            float* W, int64_t n, uint32_t flags);
-/* Bind an SFB layer's parameters (W: M x N, bias: M or NULL). */
+/* Bind an SFB / SF-PS layer's parameters (W: M x N, bias: M or NULL). */
 poseidon_status_t poseidon_bind_sfb_params(poseidon_ctx_t ctx, int32_t layer_id, float* W, float* bias);
 
 /* PS arena (collective over all ranks when world > 1): allocates ONE padded
@@ -240,7 +258,8 @@ poseidon_status_t poseidon_ps_layer_buffers(poseidon_ctx_t ctx, int32_t layer_id
                                             int64_t* padded_n);
 /* How SFB layer `layer_id` moves its factors at world > 1: 0 = NCCL all-gather on plain device
  * buffers, 1 = NCCL all-gather on symmetric-window buffers (FLAG_SYMM_SFB), 2 = NVLS multicast
- * broadcast (FLAG_NVLS_SFB).  Negative status for a bad id or a PS layer. */
+ * broadcast (FLAG_NVLS_SFB), 3 = SF-PS layer (NCCL send/recv of U row blocks, all-gather of V, broadcast of
+ * the masters' W rows).  Negative status for a bad id or a PS layer. */
 int32_t poseidon_sfb_path(poseidon_ctx_t ctx, int32_t layer_id);
 /* Human-readable state of the fused NVLS PS path ("active", "not requested", or the NCCL error). */
 const char* poseidon_nvls_status(poseidon_ctx_t ctx);
@@ -319,6 +338,15 @@ poseidon_status_t poseidon_ps_shard_update(const float* g, float* W, int64_t cou
 poseidon_status_t poseidon_reconstruct_sgd(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk,
                                            int64_t M, int64_t N, float* W, float alpha, int32_t recon,
                                            poseidon_stream_t stream);
+
+/* The SF-PS master's reconstruction (reading Z20): rows [m0, m1) only of the above,
+ * W[m][n] += alpha * sum_p sum_k<K Ug[p][m][k] Vg[p][n][k] for m0 <= m < m1 and every n, with
+ * Ug [P][M][ldk] the full gather buffer (M rows per worker block) and W the full M x N matrix;
+ * rows outside [m0, m1) are not touched.  0 <= m0 <= m1 <= M.  TF32 path: as above, and
+ * W + m0*N, Ug + m0*ldk must stay 16-byte aligned (N, ldk multiples of 4). */
+poseidon_status_t poseidon_reconstruct_sgd_rows(const float* Ug, const float* Vg, int32_t P, int64_t K,
+                                                int64_t ldk, int64_t M, int64_t m0, int64_t m1, int64_t N,
+                                                float* W, float alpha, int32_t recon, poseidon_stream_t stream);
 
 #ifdef __cplusplus
 }

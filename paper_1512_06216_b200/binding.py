@@ -20,11 +20,12 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "poseidon.h")
 OK = 0
 ERR_INVALID_ARG, ERR_NOT_INITIALIZED, ERR_CUDA, ERR_NCCL = -1, -2, -3, -4
 ERR_SHAPE, ERR_ALIGNMENT, ERR_UNSUPPORTED, ERR_STATE = -5, -6, -7, -8
-SCHEME_PS, SCHEME_SFB = 0, 1
+SCHEME_PS, SCHEME_SFB, SCHEME_SFPS = 0, 1, 2
 LAYER_CONV, LAYER_FC = 0, 1
 RECON_TF32, RECON_FP32 = 0, 1
 FLAG_DWBP_OFF, FLAG_NO_PRIORITY, FLAG_NVLS_PS, FLAG_SYMM_SFB, FLAG_NVLS_SFB, FLAG_SSP1 = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
-SFB_PATH_NCCL, SFB_PATH_NCCL_SYMM, SFB_PATH_NVLS = 0, 1, 2
+FLAG_SFPS = 0x40
+SFB_PATH_NCCL, SFB_PATH_NCCL_SYMM, SFB_PATH_NVLS, SFB_PATH_SFPS = 0, 1, 2, 3
 PS_ZERO_GRAD = 0x1
 
 _STATUS_NAMES = {0: "OK", -1: "INVALID_ARG", -2: "NOT_INITIALIZED", -3: "CUDA", -4: "NCCL",
@@ -120,6 +121,8 @@ _SIGS = {
     "poseidon_ps_simulated": (_i32, [_vp, _i32, _vp, _i64, _f, _vp]),
     "poseidon_ps_shard_update": (_i32, [_vp, _vp, _i64, _f, _vp, _vp]),
     "poseidon_reconstruct_sgd": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _f, _i32, _vp]),
+    "poseidon_reconstruct_sgd_rows": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _f, _i32,
+                                             _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(lib, _name)
@@ -331,6 +334,11 @@ def ps_shard_update(g, W, count, alpha, stats=None, stream=None):
 def reconstruct_sgd(Ug, Vg, P, K, ldk, M, N, W, alpha, recon=RECON_TF32, stream=None):
     _check(lib.poseidon_reconstruct_sgd(_ptr(Ug), _ptr(Vg), P, K, ldk, M, N, _ptr(W), float(alpha), recon,
                                         _stream(stream)))
+
+
+def reconstruct_sgd_rows(Ug, Vg, P, K, ldk, M, m0, m1, N, W, alpha, recon=RECON_TF32, stream=None):
+    _check(lib.poseidon_reconstruct_sgd_rows(_ptr(Ug), _ptr(Vg), P, K, ldk, M, m0, m1, N, _ptr(W), float(alpha),
+                                             recon, _stream(stream)))
 
 
 class _CudaArray:

@@ -101,6 +101,8 @@ struct Layer {
   ncclWindow_t win = nullptr;
   ncclComm_t win_comm = nullptr;
   bool bcast = false;   // POSEIDON_FLAG_NVLS_SFB: factors broadcast by the multicast kernel
+  // SF-PS (scheme 2, reading Z20): output rows [rb, re) this rank is the master of (O2 on the rows)
+  int64_t rb = 0, re = 0;
   float *stU = nullptr, *stV = nullptr;
   float *W = nullptr, *bias = nullptr;  // bound SFB params
   // PS: caller-owned padded flat buffers
@@ -333,6 +335,120 @@ poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float*
   return POSEIDON_OK;
 }
 
+// SF-PS (Alg. 3 else-branch, "Send u, v to the master node; Synchronize A_i from the
+// master node"; reading Z20): the master is sharded by output rows, rank q owns rows
+// [qb, qe) = poseidon_shard_range(M, P, q).  Step 1 on the comm stream: every worker sends its
+// error-message rows of q's block (its U slot, rows [qb, qe), contiguous in the K-major layout) to
+// master q and its inputs V to everyone (all-gather, which is "send v to every master"), plus the
+// per-worker bias sums.  Records e.start and e.gathered.
+poseidon_status_t sfps_comm(poseidon_ctx_t c, Layer& L, EvSet& e, cudaEvent_t wait_ev, IterRecord& r) {
+  const int P = c->world;
+  CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
+  CU_TRY(cudaEventRecord(e.start, c->comm_stream));
+  e.g_eff = e.start;
+  if (P <= 1) return POSEIDON_OK;
+  const size_t ucount = (size_t)(L.M * L.ldk), vcount = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
+  NC_TRY(ncclGroupStart());
+  NC_TRY(ncclAllGather(L.Vg + (size_t)c->rank * vcount, L.Vg, vcount, ncclFloat32, c->comm, c->comm_stream));
+  NC_TRY(ncclAllGather(L.Bs + (size_t)c->rank * bcount, L.Bs, bcount, ncclFloat32, c->comm, c->comm_stream));
+  NC_TRY(ncclGroupEnd());
+  uint64_t sent = (uint64_t)(vcount + bcount) * 4u, recv = (uint64_t)(vcount + bcount) * 4u * (uint64_t)(P - 1);
+  NC_TRY(ncclGroupStart());
+  const size_t own = (size_t)(L.re - L.rb) * (size_t)L.ldk;
+  for (int q = 0; q < P; ++q) {
+    if (q == c->rank) continue;
+    int64_t qb, qe, pad;
+    poseidon_shard_range(L.M, P, q, &qb, &qe, &pad);
+    if (qe > qb) {
+      const size_t cnt = (size_t)(qe - qb) * (size_t)L.ldk;
+      NC_TRY(ncclSend(L.Ug + (size_t)c->rank * ucount + (size_t)qb * L.ldk, cnt, ncclFloat32, q, c->comm,
+                      c->comm_stream));
+      sent += (uint64_t)cnt * 4u;
+    }
+    if (own > 0) {
+      NC_TRY(ncclRecv(L.Ug + (size_t)q * ucount + (size_t)L.rb * L.ldk, own, ncclFloat32, q, c->comm,
+                      c->comm_stream));
+      recv += (uint64_t)own * 4u;
+    }
+  }
+  NC_TRY(ncclGroupEnd());
+  r.sent += sent;
+  r.recv += recv;
+  CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+  e.g_eff = e.gathered;
+  return POSEIDON_OK;
+}
+
+// SF-PS step 2: master r reconstructs only its rows, W[rb:re] += alpha * sum_p U_p[rb:re]^T V_p (K1 on
+// a row block of the gather buffer, recon stream), then every master broadcasts its updated rows to
+// the other workers (comm stream) and the bias (M floats, from the gathered per-worker sums) is
+// updated on every rank alike.  Records kstart / kend / done.
+poseidon_status_t sfps_update(poseidon_ctx_t c, Layer& L, float* W, float* bias, float lr, cudaEvent_t src_g,
+                              EvSet& dst, IterRecord& r) {
+  const int P = c->world;
+  CU_TRY(cudaStreamWaitEvent(c->recon_stream, src_g, 0));
+  CU_TRY(cudaEventRecord(dst.kstart, c->recon_stream));
+  dst.ks_eff = dst.kstart;
+  dst.ke_eff = dst.kend;
+  const float alpha = -lr / (float)P;
+  const bool mom = (L.vel != nullptr);
+  const int64_t mb = L.re - L.rb;
+  cudaError_t err = cudaSuccess;
+  if (mb > 0) {
+    float* target = (mom ? L.vel : W) + (size_t)L.rb * L.N;
+    const float a1 = mom ? (lr / (float)P) : alpha, b1 = mom ? L.mu : 1.0f;
+    const float* Ub = L.Ug + (size_t)L.rb * L.ldk;
+    if (L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(Ub, L.Vg, L.ldk, mb, L.N, target))
+      err = launch_recon_tcgen05(Ub, L.Vg, P, L.K, L.ldk, mb, L.N, target, a1, b1, c->recon_stream, nullptr, L.M);
+    else
+      err = launch_recon_simt(Ub, L.Vg, P, L.K, L.ldk, mb, L.N, target, a1, b1, c->recon_stream, L.M);
+    if (err != cudaSuccess) return cuda_fail(err, "SF-PS row-block reconstruct+sgd launch");
+    if (mom) {
+      err = launch_momentum_apply(W + (size_t)L.rb * L.N, L.vel + (size_t)L.rb * L.N, mb * L.N, lr * L.wd,
+                                  c->recon_stream);
+      if (err != cudaSuccess) return cuda_fail(err, "momentum apply launch");
+    }
+    if ((err = debug_sync(c->recon_stream, "SF-PS K1")) != cudaSuccess) return cuda_fail(err, "SF-PS K1");
+  }
+  CU_TRY(cudaEventRecord(dst.kend, c->recon_stream));
+  CU_TRY(cudaStreamWaitEvent(c->comm_stream, dst.kend, 0));
+  if (P > 1) {
+    NC_TRY(ncclGroupStart());
+    for (int q = 0; q < P; ++q) {
+      int64_t qb, qe, pad;
+      poseidon_shard_range(L.M, P, q, &qb, &qe, &pad);
+      if (qe <= qb) continue;
+      float* rows = W + (size_t)qb * L.N;
+      const size_t cnt = (size_t)(qe - qb) * (size_t)L.N;
+      NC_TRY(ncclBroadcast(rows, rows, cnt, ncclFloat32, q, c->comm, c->comm_stream));
+      if (q == c->rank) r.sent += (uint64_t)cnt * 4u;
+      else r.recv += (uint64_t)cnt * 4u;
+    }
+    NC_TRY(ncclGroupEnd());
+  }
+  if (bias) {
+    err = mom ? launch_bias_momentum(L.Bs, L.M, P, bias, L.vel_b, L.M, lr, L.mu, L.wd, c->comm_stream)
+              : launch_bias_update(L.Bs, L.M, P, bias, L.M, alpha, c->comm_stream);
+    if (err != cudaSuccess) return cuda_fail(err, "bias update launch");
+  }
+  CU_TRY(cudaEventRecord(dst.done, c->comm_stream));
+  return POSEIDON_OK;
+}
+
+// BSP sync of a factor layer: SFB or SF-PS.
+poseidon_status_t launch_factor_sync(poseidon_ctx_t c, int32_t id, Layer& L, float* W, float* bias, float lr,
+                                     cudaEvent_t wait_ev) {
+  if (L.scheme == POSEIDON_SCHEME_SFB) return launch_sfb_comm(c, id, L, W, bias, lr, wait_ev);
+  EvSet& e = L.ev[c->iter % RING];
+  IterRecord& r = open_record(c);
+  poseidon_status_t st = sfps_comm(c, L, e, wait_ev, r);
+  if (st) return st;
+  st = sfps_update(c, L, W, bias, lr, e.g_eff, e, r);
+  if (st) return st;
+  r.layers.push_back(id);
+  return POSEIDON_OK;
+}
+
 bool ps_fused(poseidon_ctx_t c, const Layer& L) { return c->world > 1 && c->ps_nvls && L.in_arena; }
 
 // PS reduce-scatter leg (Alg. 3 line 1-2 / Alg. 1 "Collect gradients") of gradient buffer `grad` on
@@ -517,7 +633,7 @@ poseidon_status_t sfb_after_pack(poseidon_ctx_t c, int32_t id, Layer& L, float* 
     open_record(c);
     return POSEIDON_OK;
   }
-  return launch_sfb_comm(c, id, L, W, bias, lr, e.ready);
+  return launch_factor_sync(c, id, L, W, bias, lr, e.ready);
 }
 
 poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t ldU, const float* V, int64_t ldV,
@@ -686,12 +802,18 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
   if (id < 0 || id >= MAX_LAYERS) return fail(POSEIDON_ERR_INVALID_ARG, "layer_id out of range [0,4096)");
   if (kind != POSEIDON_LAYER_CONV && kind != POSEIDON_LAYER_FC) return fail(POSEIDON_ERR_INVALID_ARG, "bad kind");
   if (M <= 0 || N <= 0 || K <= 0) return fail(POSEIDON_ERR_SHAPE, "M, N, K must be positive");
-  if (scheme_override < -1 || scheme_override > 1) return fail(POSEIDON_ERR_INVALID_ARG, "bad scheme_override");
+  if (scheme_override < -1 || scheme_override > 2) return fail(POSEIDON_ERR_INVALID_ARG, "bad scheme_override");
   int32_t rule = poseidon_choose_scheme(kind, M, N, K, c->world, nullptr);
   if (rule < 0) return (poseidon_status_t)rule;
-  const int32_t scheme = scheme_override >= 0 ? scheme_override : rule;
-  if (scheme == POSEIDON_SCHEME_SFB && kind != POSEIDON_LAYER_FC)
-    return fail(POSEIDON_ERR_INVALID_ARG, "SFB needs an FC layer (Alg. 3)");
+  int32_t scheme = scheme_override >= 0 ? scheme_override : rule;
+  // FLAG_SFPS: an FC layer the rule sends to the server runs Alg. 3's else-branch literally
+  if (scheme_override < 0 && scheme == POSEIDON_SCHEME_PS && kind == POSEIDON_LAYER_FC &&
+      (c->flags & POSEIDON_FLAG_SFPS))
+    scheme = POSEIDON_SCHEME_SFPS;
+  if (scheme != POSEIDON_SCHEME_PS && kind != POSEIDON_LAYER_FC)
+    return fail(POSEIDON_ERR_INVALID_ARG, "SFB / SF-PS need an FC layer (Alg. 3)");
+  if (scheme == POSEIDON_SCHEME_SFPS && c->ssp)
+    return fail(POSEIDON_ERR_UNSUPPORTED, "SF-PS layers are not supported with FLAG_SSP1");
   cudaSetDevice(c->device);
   if (id >= (int32_t)c->layers.size()) c->layers.resize((size_t)id + 1);
   Layer& L = c->layers[id];
@@ -707,7 +829,11 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
   L.K = K;
   L.has_bias = has_bias != 0;
   L.scheme = scheme;
-  if (scheme == POSEIDON_SCHEME_SFB) {
+  if (scheme == POSEIDON_SCHEME_SFPS) {
+    int64_t pad;
+    poseidon_shard_range(M, c->world, c->rank, &L.rb, &L.re, &pad);
+  }
+  if (scheme != POSEIDON_SCHEME_PS) {
     L.ldk = round_up(K, 4);
     const size_t P = (size_t)c->world;
     const size_t ub = P * (size_t)(M * L.ldk) * 4, vb = P * (size_t)(N * L.ldk) * 4, bb = P * (size_t)M * 4;
@@ -736,7 +862,7 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
             L.Bs2 = reinterpret_cast<float*>(b0 + one + ua + va);
           }
           placed = true;
-          L.bcast = c->want_nvls_sfb && ensure_devcomm(c);
+          L.bcast = scheme == POSEIDON_SCHEME_SFB && c->want_nvls_sfb && ensure_devcomm(c);
         } else {
           ncclMemFree(base);
         }
@@ -773,7 +899,7 @@ poseidon_status_t poseidon_sfb_slot(poseidon_ctx_t c, int32_t id, float** U_slot
   Layer* L;
   poseidon_status_t st = check_layer(c, id, &L);
   if (st) return st;
-  if (L->scheme != POSEIDON_SCHEME_SFB) return fail(POSEIDON_ERR_STATE, "layer is not an SFB layer");
+  if (L->scheme == POSEIDON_SCHEME_PS) return fail(POSEIDON_ERR_STATE, "layer is not an SFB / SF-PS layer");
   if (!L->stU) {
     cudaSetDevice(c->device);
     CU_TRY(cudaMalloc(&L->stU, (size_t)(L->K * L->M) * 4));
@@ -813,7 +939,7 @@ poseidon_status_t poseidon_bind_sfb_params(poseidon_ctx_t c, int32_t id, float* 
   Layer* L;
   poseidon_status_t st = check_layer(c, id, &L);
   if (st) return st;
-  if (L->scheme != POSEIDON_SCHEME_SFB) return fail(POSEIDON_ERR_STATE, "layer is not an SFB layer");
+  if (L->scheme == POSEIDON_SCHEME_PS) return fail(POSEIDON_ERR_STATE, "layer is not an SFB / SF-PS layer");
   if (!W) return fail(POSEIDON_ERR_INVALID_ARG, "W is NULL");
   if (bias && !L->has_bias) return fail(POSEIDON_ERR_INVALID_ARG, "layer registered without bias");
   L->W = W;
@@ -999,7 +1125,8 @@ int32_t poseidon_sfb_path(poseidon_ctx_t c, int32_t id) {
   Layer* L;
   poseidon_status_t st = check_layer(c, id, &L);
   if (st) return st;
-  if (L->scheme != POSEIDON_SCHEME_SFB) return fail(POSEIDON_ERR_STATE, "layer is not an SFB layer");
+  if (L->scheme == POSEIDON_SCHEME_PS) return fail(POSEIDON_ERR_STATE, "layer is not an SFB / SF-PS layer");
+  if (L->scheme == POSEIDON_SCHEME_SFPS) return 3;
   return L->bcast ? 2 : (L->symm ? 1 : 0);
 }
 
@@ -1022,7 +1149,7 @@ static poseidon_status_t set_momentum_one(poseidon_ctx_t c, Layer& L, float mu, 
   if (L.vel) return POSEIDON_OK;  // keep the existing velocity
   cudaSetDevice(c->device);
   size_t count;
-  if (L.scheme == POSEIDON_SCHEME_SFB) {
+  if (L.scheme != POSEIDON_SCHEME_PS) {   // SFB: replicated; SF-PS: only the master's rows are used
     count = (size_t)(L.M * L.N);
     if (L.has_bias) {
       CU_TRY(cudaMalloc(&L.vel_b, (size_t)L.M * 4));
@@ -1087,7 +1214,7 @@ poseidon_status_t poseidon_sync_fc_sfb(poseidon_ctx_t c, int32_t id, const float
   Layer* L;
   poseidon_status_t st = check_layer(c, id, &L);
   if (st) return st;
-  if (L->scheme != POSEIDON_SCHEME_SFB) return fail(POSEIDON_ERR_STATE, "layer is not an SFB layer");
+  if (L->scheme == POSEIDON_SCHEME_PS) return fail(POSEIDON_ERR_STATE, "layer is not an SFB / SF-PS layer");
   if (!U || !V) return fail(POSEIDON_ERR_INVALID_ARG, "U/V is NULL");
   if (!W) W = L->W;
   if (!bias) bias = L->bias;
@@ -1233,8 +1360,8 @@ poseidon_status_t poseidon_iteration_end(poseidon_ctx_t c, poseidon_stream_t com
       Layer& L = resolve(c, id);
       if (!L.pending) continue;
       L.pending = false;
-      st = (L.scheme == POSEIDON_SCHEME_SFB)
-               ? launch_sfb_comm(c, id, L, L.pending_W, L.pending_bias, L.pending_lr, r.bwd_end)
+      st = (L.scheme != POSEIDON_SCHEME_PS)
+               ? launch_factor_sync(c, id, L, L.pending_W, L.pending_bias, L.pending_lr, r.bwd_end)
                : launch_ps_comm(c, id, L, L.pending_grad, L.pending_W, L.pending_lr, r.bwd_end);
       if (st) return st;
     }
@@ -1266,7 +1393,7 @@ poseidon_status_t poseidon_get_iter_stats(poseidon_ctx_t c, int32_t ago, poseido
     first_ready = std::max(first_ready, elapsed(e.ready, r.bwd_end));
     out->sync_total_ms += elapsed(e.start, e.done);
     out->queue_ms += elapsed(e.ready, e.start);
-    if (L.scheme == POSEIDON_SCHEME_SFB)
+    if (L.scheme != POSEIDON_SCHEME_PS)
       out->recon_ms += elapsed(e.ks_eff, e.ke_eff);
     else
       out->ps_update_ms += elapsed(e.ks_eff, e.ke_eff);
@@ -1396,6 +1523,29 @@ poseidon_status_t poseidon_reconstruct_sgd(const float* Ug, const float* Vg, int
     return fail(POSEIDON_ERR_INVALID_ARG, "bad recon");
   }
   if (err != cudaSuccess) return cuda_fail(err, "reconstruct_sgd launch");
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_reconstruct_sgd_rows(const float* Ug, const float* Vg, int32_t P, int64_t K,
+                                                int64_t ldk, int64_t M, int64_t m0, int64_t m1, int64_t N,
+                                                float* W, float alpha, int32_t recon, poseidon_stream_t stream) {
+  if (!Ug || !Vg || !W || P < 1 || K < 0 || M <= 0 || N <= 0 || ldk < K || m0 < 0 || m1 < m0 || m1 > M)
+    return fail(POSEIDON_ERR_INVALID_ARG, "reconstruct_sgd_rows: bad arguments");
+  if (m1 == m0 || K == 0) return POSEIDON_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const float* Ub = Ug + (size_t)m0 * ldk;
+  float* Wb = W + (size_t)m0 * N;
+  cudaError_t err;
+  if (recon == POSEIDON_RECON_TF32) {
+    if (!recon_tcgen05_supported(Ub, Vg, ldk, m1 - m0, N, Wb))
+      return fail(POSEIDON_ERR_ALIGNMENT, "tcgen05 path needs 16-B aligned row blocks and ldk, N multiples of 4");
+    err = launch_recon_tcgen05(Ub, Vg, P, K, ldk, m1 - m0, N, Wb, alpha, 1.0f, s, nullptr, M);
+  } else if (recon == POSEIDON_RECON_FP32) {
+    err = launch_recon_simt(Ub, Vg, P, K, ldk, m1 - m0, N, Wb, alpha, 1.0f, s, M);
+  } else {
+    return fail(POSEIDON_ERR_INVALID_ARG, "bad recon");
+  }
+  if (err != cudaSuccess) return cuda_fail(err, "reconstruct_sgd_rows launch");
   return POSEIDON_OK;
 }
 

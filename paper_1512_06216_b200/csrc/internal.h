@@ -52,14 +52,17 @@ cudaError_t launch_bias_update(const float* bs, int64_t ld, int32_t P, float* bi
                                cudaStream_t s);
 
 // K1r: W[M x N] += alpha * sum_p sum_k Ug[p][m][k] Vg[p][n][k] on CUDA cores (fp32 FMA).
+// ldm (0 = M): rows per worker block of Ug, so Ug may point at row m0 of a larger gather buffer and
+// M be the number of rows of the block (SF-PS reconstructs only its master's rows).
 cudaError_t launch_recon_simt(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
-                              int64_t N, float* W, float alpha, float beta, cudaStream_t s);
+                              int64_t N, float* W, float alpha, float beta, cudaStream_t s, int64_t ldm = 0);
 
 // K1: the same on tcgen05 (TF32 operands, fp32 TMEM accumulators).  Returns cudaErrorNotSupported
 // when TMA cannot describe the buffers.  Tensor maps are encoded per call (host only, ~us).
 // Both compute W' = fmaf(alpha, acc, beta * W) (beta = 1: SGD; beta = mu: velocity update, f4).
 cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
-                                 int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg = nullptr);
+                                 int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg = nullptr,
+                                 int64_t ldm = 0);
 bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int64_t M, int64_t N, const float* W);
 
 }  // namespace poseidon

@@ -795,9 +795,10 @@ int sm_count_k1() {
 namespace {
 struct MapKey {
   const void *u, *v, *w;
-  int64_t P, K, ldk, M, N;
+  int64_t P, K, ldk, M, N, ldm;
   bool operator==(const MapKey& o) const {
-    return u == o.u && v == o.v && w == o.w && P == o.P && K == o.K && ldk == o.ldk && M == o.M && N == o.N;
+    return u == o.u && v == o.v && w == o.w && P == o.P && K == o.K && ldk == o.ldk && M == o.M && N == o.N &&
+           ldm == o.ldm;
   }
 };
 struct MapEntry {
@@ -835,18 +836,23 @@ bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int6
 }
 
 cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
-                                 int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg) {
+                                 int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg,
+                                 int64_t ldm) {
   if (M <= 0 || N <= 0 || K <= 0 || P <= 0) return cudaSuccess;
+  if (ldm <= 0) ldm = M;
+  if (ldm < M) return cudaErrorInvalidValue;
   if (!recon_tcgen05_supported(Ug, Vg, ldk, M, N, W) || ldk < K) return cudaErrorNotSupported;
   CUtensorMap tmA, tmB, tmW, tmB2;
   const int variant = knobs().variant;
   // Tensor maps are cached per (buffers, shape): encoding four of them costs ~10 us of host time per
   // launch, which lands on the step whenever the GPU is not far behind the host (small layers).
-  const MapKey key{Ug, Vg, W, P, K, ldk, M, N};
+  const MapKey key{Ug, Vg, W, P, K, ldk, M, N, ldm};
   if (dbg == nullptr && map_cache_get(key, &tmA, &tmB, &tmW, &tmB2)) goto have_maps;
   {
   const uint64_t dA[3] = {(uint64_t)ldk, (uint64_t)M, (uint64_t)P};
-  const uint64_t sA[2] = {(uint64_t)ldk * 4, (uint64_t)ldk * 4 * (uint64_t)M};
+  // rows [M, ldm) of a worker block belong to other masters (SF-PS): outside the map, so TMA
+  // fills them with zeros
+  const uint64_t sA[2] = {(uint64_t)ldk * 4, (uint64_t)ldk * 4 * (uint64_t)ldm};
   const uint32_t bA[3] = {BK, BM, 1};
   const uint64_t dB[3] = {(uint64_t)ldk, (uint64_t)N, (uint64_t)P};
   const uint64_t sB[2] = {(uint64_t)ldk * 4, (uint64_t)ldk * 4 * (uint64_t)N};

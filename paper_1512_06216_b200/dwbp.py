@@ -137,12 +137,14 @@ class PoseidonSync:
             override = B.SCHEME_PS
         elif scheme == "sfb" and kind == B.LAYER_FC:
             override = B.SCHEME_SFB
+        elif scheme == "sfps" and kind == B.LAYER_FC:
+            override = B.SCHEME_SFPS
         has_bias = mod.bias is not None
         chosen = self.ctx.register_layer(lid, kind, M, N, self.K, has_bias, override)
         plan = LayerPlan(lid, name, mod, kind, M, N, self.K, chosen, rule, costs)
         self.plans.append(plan)
         self.by_module[mod] = plan
-        if chosen == B.SCHEME_SFB:
+        if chosen in (B.SCHEME_SFB, B.SCHEME_SFPS):   # factor schemes: the local dW is never formed
             self.ctx.set_recon(recon, lid)
             mod.weight.data = mod.weight.data.contiguous()
             self.ctx.bind_sfb_params(lid, mod.weight, mod.bias)
@@ -261,7 +263,7 @@ class PoseidonSync:
             mpick, t_sfb, t_ps = B.choose_scheme_model(p.kind, p.M, p.N, p.K, self.ctx.world)
             out.append({"id": p.layer_id, "name": p.name, "kind": "fc" if p.kind == B.LAYER_FC else "conv",
                         "M": p.M, "N": p.N, "K": p.K,
-                        "scheme": "SFB" if p.scheme == B.SCHEME_SFB else "PS",
+                        "scheme": {B.SCHEME_SFB: "SFB", B.SCHEME_SFPS: "SFPS"}.get(p.scheme, "PS"),
                         "rule": "SFB" if p.rule_scheme == B.SCHEME_SFB else "PS",
                         "model": "SFB" if mpick == B.SCHEME_SFB else "PS",
                         "model_t_sfb_us": round(t_sfb, 1), "model_t_ps_us": round(t_ps, 1),

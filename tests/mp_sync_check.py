@@ -13,6 +13,10 @@ Checks, at world = P:
      auto and forced PS, DWBP on and off): all ranks' parameters
      bit-identical, DWBP on == off bitwise, and the step equals single-GPU SGD
      on the concatenated P*K batch (torch fp32 reference, TF32 gate).
+  8. SF-PS (the literal else-branch of Alg. 3, reading Z20): integer variant bit-exact vs O11 on three
+     shapes (masters with no rows at P = 4), plain / symmetric buffers / DWBP off, both kernels, NCCL
+     byte counts; random factors with momentum vs O4m; FLAG_SFPS auto-selection; CIFAR-quick with
+     every FC layer as SF-PS in test 4.
   6. SSP, staleness 1: SFB + PS over 4 iterations and a flush, integer variant bit-exact vs O10 on
      the NCCL and the NVLS paths.
   7. PS buckets: six layers of mixed sizes, NCCL and fused NVLS paths, integer bit-exact per layer.
@@ -269,6 +273,7 @@ def main():
     Kc = 16
     results = {}
     variants = [(sc, dw, nv) for sc in ("auto", "ps") for dw in ("on", "off") for nv in (False, True)]
+    variants += [("sfps", dw, False) for dw in ("on", "off")]   # every FC layer as SF-PS
     for scheme, dwbp, nv in variants:
         if True:
             c2 = new_ctx((pz.FLAG_DWBP_OFF if dwbp == "off" else 0) | (pz.FLAG_NVLS_PS if nv else 0))
@@ -301,10 +306,9 @@ def main():
                 assert err < 2e-3, (name, err, scheme, dwbp, nv)
             results[(scheme, dwbp, nv)] = flat.cpu()
             c2.close()
-    for scheme in ("auto", "ps"):
-        for nv in (False, True):
-            assert torch.equal(results[(scheme, "on", nv)], results[(scheme, "off", nv)]), \
-                f"DWBP on/off differ ({scheme}, nvls {nv})"
+    for scheme, nv in [(sc, nv) for sc in ("auto", "ps") for nv in (False, True)] + [("sfps", False)]:
+        assert torch.equal(results[(scheme, "on", nv)], results[(scheme, "off", nv)]), \
+            f"DWBP on/off differ ({scheme}, nvls {nv})"
     # ---- 6. SSP with staleness 1 (FLAG_SSP1, reading Z19): SFB + PS (arena) over 4 iterations and a
     #          flush, integer variant bit-exact vs O10, on the NCCL paths and on the NVLS paths ----
     from paper_1512_06216_b200.binding import device_view
@@ -397,6 +401,73 @@ def main():
             print(f"buckets flags={flags}: {st['n_layers']} syncs for {len(shapes)} layers, PS {cb.nvls_status()}",
                   flush=True)
         cb.close()
+
+    # ---- 8. SF-PS (Alg. 3 else-branch, reading Z20): U rows to their masters, V all-gathered, K1 on the
+    #          master's rows, masters broadcast their rows.  Integer variant bit-exact vs O11 (both
+    #          kernels, plain and symmetric-window buffers, DWBP off), three shapes: C1, M=40 (masters with
+    #          8 rows and with none at P=4), fc8-like 1000 x 4096 with ragged K; 2 iterations; bytes ----
+    for flags in (0, pz.FLAG_SYMM_SFB, pz.FLAG_DWBP_OFF):
+        cp = new_ctx(flags)
+        shapes = [(0, 128, 256, 8), (1, 40, 72, 4), (2, 1000, 4096, 33)]
+        for lid, M_, N_, K_ in shapes:
+            assert cp.register_layer(lid, pz.LAYER_FC, M_, N_, K_, True, pz.SCHEME_SFPS) == pz.SCHEME_SFPS
+            assert cp.sfb_path(lid) == pz.SFB_PATH_SFPS
+        for it in range(2):
+            cp.set_recon(pz.RECON_FP32 if it == 1 else pz.RECON_TF32)
+            outs = []
+            for lid, M_, N_, K_ in shapes:
+                W, b, Us, Vs, lr = S.integer_factors(M_, N_, K_, P, seed=900 + 10 * it + lid)
+                Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+                cp.sync_fc_sfb(lid, torch.from_numpy(Us[rank]).to(dev), torch.from_numpy(Vs[rank]).to(dev), Wd, bd, lr)
+                outs.append((W, b, Us, Vs, lr, Wd, bd))
+            st = cp.iteration_end(stats=True)
+            for lid, (W, b, Us, Vs, lr, Wd, bd) in enumerate(outs):
+                cp.wait_layer(lid)
+            torch.cuda.synchronize()
+            for lid, (W, b, Us, Vs, lr, Wd, bd) in enumerate(outs):
+                W11, b11, _ = O.sf_ps_simulated(W, b, Us, Vs, lr)
+                assert np.array_equal(Wd.cpu().numpy().astype(np.float64), W11), f"SF-PS flags={flags} it={it} lid={lid}"
+                assert np.array_equal(bd.cpu().numpy().astype(np.float64), b11)
+                assert allsame(Wd) and allsame(bd)
+            # bytes through NCCL per rank: V + bias sums all-gathered, U rows to / from the masters,
+            # the masters' rows broadcast
+            exp_sent = exp_recv = 0
+            for lid, M_, N_, K_ in shapes:
+                ldk = (K_ + 3) // 4 * 4
+                if P == 1:
+                    continue
+                rows = [pz.shard_range(M_, P, q)[:2] for q in range(P)]
+                own = rows[rank][1] - rows[rank][0]
+                exp_sent += (N_ * ldk + M_) * 4 + sum((e - b_) * ldk * 4 for q, (b_, e) in enumerate(rows) if q != rank) \
+                    + own * N_ * 4
+                exp_recv += (N_ * ldk + M_) * 4 * (P - 1) + own * ldk * 4 * (P - 1) \
+                    + sum((e - b_) * N_ * 4 for q, (b_, e) in enumerate(rows) if q != rank)
+            assert st["nccl_bytes_sent"] == exp_sent and st["nccl_bytes_recv"] == exp_recv, (st, exp_sent, exp_recv)
+        cp.close()
+    # random factors + momentum (two steps, TF32 gate vs O4m, which O11 equals) and FLAG_SFPS auto-selection
+    cp = new_ctx(pz.FLAG_SFPS)
+    M_, N_, K_, lr_m, mu_m, wd_m = 300, 520, 16, 0.2, 0.9, 1e-2
+    cp.register_layer(0, pz.LAYER_FC, M_, N_, K_, True, pz.SCHEME_SFPS)
+    expect_auto = pz.SCHEME_SFB if P <= 2 else pz.SCHEME_SFPS   # C2 ip2 10x64, K=100: rule PS at P >= 3
+    assert cp.register_layer(1, pz.LAYER_FC, 10, 64, 100) == expect_auto
+    assert cp.register_layer(2, pz.LAYER_CONV, 10, 64, 100) == pz.SCHEME_PS
+    cp.set_lr(lr_m)
+    cp.set_momentum(mu_m, wd_m, 0)
+    W, b = S.fc_weights_randbias(M_, N_)
+    Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+    Wr, br = W.astype(np.float64), b.astype(np.float64)
+    VW, Vb = np.zeros_like(Wr), np.zeros_like(br)
+    for t in range(2):
+        Us, Vs = S.hidden_factors(M_, N_, K_, P, seed=950 + t)
+        cp.sync_fc_sfb(0, torch.from_numpy(Us[rank]).to(dev), torch.from_numpy(Vs[rank]).to(dev), Wd, bd, lr_m)
+        cp.wait_layer(0)
+        cp.iteration_end()
+        Wr, br, VW, Vb = O.sync_step_momentum(Wr, br, VW, Vb, Us, Vs, lr_m, mu_m, wd_m)
+    torch.cuda.synchronize()
+    assert O.update_error_fp32(W, Wd.cpu().numpy(), Wr) <= 2e-3, "SF-PS momentum"
+    assert O.update_error_fp32(b, bd.cpu().numpy(), br) <= 1e-5, "SF-PS bias momentum"
+    assert allsame(Wd) and allsame(bd)
+    cp.close()
 
     # ---- 5. full size in bench.py's N > 1 launch configuration (SYMM_SFB | NVLS_PS): C3 fc6 as SFB
     #          (4096 x 9216, K = 256) and a 37.7M-parameter PS layer in the NVLS arena, sampled against

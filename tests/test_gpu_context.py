@@ -28,6 +28,29 @@ def host(t):
     return t.detach().cpu().numpy()
 
 
+def test_context_sfps_world1(pz):
+    """SF-PS at P = 1 (scheme_override = 2): the only master owns every row, so the step is K1 on the
+    local factors (integer variant bit-exact vs O11); the bias follows the same update."""
+    ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device())
+    M, N, K = 130, 64, 5
+    assert ctx.register_layer(0, pz.LAYER_FC, M, N, K, scheme_override=pz.SCHEME_SFPS) == pz.SCHEME_SFPS
+    assert ctx.sfb_path(0) == pz.SFB_PATH_SFPS
+    with pytest.raises(pz.PoseidonError):
+        ctx.register_layer(1, pz.LAYER_CONV, M, N, K, scheme_override=pz.SCHEME_SFPS)
+    for recon in (pz.RECON_TF32, pz.RECON_FP32):
+        ctx.set_recon(recon, 0)
+        W, b, Us, Vs, lr = S.integer_factors(M, N, K, 1, seed=31)
+        Wd, bd = dev(W), dev(b)
+        ctx.sync_fc_sfb(0, dev(Us[0]), dev(Vs[0]), Wd, bd, lr)
+        ctx.wait_layer(0)
+        st = ctx.iteration_end(stats=True)
+        W1, b1, _ = O.sf_ps_simulated(W, b, Us, Vs, lr)
+        assert np.array_equal(host(Wd).astype(np.float64), W1)
+        assert np.array_equal(host(bd).astype(np.float64), b1)
+        assert st["nccl_bytes_sent"] == 0 and st["n_layers"] == 1
+    ctx.close()
+
+
 def test_context_sfb_and_ps_world1(pz):
     ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device())
     M, N, K = 128, 256, 8

@@ -217,6 +217,31 @@ def test_reconstruct_sgd_gather_layout(pz, recon):
     assert np.array_equal(host(Wd).astype(np.float64), ref)
 
 
+@pytest.mark.parametrize("recon", ["fp32", "tf32"])
+@pytest.mark.parametrize("m0,m1", [(0, 200), (0, 96), (96, 200), (33, 161), (199, 200), (50, 50)])
+def test_reconstruct_sgd_rows_master_block(pz, recon, m0, m1):
+    """SF-PS master (reading Z20): K1/K1r on rows [m0, m1) of the gather buffer, integer variant bit-exact
+    vs the oracle's O4 rows; every other row untouched.  (33, 161) spans tiles with a ragged start,
+    (199, 200) is a one-row block, (50, 50) an empty master."""
+    M, N, K, P, ldk = 200, 300, 6, 4, 8
+    g = S.rng(78)
+    U = np.zeros((P, M, ldk), np.float32)
+    V = np.zeros((P, N, ldk), np.float32)
+    U[:, :, :K] = g.integers(-3, 4, size=(P, M, K))
+    V[:, :, :K] = g.integers(0, 4, size=(P, N, K))
+    W = (g.integers(-1023, 1024, size=(M, N)) * 2.0 ** -10).astype(np.float32)
+    lr = 2.0 ** -7
+    Wd = dev(W)
+    pz.reconstruct_sgd_rows(dev(U), dev(V), P, K, ldk, M, m0, m1, N, Wd, -lr / P,
+                            recon=pz.RECON_FP32 if recon == "fp32" else pz.RECON_TF32)
+    Us = [U[p, :, :K].T.copy() for p in range(P)]
+    Vs = [V[p, :, :K].T.copy() for p in range(P)]
+    W1, _ = O.sync_step(W, None, Us, Vs, lr)
+    ref = W.astype(np.float64)
+    ref[m0:m1] = W1[m0:m1]
+    assert np.array_equal(host(Wd).astype(np.float64), ref)
+
+
 # ------------------------------------------- full size, sampled rows ----
 def _sampled_rows(M, n=48, seed=0):
     g = S.rng(seed)

@@ -6,7 +6,9 @@ layer, M=21841, N=4096), against the paper's rule (Alg. 3).
 For every K it measures, with CUDA events on the calling stream and the max over ranks:
   * SFB sync   : pack + all-gather of the factors + K1 reconstruct+SGD (poseidon_sync_fc_sfb);
   * PS sync    : reduce-scatter + K2 + all-gather (or the fused NVLS kernel) of the full gradient;
-  * wgrad      : the local dW = G^T X GEMM (cuBLAS TF32) that PS needs and SFB skips.
+  * SF-PS sync : the literal Alg. 3 else-branch (reading Z20): U rows to their masters + all-gather
+                 of V + K1 on the master's rows + broadcast of the rows (scheme_override = SFPS);
+  * wgrad      : the local dW = G^T X GEMM (cuBLAS TF32) that PS needs and SFB / SF-PS skip.
 and prints one JSON line per K with the rule's choice, the measured winner for sync-only and
 sync+wgrad, and the regret of the rule.
 """
@@ -74,6 +76,7 @@ def main():
         rule, costs = pz.choose_scheme(pz.LAYER_FC, M, N, K, world)
         ctx.register_layer(lid, pz.LAYER_FC, M, N, K, True, pz.SCHEME_SFB)
         ctx.register_layer(lid + 1, pz.LAYER_FC, M, N, K, True, pz.SCHEME_PS)
+        ctx.register_layer(lid + 2, pz.LAYER_FC, M, N, K, True, pz.SCHEME_SFPS)
         ctx.bind_ps_buffers(lid + 1, flat_g, flat_w, n, pz.PS_ZERO_GRAD)
         U = torch.randn(K, M, device=dev) / K
         V = torch.randn(K, N, device=dev).relu()
@@ -86,12 +89,16 @@ def main():
             ctx.sync_ps(lid + 1, flat_g, flat_w, n, 0.01, s)
             ctx.wait_layer(lid + 1, s)
 
+        def sfps():
+            ctx.sync_fc_sfb(lid + 2, U, V, W, b, 0.01, s)
+            ctx.wait_layer(lid + 2, s)
+
         gview = flat_g[: M * N].view(M, N)
 
         def wgrad():
             torch.mm(U.t(), V, out=gview)
 
-        t_sfb, t_ps, t_wg = timed(sfb), timed(ps), timed(wgrad)
+        t_sfb, t_ps, t_wg, t_sfps = timed(sfb), timed(ps), timed(wgrad), timed(sfps)
         ctx.iteration_end(s)
         meas_sync = pz.SCHEME_SFB if t_sfb <= t_ps else pz.SCHEME_PS
         meas_total = pz.SCHEME_SFB if t_sfb <= t_ps + t_wg else pz.SCHEME_PS
@@ -102,9 +109,11 @@ def main():
             print(json.dumps({"P": world, "M": M, "N": N, "K": K, "rule": name[rule],
                               "cost_sfb": costs[0], "cost_sf_ps": costs[1],
                               "sfb_ms": round(t_sfb, 4), "ps_ms": round(t_ps, 4), "wgrad_ms": round(t_wg, 4),
+                              "sfps_ms": round(t_sfps, 4),
+                              "winner_of_three": min((t_sfb, "SFB"), (t_ps + t_wg, "PS"), (t_sfps, "SFPS"))[1],
                               "winner_sync_only": name[meas_sync], "winner_with_wgrad": name[meas_total],
                               "rule_regret_ms": round(pick_t - best_t, 4)}), flush=True)
-        lid += 2
+        lid += 3
         del U, V
     ctx.close()
     if world > 1:
