@@ -412,7 +412,16 @@ poseidon_status_t sfps_update(poseidon_ctx_t c, Layer& L, float* W, float* bias,
   }
   CU_TRY(cudaEventRecord(dst.kend, c->recon_stream));
   CU_TRY(cudaStreamWaitEvent(c->comm_stream, dst.kend, 0));
-  if (P > 1) {
+  int64_t S0b, S0e, S0pad;
+  poseidon_shard_range(L.M, P, 0, &S0b, &S0e, &S0pad);
+  if (P > 1 && S0pad == L.M) {
+    // every master owns the same number of rows and W is exactly P row blocks: the row broadcast is an
+    // in-place all-gather (bandwidth-optimal, one collective)
+    const size_t cnt = (size_t)(L.re - L.rb) * (size_t)L.N;
+    NC_TRY(ncclAllGather(W + (size_t)L.rb * L.N, W, cnt, ncclFloat32, c->comm, c->comm_stream));
+    r.sent += (uint64_t)cnt * 4u;
+    r.recv += (uint64_t)cnt * 4u * (uint64_t)(P - 1);
+  } else if (P > 1) {
     NC_TRY(ncclGroupStart());
     for (int q = 0; q < P; ++q) {
       int64_t qb, qe, pad;
