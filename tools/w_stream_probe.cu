@@ -4,6 +4,7 @@
 // V1: 128B-swizzled boxes {32 cols, 128 rows} (K1's current epilogue pattern), coalesced STG write-back
 // V2: unswizzled boxes {256 cols, 16 rows} (1 KB contiguous row segments), coalesced STG write-back
 // V3: plain coalesced LDG/STG (no TMA, no smem)
+// V4: V1's boxes, result written back into the smem slot and stored with a TMA bulk tensor store
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -35,6 +36,12 @@ __device__ __forceinline__ void tma2d(const CUtensorMap* m, uint64_t* bar, void*
       : "memory");
 }
 
+__device__ __forceinline__ void tma2d_store(const CUtensorMap* m, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(m), "r"(su32(src)),
+               "r"(x), "r"(y)
+               : "memory");
+}
+
 constexpr int M = 4096, N = 9216, TM = 128, TN = 256;
 #ifndef SLOTS_
 #define SLOTS_ 8
@@ -63,7 +70,7 @@ __global__ void __launch_bounds__(160, 1) probe(const __grid_constant__ CUtensor
           const uint32_t slot = g % SLOTS, ph = (g / SLOTS) & 1;
           mbar_wait(&empty[slot], ph ^ 1);
           mbar_expect(&full[slot], CH);
-          if (V == 1) tma2d(&map, &full[slot], s + slot * CH, nt * TN + c * 32, mt * TM);
+          if (V == 1 || V == 4) tma2d(&map, &full[slot], s + slot * CH, nt * TN + c * 32, mt * TM);
           else tma2d(&map, &full[slot], s + slot * CH, nt * TN, mt * TM + c * 16);
         }
       }
@@ -78,7 +85,27 @@ __global__ void __launch_bounds__(160, 1) probe(const __grid_constant__ CUtensor
       const uint32_t slot = g % SLOTS, ph = (g / SLOTS) & 1;
       mbar_wait(&full[slot], ph);
       const uint8_t* base = s + slot * CH;
-      if (V == 1) {
+      if (V == 4) {
+        const int jj = t & 7;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rr = i * 16 + (t >> 3);
+          float4* pv = (float4*)(base + rr * 128 + ((jj ^ (rr & 7)) << 4));
+          float4 v = *pv;
+          v.x += 1e-3f; v.y += 1e-3f; v.z += 1e-3f; v.w += 1e-3f;
+          *pv = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (t == 0) {
+          tma2d_store(&map, base, nt * TN + c * 32, mt * TM);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          // allow 2 stores in flight: the store of chunk g-2 has finished reading its slot
+          asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+          if (g >= 2) mbar_arrive(&empty[(g - 2) % SLOTS]);
+        }
+        continue;
+      } else if (V == 1) {
         const int jj = t & 7;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -101,6 +128,7 @@ __global__ void __launch_bounds__(160, 1) probe(const __grid_constant__ CUtensor
       if (t == 0) mbar_arrive(&empty[slot]);
     }
   }
+  if (V == 4 && t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 __global__ void v3(float4* W, size_t n4) {
@@ -134,16 +162,18 @@ int main() {
   const int smem = SLOTS * CH + 2048;
   cudaFuncSetAttribute(probe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(probe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(probe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const double bytes = 8.0 * M * N;
-  for (int v = 1; v <= 3; ++v) {
+  for (int v = 1; v <= 4; ++v) {
     float best = 1e9;
     for (int it = 0; it < 6; ++it) {
       cudaEventRecord(a);
       if (v == 1) probe<1><<<148, 160, smem>>>(m1, W);
       else if (v == 2) probe<2><<<148, 160, smem>>>(m2, W);
+      else if (v == 4) probe<4><<<148, 160, smem>>>(m1, W);
       else v3<<<(M * N / 4 + 1023) / 1024, 256>>>((float4*)W, (size_t)M * N / 4);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
