@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -167,13 +168,14 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const double bytes = 8.0 * M * N;
+  const int grid = getenv("GRID") ? atoi(getenv("GRID")) : 148;
   for (int v = 1; v <= 4; ++v) {
     float best = 1e9;
     for (int it = 0; it < 6; ++it) {
       cudaEventRecord(a);
-      if (v == 1) probe<1><<<148, 160, smem>>>(m1, W);
-      else if (v == 2) probe<2><<<148, 160, smem>>>(m2, W);
-      else if (v == 4) probe<4><<<148, 160, smem>>>(m1, W);
+      if (v == 1) probe<1><<<grid, 160, smem>>>(m1, W);
+      else if (v == 2) probe<2><<<grid, 160, smem>>>(m2, W);
+      else if (v == 4) probe<4><<<grid, 160, smem>>>(m1, W);
       else v3<<<(M * N / 4 + 1023) / 1024, 256>>>((float4*)W, (size_t)M * N / 4);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
