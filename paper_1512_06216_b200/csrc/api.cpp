@@ -765,7 +765,11 @@ poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, 
   if (world > 1) {
     ncclUniqueId id;
     memcpy(id.internal, topo->nccl_id, 128);
-    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, topo->rank);
+    // POSEIDON_NCCL_CTA_POLICY (experiment knob): NCCL_CTA_POLICY_EFFICIENCY (1) / _ZERO (2; copy-engine
+    // collectives on symmetric windows where NCCL supports them)
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    if (const char* pol = getenv("POSEIDON_NCCL_CTA_POLICY")) cfg.CTAPolicy = atoi(pol);
+    ncclResult_t r = ncclCommInitRankConfig(&c->comm, world, id, topo->rank, &cfg);
     if (r != ncclSuccess) {
       delete c;
       return fail(POSEIDON_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));

@@ -1,6 +1,6 @@
 """Collective bus bandwidth on NVLink 5 (nccl-tests conventions: busbw = algbw * (P-1)/P).
 
-    torchrun --nproc-per-node P tools/collective_bench.py [--ps-only]
+    torchrun --nproc-per-node P tools/collective_bench.py [--ps-only | --sfb-only]
 
 (a) raw NCCL all-gather / reduce-scatter through torch.distributed (the same libnccl.so.2 the
     library links), message sizes per rank 1 MB .. 512 MB;
@@ -48,7 +48,8 @@ def main():
             print(json.dumps(d), flush=True)
 
     only_ps = "--ps-only" in sys.argv
-    for mb in (() if only_ps else (1, 4, 16, 64, 256, 512)):
+    only_sfb = "--sfb-only" in sys.argv
+    for mb in (() if (only_ps or only_sfb) else (1, 4, 16, 64, 256, 512)):
         n = mb * (1 << 20) // 4
         x = torch.randn(n, device=dev)
         y = torch.empty(n * P, device=dev)
@@ -95,6 +96,7 @@ def main():
             per_rank = K * (M + N + M // K + 1) * 4  # U + V slot (+ bias column sums) per rank
             alg = per_rank * P / (t / 1e3) / 1e9
             out({"what": f"poseidon SFB all-gather ({name}, K=256, {tag})", "P": P, "path": ctx.sfb_path(lid),
+                 "cta_policy": os.environ.get("POSEIDON_NCCL_CTA_POLICY", "default"),
                  "MB_per_rank": round(per_rank / 2**20, 2), "ms": round(t, 4),
                  "busbw_GBps": round(alg * (P - 1) / P, 1)})
         ctx.close()
@@ -102,7 +104,7 @@ def main():
     # (b2) PS of a 37.7M-parameter layer: NCCL path vs fused NVLS kernel
     M, N = 4096, 9216
     n = M * N
-    for nv in ((True,) if only_ps else (False, True)):
+    for nv in (() if only_sfb else (True,) if only_ps else (False, True)):
         c = new_ctx(pz.FLAG_NVLS_PS if nv else 0)
         c.register_layer(0, pz.LAYER_FC, M, N, 256, False, pz.SCHEME_PS)
         if nv:
