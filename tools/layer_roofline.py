@@ -7,7 +7,8 @@ DWBP glue makes), `reps` times with a barrier before each, and the library's dev
 `start_to_done` (collectives + update kernels) is taken: median over reps, max over ranks.
 A ~100 us device spin precedes every timed sync so that all of its launches are queued before it runs.
 Also measured: alpha (8-byte NCCL all-gather) and the NCCL all-gather busbw at 256 MB per rank.
-PS layers run both on the NCCL path and (P > 1) on the fused NVLS kernel.
+PS layers run both on the NCCL path and (P > 1) on the fused NVLS kernel; at P > 1 every FC layer is
+also synced as SF-PS (the literal else-branch of Alg. 3, reading Z20; scheme_override = SFPS).
 Prints JSON lines (rank 0); tools/layer_roofline_md.py applies the §8(d) roofline formulas.
 """
 import argparse
@@ -24,6 +25,7 @@ import paper_1512_06216_b200 as pz  # noqa: E402
 from drivers.cnn import CONFIGS  # noqa: E402
 
 BW_NVL_SPEC = 900e9
+SFPS_ID = 2000   # layer ids of the SF-PS registrations of the FC layers
 SLEEP_CYCLES = 200_000
 
 
@@ -112,6 +114,8 @@ def main():
             if nv is not None and sch == pz.SCHEME_PS:
                 nv.register_layer(lid, kind, M, N, K, hb, pz.SCHEME_PS)
             plan.append((name, lid, kind, M, N, K, sch, n, hb))
+            if P > 1 and kind == pz.LAYER_FC:
+                ctx.register_layer(SFPS_ID + lid, kind, M, N, K, hb, pz.SCHEME_SFPS)
             lid += 1
     nvls_active = nv.ps_arena() if nv is not None else False
     out({"P": P, "nvls": nv.nvls_status() if nv is not None else "P=1", "layers": len(plan)})
@@ -149,6 +153,13 @@ def main():
             if nvls_active:
                 rows["ps_nvls"] = measure(nv, l, lambda: nv.backprop_hook(l, s))
             del g, w
+        if P > 1 and kind == pz.LAYER_FC:
+            U = torch.randn(K, M, device=dev) / K
+            V = torch.randn(K, N, device=dev).relu()
+            W = torch.zeros(M, N, device=dev)
+            b = torch.zeros(M, device=dev) if hb else None
+            rows["sfps"] = measure(ctx, SFPS_ID + l, lambda: ctx.sync_fc_sfb(SFPS_ID + l, U, V, W, b, 1e-3, s))
+            del U, V, W, b
         for path, t in rows.items():
             out({"P": P, "layer": name, "M": M, "N": N, "K": K, "n": n, "scheme": path,
                  "measured_us": round(t * 1e6, 2)})

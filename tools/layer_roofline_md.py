@@ -5,8 +5,11 @@
 Two bounds per layer:
   bandwidth roof  SFB: (P-1)K(M+N)4/BW_nvl + max(2MNPK/TC, (8MN + 4PK(M+N) + 8M)/BW_hbm)
                   PS:  2(P-1)/P 4n/BW_nvl + 12n/P/BW_hbm
+                  SF-PS (R = ceil(M/P) rows per master): ((P-1)K(N+R) + (M-R)N)4/BW_nvl
+                       + max(2RNPK/TC, (8RN + 4PK(R+N))/BW_hbm)
   effective roof  each term raised to its latency floor: a collective costs at least alpha (SFB: one
-                  all-gather; PS: reduce-scatter + all-gather = 2 alpha), a kernel at least T_LAUNCH.
+                  all-gather; PS: reduce-scatter + all-gather = 2 alpha; SF-PS: factor exchange + row push =
+                  3 alpha), a kernel at least T_LAUNCH.
 alpha = the 8-byte NCCL all-gather measured in the same run; T_LAUNCH = 2 us.
 """
 import json
@@ -17,7 +20,12 @@ TC_TF32, BW_HBM, BW_NVL, T_LAUNCH = 794e12, 6543.7e9, 900e9, 2e-6
 
 def bounds(d, P, alpha):
     M, N, K, n = d["M"], d["N"], d["K"], d["n"]
-    if d["scheme"] == "sfb":
+    if d["scheme"] == "sfps":
+        R = -(-M // P)
+        comm = ((P - 1) * K * (N + R) + (M - R) * N) * 4 / BW_NVL
+        kern = max(2.0 * R * N * P * K / TC_TF32, (8.0 * R * N + 4.0 * P * K * (R + N)) / BW_HBM)
+        comm_eff = max(comm, 3 * alpha)
+    elif d["scheme"] == "sfb":
         comm = (P - 1) * K * (M + N) * 4 / BW_NVL
         kern = max(2.0 * M * N * P * K / TC_TF32, (8.0 * M * N + 4.0 * P * K * (M + N) + 8.0 * M) / BW_HBM)
         comm_eff = max(comm, alpha) if P > 1 else 0.0
@@ -37,7 +45,8 @@ def main():
              "roofline (NVLink 5 900 GB/s, TF32 794 TFLOP/s, HBM 6543.7 GB/s).  `eff roof`: the same with every",
              "collective raised to the measured 8-byte NCCL latency alpha (PS: 2 alpha) and every kernel to 2 us.",
              "ps_nccl = NCCL reduce-scatter + K2 + all-gather; ps_nvls = the fused multimem kernel; sfb = NCCL",
-             "all-gather of the factors + K1.", ""]
+             "all-gather of the factors + K1; sfps = the literal else-branch of Alg. 3 (reading Z20): U rows to",
+             "their masters, V all-gathered, K1 on the master's rows, rows pushed back.", ""]
     for f in files:
         L = [json.loads(l) for l in open(f) if l.startswith("{")]
         head = [d for d in L if "alpha_us" in d][0]
