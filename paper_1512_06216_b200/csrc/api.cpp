@@ -251,10 +251,15 @@ int next_set(poseidon_ctx_t c, const Layer& L) { return c->ssp ? (int)(L.nsync &
 poseidon_status_t sfb_comm(poseidon_ctx_t c, Layer& L, int set, EvSet& e, cudaEvent_t wait_ev, IterRecord& r) {
   const int P = c->world;
   const GatherSet g = gather_set(L, set);
+  if (P <= 1) {   // nothing to gather: the sync starts on the reconstruction stream (one stream hop less)
+    CU_TRY(cudaStreamWaitEvent(c->recon_stream, wait_ev, 0));
+    CU_TRY(cudaEventRecord(e.start, c->recon_stream));
+    e.g_eff = e.start;
+    return POSEIDON_OK;
+  }
   CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
   e.g_eff = e.start;
-  if (P <= 1) return POSEIDON_OK;
   const size_t ucount = (size_t)(L.M * L.ldk), vcount = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
   const uint64_t per = (uint64_t)(ucount + vcount + bcount) * 4u;
   if (L.bcast) {
@@ -291,8 +296,14 @@ poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, floa
   const GatherSet g = gather_set(L, set);
   CU_TRY(cudaStreamWaitEvent(c->recon_stream, src_g, 0));
   if (extra) CU_TRY(cudaStreamWaitEvent(c->recon_stream, extra, 0));
-  CU_TRY(cudaEventRecord(dst.kstart, c->recon_stream));
-  dst.ks_eff = dst.kstart;
+  // an event record costs ~1 us of stream time: record only the events whose times differ (BSP at P = 1
+  // the sync's start was just recorded on this stream; with nothing after K1, its end is `done`)
+  if (P <= 1 && src_g == dst.start && !extra) {
+    dst.ks_eff = dst.start;
+  } else {
+    CU_TRY(cudaEventRecord(dst.kstart, c->recon_stream));
+    dst.ks_eff = dst.kstart;
+  }
   dst.ke_eff = dst.kend;
   const float alpha = -lr / (float)P;
   cudaError_t err;
@@ -301,8 +312,10 @@ poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, floa
   // v_partial = fmaf(lr/P, acc, mu * v), then momentum_apply: v += lr*wd*w, w -= v.
   float* target = mom ? L.vel : W;
   const float a1 = mom ? (lr / (float)P) : alpha, b1 = mom ? L.mu : 1.0f;
+  bool bias_done = false;   // plain SGD: K1 updates the bias with otherwise idle lanes (no extra launch)
   if (L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(g.U, g.V, L.ldk, L.M, L.N, target))
-    err = launch_recon_tcgen05(g.U, g.V, P, L.K, L.ldk, L.M, L.N, target, a1, b1, c->recon_stream);
+    err = launch_recon_tcgen05(g.U, g.V, P, L.K, L.ldk, L.M, L.N, target, a1, b1, c->recon_stream, nullptr, 0,
+                               mom ? nullptr : g.B, mom ? nullptr : bias, &bias_done);
   else
     err = launch_recon_simt(g.U, g.V, P, L.K, L.ldk, L.M, L.N, target, a1, b1, c->recon_stream);
   if (err != cudaSuccess) return cuda_fail(err, "reconstruct+sgd launch");
@@ -311,8 +324,11 @@ poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, floa
     if (err != cudaSuccess) return cuda_fail(err, "momentum apply launch");
   }
   if ((err = debug_sync(c->recon_stream, "K1/K1r reconstruct+sgd")) != cudaSuccess) return cuda_fail(err, "K1");
-  CU_TRY(cudaEventRecord(dst.kend, c->recon_stream));  // kernel_ms = K1/K1r alone
-  if (bias) {
+  if (bias && !bias_done)
+    CU_TRY(cudaEventRecord(dst.kend, c->recon_stream));  // kernel_ms = K1/K1r alone
+  else
+    dst.ke_eff = dst.done;
+  if (bias && !bias_done) {
     err = mom ? launch_bias_momentum(g.B, L.M, P, bias, L.vel_b, L.M, lr, L.mu, L.wd, c->recon_stream)
               : launch_bias_update(g.B, L.M, P, bias, L.M, alpha, c->recon_stream);
     if (err != cudaSuccess) return cuda_fail(err, "bias update launch");

@@ -62,7 +62,10 @@ cudaError_t launch_recon_simt(const float* Ug, const float* Vg, int32_t P, int64
 // Both compute W' = fmaf(alpha, acc, beta * W) (beta = 1: SGD; beta = mu: velocity update, f4).
 cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
                                  int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg = nullptr,
-                                 int64_t ldm = 0);
+                                 int64_t ldm = 0, const float* bs = nullptr, float* bias = nullptr,
+                                 bool* bias_done = nullptr);
+// (bs, bias, bias_done): optional plain-SGD bias update fused into K1 (bias[m] = fmaf(alpha, sum_p bs[p*M+m],
+// bias[m]), bs [P][M] with M the block's row count); *bias_done tells whether the kernel took it.
 bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int64_t M, int64_t N, const float* W);
 
 }  // namespace poseidon

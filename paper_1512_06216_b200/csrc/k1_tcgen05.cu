@@ -229,6 +229,11 @@ struct Params {
   float alpha;
   float beta;   // W' = fmaf(alpha, acc, beta * W): 1 for SGD; mu when the target is a velocity (f4)
   float* dbg;  // debug dump (tile 0 of CTA 0): smem stage 0 of A|B, raw accumulator; NULL in production
+  // fused bias update of the 2-SM kernel (plain SGD): bias[m] = fmaf(alpha, sum_p bs[p*M + m], bias[m]) for
+  // m < M, done by the idle lanes of the W-producer warp; NULL when the host runs the separate kernel
+  const float* bs;
+  float* bias;
+  int32_t nP;
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& mt, int& nt) {
@@ -604,6 +609,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     }
   } else if (warp == 2) {
     // ===================== W tile TMA producer (both CTAs, own rows) =====================
+    if (lane > 0 && p.bias != nullptr) {
+      // the bias update (Z9: per-worker column sums of U, already gathered) on lanes 1..31 of every CTA
+      for (int m = (int)blockIdx.x * 31 + (lane - 1); m < p.M; m += (int)gridDim.x * 31) {
+        float sum = 0.f;
+        for (int w = 0; w < p.nP; ++w) sum += p.bs[(size_t)w * p.M + m];
+        p.bias[m] = fmaf(p.alpha, sum, p.bias[m]);
+      }
+    }
     if (lane == 0 && p.mode != 7) {
       const uint64_t pol = p.w_policy ? policy_evict_normal() : policy_evict_first();
       uint32_t g = 0;
@@ -736,8 +749,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
 //   POSEIDON_K1_MODE=1|2|3  W streaming only / no update / loads only (no MMA in modes 1-3)
 //   POSEIDON_K1_MODE=5|6    TMEM loads without MMA / MMA + accumulator handshake without TMEM loads
 //   POSEIDON_K1_MODE=7      operands + MMA + TMEM loads, no W traffic
+//   POSEIDON_K1_FUSE_BIAS=0 bias update as a separate kernel after K1 (A/B of the fused update)
 struct K1Knobs {
-  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0;
+  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0, fbias = 1;
   K1Knobs() {
     if (const char* v = getenv("POSEIDON_K1_VARIANT")) variant = (v[0] == '1') ? 1 : 2;
     if (const char* r = getenv("POSEIDON_K1_RASTER")) raster = (r[0] == 'm') ? 1 : 0;
@@ -745,6 +759,7 @@ struct K1Knobs {
     if (const char* e = getenv("POSEIDON_K1_EPI")) epi = (e[0] == '1') ? 1 : 2;
     if (const char* w = getenv("POSEIDON_K1_WPOL")) wpol = w[0] - '0';
     if (const char* m = getenv("POSEIDON_K1_MODE")) mode = m[0] - '0';
+    if (const char* f = getenv("POSEIDON_K1_FUSE_BIAS")) fbias = f[0] - '0';
   }
 };
 const K1Knobs& knobs() {
@@ -837,7 +852,8 @@ bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int6
 
 cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
                                  int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg,
-                                 int64_t ldm) {
+                                 int64_t ldm, const float* bs, float* bias, bool* bias_done) {
+  if (bias_done) *bias_done = false;
   if (M <= 0 || N <= 0 || K <= 0 || P <= 0) return cudaSuccess;
   if (ldm <= 0) ldm = M;
   if (ldm < M) return cudaErrorInvalidValue;
@@ -880,6 +896,9 @@ have_maps:
   p.beta = beta;
   p.dbg = dbg;
   p.W = W;
+  p.bs = nullptr;
+  p.bias = nullptr;
+  p.nP = P;
   // Raster (measured, tools/k1_sweep.sh): when both factor buffers fit comfortably in L2 the waves
   // walk N so each wave's W tiles are whole row segments; otherwise consecutive tiles walk the
   // dimension whose operand is smaller, so the operand re-swept every wave stays L2-resident.
@@ -894,6 +913,11 @@ have_maps:
   p.mode = knobs().mode;
   if (variant == 2 && dbg == nullptr) {
     tmB = tmB2;
+    if (knobs().fbias && bias != nullptr && bs != nullptr && bias_done != nullptr && M < (1 << 30)) {
+      p.bs = bs;
+      p.bias = bias;
+      *bias_done = true;
+    }
     p.m_tiles = (int32_t)((M + k2sm::BM - 1) / k2sm::BM);
     p.n_tiles = (int32_t)((N + k2sm::BN - 1) / k2sm::BN);
     p.num_tiles = p.m_tiles * p.n_tiles;
