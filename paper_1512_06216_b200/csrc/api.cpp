@@ -230,6 +230,27 @@ bool ensure_devcomm(poseidon_ctx_t c) {
   return c->nvls != nullptr;
 }
 
+// Ordering fuzz (SURVEY §5 "ordering-fuzz mode"; test aid, off unless POSEIDON_FUZZ_US is set): after the
+// dependencies of each collective leg and each update kernel are in place, a pseudo-random sleep of up to
+// POSEIDON_FUZZ_US microseconds on the stream about to run it.  Results must not change
+// (tests/test_gpu_dwbp.py): only timing moves.
+poseidon_status_t fuzz(cudaStream_t s) {
+  static const uint32_t max_ns = [] {
+    const char* v = getenv("POSEIDON_FUZZ_US");
+    return v ? (uint32_t)(atof(v) * 1000.0) : 0u;
+  }();
+  if (max_ns == 0) return POSEIDON_OK;
+  static uint64_t state = 0x9E3779B97F4A7C15ull;
+  state = state * 6364136223846793005ull + 1442695040888963407ull;
+  CU_TRY(launch_fuzz_sleep((uint32_t)((state >> 33) % max_ns), s));
+  return POSEIDON_OK;
+}
+#define FZ(stream)                          \
+  do {                                      \
+    poseidon_status_t fz_ = fuzz(stream);   \
+    if (fz_) return fz_;                    \
+  } while (0)
+
 // Producer-side prologue shared by both schemes: the previous sync of this
 // layer must be finished before its buffers are rewritten.
 poseidon_status_t producer_guard(poseidon_ctx_t c, Layer& L, cudaStream_t producer) {
@@ -253,11 +274,13 @@ poseidon_status_t sfb_comm(poseidon_ctx_t c, Layer& L, int set, EvSet& e, cudaEv
   const GatherSet g = gather_set(L, set);
   if (P <= 1) {   // nothing to gather: the sync starts on the reconstruction stream (one stream hop less)
     CU_TRY(cudaStreamWaitEvent(c->recon_stream, wait_ev, 0));
+    FZ(c->recon_stream);
     CU_TRY(cudaEventRecord(e.start, c->recon_stream));
     e.g_eff = e.start;
     return POSEIDON_OK;
   }
   CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
+  FZ(c->comm_stream);
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
   e.g_eff = e.start;
   const size_t ucount = (size_t)(L.M * L.ldk), vcount = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
@@ -296,6 +319,7 @@ poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, floa
   const GatherSet g = gather_set(L, set);
   CU_TRY(cudaStreamWaitEvent(c->recon_stream, src_g, 0));
   if (extra) CU_TRY(cudaStreamWaitEvent(c->recon_stream, extra, 0));
+  FZ(c->recon_stream);
   // an event record costs ~1 us of stream time: record only the events whose times differ (BSP at P = 1
   // the sync's start was just recorded on this stream; with nothing after K1, its end is `done`)
   if (P <= 1 && src_g == dst.start && !extra) {
@@ -360,6 +384,7 @@ poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float*
 poseidon_status_t sfps_comm(poseidon_ctx_t c, Layer& L, EvSet& e, cudaEvent_t wait_ev, IterRecord& r) {
   const int P = c->world;
   CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
+  FZ(c->comm_stream);
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
   e.g_eff = e.start;
   if (P <= 1) return POSEIDON_OK;
@@ -403,6 +428,7 @@ poseidon_status_t sfps_update(poseidon_ctx_t c, Layer& L, float* W, float* bias,
                               EvSet& dst, IterRecord& r) {
   const int P = c->world;
   CU_TRY(cudaStreamWaitEvent(c->recon_stream, src_g, 0));
+  FZ(c->recon_stream);
   CU_TRY(cudaEventRecord(dst.kstart, c->recon_stream));
   dst.ks_eff = dst.kstart;
   dst.ke_eff = dst.kend;
@@ -428,6 +454,7 @@ poseidon_status_t sfps_update(poseidon_ctx_t c, Layer& L, float* W, float* bias,
   }
   CU_TRY(cudaEventRecord(dst.kend, c->recon_stream));
   CU_TRY(cudaStreamWaitEvent(c->comm_stream, dst.kend, 0));
+  FZ(c->comm_stream);
   int64_t S0b, S0e, S0pad;
   poseidon_shard_range(L.M, P, 0, &S0b, &S0e, &S0pad);
   if (P > 1 && S0pad == L.M) {
@@ -482,6 +509,7 @@ bool ps_fused(poseidon_ctx_t c, const Layer& L) { return c->world > 1 && c->ps_n
 poseidon_status_t ps_comm(poseidon_ctx_t c, Layer& L, float* grad, EvSet& e, cudaEvent_t wait_ev, IterRecord& r) {
   const int P = c->world;
   CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
+  FZ(c->comm_stream);
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
   e.g_eff = e.ks_eff = e.start;
   if (ps_fused(c, L) || P <= 1) return POSEIDON_OK;
@@ -569,6 +597,7 @@ poseidon_status_t ps_comm_allreduce(poseidon_ctx_t c, Layer& L, float* grad, EvS
                                     IterRecord& r) {
   const int P = c->world;
   CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
+  FZ(c->comm_stream);
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
   e.g_eff = e.start;
   if (P <= 1) return POSEIDON_OK;
@@ -589,6 +618,7 @@ poseidon_status_t ps_update_local(poseidon_ctx_t c, Layer& L, float* grad, float
   const int P = c->world;
   CU_TRY(cudaStreamWaitEvent(c->recon_stream, src_g, 0));
   if (extra) CU_TRY(cudaStreamWaitEvent(c->recon_stream, extra, 0));
+  FZ(c->recon_stream);
   CU_TRY(cudaEventRecord(dst.kstart, c->recon_stream));
   dst.ks_eff = dst.kstart;
   dst.ke_eff = dst.done;

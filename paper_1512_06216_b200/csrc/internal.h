@@ -51,6 +51,9 @@ cudaError_t launch_bias_momentum(const float* bs, int64_t ld, int32_t P, float* 
 cudaError_t launch_bias_update(const float* bs, int64_t ld, int32_t P, float* bias, int64_t M, float alpha,
                                cudaStream_t s);
 
+// Ordering fuzz (test aid, POSEIDON_FUZZ_US): a single-thread kernel that sleeps `ns` on stream s.
+cudaError_t launch_fuzz_sleep(uint32_t ns, cudaStream_t s);
+
 // K1r: W[M x N] += alpha * sum_p sum_k Ug[p][m][k] Vg[p][n][k] on CUDA cores (fp32 FMA).
 // ldm (0 = M): rows per worker block of Ug, so Ug may point at row m0 of a larger gather buffer and
 // M be the number of rows of the block (SF-PS reconstructs only its master's rows).

@@ -176,7 +176,22 @@ int grid_for(int64_t work_items, int threads) {
   return (int)(blocks < 1 ? 1 : (blocks < cap ? blocks : cap));
 }
 
+// Ordering fuzz (POSEIDON_FUZZ_US, test aid): one thread spins for `ns` nanoseconds.
+__global__ void fuzz_sleep_kernel(uint32_t ns) {
+  uint32_t left = ns;
+  while (left > 0) {
+    const uint32_t step = left > 1000u ? 1000u : left;
+    __nanosleep(step);
+    left -= step;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_fuzz_sleep(uint32_t ns, cudaStream_t s) {
+  fuzz_sleep_kernel<<<1, 1, 0, s>>>(ns);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_ps_shard_update(const float* g, float* W, int64_t count, float alpha, float* stats,
                                    cudaStream_t s) {
