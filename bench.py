@@ -47,7 +47,8 @@ def parse():
                     help="fused one-kernel NVLink-SHARP PS sync (f1); auto = on when N > 1")
     ap.add_argument("--sfb-wire", default="auto", choices=["auto", "nccl", "symm", "nvls"],
                     help="SFB factor broadcast: NCCL all-gather on plain buffers, on NCCL symmetric windows, "
-                         "or the library's NVLS multicast kernel; auto = symm when N > 1")
+                         "or the library's broadcast kernel on symmetric windows (peer stores over NVLink; "
+                         "POSEIDON_SFB_BCAST=mc for the multicast variant); auto = nvls when N > 1")
     ap.add_argument("--ssp", type=int, default=0, choices=[0, 1],
                     help="staleness s of the SSP consistency model (P:L399-402, E11); 0 = BSP (the paper's "
                          "headline setting)")
@@ -276,7 +277,9 @@ def run_poseidon(args):
     use_nvls = world > 1 and args.nvls != "off"
     if use_nvls:
         flags |= pz.FLAG_NVLS_PS
-    sfb_wire = ("symm" if args.sfb_wire == "auto" else args.sfb_wire) if world > 1 else "none (P=1)"
+    # auto at N > 1: the library's own factor broadcast (peer stores over NVLink, 32 CTAs; profiles/
+    # collectives_r1.md: faster than NCCL's symmetric all-gather alone and equal or better in the step)
+    sfb_wire = ("nvls" if args.sfb_wire == "auto" else args.sfb_wire) if world > 1 else "none (P=1)"
     flags |= {"symm": pz.FLAG_SYMM_SFB, "nvls": pz.FLAG_NVLS_SFB}.get(sfb_wire, 0)
     if args.ssp:
         flags |= pz.FLAG_SSP1

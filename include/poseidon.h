@@ -88,9 +88,11 @@ typedef struct {
 #define POSEIDON_FLAG_SYMM_SFB 0x8u    /* SFB gather buffers in NCCL symmetric windows (NCCL's symmetric-memory
                                          all-gather kernels); registration is collective, so every rank must
                                          register the same layers in the same order */
-#define POSEIDON_FLAG_NVLS_SFB 0x10u   /* SFB factor "broadcast" as one NVLink-SHARP multicast store per
-                                         rank into symmetric gather buffers, instead of an NCCL all-gather
-                                         (implies POSEIDON_FLAG_SYMM_SFB) */
+#define POSEIDON_FLAG_NVLS_SFB 0x10u   /* SFB factor "broadcast" by the library's own kernel on symmetric
+                                         gather buffers instead of an NCCL all-gather (implies
+                                         POSEIDON_FLAG_SYMM_SFB): LSA barrier, this rank's slots stored into
+                                         every peer's buffers over NVLink (default) or as one NVLink-SHARP
+                                         multicast store (env POSEIDON_SFB_BCAST=mc), LSA barrier */
 #define POSEIDON_FLAG_SSP1 0x20u       /* stale synchronous parallel with staleness s = 1 (
                                          reading Z19): the update of a layer's sync t is applied at the
                                          layer's hook of iteration t+1, after that backward has read W, so
@@ -257,8 +259,8 @@ poseidon_status_t poseidon_set_ps_buckets(poseidon_ctx_t ctx, int64_t bucket_byt
 poseidon_status_t poseidon_ps_layer_buffers(poseidon_ctx_t ctx, int32_t layer_id, float** grad, float** W,
                                             int64_t* padded_n);
 /* How SFB layer `layer_id` moves its factors at world > 1: 0 = NCCL all-gather on plain device
- * buffers, 1 = NCCL all-gather on symmetric-window buffers (FLAG_SYMM_SFB), 2 = NVLS multicast
- * broadcast (FLAG_NVLS_SFB), 3 = SF-PS layer (NCCL send/recv of U row blocks, all-gather of V, broadcast of
+ * buffers, 1 = NCCL all-gather on symmetric-window buffers (FLAG_SYMM_SFB), 2 = the library's
+ * broadcast kernel (FLAG_NVLS_SFB), 3 = SF-PS layer (NCCL send/recv of U row blocks, all-gather of V, broadcast of
  * the masters' W rows).  Negative status for a bad id or a PS layer. */
 int32_t poseidon_sfb_path(poseidon_ctx_t ctx, int32_t layer_id);
 /* Human-readable state of the fused NVLS PS path ("active", "not requested", or the NCCL error). */

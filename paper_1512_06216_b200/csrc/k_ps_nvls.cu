@@ -123,7 +123,9 @@ struct BcastSeg {
 // own factor slots once into the multicast address and the switch writes them into every rank's
 // gather buffers.  Barrier first (every rank has packed its slots and finished reading the previous
 // iteration's gather buffers), barrier last (every rank's stores have landed before K1 reads them).
-template <int U>
+// P2P = false: one multimem.st per 16 B (the switch replicates it to every rank);
+// P2P = true: plain st.global of the same 16 B into each peer's window copy over NVLink (P-1 stores)
+template <int U, bool P2P>
 __global__ void __launch_bounds__(256) sfb_bcast_kernel(const __grid_constant__ ncclDevComm comm, ncclWindow_t win,
                                                         BcastSeg s0, BcastSeg s1, BcastSeg s2) {
   ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamTagLsa(), blockIdx.x, /*multimem=*/true);
@@ -136,26 +138,55 @@ __global__ void __launch_bounds__(256) sfb_bcast_kernel(const __grid_constant__ 
     // slots of odd length (the bias sums, M floats) start off 16-B alignment on ranks > 0: scalar head
     const int64_t head = sg.n < ((4 - ((int64_t)(sg.off >> 2) & 3)) & 3) ? sg.n : ((4 - ((int64_t)(sg.off >> 2) & 3)) & 3);
     const float* src0 = static_cast<const float*>(ncclGetLocalPointer(win, sg.off));
-    float* dst0 = static_cast<float*>(ncclGetLsaMultimemPointer(win, sg.off, comm));
-    if (blockIdx.x == 0 && threadIdx.x < head) mm_st(dst0 + threadIdx.x, src0[threadIdx.x]);
-    const float* src = src0 + head;
-    float* dst = dst0 + head;
     const int64_t nb = sg.n - head;
     const int64_t n4 = nb >> 2;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
-      float4 v[U];
+    const float* src = src0 + head;
+    if (!P2P) {
+      float* dst0 = static_cast<float*>(ncclGetLsaMultimemPointer(win, sg.off, comm));
+      if (blockIdx.x == 0 && threadIdx.x < head) mm_st(dst0 + threadIdx.x, src0[threadIdx.x]);
+      float* dst = dst0 + head;
+      for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+        float4 v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t i = i0 + u * stride;
-        if (i < n4) v[u] = *reinterpret_cast<const float4*>(src + 4 * i);
+        for (int u = 0; u < U; ++u) {
+          const int64_t i = i0 + u * stride;
+          if (i < n4) v[u] = *reinterpret_cast<const float4*>(src + 4 * i);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t i = i0 + u * stride;
+          if (i < n4) mm_st_v4(dst + 4 * i, v[u]);
+        }
       }
+      if (blockIdx.x == 0 && threadIdx.x < (nb & 3)) mm_st(dst + 4 * n4 + threadIdx.x, src[4 * n4 + threadIdx.x]);
+    } else {
+      const ncclTeam lsa = ncclTeamLsa(comm);
+      for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+        float4 v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t i = i0 + u * stride;
-        if (i < n4) mm_st_v4(dst + 4 * i, v[u]);
+        for (int u = 0; u < U; ++u) {
+          const int64_t i = i0 + u * stride;
+          if (i < n4) v[u] = *reinterpret_cast<const float4*>(src + 4 * i);
+        }
+        for (int d = 1; d < lsa.nRanks; ++d) {
+          const int q = (lsa.rank + d) % lsa.nRanks;   // each rank starts with a different peer
+          float* dst = static_cast<float*>(ncclGetLsaPointer(win, sg.off, q)) + head;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * stride;
+            if (i < n4) *reinterpret_cast<float4*>(dst + 4 * i) = v[u];
+          }
+        }
+      }
+      if (blockIdx.x == 0 && (threadIdx.x < head || threadIdx.x < (nb & 3))) {
+        for (int d = 1; d < lsa.nRanks; ++d) {
+          const int q = (lsa.rank + d) % lsa.nRanks;
+          float* dst0 = static_cast<float*>(ncclGetLsaPointer(win, sg.off, q));
+          if (threadIdx.x < head) dst0[threadIdx.x] = src0[threadIdx.x];
+          if (threadIdx.x < (nb & 3)) dst0[head + 4 * n4 + threadIdx.x] = src[4 * n4 + threadIdx.x];
+        }
       }
     }
-    if (blockIdx.x == 0 && threadIdx.x < (nb & 3)) mm_st(dst + 4 * n4 + threadIdx.x, src[4 * n4 + threadIdx.x]);
   }
   bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
 }
@@ -202,13 +233,33 @@ cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww
 
 cudaError_t launch_sfb_bcast_nvls(const NvlsState* st, ncclWindow_t win, size_t off_u, int64_t n_u, size_t off_v,
                                   int64_t n_v, size_t off_b, int64_t n_b, int max_blocks, cudaStream_t s) {
+  // default: per-peer NVLink stores (measured faster than one multicast store for 8-25 MB slots,
+  // profiles/collectives_r1.md); POSEIDON_SFB_BCAST=mc selects the multicast variant
+  static const bool p2p = [] {
+    const char* v = getenv("POSEIDON_SFB_BCAST");
+    return !(v != nullptr && v[0] == 'm');
+  }();
   // identical grid on every rank (the slot sizes are the same everywhere)
   const int64_t n4 = (n_u + n_v + n_b) / 4;
   int blocks = (int)((n4 + 1023) / 1024);
   if (blocks < 1) blocks = 1;
+  static const int env_grid = [] {   // experiment knob: cap the broadcast's CTAs (SM share vs bandwidth)
+    const char* v = getenv("POSEIDON_SFB_BCAST_GRID");
+    return v ? atoi(v) : 0;
+  }();
+  // Default cap (tools/collective_bench.py + bench.py sweeps, profiles/collectives_r1.md): 32 CTAs move the
+  // slots as fast as 128 at P = 2 and 4 and leave the SMs to the backward that DWBP overlaps them with (128
+  // CTAs cost ~1% images/s in the step); with more peers to feed, 64 (P > 4; not measured: 4-GPU pool).
+  const int nranks = ncclTeamLsa(st->dev).nRanks;
+  int cap = env_grid > 0 ? env_grid : (p2p ? (nranks > 4 ? 64 : 32) : max_blocks);
+  if (cap < max_blocks) max_blocks = cap;
   if (blocks > max_blocks) blocks = max_blocks;
-  sfb_bcast_kernel<4><<<blocks, 256, 0, s>>>(st->dev, win, BcastSeg{off_u, n_u}, BcastSeg{off_v, n_v},
-                                            BcastSeg{off_b, n_b});
+  if (p2p)
+    sfb_bcast_kernel<4, true><<<blocks, 256, 0, s>>>(st->dev, win, BcastSeg{off_u, n_u}, BcastSeg{off_v, n_v},
+                                                     BcastSeg{off_b, n_b});
+  else
+    sfb_bcast_kernel<4, false><<<blocks, 256, 0, s>>>(st->dev, win, BcastSeg{off_u, n_u}, BcastSeg{off_v, n_v},
+                                                      BcastSeg{off_b, n_b});
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }

@@ -20,7 +20,8 @@ Checks, at world = P:
   6. SSP, staleness 1: SFB + PS over 4 iterations and a flush, integer variant bit-exact vs O10 on
      the NCCL and the NVLS paths.
   7. PS buckets: six layers of mixed sizes, NCCL and fused NVLS paths, integer bit-exact per layer.
-  5. Full size in bench.py's N > 1 configuration: C3 fc6 SFB on symmetric windows (sampled rows vs O4)
+  5. Full size in bench.py's N > 1 configuration: C3 fc6 SFB through the library's broadcast kernel (sampled
+     rows vs O4)
      and a 37.7M-parameter PS layer through the fused NVLS kernel (sampled elements vs O6).
 Prints "MP_OK <rank>" on success; any failure raises.
 """
@@ -469,10 +470,10 @@ def main():
     assert allsame(Wd) and allsame(bd)
     cp.close()
 
-    # ---- 5. full size in bench.py's N > 1 launch configuration (SYMM_SFB | NVLS_PS): C3 fc6 as SFB
+    # ---- 5. full size in bench.py's N > 1 launch configuration (NVLS_SFB | NVLS_PS): C3 fc6 as SFB
     #          (4096 x 9216, K = 256) and a 37.7M-parameter PS layer in the NVLS arena, sampled against
     #          the oracle (O4 rows / O6 elements) ----
-    cf = new_ctx(pz.FLAG_SYMM_SFB | pz.FLAG_NVLS_PS)
+    cf = new_ctx(pz.FLAG_NVLS_SFB | pz.FLAG_NVLS_PS)
     M, N, K = 4096, 9216, 256
     assert cf.register_layer(0, pz.LAYER_FC, M, N, K) == pz.SCHEME_SFB
     cf.register_layer(1, pz.LAYER_CONV, M, N, 1, True, pz.SCHEME_PS)
@@ -500,7 +501,7 @@ def main():
     rows = np.unique(np.concatenate([[0, 1, 255, 256, M - 1], S.rng(502).integers(0, M, 43)]))
     Wr, br = O.sync_step_rows(W[rows], b[rows], Us, Vs, 0.5, rows)
     Wout = Wd.cpu().numpy()
-    assert O.update_error(W[rows], Wout[rows], Wr) <= 2e-3, "full-size SFB (symmetric wire) off the TF32 gate"
+    assert O.update_error(W[rows], Wout[rows], Wr) <= 2e-3, "full-size SFB (broadcast kernel) off the TF32 gate"
     assert O.update_error_fp32(b[rows], bd.cpu().numpy()[rows], br) <= 1e-5
     assert allsame(Wd) and allsame(bd)
     idx = np.unique(np.concatenate([[0, n - 1, n // P, padded // P - 1], S.rng(603).integers(0, n, 4093)]))
