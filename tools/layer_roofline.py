@@ -100,8 +100,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         return pz.Context(rank=rank, world=world, device=local, nccl_id=obj[0], flags=flags)
 
-    # bench.py's N > 1 configuration: SFB factors on NCCL symmetric windows; PS on both paths
-    ctx = new_ctx(pz.FLAG_SYMM_SFB if P > 1 else 0)
+    # bench.py's N > 1 configuration: SFB factors through the library broadcast kernel; PS on both paths
+    ctx = new_ctx(pz.FLAG_NVLS_SFB if P > 1 else 0)
     nv = new_ctx(pz.FLAG_NVLS_PS) if P > 1 else None
     plan = []   # (name, lid, kind, M, N, K, scheme, n)
     lid = 0

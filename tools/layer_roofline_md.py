@@ -45,8 +45,8 @@ def main():
              "queued; time = the library's device events start -> done).  `bw roof`: SURVEY §8(d) bandwidth",
              "roofline (NVLink 5 900 GB/s, TF32 794 TFLOP/s, HBM 6543.7 GB/s).  `eff roof`: the same with every",
              "collective raised to the measured 8-byte NCCL latency alpha (PS: 2 alpha) and every kernel to 2 us.",
-             "ps_nccl = NCCL reduce-scatter + K2 + all-gather; ps_nvls = the fused multimem kernel; sfb = NCCL",
-             "all-gather of the factors + K1; `meas roof`: the effective roof with NVLink at the busbw NCCL itself",
+             "ps_nccl = NCCL reduce-scatter + K2 + all-gather; ps_nvls = the fused multimem kernel; sfb = the library's",
+             "factor broadcast kernel (bench default at P > 1) + K1; `meas roof`: the effective roof with NVLink at the busbw NCCL itself",
              "reaches for 256 MB all-gathers in the same run (SURVEY §8(d): against the spec and the measured peak);",
              "sfps = the literal else-branch of Alg. 3 (reading Z20): U rows to",
              "their masters, V all-gathered, K1 on the master's rows, rows pushed back.", ""]
