@@ -38,6 +38,9 @@ def parse():
     ap.add_argument("--config", default="C3", choices=["C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="poseidon", choices=["poseidon", "reference"])
     ap.add_argument("--scheme", default=None, choices=[None, "auto", "ps", "sfb", "sfps"])
+    ap.add_argument("--early-v", default="auto", choices=["auto", "on", "off"],
+                    help="broadcast SFB layer inputs at forward time (POSEIDON_FLAG_EARLY_V); auto = on when N > 1 "
+                         "(profiles/early_v_r1.md: summed sync -25%%, exposed sync -40%%, images/s unchanged)")
     ap.add_argument("--else-branch", default="ps", choices=["ps", "sfps"],
                     help="how FC layers the SACP rule sends to the server execute: full-gradient PS (reading Z7) "
                          "or the literal sharded SF-PS of Alg. 3 (reading Z20, POSEIDON_FLAG_SFPS)")
@@ -285,6 +288,9 @@ def run_poseidon(args):
         flags |= pz.FLAG_SSP1
     if args.else_branch == "sfps":
         flags |= pz.FLAG_SFPS
+    early_v = args.early_v == "on" or (args.early_v == "auto" and world > 1)
+    if early_v:
+        flags |= pz.FLAG_EARLY_V
     ctx = pz.Context(rank=rank, world=world, device=local, nccl_id=nccl_id, flags=flags)
 
     torch.manual_seed(6216)          # identical weights on every rank
@@ -496,7 +502,7 @@ def run_poseidon(args):
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "tf32" if args.recon == "tf32" else "f32", "data": "synthetic",
             "config": workload_config(args, cfg, world),
-            "details": {"scheme": scheme, "else_branch": args.else_branch, "dwbp": args.dwbp, "recon": args.recon, "lr": args.lr,
+            "details": {"scheme": scheme, "else_branch": args.else_branch, "early_v": early_v, "dwbp": args.dwbp, "recon": args.recon, "lr": args.lr,
                         "momentum": args.momentum, "weight_decay": args.weight_decay,
                         "memory_format": args.memory_format,
                         "ps_path": ("nvls-fused" if sync.nvls_active else

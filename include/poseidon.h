@@ -102,6 +102,9 @@ typedef struct {
 #define POSEIDON_FLAG_SFPS 0x40u       /* FC layers the rule sends to the server (Alg. 3 else-branch) run as
                                          sharded SF-PS (POSEIDON_SCHEME_SFPS) instead of full-gradient PS.
                                          Not combined with POSEIDON_FLAG_SSP1. */
+#define POSEIDON_FLAG_EARLY_V 0x80u    /* enables poseidon_sfb_post_input: an SFB layer's input factors V may be
+                                         broadcast during the forward pass (BSP with DWBP only: not combined
+                                         with POSEIDON_FLAG_SSP1 or POSEIDON_FLAG_DWBP_OFF) */
 
 typedef struct poseidon_ctx* poseidon_ctx_t;
 
@@ -181,6 +184,17 @@ poseidon_status_t poseidon_sync_ps(poseidon_ctx_t ctx, int32_t layer_id, float* 
  * sync on the library streams right away (or at iteration_end under
  * POSEIDON_FLAG_DWBP_OFF). */
 poseidon_status_t poseidon_backprop_hook(poseidon_ctx_t ctx, int32_t layer_id, poseidon_stream_t stream);
+
+/* Early input broadcast (POSEIDON_FLAG_EARLY_V; DWBP's "communicate as soon as the data exists" applied to
+ * the sufficient factors): V, the layer input a_i of Eq. 5 (K x N, row stride ldV >= N, device), is final
+ * once the forward pass has produced it, so it is packed into this rank's slot on `stream` and its
+ * broadcast (all-gather / broadcast kernel, whichever wire the layer uses) starts on the comm stream right
+ * away, overlapping the rest of the forward and the backward.  The layer's next sync (sync_fc_sfb or
+ * backprop_hook) then packs and broadcasts only U and the bias sums and reconstructs from the early V; its
+ * V argument is ignored.  The result is bit-identical to the plain sync (the same values in the same gather
+ * layout).  SFB layers only (ERR_STATE otherwise); at most one post per sync (ERR_STATE). */
+poseidon_status_t poseidon_sfb_post_input(poseidon_ctx_t ctx, int32_t layer_id, const float* V, int64_t ldV,
+                                          poseidon_stream_t stream);
 
 /* Hardware figures for the measured-cost model (GB/s, TFLOP/s, microseconds). */
 typedef struct {

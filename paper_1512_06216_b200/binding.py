@@ -24,7 +24,7 @@ SCHEME_PS, SCHEME_SFB, SCHEME_SFPS = 0, 1, 2
 LAYER_CONV, LAYER_FC = 0, 1
 RECON_TF32, RECON_FP32 = 0, 1
 FLAG_DWBP_OFF, FLAG_NO_PRIORITY, FLAG_NVLS_PS, FLAG_SYMM_SFB, FLAG_NVLS_SFB, FLAG_SSP1 = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
-FLAG_SFPS = 0x40
+FLAG_SFPS, FLAG_EARLY_V = 0x40, 0x80
 SFB_PATH_NCCL, SFB_PATH_NCCL_SYMM, SFB_PATH_NVLS, SFB_PATH_SFPS = 0, 1, 2, 3
 PS_ZERO_GRAD = 0x1
 
@@ -92,6 +92,7 @@ _SIGS = {
     "poseidon_choose_scheme_model": (_i32, [_i32, _i64, _i64, _i64, _i32, _P(Hardware),
                                             _P(ctypes.c_double), _P(ctypes.c_double)]),
     "poseidon_sync_fc_sfb": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _f, _vp]),
+    "poseidon_sfb_post_input": (_i32, [_vp, _i32, _vp, _i64, _vp]),
     "poseidon_sync_ps": (_i32, [_vp, _i32, _vp, _vp, _i64, _f, _vp]),
     "poseidon_backprop_hook": (_i32, [_vp, _i32, _vp]),
     "poseidon_get_unique_id": (_i32, [_P(ctypes.c_uint8)]),
@@ -291,6 +292,10 @@ class Context:
     def sync_fc_sfb(self, layer_id, U, V, W=None, bias=None, lr=0.0, producer=None):
         _check(lib.poseidon_sync_fc_sfb(self.h, layer_id, _ptr(U), _ptr(V), _ptr(W), _ptr(bias), float(lr),
                                         _stream(producer)))
+
+    def sfb_post_input(self, layer_id, V, stream=None):
+        """FLAG_EARLY_V: pack and broadcast the layer input V (K x N, row-major) now (forward time)."""
+        _check(lib.poseidon_sfb_post_input(self.h, layer_id, _ptr(V), V.stride(0), _stream(stream)))
 
     def sync_ps(self, layer_id, grad, W, n, lr, producer=None):
         _check(lib.poseidon_sync_ps(self.h, layer_id, _ptr(grad), _ptr(W), n, float(lr), _stream(producer)))

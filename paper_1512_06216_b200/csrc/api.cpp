@@ -78,6 +78,8 @@ constexpr int MAX_LAYERS = 4096;
 struct EvSet {
   cudaEvent_t ready = nullptr, start = nullptr, gathered = nullptr, kstart = nullptr, kend = nullptr,
               done = nullptr;
+  // early input broadcast (FLAG_EARLY_V): V packed (producer stream), V broadcast done (comm stream)
+  cudaEvent_t vready = nullptr, vgath = nullptr;
   // The events the statistics read for "collective done", "kernel start" and "kernel end".  An event
   // record costs ~1 us of stream time, so a sync records only the events whose time differs from
   // one already recorded (e.g. the fused NVLS kernel: ready, start, done) and aliases the rest.
@@ -103,6 +105,9 @@ struct Layer {
   bool bcast = false;   // POSEIDON_FLAG_NVLS_SFB: factors broadcast by the multicast kernel
   // SF-PS (scheme 2, reading Z20): output rows [rb, re) this rank is the master of (O2 on the rows)
   int64_t rb = 0, re = 0;
+  // FLAG_EARLY_V: this sync's V was packed and broadcast by poseidon_sfb_post_input (events in ev[v_iter])
+  bool v_posted = false;
+  int64_t v_iter = -1;
   float *stU = nullptr, *stV = nullptr;
   float *W = nullptr, *bias = nullptr;  // bound SFB params
   // PS: caller-owned padded flat buffers
@@ -202,7 +207,7 @@ poseidon_status_t ensure_events(Layer& L) {
   if (L.events_created) return POSEIDON_OK;
   for (int i = 0; i < RING; ++i) {
     EvSet& e = L.ev[i];
-    cudaEvent_t* all[] = {&e.ready, &e.start, &e.gathered, &e.kstart, &e.kend, &e.done};
+    cudaEvent_t* all[] = {&e.ready, &e.start, &e.gathered, &e.kstart, &e.kend, &e.done, &e.vready, &e.vgath};
     for (cudaEvent_t* p : all) CU_TRY(cudaEventCreate(p));
   }
   L.events_created = true;
@@ -283,7 +288,8 @@ poseidon_status_t sfb_comm(poseidon_ctx_t c, Layer& L, int set, EvSet& e, cudaEv
   FZ(c->comm_stream);
   CU_TRY(cudaEventRecord(e.start, c->comm_stream));
   e.g_eff = e.start;
-  const size_t ucount = (size_t)(L.M * L.ldk), vcount = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
+  const size_t ucount = (size_t)(L.M * L.ldk), vfull = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
+  const size_t vcount = L.v_posted ? 0 : vfull;   // early V: already broadcast during the forward pass
   const uint64_t per = (uint64_t)(ucount + vcount + bcount) * 4u;
   if (L.bcast) {
     // the paper's "broadcast" done by the NVSwitch: one multicast store of this rank's slots lands in
@@ -291,7 +297,7 @@ poseidon_status_t sfb_comm(poseidon_ctx_t c, Layer& L, int set, EvSet& e, cudaEv
     const size_t ub = (size_t)((char*)g.U - (char*)L.symm), vb = (size_t)((char*)g.V - (char*)L.symm),
                  bb = (size_t)((char*)g.B - (char*)L.symm);
     cudaError_t err = launch_sfb_bcast_nvls(c->nvls, L.win, ub + (size_t)c->rank * ucount * 4, (int64_t)ucount,
-                                            vb + (size_t)c->rank * vcount * 4, (int64_t)vcount,
+                                            vb + (size_t)c->rank * vfull * 4, (int64_t)vcount,
                                             bb + (size_t)c->rank * bcount * 4, (int64_t)bcount, kNvlsBlocks,
                                             c->comm_stream);
     if (err != cudaSuccess) return cuda_fail(err, "NVLS factor broadcast launch");
@@ -299,7 +305,8 @@ poseidon_status_t sfb_comm(poseidon_ctx_t c, Layer& L, int set, EvSet& e, cudaEv
   } else {
     NC_TRY(ncclGroupStart());
     NC_TRY(ncclAllGather(g.U + (size_t)c->rank * ucount, g.U, ucount, ncclFloat32, c->comm, c->comm_stream));
-    NC_TRY(ncclAllGather(g.V + (size_t)c->rank * vcount, g.V, vcount, ncclFloat32, c->comm, c->comm_stream));
+    if (vcount)
+      NC_TRY(ncclAllGather(g.V + (size_t)c->rank * vcount, g.V, vcount, ncclFloat32, c->comm, c->comm_stream));
     NC_TRY(ncclAllGather(g.B + (size_t)c->rank * bcount, g.B, bcount, ncclFloat32, c->comm, c->comm_stream));
     NC_TRY(ncclGroupEnd());
     r.sent += per;  // handed to NCCL once; NCCL forwards it to P-1 peers
@@ -319,6 +326,7 @@ poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, floa
   const GatherSet g = gather_set(L, set);
   CU_TRY(cudaStreamWaitEvent(c->recon_stream, src_g, 0));
   if (extra) CU_TRY(cudaStreamWaitEvent(c->recon_stream, extra, 0));
+  if (L.v_posted) CU_TRY(cudaStreamWaitEvent(c->recon_stream, L.ev[L.v_iter % RING].vgath, 0));
   FZ(c->recon_stream);
   // an event record costs ~1 us of stream time: record only the events whose times differ (BSP at P = 1
   // the sync's start was just recorded on this stream; with nothing after K1, its end is `done`)
@@ -688,7 +696,9 @@ poseidon_status_t sfb_after_pack(poseidon_ctx_t c, int32_t id, Layer& L, float* 
     open_record(c);
     return POSEIDON_OK;
   }
-  return launch_factor_sync(c, id, L, W, bias, lr, e.ready);
+  poseidon_status_t st = launch_factor_sync(c, id, L, W, bias, lr, e.ready);
+  L.v_posted = false;
+  return st;
 }
 
 poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t ldU, const float* V, int64_t ldV,
@@ -700,8 +710,10 @@ poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t l
   float* b_slot = g.B + (size_t)c->rank * L.M;
   cudaError_t err = launch_pack_t(U, ldU, u_slot, L.ldk, L.K, L.M, round, b_slot, producer);
   if (err != cudaSuccess) return cuda_fail(err, "pack U launch");
-  err = launch_pack_t(V, ldV, v_slot, L.ldk, L.K, L.N, round, nullptr, producer);
-  if (err != cudaSuccess) return cuda_fail(err, "pack V launch");
+  if (!L.v_posted) {
+    err = launch_pack_t(V, ldV, v_slot, L.ldk, L.K, L.N, round, nullptr, producer);
+    if (err != cudaSuccess) return cuda_fail(err, "pack V launch");
+  }
   if ((err = debug_sync(producer, "K3 pack")) != cudaSuccess) return cuda_fail(err, "K3");
   return POSEIDON_OK;
 }
@@ -725,7 +737,7 @@ void free_layer(Layer& L) {
   if (L.events_created) {
     for (int i = 0; i < RING; ++i) {
       EvSet& e = L.ev[i];
-      cudaEvent_t all[] = {e.ready, e.start, e.gathered, e.kstart, e.kend, e.done};
+      cudaEvent_t all[] = {e.ready, e.start, e.gathered, e.kstart, e.kend, e.done, e.vready, e.vgath};
       for (cudaEvent_t ev : all)
         if (ev) cudaEventDestroy(ev);
       e = EvSet{};
@@ -784,6 +796,8 @@ poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, 
   }
   if ((topo->flags & POSEIDON_FLAG_SSP1) && (topo->flags & POSEIDON_FLAG_DWBP_OFF))
     return fail(POSEIDON_ERR_INVALID_ARG, "FLAG_SSP1 needs DWBP (the stale update is applied at the next hook)");
+  if ((topo->flags & POSEIDON_FLAG_EARLY_V) && (topo->flags & (POSEIDON_FLAG_SSP1 | POSEIDON_FLAG_DWBP_OFF)))
+    return fail(POSEIDON_ERR_INVALID_ARG, "FLAG_EARLY_V is a BSP + DWBP schedule (not with SSP1 / DWBP_OFF)");
   auto* c = new poseidon_ctx();
   c->rank = topo->rank;
   c->world = world;
@@ -1286,6 +1300,49 @@ poseidon_status_t poseidon_sync_fc_sfb(poseidon_ctx_t c, int32_t id, const float
   st = pack_sfb(c, *L, U, L->M, V, L->N, ps);
   if (st) return st;
   return sfb_after_pack(c, id, *L, W, bias, lr, ps);
+}
+
+poseidon_status_t poseidon_sfb_post_input(poseidon_ctx_t c, int32_t id, const float* V, int64_t ldV,
+                                          poseidon_stream_t stream) {
+  Layer* L;
+  poseidon_status_t st = check_layer(c, id, &L);
+  if (st) return st;
+  if (!(c->flags & POSEIDON_FLAG_EARLY_V)) return fail(POSEIDON_ERR_STATE, "context created without FLAG_EARLY_V");
+  if (L->scheme != POSEIDON_SCHEME_SFB) return fail(POSEIDON_ERR_STATE, "early input broadcast needs an SFB layer");
+  if (!V || ldV < L->N) return fail(POSEIDON_ERR_INVALID_ARG, "V is NULL or ldV < N");
+  if (L->v_posted) return fail(POSEIDON_ERR_STATE, "V already posted for this sync");
+  cudaStream_t ps = reinterpret_cast<cudaStream_t>(stream);
+  st = producer_guard(c, *L, ps);   // the previous sync's K1 no longer reads the gather buffers
+  if (st) return st;
+  const int P = c->world;
+  const bool round = (L->recon == POSEIDON_RECON_TF32);
+  float* v_slot = L->Vg + (size_t)c->rank * L->N * L->ldk;
+  cudaError_t err = launch_pack_t(V, ldV, v_slot, L->ldk, L->K, L->N, round, nullptr, ps);
+  if (err != cudaSuccess) return cuda_fail(err, "pack V launch");
+  EvSet& e = L->ev[c->iter % RING];
+  CU_TRY(cudaEventRecord(e.vready, ps));
+  if (P > 1) {
+    IterRecord& r = open_record(c);
+    const size_t vcount = (size_t)(L->N * L->ldk);
+    CU_TRY(cudaStreamWaitEvent(c->comm_stream, e.vready, 0));
+    FZ(c->comm_stream);
+    if (L->bcast) {
+      const size_t vb = (size_t)((char*)L->Vg - (char*)L->symm);
+      err = launch_sfb_bcast_nvls(c->nvls, L->win, 0, 0, vb + (size_t)c->rank * vcount * 4, (int64_t)vcount, 0, 0,
+                                  kNvlsBlocks, c->comm_stream);
+      if (err != cudaSuccess) return cuda_fail(err, "early V broadcast launch");
+    } else {
+      NC_TRY(ncclAllGather(L->Vg + (size_t)c->rank * vcount, L->Vg, vcount, ncclFloat32, c->comm, c->comm_stream));
+    }
+    r.sent += (uint64_t)vcount * 4u;
+    r.recv += (uint64_t)vcount * 4u * (uint64_t)(P - 1);
+    CU_TRY(cudaEventRecord(e.vgath, c->comm_stream));
+  } else {
+    CU_TRY(cudaEventRecord(e.vgath, ps));
+  }
+  L->v_posted = true;
+  L->v_iter = c->iter;
+  return POSEIDON_OK;
 }
 
 poseidon_status_t poseidon_sync_ps(poseidon_ctx_t c, int32_t id, float* grad, float* W, int64_t n, float lr,

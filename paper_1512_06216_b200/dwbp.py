@@ -69,6 +69,10 @@ class SFBLinearFunction(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, weight, bias, plan, sync):
+        if sync.early_v and plan.scheme == B.SCHEME_SFB:
+            # FLAG_EARLY_V: the input factors V = a_i are final now; their broadcast overlaps the rest of
+            # the forward and the backward (the hook then moves only U)
+            sync.ctx.sfb_post_input(plan.layer_id, x.contiguous(), torch.cuda.current_stream())
         ctx.save_for_backward(x, weight)
         ctx.plan = plan
         ctx.sync = sync
@@ -103,6 +107,7 @@ class PoseidonSync:
         self.by_module: Dict[nn.Module, LayerPlan] = {}
         ctx.set_lr(self.lr)
         self.ssp = bool(getattr(ctx, "flags", 0) & B.FLAG_SSP1)
+        self.early_v = bool(getattr(ctx, "flags", 0) & B.FLAG_EARLY_V)
         if self.ssp and not arena:
             raise ValueError("FLAG_SSP1 needs the library arena (arena=True): PS gradients are double-buffered")
         self.arena = arena

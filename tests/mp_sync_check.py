@@ -17,6 +17,8 @@ Checks, at world = P:
      shapes (masters with no rows at P = 4), plain / symmetric buffers / DWBP off, both kernels, NCCL
      byte counts; random factors with momentum vs O4m; FLAG_SFPS auto-selection; CIFAR-quick with
      every FC layer as SF-PS in test 4.
+  9. Early input broadcast (FLAG_EARLY_V): V posted at forward time, NCCL and broadcast-kernel wires,
+     integer bit-exact vs O4 with garbage V at the sync; CIFAR-quick training bit-identical to the plain run.
   6. SSP, staleness 1: SFB + PS over 4 iterations and a flush, integer variant bit-exact vs O10 on
      the NCCL and the NVLS paths.
   7. PS buckets: six layers of mixed sizes, NCCL and fused NVLS paths, integer bit-exact per layer.
@@ -307,6 +309,24 @@ def main():
                 assert err < 2e-3, (name, err, scheme, dwbp, nv)
             results[(scheme, dwbp, nv)] = flat.cpu()
             c2.close()
+    # the same training with the SFB inputs broadcast at forward time (FLAG_EARLY_V): bit-identical
+    c2 = new_ctx(pz.FLAG_EARLY_V)
+    torch.manual_seed(1234)
+    model = CifarQuick().to(dev)
+    sync = PoseidonSync(model, c2, K=Kc, lr=0.05, scheme="auto", recon=pz.RECON_TF32)
+    assert sync.early_v
+    for it in range(2):
+        gen = torch.Generator().manual_seed(100 + it)
+        xall = torch.rand(P * Kc, 3, 32, 32, generator=gen).to(dev)
+        yall = torch.randint(0, 10, (P * Kc,), generator=gen).to(dev)
+        xb, yb = xall[rank * Kc:(rank + 1) * Kc], yall[rank * Kc:(rank + 1) * Kc]
+        F.cross_entropy(model(xb), yb).backward()
+        sync.iteration_end()
+    sync.wait_all()
+    torch.cuda.synchronize()
+    flat = torch.cat([p.detach().reshape(-1) for p in model.parameters()]).cpu()
+    assert torch.equal(flat, results[("auto", "on", False)]), "early V changed the result"
+    c2.close()
     for scheme, nv in [(sc, nv) for sc in ("auto", "ps") for nv in (False, True)] + [("sfps", False)]:
         assert torch.equal(results[(scheme, "on", nv)], results[(scheme, "off", nv)]), \
             f"DWBP on/off differ ({scheme}, nvls {nv})"
@@ -469,6 +489,41 @@ def main():
     assert O.update_error_fp32(b, bd.cpu().numpy(), br) <= 1e-5, "SF-PS bias momentum"
     assert allsame(Wd) and allsame(bd)
     cp.close()
+
+    # ---- 9. early input broadcast (FLAG_EARLY_V): V posted at "forward" time, only U at the sync (whose V
+    #          argument is garbage here); NCCL and broadcast-kernel wires; integer bit-exact vs O4, two
+    #          iterations, and the same NCCL byte total as the plain sync ----
+    for flags in (pz.FLAG_EARLY_V, pz.FLAG_EARLY_V | pz.FLAG_NVLS_SFB):
+        ce = new_ctx(flags)
+        shapes = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 1000, 4096, 33)]
+        for lid, M_, N_, K_ in shapes:
+            assert ce.register_layer(lid, pz.LAYER_FC, M_, N_, K_) == pz.SCHEME_SFB
+        for it in range(2):
+            outs = []
+            for lid, M_, N_, K_ in shapes:   # "forward": every layer posts its input
+                W, b, Us, Vs, lr = S.integer_factors(M_, N_, K_, P, seed=700 + 10 * it + lid)
+                ce.sfb_post_input(lid, torch.from_numpy(Vs[rank]).to(dev))
+                outs.append((W, b, Us, Vs, lr))
+            res = []
+            for lid, (W, b, Us, Vs, lr) in reversed(list(enumerate(outs))):   # "backward": top layer first
+                Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+                junk = torch.full((Vs[rank].shape[0], Vs[rank].shape[1]), 5.0, device=dev)
+                ce.sync_fc_sfb(lid, torch.from_numpy(Us[rank]).to(dev), junk, Wd, bd, lr)
+                res.append((lid, Wd, bd))
+            st = ce.iteration_end(stats=True)
+            for lid, Wd, bd in res:
+                ce.wait_layer(lid)
+            torch.cuda.synchronize()
+            for lid, Wd, bd in res:
+                W, b, Us, Vs, lr = outs[lid]
+                W1, b1 = O.sync_step(W, b, Us, Vs, lr)
+                assert np.array_equal(Wd.cpu().numpy().astype(np.float64), W1), f"early V flags={flags} lid={lid}"
+                assert np.array_equal(bd.cpu().numpy().astype(np.float64), b1)
+                assert allsame(Wd) and allsame(bd)
+            ldks = [(K_ + 3) // 4 * 4 for _, _, _, K_ in shapes]
+            per = sum((M_ * l + N_ * l + M_) * 4 for (_, M_, N_, _), l in zip(shapes, ldks))
+            assert st["nccl_bytes_recv"] == per * (P - 1), st
+        ce.close()
 
     # ---- 5. full size in bench.py's N > 1 launch configuration (NVLS_SFB | NVLS_PS): C3 fc6 as SFB
     #          (4096 x 9216, K = 256) and a 37.7M-parameter PS layer in the NVLS arena, sampled against

@@ -51,6 +51,37 @@ def test_context_sfps_world1(pz):
     ctx.close()
 
 
+def test_context_early_input_world1(pz):
+    """FLAG_EARLY_V at P = 1: V posted at forward time, the sync's own V argument ignored (garbage here),
+    integer variant bit-exact vs O4 over two syncs; misuse is refused."""
+    ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device(), flags=pz.FLAG_EARLY_V)
+    M, N, K = 70, 132, 6
+    assert ctx.register_layer(0, pz.LAYER_FC, M, N, K) == pz.SCHEME_SFB
+    ctx.register_layer(1, pz.LAYER_CONV, 8, 8, K)
+    W, b, _, _, lr = S.integer_factors(M, N, K, 1, seed=41)
+    Wd, bd = dev(W), dev(b)
+    Wr, br = W.astype(np.float64), b.astype(np.float64)
+    for t in range(2):
+        _, _, Us, Vs, _ = S.integer_factors(M, N, K, 1, seed=50 + t)
+        ctx.sfb_post_input(0, dev(Vs[0]))
+        with pytest.raises(pz.PoseidonError):
+            ctx.sfb_post_input(0, dev(Vs[0]))           # one post per sync
+        ctx.sync_fc_sfb(0, dev(Us[0]), dev(np.full_like(Vs[0], 7.0)), Wd, bd, lr)
+        ctx.wait_layer(0)
+        ctx.iteration_end()
+        Wr, br = O.sync_step(Wr, br, Us, Vs, lr)
+        assert np.array_equal(host(Wd).astype(np.float64), Wr)
+        assert np.array_equal(host(bd).astype(np.float64), br)
+    with pytest.raises(pz.PoseidonError):
+        ctx.sfb_post_input(1, dev(np.zeros((K, 8), np.float32)))   # not an SFB layer
+    ctx.close()
+    plain = pz.Context(rank=0, world=1, device=torch.cuda.current_device())
+    plain.register_layer(0, pz.LAYER_FC, M, N, K)
+    with pytest.raises(pz.PoseidonError):
+        plain.sfb_post_input(0, dev(np.zeros((K, N), np.float32)))  # context without FLAG_EARLY_V
+    plain.close()
+
+
 def test_context_sfb_and_ps_world1(pz):
     ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device())
     M, N, K = 128, 256, 8
