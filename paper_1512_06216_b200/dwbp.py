@@ -68,8 +68,8 @@ class SFBLinearFunction(torch.autograd.Function):
     """y = x W^T + b; backward returns dX only and triggers the SFB sync."""
 
     @staticmethod
-    def forward(ctx, x, weight, bias, plan, sync):
-        if sync.early_v and plan.scheme == B.SCHEME_SFB:
+    def forward(ctx, x, weight, bias, plan, sync, post_input):
+        if post_input:
             # FLAG_EARLY_V: the input factors V = a_i are final now; their broadcast overlaps the rest of
             # the forward and the backward (the hook then moves only U)
             sync.ctx.sfb_post_input(plan.layer_id, x.contiguous(), torch.cuda.current_stream())
@@ -89,7 +89,7 @@ class SFBLinearFunction(torch.autograd.Function):
         # update of W on the library's stream is ordered after this read by the ready event.
         grad_x = grad_out @ weight if ctx.needs_input_grad[0] else None
         ctx.sync.sfb_backward(ctx.plan, grad_out, x.contiguous(), weight, ctx.bias)
-        return grad_x, None, None, None, None
+        return grad_x, None, None, None, None, None
 
 
 class PoseidonSync:
@@ -216,7 +216,10 @@ class PoseidonSync:
         sync = self
 
         def forward(x):
-            return SFBLinearFunction.apply(x, mod.weight, mod.bias, plan, sync)
+            # grad mode is read HERE (autograd runs Function.forward under no_grad): a forward that will
+            # not be backpropagated (evaluation) posts no inputs
+            post = sync.early_v and plan.scheme == B.SCHEME_SFB and torch.is_grad_enabled()
+            return SFBLinearFunction.apply(x, mod.weight, mod.bias, plan, sync, post)
 
         mod.forward = forward
 

@@ -1,0 +1,64 @@
+"""Host-side checks of the DWBP glue (no GPU): the SFB Linear wrapper posts the layer input for the early
+input broadcast only in a forward that will be backpropagated, hands (grad_out, input) to the library in
+backward, and returns dX = grad_out @ W (Alg. 2 line 7) without forming dW.  The library context is a
+recording stand-in; all arithmetic checked here is the wrapper's own dX."""
+import pytest
+import torch
+import torch.nn as nn
+
+from paper_1512_06216_b200 import binding as B
+from paper_1512_06216_b200.dwbp import LayerPlan, PoseidonSync
+
+
+class _RecordingCtx:
+    def __init__(self):
+        self.posted, self.synced = [], []
+
+    def sfb_post_input(self, layer_id, V, stream=None):
+        self.posted.append((layer_id, V.detach().clone()))
+
+    def sync_fc_sfb(self, layer_id, U, V, W=None, bias=None, lr=0.0, producer=None):
+        self.synced.append((layer_id, U.detach().clone(), V.detach().clone()))
+
+
+@pytest.fixture
+def wrapped(monkeypatch):
+    monkeypatch.setattr(torch.cuda, "current_stream", lambda *a, **k: None)
+    torch.manual_seed(0)
+    mod = nn.Linear(6, 4)
+    sync = PoseidonSync.__new__(PoseidonSync)   # no library context: only the wrapper is under test
+    sync.ctx = _RecordingCtx()
+    sync.lr = 0.1
+    sync.early_v = True
+    plan = LayerPlan(3, "fc", mod, B.LAYER_FC, 4, 6, 5, B.SCHEME_SFB, B.SCHEME_SFB, (0, 0, 0))
+    sync._wrap_linear(mod, plan)
+    return mod, sync
+
+
+def test_forward_posts_input_and_backward_hands_factors(wrapped):
+    mod, sync = wrapped
+    x = torch.randn(5, 6, requires_grad=True)
+    y = mod(x)
+    assert torch.allclose(y, x @ mod.weight.t() + mod.bias)
+    assert len(sync.ctx.posted) == 1 and sync.ctx.posted[0][0] == 3
+    assert torch.equal(sync.ctx.posted[0][1], x.detach())
+    g = torch.randn(5, 4)
+    y.backward(g)
+    (lid, U, V), = sync.ctx.synced
+    assert lid == 3 and torch.equal(U, g) and torch.equal(V, x.detach())
+    assert torch.allclose(x.grad, g @ mod.weight.detach())
+    assert mod.weight.grad is None   # the local dW is never formed (Eq. 5: the factors travel instead)
+
+
+def test_no_grad_forward_posts_nothing(wrapped):
+    mod, sync = wrapped
+    with torch.no_grad():
+        mod(torch.randn(5, 6))
+    assert sync.ctx.posted == []
+
+
+def test_early_v_off_posts_nothing(wrapped):
+    mod, sync = wrapped
+    sync.early_v = False
+    mod(torch.randn(5, 6, requires_grad=True))
+    assert sync.ctx.posted == []

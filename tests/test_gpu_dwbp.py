@@ -90,3 +90,38 @@ def test_ordering_fuzz_changes_timing_not_results(pz, tmp_path, dwbp_on):
                        env=env, cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     assert torch.equal(torch.load(out), ref)
+
+
+def test_early_input_broadcast_is_bit_identical(pz):
+    """FLAG_EARLY_V through the glue at P = 1: every SFB layer posts its input in the forward (counted), and
+    the trained parameters equal the plain run bit for bit."""
+    import torch.nn.functional as F
+    from paper_1512_06216_b200.dwbp import PoseidonSync
+    from drivers.cnn import CifarQuick
+
+    dev = torch.device("cuda", 0)
+    out = {}
+    for flags in (0, pz.FLAG_EARLY_V):
+        ctx = pz.Context(rank=0, world=1, device=0, flags=flags)
+        posts = []
+        orig = ctx.sfb_post_input
+        ctx.sfb_post_input = lambda lid, V, stream=None, _o=orig: (posts.append(lid), _o(lid, V, stream))
+        torch.manual_seed(6216)
+        model = CifarQuick().to(dev)
+        sync = PoseidonSync(model, ctx, K=64, lr=0.01)
+        g = torch.Generator(device=dev)
+        g.manual_seed(1512)
+        for _ in range(3):
+            x = torch.rand((64, 3, 32, 32), device=dev, generator=g)
+            y = torch.randint(0, 10, (64,), device=dev, generator=g)
+            F.cross_entropy(model(x), y).backward()
+            sync.iteration_end()
+        with torch.no_grad():
+            model(x)                     # an evaluation forward posts nothing
+        sync.wait_all()
+        torch.cuda.synchronize()
+        n_sfb = sum(1 for p in sync.plans if p.scheme == pz.SCHEME_SFB)
+        assert len(posts) == (3 * n_sfb if flags else 0), posts
+        out[flags] = torch.cat([p.detach().reshape(-1) for p in model.parameters()]).cpu()
+        ctx.close()
+    assert torch.equal(out[0], out[pz.FLAG_EARLY_V])
