@@ -14,6 +14,9 @@ next-forward barrier.  The optimiser step IS the sync (Alg. 1/3).  Metric
 roofline fraction of the dominant sync kernel.  Default config C3 (AlexNet,
 batch 256/GPU): the config the north-star target is stated on and the only
 one that exercises every hot-path step (SFB on FC + PS on conv + DWBP).
+Defaults at N > 1: PS layers sync with the fused NVLink-SHARP kernel, SFB
+factors move through the library's broadcast kernel, and SFB layer inputs are
+broadcast at forward time (early V); every option has a flag to A/B it.
 """
 from __future__ import annotations
 
