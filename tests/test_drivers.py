@@ -42,3 +42,27 @@ def test_googlenet_structure():
     with torch.device("meta"):
         y = GoogLeNet()(torch.empty(2, 3, 224, 224))
     assert y.shape == (2, 1000)
+
+
+def test_alexnet_flop_split_matches_table():
+    """Forward FLOPs per image (2 x multiply-adds of every conv / FC, from the layers' own output shapes)
+    against Table tb:distribution."""
+    g = _g()["alexnet_flops"]
+    flops = {"conv": 0, "fc": 0}
+
+    def hook(mod, inp, out):
+        if isinstance(mod, torch.nn.Conv2d):
+            k = mod.in_channels // mod.groups * mod.kernel_size[0] * mod.kernel_size[1]
+            flops["conv"] += 2 * out[0].numel() * k
+        else:
+            flops["fc"] += 2 * mod.in_features * mod.out_features
+
+    with torch.device("meta"):
+        m = AlexNet()
+        for x in m.modules():
+            if isinstance(x, (torch.nn.Conv2d, torch.nn.Linear)):
+                x.register_forward_hook(hook)
+        m(torch.empty(1, 3, 227, 227))
+    assert round(flops["fc"] / 1e6) == g["fc_mflops"]
+    assert abs(flops["conv"] / 1e6 / g["conv_mflops"] - 1) < 0.02
+    assert abs(100 * flops["conv"] / (flops["conv"] + flops["fc"]) - g["conv_pct"]) < 0.2
