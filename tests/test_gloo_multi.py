@@ -1,7 +1,8 @@
 """World-size-2 CPU (gloo) tests of the N>1 host logic: NCCL-id broadcast as
 bench.py does it, cross-rank agreement of the library's host decisions (SACP
-rule, shard map), and the two exchange protocols' data layouts (rank-major
-all-gather of SFB factors; reduce-scatter / shard update / all-gather of PS)
+rule, shard map), and the exchange protocols' data layouts (rank-major
+all-gather of SFB factors; reduce-scatter / shard update / all-gather of PS;
+SF-PS's row masters from the library's row map)
 emulated with gloo collectives and checked against the oracle."""
 import os
 import socket
@@ -92,6 +93,44 @@ def _worker(rank, world, port, q):
         w1 = torch.cat(out).numpy()[:n]
         W6, b6 = O.ps_simulated(W, b, Us, Vs, 0.3)
         assert np.max(np.abs(w1 - O.flatten_params(W6, b6))) < 1e-12
+
+        # 5. SF-PS exchange (Alg. 3 else-branch, reading Z20) with the library's row map: U columns of master
+        #    m's rows to m (send/recv), V to everyone (all-gather), master reconstructs its rows, rows broadcast
+        M2 = 70                                   # 32-row masters: rank 0 owns 64 rows, rank 1 owns 6 at P = 2
+        W, b = S.fc_weights_randbias(M2, N)
+        Us, Vs = S.hidden_factors(M2, N, K, world, seed=17)
+        rows = [B.shard_range(M2, world, m)[:2] for m in range(world)]
+        assert rows == [O.row_shard_range(M2, world, m) for m in range(world)]
+        lo, hi = rows[rank]
+        mine = {rank: torch.from_numpy(np.ascontiguousarray(Us[rank][:, lo:hi]))}
+        reqs = []
+        for m in range(world):
+            if m == rank:
+                continue
+            qb, qe = rows[m]
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(Us[rank][:, qb:qe])), m))
+            mine[m] = torch.zeros(K, hi - lo, dtype=torch.float32)
+            reqs.append(dist.irecv(mine[m], m))
+        for r_ in reqs:
+            r_.wait()
+        vg = [torch.zeros(K, N, dtype=torch.float32) for _ in range(world)]
+        dist.all_gather(vg, torch.from_numpy(Vs[rank]))
+        G = sum(mine[p].double().numpy().T @ vg[p].double().numpy() for p in range(world))
+        gb = sum(mine[p].double().numpy().sum(0) for p in range(world))
+        Wout = torch.from_numpy(W.astype(np.float64).copy())
+        Wout[lo:hi] += (-0.3 / world) * torch.from_numpy(G)
+        bout = torch.from_numpy(b.astype(np.float64).copy())
+        bout[lo:hi] += (-0.3 / world) * torch.from_numpy(gb)
+        for m in range(world):
+            qb, qe = rows[m]
+            blk = Wout[qb:qe].contiguous()
+            dist.broadcast(blk, src=m)
+            Wout[qb:qe] = blk
+            bb = bout[qb:qe].contiguous()
+            dist.broadcast(bb, src=m)
+            bout[qb:qe] = bb
+        W11, b11, _ = O.sf_ps_simulated(W, b, Us, Vs, 0.3)
+        assert np.max(np.abs(Wout.numpy() - W11)) < 1e-12 and np.max(np.abs(bout.numpy() - b11)) < 1e-12
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))
