@@ -518,7 +518,7 @@ def run_poseidon(args):
             "exposed_sync_ms": exposed, "sync_total_ms": sync_total,
             "exposed_frac": (exposed / sync_total) if sync_total > 0 else None,
             "nccl_bytes_sent_per_iter": nccl_sent, "nccl_bytes_recv_per_iter": nccl_recv,
-            "layers": [{k: d[k] for k in ("name", "scheme", "rule", "model", "M", "N")} for d in sync.describe()],
+            "layers": [{k: d[k] for k in ("name", "scheme", "rule", "model", "model3", "M", "N")} for d in sync.describe()],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk,
         }

@@ -211,6 +211,13 @@ typedef struct {
  * Pure host code.  t_sfb_us / t_ps_us may be NULL. */
 int32_t poseidon_choose_scheme_model(int32_t kind, int64_t M, int64_t N, int64_t K, int32_t P,
                                      const poseidon_hw_t* hw, double* t_sfb_us, double* t_ps_us);
+/* The same model with SF-PS (Alg. 3's else-branch executed literally, reading Z20) as a third execution:
+ * pack + V all-gather + U rows to their masters + K1 on the largest master's rows + row push.  Returns the
+ * predicted-fastest POSEIDON_SCHEME_* (non-FC -> PS) or a negative status; pure host code; outputs
+ * nullable. */
+int32_t poseidon_choose_scheme_model3(int32_t kind, int64_t M, int64_t N, int64_t K, int32_t P,
+                                      const poseidon_hw_t* hw, double* t_sfb_us, double* t_ps_us,
+                                      double* t_sfps_us);
 
 /* ================================ helpers ================================= */
 

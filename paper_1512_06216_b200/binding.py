@@ -91,6 +91,8 @@ _SIGS = {
     "poseidon_choose_scheme": (_i32, [_i32, _i64, _i64, _i64, _i32, _P(Costs)]),
     "poseidon_choose_scheme_model": (_i32, [_i32, _i64, _i64, _i64, _i32, _P(Hardware),
                                             _P(ctypes.c_double), _P(ctypes.c_double)]),
+    "poseidon_choose_scheme_model3": (_i32, [_i32, _i64, _i64, _i64, _i32, _P(Hardware), _P(ctypes.c_double),
+                                             _P(ctypes.c_double), _P(ctypes.c_double)]),
     "poseidon_sync_fc_sfb": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _f, _vp]),
     "poseidon_sfb_post_input": (_i32, [_vp, _i32, _vp, _i64, _vp]),
     "poseidon_sync_ps": (_i32, [_vp, _i32, _vp, _vp, _i64, _f, _vp]),
@@ -188,6 +190,17 @@ def choose_scheme_model(kind: int, M: int, N: int, K: int, P: int, hw: Optional[
     if r < 0:
         raise PoseidonError(r, last_error())
     return r, ts.value, tp.value
+
+
+def choose_scheme_model3(kind: int, M: int, N: int, K: int, P: int, hw: Optional[dict] = None):
+    """Model pick among PS / SFB / SF-PS: (scheme, t_sfb_us, t_ps_us, t_sfps_us); reported beside the rule."""
+    h = Hardware(**(hw or B200_HW))
+    ts, tp, tf = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    r = lib.poseidon_choose_scheme_model3(kind, M, N, K, P, ctypes.byref(h), ctypes.byref(ts), ctypes.byref(tp),
+                                          ctypes.byref(tf))
+    if r < 0:
+        raise PoseidonError(r, last_error())
+    return r, ts.value, tp.value, tf.value
 
 
 def shard_range(n: int, P: int, rank: int) -> Tuple[int, int, int]:

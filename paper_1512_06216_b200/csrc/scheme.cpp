@@ -88,3 +88,36 @@ extern "C" int32_t poseidon_choose_scheme_model(int32_t kind, int64_t M, int64_t
   if (kind != POSEIDON_LAYER_FC) return POSEIDON_SCHEME_PS;
   return t_sfb <= t_ps ? POSEIDON_SCHEME_SFB : POSEIDON_SCHEME_PS;
 }
+
+// The same model with the literal else-branch of Alg. 3 as a third execution (SF-PS, reading Z20):
+// pack + V all-gather + U rows to their masters + K1 on the master's R = 32-aligned ceil(M/P) rows + the
+// masters' rows pushed to everyone.  Returns 0 (PS), 1 (SFB) or 2 (SF-PS), whichever is predicted fastest
+// (non-FC -> PS); reported beside the rule (profiles/sfps_crossover_r1.md for the measurements).
+extern "C" int32_t poseidon_choose_scheme_model3(int32_t kind, int64_t M, int64_t N, int64_t K, int32_t P,
+                                                 const poseidon_hw_t* hw, double* t_sfb_us, double* t_ps_us,
+                                                 double* t_sfps_us) {
+  using namespace poseidon;
+  double ts = 0.0, tp = 0.0;
+  const int32_t two = poseidon_choose_scheme_model(kind, M, N, K, P, hw, &ts, &tp);
+  if (two < 0) return two;
+  const double m = (double)M, n = (double)N, k = (double)K, p = (double)P;
+  const double nvl = hw->nvlink_gbps * 1e9, hbm = hw->hbm_gbps * 1e9, tc = hw->tensor_tflops * 1e12;
+  const double alpha = hw->collective_latency_us * 1e-6;
+  const double ldk = 4.0 * ((K + 3) / 4);
+  int64_t b0 = 0, e0 = 0, pad = 0;
+  poseidon_shard_range(M, P, 0, &b0, &e0, &pad);
+  const double r = (double)(e0 - b0);   // the largest master's rows (rank 0 owns a full shard)
+  const double t_pack = 8.0 * k * (m + n) / hbm;
+  const double t_comm = (P > 1) ? ((p - 1.0) * ldk * n * 4.0 / nvl + (p - 1.0) * ldk * r * 4.0 / nvl +
+                                   (m - r) * n * 4.0 / nvl + 3.0 * alpha)
+                                : 0.0;
+  const double t_k1 = std::max(2.0 * r * n * p * k / tc, (8.0 * r * n + 4.0 * p * ldk * (r + n)) / hbm);
+  const double tf = t_pack + t_comm + t_k1;
+  if (t_sfb_us) *t_sfb_us = ts;
+  if (t_ps_us) *t_ps_us = tp;
+  if (t_sfps_us) *t_sfps_us = tf * 1e6;
+  if (kind != POSEIDON_LAYER_FC) return POSEIDON_SCHEME_PS;
+  const double best2 = std::min(ts, tp);
+  if (tf * 1e6 < best2) return POSEIDON_SCHEME_SFPS;
+  return two;
+}

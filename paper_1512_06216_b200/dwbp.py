@@ -269,11 +269,14 @@ class PoseidonSync:
         out = []
         for p in self.plans:
             mpick, t_sfb, t_ps = B.choose_scheme_model(p.kind, p.M, p.N, p.K, self.ctx.world)
+            m3, _, _, t_sfps = B.choose_scheme_model3(p.kind, p.M, p.N, p.K, self.ctx.world)
             out.append({"id": p.layer_id, "name": p.name, "kind": "fc" if p.kind == B.LAYER_FC else "conv",
                         "M": p.M, "N": p.N, "K": p.K,
                         "scheme": {B.SCHEME_SFB: "SFB", B.SCHEME_SFPS: "SFPS"}.get(p.scheme, "PS"),
                         "rule": "SFB" if p.rule_scheme == B.SCHEME_SFB else "PS",
                         "model": "SFB" if mpick == B.SCHEME_SFB else "PS",
+                        "model3": {B.SCHEME_SFB: "SFB", B.SCHEME_SFPS: "SFPS"}.get(m3, "PS"),
                         "model_t_sfb_us": round(t_sfb, 1), "model_t_ps_us": round(t_ps, 1),
+                        "model_t_sfps_us": round(t_sfps, 1),
                         "cost_sfb": p.costs[0], "cost_sf_ps": p.costs[1], "cost_full_ps": p.costs[2]})
         return out

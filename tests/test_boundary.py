@@ -110,3 +110,21 @@ def test_flag_values_match_header():
     assert "FLAG_NVLS_SFB" in defs and "FLAG_SYMM_SFB" in defs
     for name, val in defs.items():
         assert getattr(B, name) == int(val, 16), name
+
+
+def test_measured_cost_model3_against_the_measured_winners():
+    """The three-way model (PS / SFB / SF-PS, reported beside the rule) against every measured point of
+    profiles/sfps_crossover_r1.jsonl (SFB, PS + wgrad, SF-PS timed on 2 and 4 B200).  The model does not
+    know cuBLAS's misaligned-wgrad penalty on the 21841-row layer, so it is held to 80% agreement."""
+    import json
+    from paper_1512_06216_b200 import binding as Bn
+    name = {pz.SCHEME_PS: "PS", pz.SCHEME_SFB: "SFB", pz.SCHEME_SFPS: "SFPS"}
+    pts = [json.loads(l) for l in open(os.path.join(ROOT, "profiles", "sfps_crossover_r1.jsonl"))]
+    hits = sum(name[Bn.choose_scheme_model3(1, d["M"], d["N"], d["K"], d["P"])[0]] == d["winner_of_three"]
+               for d in pts)
+    assert len(pts) >= 30 and hits >= 0.8 * len(pts), (hits, len(pts))
+    # the regime the measurements single out: the 21841-way layer at 4 GPUs, K = 2048 -> SF-PS
+    assert Bn.choose_scheme_model3(1, 21841, 4096, 2048, 4)[0] == pz.SCHEME_SFPS
+    assert Bn.choose_scheme_model3(0, 96, 363, 256, 4)[0] == pz.SCHEME_PS
+    r, ts, tp, tf = Bn.choose_scheme_model3(1, 4096, 9216, 256, 4)
+    assert r == pz.SCHEME_SFB and 0 < ts < tf < tp
