@@ -62,3 +62,21 @@ def test_early_v_off_posts_nothing(wrapped):
     sync.early_v = False
     mod(torch.randn(5, 6, requires_grad=True))
     assert sync.ctx.posted == []
+
+
+def test_describe_reports_rule_and_models():
+    """describe() (bench.py's per-layer JSON) names the executed scheme, the paper's rule and both model picks."""
+    class _Ctx:
+        world = 4
+
+    sync = PoseidonSync.__new__(PoseidonSync)
+    sync.ctx = _Ctx()
+    fc6 = LayerPlan(5, "fc6", None, B.LAYER_FC, 4096, 9216, 256, B.SCHEME_SFB, B.SCHEME_SFB,
+                    B.choose_scheme(B.LAYER_FC, 4096, 9216, 256, 4)[1])
+    big = LayerPlan(7, "fc8", None, B.LAYER_FC, 21841, 4096, 2048, B.SCHEME_SFPS, B.SCHEME_SFB,
+                    B.choose_scheme(B.LAYER_FC, 21841, 4096, 2048, 4)[1])
+    sync.plans = [fc6, big]
+    d = {x["name"]: x for x in sync.describe()}
+    assert d["fc6"]["scheme"] == "SFB" and d["fc6"]["rule"] == "SFB" and d["fc6"]["model3"] == "SFB"
+    assert d["fc8"]["scheme"] == "SFPS" and d["fc8"]["model3"] == "SFPS"
+    assert d["fc8"]["model_t_sfps_us"] < d["fc8"]["model_t_sfb_us"]
