@@ -128,3 +128,27 @@ def test_measured_cost_model3_against_the_measured_winners():
     assert Bn.choose_scheme_model3(0, 96, 363, 256, 4)[0] == pz.SCHEME_PS
     r, ts, tp, tf = Bn.choose_scheme_model3(1, 4096, 9216, 256, 4)
     assert r == pz.SCHEME_SFB and 0 < ts < tf < tp
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """The boundary is a C ABI: include/poseidon.h compiles as C99 with warnings as errors, and a C program
+    links libposeidon.so and gets the paper's printed decision (P=4, K=256, M=N=4096 -> SFB with
+    C_sfb = 18,874,368 floats) without any C++ or torch on its side."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    src = tmp_path / "abi.c"
+    src.write_text('#include "poseidon.h"\n#include <stdio.h>\n'
+                   "int main(void) { poseidon_costs_t c; int32_t s = poseidon_choose_scheme(POSEIDON_LAYER_FC, "
+                   "4096, 4096, 256, 4, &c);\n"
+                   '  printf("%d %llu\\n", (int)s, (unsigned long long)c.sfb); return 0; }\n')
+    libdir = os.path.join(ROOT, "paper_1512_06216_b200")
+    exe = tmp_path / "abi"
+    r = subprocess.run([gcc, "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        str(src), "-L", libdir, "-lposeidon", f"-Wl,-rpath,{libdir}", "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0 and out.stdout.split() == ["1", "18874368"], out.stdout + out.stderr
