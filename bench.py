@@ -403,6 +403,27 @@ def run_poseidon(args):
                      else f"K1r recon_simt ({top.name})", "kernel_ms": kms,
                      "algorithmic_flops": flops, "algorithmic_bytes": byts,
                      "peak_source": f"{peaks['source']} (tf32 = bf16 sustained x 1.1/2.25)"})
+        if args.recon == "tf32":
+            # context for `frac` (which is the in-step number): the same K1 launch on the same shape ALONE,
+            # after the timed region, each launch queued behind a device spin (device time only)
+            Ug = torch.randn(P, M, ldk, device=dev).mul_(0.01)
+            Vg = torch.randn(P, N, ldk, device=dev).relu_()
+            Wt = torch.zeros(M, N, device=dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ts = []
+            for _ in range(6):
+                torch.cuda._sleep(200_000)
+                e0.record(stream)
+                pz.reconstruct_sgd(Ug, Vg, P, Kf, ldk, M, N, Wt, -1e-3, stream=stream)
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            iso = statistics.median(ts[1:])
+            iso_ach = (flops / (iso / 1e3) / 1e12) if roof["bound"] == "tensor" else (byts / (iso / 1e3) / 1e9)
+            roof.update({"isolated_kernel_ms": iso, "isolated_frac": iso_ach / roof["peak"],
+                         "isolated_note": "same K1 launch alone after the timed region (not part of value); "
+                                          "frac is the in-step number, where DWBP runs K1 beside the backward"})
+            del Ug, Vg, Wt
     else:
         top = max(sync.plans, key=lambda p: p.n)
         kms = statistics.mean(ctx.layer_stats(top.layer_id, a)["kernel_ms"] for a in range(n_stats))
