@@ -245,15 +245,21 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t ctx, int32_t layer_id, 
 /* Staging slot of an SFB / SF-PS layer for poseidon_backprop_hook: library-owned
  * device buffers U [K x M] (*ld_u = M) and V [K x N] (*ld_v = N), row-major,
  * allocated on first call.  The caller writes the factors there (ordered
- * before the hook's stream), then calls poseidon_backprop_hook. */
+ * before the hook's stream), then calls poseidon_backprop_hook.  Errors: ERR_STATE (a PS layer), ERR_CUDA
+ * (allocation). */
 poseidon_status_t poseidon_sfb_slot(poseidon_ctx_t ctx, int32_t layer_id, float** U_slot,
                                     int64_t* ld_u, float** V_slot, int64_t* ld_v);
 
 #define POSEIDON_PS_ZERO_GRAD 0x1u
-/* Bind a PS layer's padded flat buffers (caller-owned, padded_n floats each). */
+/* Bind a PS layer's padded flat buffers: grad and W caller-owned device buffers of padded_n floats each
+ * (poseidon_shard_range), 16-byte aligned, holding W row-major then the bias (n = M*N, + M with bias).
+ * flags: POSEIDON_PS_ZERO_GRAD -> the library zeroes grad (padding included) after each sync.  Errors:
+ * ERR_STATE (unregistered or not a PS layer), ERR_INVALID_ARG (NULL), ERR_ALIGNMENT, ERR_SHAPE (n). */
 poseidon_status_t poseidon_bind_ps_buffers(poseidon_ctx_t ctx, int32_t layer_id, float* grad,
                                            float* W, int64_t n, uint32_t flags);
-/* Bind an SFB / SF-PS layer's parameters (W: M x N, bias: M or NULL). */
+/* Bind an SFB / SF-PS layer's parameters for poseidon_backprop_hook: W caller-owned M x N row-major
+ * device buffer (16-byte aligned), bias M floats or NULL.  Errors: ERR_STATE (a PS layer),
+ * ERR_INVALID_ARG (W NULL, or a bias for a layer registered without one). */
 poseidon_status_t poseidon_bind_sfb_params(poseidon_ctx_t ctx, int32_t layer_id, float* W, float* bias);
 
 /* PS arena (collective over all ranks when world > 1): allocates ONE padded
@@ -287,7 +293,9 @@ int32_t poseidon_sfb_path(poseidon_ctx_t ctx, int32_t layer_id);
 /* Human-readable state of the fused NVLS PS path ("active", "not requested", or the NCCL error). */
 const char* poseidon_nvls_status(poseidon_ctx_t ctx);
 
-poseidon_status_t poseidon_set_lr(poseidon_ctx_t ctx, float lr);           /* lr used by backprop_hook */
+/* lr used by poseidon_backprop_hook from the next hook on (sync_* take theirs as an argument).
+ * ERR_NOT_INITIALIZED for a NULL context. */
+poseidon_status_t poseidon_set_lr(poseidon_ctx_t ctx, float lr);
 
 /* Lambda of Eq. 3 / Alg. 3 line 8, applied once at the aggregation point
  * (oracle O4m):  g = (1/P) sum_p grad_p;  v = mu v + lr (g + weight_decay * w);
@@ -297,6 +305,9 @@ poseidon_status_t poseidon_set_lr(poseidon_ctx_t ctx, float lr);           /* lr
  * rank's shard (the shard owner is the only one that updates it).  layer_id -1 = every registered
  * layer; mu = weight_decay = 0 returns the layer to plain SGD.  0 <= mu < 1, weight_decay >= 0. */
 poseidon_status_t poseidon_set_momentum(poseidon_ctx_t ctx, int32_t layer_id, float mu, float weight_decay);
+/* Reconstruction kernel of a factor layer (POSEIDON_RECON_TF32: K1 on tcgen05, POSEIDON_RECON_FP32: K1r),
+ * layer_id -1 = every layer.  Takes effect at the layer's next pack (the TF32 path rounds the factors when
+ * packing).  Errors: ERR_INVALID_ARG (bad recon), ERR_STATE (unregistered layer). */
 poseidon_status_t poseidon_set_recon(poseidon_ctx_t ctx, int32_t layer_id /* -1: all */, int32_t recon);
 
 /* SSP (POSEIDON_FLAG_SSP1): apply every layer's deferred update now (in layer-id order, identical on
