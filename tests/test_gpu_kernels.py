@@ -251,7 +251,9 @@ def _sampled_rows(M, n=48, seed=0):
 
 @pytest.mark.parametrize("M,N,K,P", [(4096, 9216, 256, 8),     # C3 fc6 at P=8 (bench launch shape x8 rows)
                                      (4096, 9216, 256, 1),     # C3 fc6 at P=1 (bench N=1 launch)
-                                     (21841, 4096, 256, 2)])   # C5 softmax FC (M not a multiple of 4)
+                                     (21841, 4096, 256, 2),    # C5 softmax FC (M not a multiple of 4)
+                                     (21841, 4096, 32, 8),     # C5 sweep: smallest K, P = 8 simulated workers
+                                     (21841, 4096, 2048, 4)])  # C5 sweep: largest K (P*K = 8192)
 def test_sfb_full_size_sampled_rows(pz, M, N, K, P):
     W, b = S.fc_weights_randbias(M, N)
     Us, Vs = S.hidden_factors(M, N, K, P)
