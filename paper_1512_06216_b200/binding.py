@@ -153,11 +153,16 @@ def _check(code: int):
 
 
 def _ptr(t) -> Optional[int]:
-    """Device pointer of a tensor (None -> NULL); ints pass through."""
+    """Device pointer of a tensor (None -> NULL); ints pass through.  The C ABI takes plain row-major fp32
+    pointers, so a tensor must be float32 and contiguous (a strided view would be read as if it were not)."""
     if t is None:
         return None
     if isinstance(t, int):
         return t
+    if getattr(t, "dtype", None) is not None and str(t.dtype) != "torch.float32":
+        raise TypeError(f"libposeidon takes float32 buffers, got {t.dtype}")
+    if hasattr(t, "is_contiguous") and not t.is_contiguous():
+        raise ValueError("libposeidon takes contiguous row-major buffers (call .contiguous())")
     return t.data_ptr()
 
 

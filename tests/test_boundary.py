@@ -152,3 +152,17 @@ def test_header_is_plain_c_and_links(tmp_path):
     assert r.returncode == 0, r.stderr
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
     assert out.returncode == 0 and out.stdout.split() == ["1", "18874368"], out.stdout + out.stderr
+
+
+def test_binding_refuses_buffers_the_abi_would_misread():
+    """The binding only marshals pointers: a strided view or a non-fp32 tensor would be read as contiguous fp32
+    by the library, so it is refused before any call."""
+    import torch
+    from paper_1512_06216_b200 import binding as Bn
+    t = torch.zeros(4, 6)
+    assert Bn._ptr(t) == t.data_ptr() and Bn._ptr(None) is None and Bn._ptr(1234) == 1234
+    assert Bn._ptr(t[1:]) == t[1:].data_ptr()          # a contiguous slice is fine
+    with pytest.raises(ValueError):
+        Bn._ptr(t.t())
+    with pytest.raises(TypeError):
+        Bn._ptr(torch.zeros(4, dtype=torch.float64))
