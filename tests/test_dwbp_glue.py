@@ -80,3 +80,75 @@ def test_describe_reports_rule_and_models():
     assert d["fc6"]["scheme"] == "SFB" and d["fc6"]["rule"] == "SFB" and d["fc6"]["model3"] == "SFB"
     assert d["fc8"]["scheme"] == "SFPS" and d["fc8"]["model3"] == "SFPS"
     assert d["fc8"]["model_t_sfps_us"] < d["fc8"]["model_t_sfb_us"]
+
+
+class _FakeContext:
+    """Stands in for B.Context on the host: records the calls the glue makes, takes the paper's rule for the
+    scheme (no library state, no device)."""
+
+    def __init__(self, flags=0):
+        self.world, self.rank, self.flags = 1, 0, flags
+        self.calls = []
+
+    def set_lr(self, lr):
+        pass
+
+    def register_layer(self, lid, kind, M, N, K, has_bias=True, scheme_override=-1):
+        return scheme_override if scheme_override >= 0 else B.choose_scheme(kind, M, N, K, self.world)[0]
+
+    def set_recon(self, recon, lid=-1):
+        pass
+
+    def bind_sfb_params(self, lid, W, bias):
+        pass
+
+    def bind_ps_buffers(self, lid, grad, W, n, flags=0):
+        pass
+
+    def backprop_hook(self, lid, stream=None):
+        self.calls.append(("sync", lid))
+
+    def sync_fc_sfb(self, lid, U, V, W=None, bias=None, lr=0.0, producer=None):
+        self.calls.append(("sync", lid))
+
+    def sfb_post_input(self, lid, V, stream=None):
+        self.calls.append(("post", lid))
+
+    def wait_layer(self, lid, stream=None):
+        self.calls.append(("wait", lid))
+
+    def iteration_end(self, stream=None, stats=False):
+        self.calls.append(("end", -1))
+
+
+def test_dwbp_hook_order_and_next_forward_barrier(monkeypatch):
+    """Alg. 2 on the host side (SURVEY T4 enqueue order): within one backward every layer's sync is issued
+    exactly once, top layer first (the order the collectives must have on every rank), SFB layers from the
+    layer's own backward (their inputs posted in the forward when early V is on), PS layers once all their
+    gradients have accumulated; the next forward of layer i waits for layer i's sync before it runs."""
+    from drivers.cnn import CifarQuick
+    monkeypatch.setattr(torch.cuda, "current_stream", lambda *a, **k: None)
+    for flags in (0, B.FLAG_EARLY_V):
+        torch.manual_seed(0)
+        model = CifarQuick()
+        ctx = _FakeContext(flags)
+        sync = PoseidonSync(model, ctx, K=4, lr=0.1)
+        ids = [p.layer_id for p in sync.plans]
+        assert [p.name for p in sync.plans] == ["conv1", "conv2", "conv3", "ip1", "ip2"]
+        sfb = [p.layer_id for p in sync.plans if p.scheme == B.SCHEME_SFB]
+        assert sfb == [3, 4]   # the rule at P = 1: the FC layers broadcast their factors
+        for it in range(2):
+            ctx.calls.clear()
+            x, y = torch.rand(4, 3, 32, 32), torch.randint(0, 10, (4,))
+            out = model(x)
+            torch.nn.functional.cross_entropy(out, y).backward()
+            sync.iteration_end()
+            waits = [lid for c, lid in ctx.calls if c == "wait"]
+            posts = [lid for c, lid in ctx.calls if c == "post"]
+            syncs = [lid for c, lid in ctx.calls if c == "sync"]
+            assert waits == ids                         # next-forward barrier, in forward order
+            assert posts == (sfb if flags else [])      # early V: in the forward, SFB layers only
+            assert syncs == ids[::-1]                   # DWBP: top -> bottom, once each
+            first_sync = min(i for i, c in enumerate(ctx.calls) if c[0] == "sync")
+            assert all(i < first_sync for i, c in enumerate(ctx.calls) if c[0] in ("wait", "post"))
+            assert ctx.calls[-1] == ("end", -1)
