@@ -133,8 +133,12 @@ typedef struct {
 
 /* Create a context for this process's GPU.  world must equal topo->world.
  * world > 1 creates an NCCL communicator from topo->nccl_id (collective over
- * all ranks) and requires single-node all-pairs peer access
- * (POSEIDON_ERR_UNSUPPORTED otherwise; there is no other backend). */
+ * all ranks) and requires single-node all-pairs peer access between the GPUs
+ * the ranks actually use (their PCI bus ids are all-gathered through the new
+ * communicator and checked with cudaDeviceCanAccessPeer; a peer GPU not visible
+ * to this process is reached by NCCL through CUDA IPC).  Two ranks on one GPU or
+ * a pair without peer access -> POSEIDON_ERR_UNSUPPORTED (there is no other
+ * backend). */
 poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, poseidon_ctx_t* out);
 
 /* SACP decision, Alg. 3: kind != FC -> PS; FC -> SFB iff
@@ -312,7 +316,9 @@ poseidon_status_t poseidon_set_recon(poseidon_ctx_t ctx, int32_t layer_id /* -1:
 
 /* SSP (POSEIDON_FLAG_SSP1): apply every layer's deferred update now (in layer-id order, identical on
  * every rank: collective).  Call it on all ranks after the last iteration (and before reading the
- * parameters); afterwards poseidon_wait_layer orders a consumer after the updates.  No-op without SSP. */
+ * parameters); afterwards poseidon_wait_layer orders a consumer after the updates.  The flush is an
+ * iteration record of its own: it closes and advances the iteration counter (its statistics are
+ * poseidon_get_iter_stats(ago = 0)), so training may continue after it.  No-op without SSP. */
 poseidon_status_t poseidon_flush(poseidon_ctx_t ctx, poseidon_stream_t stream);
 
 /* Next-forward barrier: `consumer` waits until layer_id's latest sync is done

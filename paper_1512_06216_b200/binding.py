@@ -240,6 +240,7 @@ class Context:
         _check(lib.poseidon_init(world, ctypes.byref(topo), ctypes.byref(h)))
         self.h = h
         self.rank, self.world, self.device, self.flags = rank, world, device, flags
+        self._shapes = {}
 
     def close(self):
         if getattr(self, "h", None):
@@ -256,7 +257,18 @@ class Context:
         out = _i32()
         _check(lib.poseidon_register_layer(self.h, layer_id, kind, M, N, K, int(bool(has_bias)),
                                            scheme_override, ctypes.byref(out)))
+        self._shapes[layer_id] = (M, N, K)
         return out.value
+
+    def _check_factor(self, layer_id, name, t, cols):
+        """The C ABI reads a factor tensor as K rows x `cols` with the registered K: refuse any other shape
+        (a short last batch would make the pack read past the end, a longer one would drop samples)."""
+        if t is None or isinstance(t, int) or layer_id not in self._shapes:
+            return
+        K = self._shapes[layer_id][2]
+        if tuple(t.shape) != (K, cols):
+            raise ValueError(f"layer {layer_id}: {name} must be ({K}, {cols}) = (registered K, "
+                             f"{'M' if name == 'U' else 'N'}), got {tuple(t.shape)}")
 
     def sfb_slot(self, layer_id):
         u, v, lu, lv = _vp(), _vp(), _i64(), _i64()
@@ -308,11 +320,17 @@ class Context:
         _check(lib.poseidon_set_recon(self.h, layer_id, recon))
 
     def sync_fc_sfb(self, layer_id, U, V, W=None, bias=None, lr=0.0, producer=None):
+        if layer_id in self._shapes:
+            M, N, _ = self._shapes[layer_id]
+            self._check_factor(layer_id, "U", U, M)
+            self._check_factor(layer_id, "V", V, N)
         _check(lib.poseidon_sync_fc_sfb(self.h, layer_id, _ptr(U), _ptr(V), _ptr(W), _ptr(bias), float(lr),
                                         _stream(producer)))
 
     def sfb_post_input(self, layer_id, V, stream=None):
         """FLAG_EARLY_V: pack and broadcast the layer input V (K x N, row-major) now (forward time)."""
+        if layer_id in self._shapes:
+            self._check_factor(layer_id, "V", V, self._shapes[layer_id][1])
         _check(lib.poseidon_sfb_post_input(self.h, layer_id, _ptr(V), V.stride(0), _stream(stream)))
 
     def sync_ps(self, layer_id, grad, W, n, lr, producer=None):

@@ -189,6 +189,57 @@ poseidon_status_t check_ctx(poseidon_ctx_t c) {
   return POSEIDON_OK;
 }
 
+// Asynchronous NCCL failures are sticky; they surface at the next wait_layer / iteration_end /
+// get_iter_stats (include/poseidon.h "Errors").  ncclCommGetAsyncError is a host-side flag read.
+poseidon_status_t check_async(poseidon_ctx_t c) {
+  if (!c->comm) return POSEIDON_OK;
+  ncclResult_t async_err = ncclSuccess;
+  if (ncclCommGetAsyncError(c->comm, &async_err) == ncclSuccess && async_err != ncclSuccess &&
+      async_err != ncclInProgress)
+    return fail(POSEIDON_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(async_err));
+  return POSEIDON_OK;
+}
+
+// Single-node all-pairs peer access (NVLink / NVSwitch) between the devices the ranks actually use:
+// every rank's PCI bus id is all-gathered through the new communicator, mapped to this process's device
+// ordinals and checked with cudaDeviceCanAccessPeer.  A peer that is not visible in this process (per-rank
+// CUDA_VISIBLE_DEVICES) cannot be queried here; NCCL reaches it through CUDA IPC.  Two ranks on one GPU
+// are refused.
+poseidon_status_t check_peers(poseidon_ctx_t c) {
+  constexpr int kId = 64;
+  char mine[kId] = {0};
+  CU_TRY(cudaDeviceGetPCIBusId(mine, kId, c->device));
+  char* dbuf = nullptr;
+  CU_TRY(cudaMalloc(&dbuf, (size_t)kId * c->world));
+  std::vector<char> ids((size_t)kId * c->world);
+  cudaError_t ce = cudaMemcpy(dbuf + (size_t)kId * c->rank, mine, kId, cudaMemcpyHostToDevice);
+  ncclResult_t nr = ncclSuccess;
+  if (ce == cudaSuccess) nr = ncclAllGather(dbuf + (size_t)kId * c->rank, dbuf, kId, ncclUint8, c->comm, c->comm_stream);
+  if (ce == cudaSuccess && nr == ncclSuccess) ce = cudaStreamSynchronize(c->comm_stream);
+  if (ce == cudaSuccess && nr == ncclSuccess) ce = cudaMemcpy(ids.data(), dbuf, ids.size(), cudaMemcpyDeviceToHost);
+  cudaFree(dbuf);
+  if (nr != ncclSuccess) return fail(POSEIDON_ERR_NCCL, std::string("peer id all-gather: ") + ncclGetErrorString(nr));
+  if (ce != cudaSuccess) return cuda_fail(ce, "peer id exchange");
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    const char* id = ids.data() + (size_t)kId * q;
+    if (strncmp(id, mine, kId) == 0)
+      return fail(POSEIDON_ERR_UNSUPPORTED, "ranks " + std::to_string(c->rank) + " and " + std::to_string(q) +
+                                                " share GPU " + std::string(mine));
+    int d = -1;
+    if (cudaDeviceGetByPCIBusId(&d, id) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    int ok = 0;
+    CU_TRY(cudaDeviceCanAccessPeer(&ok, c->device, d));
+    if (!ok)
+      return fail(POSEIDON_ERR_UNSUPPORTED, "GPU " + std::string(mine) + " has no peer access to rank " +
+                                                std::to_string(q) + "'s GPU " + std::string(id));
+  }
+  return POSEIDON_OK;
+}
+
 poseidon_status_t check_layer(poseidon_ctx_t c, int32_t id, Layer** out) {
   if (!c) return fail(POSEIDON_ERR_NOT_INITIALIZED, "context is NULL");
   if (id < 0 || id >= MAX_LAYERS) return fail(POSEIDON_ERR_INVALID_ARG, "layer_id out of range [0,4096)");
@@ -785,15 +836,6 @@ poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, 
   if (prop.major != 10)
     return fail(POSEIDON_ERR_UNSUPPORTED, "libposeidon is built for sm_100a (B200); device is sm_" +
                                               std::to_string(prop.major) + std::to_string(prop.minor));
-  if (world > 1 && ndev >= world) {
-    // single-node all-pairs peer access (NVLink/NVSwitch); no other backend
-    for (int d = 0; d < world; ++d) {
-      if (d == topo->device) continue;
-      int ok = 0;
-      CU_TRY(cudaDeviceCanAccessPeer(&ok, topo->device, d));
-      if (!ok) return fail(POSEIDON_ERR_UNSUPPORTED, "GPUs are not all-pairs peer connected");
-    }
-  }
   if ((topo->flags & POSEIDON_FLAG_SSP1) && (topo->flags & POSEIDON_FLAG_DWBP_OFF))
     return fail(POSEIDON_ERR_INVALID_ARG, "FLAG_SSP1 needs DWBP (the stale update is applied at the next hook)");
   if ((topo->flags & POSEIDON_FLAG_EARLY_V) && (topo->flags & (POSEIDON_FLAG_SSP1 | POSEIDON_FLAG_DWBP_OFF)))
@@ -833,6 +875,12 @@ poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, 
     if (r != ncclSuccess) {
       delete c;
       return fail(POSEIDON_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    poseidon_status_t pst = check_peers(c);
+    if (pst != POSEIDON_OK) {
+      ncclCommDestroy(c->comm);
+      delete c;
+      return pst;
     }
   }
   *out = c;
@@ -1444,6 +1492,11 @@ poseidon_status_t poseidon_flush(poseidon_ctx_t c, poseidon_stream_t stream) {
     L.last_iter = c->iter;
     r.layers.push_back(id);
   }
+  // the flush is an iteration of its own (its events live in ring slot c->iter): close and advance,
+  // so hooks that follow a flush record into a fresh slot and the statistics never count a sync twice
+  CU_TRY(cudaEventRecord(r.bwd_end, s));
+  r.closed = true;
+  c->iter += 1;
   return POSEIDON_OK;
 }
 
@@ -1451,6 +1504,7 @@ poseidon_status_t poseidon_wait_layer(poseidon_ctx_t c, int32_t id, poseidon_str
   Layer* L;
   poseidon_status_t st = check_layer(c, id, &L);
   if (st) return st;
+  if ((st = check_async(c)) != POSEIDON_OK) return st;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(consumer);
   if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
     // traditional BP (Fig. dwbp (a)): the next iteration waits for every layer
@@ -1467,6 +1521,7 @@ poseidon_status_t poseidon_wait_layer(poseidon_ctx_t c, int32_t id, poseidon_str
 poseidon_status_t poseidon_iteration_end(poseidon_ctx_t c, poseidon_stream_t compute, poseidon_iter_stats_t* out) {
   poseidon_status_t st = check_ctx(c);
   if (st) return st;
+  if ((st = check_async(c)) != POSEIDON_OK) return st;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(compute);
   IterRecord& r = open_record(c);
   CU_TRY(cudaEventRecord(r.bwd_end, cs));
@@ -1520,10 +1575,7 @@ poseidon_status_t poseidon_get_iter_stats(poseidon_ctx_t c, int32_t ago, poseido
   out->nccl_bytes_recv = r.recv;
   out->n_layers = (int32_t)r.layers.size();
   out->iteration = (int32_t)it;
-  ncclResult_t async_err = ncclSuccess;
-  if (c->comm && ncclCommGetAsyncError(c->comm, &async_err) == ncclSuccess && async_err != ncclSuccess)
-    return fail(POSEIDON_ERR_NCCL, std::string("NCCL async error: ") + ncclGetErrorString(async_err));
-  return POSEIDON_OK;
+  return check_async(c);
 }
 
 poseidon_status_t poseidon_get_layer_stats(poseidon_ctx_t c, int32_t ago, int32_t id, poseidon_layer_stats_t* out) {

@@ -32,6 +32,18 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
   return r;
 }
 
+// Coherent streaming load for the kZero variant, whose gradient buffer is cleared by the same kernel:
+// no .nc (the read-only path may not alias a buffer the kernel writes) and a memory clobber, so the
+// compiler keeps every clear store after the loads.
+__device__ __forceinline__ float4 ld_stream_rw(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+
 __device__ __forceinline__ void warp_stats_flush(float sq, float bad, float* stats) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -61,15 +73,17 @@ __device__ __forceinline__ void warp_stats_flush(float sq, float bad, float* sta
 // One pass, no grid-stride loop: each thread owns 4 float4 (16 elements) spaced a block apart, all
 // loads issued before any use (8 x 16 B in flight per thread), grid = ceil(n / 4096).
 // kZero (PS_ZERO_GRAD): the kernel also clears the layer's whole padded gradient buffer zbase[0, zpad)
-// for the next iteration's accumulation — each thread zeroes the shard elements it has read, and the
-// grid-strided rest covers [0, zb) and [ze, zpad) — which saves the separate memset launch.
+// for the next iteration's accumulation — each thread zeroes the shard elements it has read (through
+// the same pointer, after its coherent loads), and the grid-strided rest covers [0, zb) and [ze, zpad)
+// — which saves the separate memset launch.  g aliases zbase + zb there, so g is neither __restrict__
+// nor read through the non-coherent path.
 template <bool kStats, bool kZero>
-__global__ void __launch_bounds__(256) ps_shard_sgd_kernel(const float* __restrict__ g, float* __restrict__ W,
-                                                            int64_t count, float alpha, float* stats,
-                                                            float* zbase, int64_t zb, int64_t ze, int64_t zpad) {
+__global__ void __launch_bounds__(256) ps_shard_sgd_kernel(float* g, float* __restrict__ W, int64_t count,
+                                                            float alpha, float* stats, float* zbase, int64_t zb,
+                                                            int64_t ze, int64_t zpad) {
   constexpr int U = 4;
   const int64_t n4 = count >> 2;
-  const float4* g4 = reinterpret_cast<const float4*>(g);
+  float4* g4 = reinterpret_cast<float4*>(g);
   float4* W4 = reinterpret_cast<float4*>(W);
   const int64_t base = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x;
   float4 a[U], w[U];
@@ -77,16 +91,15 @@ __global__ void __launch_bounds__(256) ps_shard_sgd_kernel(const float* __restri
   for (int j = 0; j < U; ++j) {
     const int64_t i = base + (int64_t)j * blockDim.x;
     if (i < n4) {
-      a[j] = ld_stream(g4 + i);
+      a[j] = kZero ? ld_stream_rw(g4 + i) : ld_stream(g4 + i);
       w[j] = W4[i];
     }
   }
   if (kZero) {
-    float4* gz4 = reinterpret_cast<float4*>(zbase + zb);
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const int64_t i = base + (int64_t)j * blockDim.x;
-      if (i < n4) gz4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < n4) g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
   float sq = 0.f, bad = 0.f;
@@ -108,10 +121,10 @@ __global__ void __launch_bounds__(256) ps_shard_sgd_kernel(const float* __restri
   // scalar tail (count % 4), block 0
   if (blockIdx.x == 0 && threadIdx.x < (count & 3)) {
     const int64_t t = (n4 << 2) + threadIdx.x;
-    const float gt = g[t];
+    const float gt = kZero ? *static_cast<volatile float*>(g + t) : g[t];
     const float u = alpha * gt;
     W[t] = fmaf(alpha, gt, W[t]);
-    if (kZero) zbase[zb + t] = 0.f;
+    if (kZero) g[t] = 0.f;
     if (kStats) { sq = fmaf(u, u, sq); bad += isfinite(u) ? 0.f : 1.f; }
   }
   if (kZero) {
@@ -205,9 +218,11 @@ cudaError_t launch_ps_shard_update(const float* g, float* W, int64_t count, floa
     const int64_t blocks = n4 > 0 ? (n4 + per_block - 1) / per_block : 1;
     const dim3 grid((unsigned)blocks);
     if (stats)
-      ps_shard_sgd_kernel<true, false><<<grid, threads, 0, s>>>(g, W, count, alpha, stats, nullptr, 0, 0, 0);
+      ps_shard_sgd_kernel<true, false><<<grid, threads, 0, s>>>(const_cast<float*>(g), W, count, alpha, stats,
+                                                                nullptr, 0, 0, 0);
     else
-      ps_shard_sgd_kernel<false, false><<<grid, threads, 0, s>>>(g, W, count, alpha, nullptr, nullptr, 0, 0, 0);
+      ps_shard_sgd_kernel<false, false><<<grid, threads, 0, s>>>(const_cast<float*>(g), W, count, alpha, nullptr,
+                                                                 nullptr, 0, 0, 0);
   }
   g_launches.fetch_add(1);
   return cudaGetLastError();

@@ -13,6 +13,13 @@
 //   3. LSA barrier: all ranks' stores landed and all reads of the local
 //      gradient are done; the local gradient buffer is then zeroed for the
 //      next iteration's accumulation.
+// LSA barrier j only pairs block j of every rank, so block j may clear only the
+// gradient elements that block j of every rank has reduced: for each owner q the
+// shard-relative float4 indices i with (i mod stride) / 256 == j, at q*S + 4i
+// (the owner's scalar tail is reduced by the block that owns its float4 index).
+// Clearing any other element could run before the owning block of another rank
+// has reduced it (the round-1 race; tests/mp_sync_check.py check 10 exposes it
+// with the in-kernel fuzz below).
 // Buffers live in NCCL symmetric windows (ncclMemAlloc +
 // ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC)); pointers come from the NCCL
 // device API (ncclGetLsaMultimemPointer / ncclGetLocalPointer).
@@ -63,13 +70,33 @@ __device__ __forceinline__ float nvls_update(float w, float g, float alpha, cons
   return w - v;
 }
 
+// Ordering fuzz inside the kernel (test aid, POSEIDON_FUZZ_US): after the entry barrier each CTA sleeps a
+// pseudo-random time below fuzz_ns, so CTAs of different ranks (and of one rank) reach their reads in
+// arbitrary order, as they do when DWBP schedules them around the backward's kernels.
+__device__ __forceinline__ void cta_fuzz(uint32_t fuzz_ns, uint32_t seed, int rank) {
+  if (fuzz_ns == 0) return;
+  if (threadIdx.x == 0) {
+    uint32_t h = seed * 0x9E3779B1u ^ (blockIdx.x * 0x85EBCA77u) ^ ((uint32_t)rank * 0xC2B2AE3Du);
+    h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+    uint32_t left = h % fuzz_ns;
+    while (left > 0) {
+      const uint32_t step = left > 1000u ? 1000u : left;
+      __nanosleep(step);
+      left -= step;
+    }
+  }
+  __syncthreads();
+}
+
 template <int U>
 __global__ void __launch_bounds__(256) ps_nvls_kernel(const __grid_constant__ ncclDevComm comm, ncclWindow_t wg,
                                                       ncclWindow_t ww, size_t off_g, size_t off_w, int64_t b,
-                                                      int64_t e, int64_t padded, float alpha, int zero_grad,
-                                                      NvlsMomentum mom) {
+                                                      int64_t e, int64_t shard, int nranks, float alpha,
+                                                      int zero_grad, NvlsMomentum mom, uint32_t fuzz_ns,
+                                                      uint32_t fuzz_seed) {
   ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamTagLsa(), blockIdx.x, /*multimem=*/true);
   bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  cta_fuzz(fuzz_ns, fuzz_seed, ncclTeamLsa(comm).rank);
 
   const float* gmc = static_cast<const float*>(ncclGetLsaMultimemPointer(wg, off_g, comm));
   float* wmc = static_cast<float*>(ncclGetLsaMultimemPointer(ww, off_w, comm));
@@ -101,16 +128,20 @@ __global__ void __launch_bounds__(256) ps_nvls_kernel(const __grid_constant__ nc
       }
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x < ((e - b) & 3)) {
+  // scalar tail (e - b) % 4: reduced by the block that owns float4 index n4 (the block that clears it)
+  if (blockIdx.x == (unsigned)((n4 % stride) / blockDim.x) && threadIdx.x < ((e - b) & 3)) {
     const int64_t k = b + 4 * n4 + threadIdx.x;
     mm_st(wmc + k, nvls_update(wloc[k], mm_ld_reduce(gmc + k), alpha, mom, k - b));
   }
 
   bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
   if (zero_grad) {
+    // exactly the float4 indices block j of every rank reduced, in every owner's shard
     float4* gl = static_cast<float4*>(ncclGetLocalPointer(wg, off_g));
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (padded >> 2); i += stride) gl[i] = z;
+    const int64_t s4 = shard >> 2;   // S is a multiple of 32
+    for (int q = 0; q < nranks; ++q)
+      for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s4; i += stride) gl[q * s4 + i] = z;
   }
 }
 
@@ -127,9 +158,11 @@ struct BcastSeg {
 // P2P = true: plain st.global of the same 16 B into each peer's window copy over NVLink (P-1 stores)
 template <int U, bool P2P>
 __global__ void __launch_bounds__(256) sfb_bcast_kernel(const __grid_constant__ ncclDevComm comm, ncclWindow_t win,
-                                                        BcastSeg s0, BcastSeg s1, BcastSeg s2) {
+                                                        BcastSeg s0, BcastSeg s1, BcastSeg s2, uint32_t fuzz_ns,
+                                                        uint32_t fuzz_seed) {
   ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamTagLsa(), blockIdx.x, /*multimem=*/true);
   bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  cta_fuzz(fuzz_ns, fuzz_seed, ncclTeamLsa(comm).rank);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const BcastSeg segs[3] = {s0, s1, s2};
 #pragma unroll 1
@@ -198,12 +231,26 @@ struct NvlsState {
   bool dev_ok = false;
 };
 
+// POSEIDON_FUZZ_US (test aid): in-kernel CTA fuzz bound in ns, and a per-launch seed
+static uint32_t fuzz_bound_ns() {
+  static const uint32_t ns = [] {
+    const char* v = getenv("POSEIDON_FUZZ_US");
+    return v ? (uint32_t)(atof(v) * 1000.0) : 0u;
+  }();
+  return ns;
+}
+static uint32_t next_fuzz_seed() {
+  static uint32_t seed = 0;
+  return ++seed;
+}
+
 cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww, size_t off_g, size_t off_w,
                            int64_t b, int64_t e, int64_t padded, float alpha, bool zero_grad, int max_blocks,
                            int64_t shard, float* vel, float inv_p, float lr, float mu, float wd, cudaStream_t s) {
   // The grid must be identical on every rank (block j of every rank meets at LSA barrier j), so it
   // is sized from the shard size S, not from this rank's (possibly shorter or empty) range.
-  (void)e;
+  const int nranks = ncclTeamLsa(st->dev).nRanks;
+  if (padded != shard * nranks || (shard & 31) != 0) return cudaErrorInvalidValue;
   const int64_t n4 = (shard + 3) / 4;
   static const int env_grid = [] {
     const char* v = getenv("POSEIDON_NVLS_GRID");
@@ -221,12 +268,14 @@ cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww
   if (blocks < 1) blocks = 1;
   if (blocks > max_blocks) blocks = max_blocks;
   NvlsMomentum mom{vel, inv_p, lr, mu, wd};
+  const uint32_t fz = fuzz_bound_ns(), seed = fz ? next_fuzz_seed() : 0u;
+  const int zg = zero_grad ? 1 : 0;
   if (env_u == 8)
-    ps_nvls_kernel<8><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, padded, alpha, zero_grad ? 1 : 0, mom);
+    ps_nvls_kernel<8><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, shard, nranks, alpha, zg, mom, fz, seed);
   else if (env_u == 2)
-    ps_nvls_kernel<2><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, padded, alpha, zero_grad ? 1 : 0, mom);
+    ps_nvls_kernel<2><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, shard, nranks, alpha, zg, mom, fz, seed);
   else
-    ps_nvls_kernel<4><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, padded, alpha, zero_grad ? 1 : 0, mom);
+    ps_nvls_kernel<4><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, shard, nranks, alpha, zg, mom, fz, seed);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }
@@ -254,12 +303,13 @@ cudaError_t launch_sfb_bcast_nvls(const NvlsState* st, ncclWindow_t win, size_t 
   int cap = env_grid > 0 ? env_grid : (p2p ? (nranks > 4 ? 64 : 32) : max_blocks);
   if (cap < max_blocks) max_blocks = cap;
   if (blocks > max_blocks) blocks = max_blocks;
+  const uint32_t fz = fuzz_bound_ns(), seed = fz ? next_fuzz_seed() : 0u;
   if (p2p)
     sfb_bcast_kernel<4, true><<<blocks, 256, 0, s>>>(st->dev, win, BcastSeg{off_u, n_u}, BcastSeg{off_v, n_v},
-                                                     BcastSeg{off_b, n_b});
+                                                     BcastSeg{off_b, n_b}, fz, seed);
   else
     sfb_bcast_kernel<4, false><<<blocks, 256, 0, s>>>(st->dev, win, BcastSeg{off_u, n_u}, BcastSeg{off_v, n_v},
-                                                      BcastSeg{off_b, n_b});
+                                                      BcastSeg{off_b, n_b}, fz, seed);
   g_launches.fetch_add(1);
   return cudaGetLastError();
 }

@@ -69,6 +69,11 @@ class SFBLinearFunction(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, weight, bias, plan, sync, post_input):
+        if x.dim() != 2 or x.shape[0] != plan.K or x.shape[1] != plan.N:
+            # the sufficient factors are K x N inputs and K x M error messages with the K the layer was
+            # registered with: a partial batch or a >2-D input would be misread by the library
+            raise ValueError(f"SFB layer {plan.name}: input must be ({plan.K}, {plan.N}) (registered per-GPU "
+                             f"batch K, in_features), got {tuple(x.shape)}")
         if post_input:
             # FLAG_EARLY_V: the input factors V = a_i are final now; their broadcast overlaps the rest of
             # the forward and the backward (the hook then moves only U)

@@ -22,6 +22,10 @@ Checks, at world = P:
   6. SSP, staleness 1: SFB + PS over 4 iterations and a flush, integer variant bit-exact vs O10 on
      the NCCL and the NVLS paths.
   7. PS buckets: six layers of mixed sizes, NCCL and fused NVLS paths, integer bit-exact per layer.
+  10. Fused NVLS PS zero-grad ordering: the five C3 conv layers' sizes (shard starts not aligned to the
+     kernel's grid stride, several CTAs per layer), four iterations of integer gradients through the
+     DWBP hook, bit-exact vs O6 every iteration.  Run with POSEIDON_FUZZ_US set, every CTA sleeps a
+     pseudo-random time after the entry barrier (`--race-only` runs just this check).
   5. Full size in bench.py's N > 1 configuration: C3 fc6 SFB through the library's broadcast kernel (sampled
      rows vs O4)
      and a 37.7M-parameter PS layer through the fused NVLS kernel (sampled elements vs O6).
@@ -51,6 +55,59 @@ def allsame(t):
     return all(torch.equal(parts[0], p) for p in parts[1:])
 
 
+def nvls_race_check(new_ctx, rank, P, dev):
+    """Check 10: every CTA of the fused NVLS PS kernel may clear only what the same-index CTAs of all
+    ranks reduced (LSA barrier j pairs block j only).  C3 conv layer sizes; 4 iterations."""
+    from paper_1512_06216_b200.binding import device_view
+    cr = new_ctx(pz.FLAG_NVLS_PS)
+    shapes = [(96, 363), (256, 1200), (384, 2304), (384, 1728), (256, 1728)]   # conv1..conv5 (M, C*kh*kw)
+    for lid, (M_, N_) in enumerate(shapes):
+        cr.register_layer(lid, pz.LAYER_CONV, M_, N_, 1, True, pz.SCHEME_PS)
+    lr = 2.0 ** -7
+    cr.set_lr(lr)
+    cr.ps_arena()
+    status = cr.nvls_status()
+    views, ws = [], []
+    for lid, (M_, N_) in enumerate(shapes):
+        n = M_ * N_ + M_
+        gp, wp, padded = cr.ps_layer_buffers(lid)
+        wv, gv = device_view(wp, (padded,)), device_view(gp, (padded,))
+        w0 = (S.rng(1000 + lid).integers(-1023, 1024, size=n) * 2.0 ** -10).astype(np.float32)
+        wv[:n] = torch.from_numpy(w0).to(dev)
+        views.append((wv, gv, n))
+        ws.append(w0.astype(np.float64))
+    bad = 0
+    for it in range(4):
+        refs = []
+        for lid, (wv, gv, n) in enumerate(views):
+            grads = S.integer_grads(n, P, seed=2000 + 10 * it + lid)
+            gv[:n] = torch.from_numpy(grads[rank]).to(dev)
+            refs.append(O.ps_step_flat(ws[lid], grads, lr))
+        torch.cuda.synchronize()
+        dist.barrier()
+        for lid in reversed(range(len(shapes))):
+            cr.backprop_hook(lid, torch.cuda.current_stream())
+        for lid in range(len(shapes)):
+            cr.wait_layer(lid)
+        cr.iteration_end()
+        torch.cuda.synchronize()
+        for lid, ((wv, gv, n), ref) in enumerate(zip(views, refs)):
+            out = wv[:n].cpu().numpy().astype(np.float64)
+            nbad = int(np.count_nonzero(out != ref))
+            if nbad:
+                print(f"[rank {rank}] NVLS race check: iteration {it} layer {lid}: {nbad} of {n} elements "
+                      f"differ from O6", flush=True)
+            bad += nbad
+            assert float(gv.abs().sum()) == 0.0, "gradient not cleared"
+            assert allsame(wv[:n].contiguous())
+            ws[lid] = ref
+    cr.close()
+    assert bad == 0, f"fused NVLS PS lost gradient contributions ({bad} elements, {status})"
+    if rank == 0:
+        print(f"NVLS race check ok ({status}, POSEIDON_FUZZ_US={os.environ.get('POSEIDON_FUZZ_US', '0')})",
+              flush=True)
+
+
 def main():
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -67,6 +124,14 @@ def main():
         obj = [pz.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         return pz.Context(rank=rank, world=world, device=local, nccl_id=obj[0], flags=flags)
+
+    if "--race-only" in sys.argv:
+        nvls_race_check(new_ctx, rank, P, dev)
+        dist.barrier()
+        print(f"MP_OK {rank}", flush=True)
+        dist.destroy_process_group()
+        return
+    nvls_race_check(new_ctx, rank, P, dev)
 
     ctx = new_ctx()
     M, N, K = 128, 256, 8

@@ -152,3 +152,25 @@ def test_dwbp_hook_order_and_next_forward_barrier(monkeypatch):
             first_sync = min(i for i, c in enumerate(ctx.calls) if c[0] == "sync")
             assert all(i < first_sync for i, c in enumerate(ctx.calls) if c[0] in ("wait", "post"))
             assert ctx.calls[-1] == ("end", -1)
+
+
+@pytest.mark.parametrize("shape", [(4, 6), (6, 6), (5, 7), (5, 2, 3)])
+def test_sfb_layer_refuses_batch_other_than_registered_K(wrapped, shape):
+    """the library reads the factors with the registered K; a partial last batch, a
+    larger batch or a >2-D input must fail loudly before anything reaches the C ABI."""
+    mod, sync = wrapped
+    with pytest.raises(ValueError, match="registered per-GPU batch K"):
+        mod(torch.randn(*shape, requires_grad=True))
+    assert sync.ctx.posted == [] and sync.ctx.synced == []
+
+
+def test_binding_refuses_factor_shapes_other_than_registered():
+    """The binding's factor check (argument marshalling: shapes against the registration) runs before
+    the C call; a context stand-in carries the registered (M, N, K)."""
+    c = B.Context.__new__(B.Context)
+    c._shapes = {0: (4, 6, 5)}
+    c._check_factor(0, "U", torch.zeros(5, 4), 4)
+    c._check_factor(0, "V", torch.zeros(5, 6), 6)
+    for bad in [(4, 4), (5, 5), (6, 4), (5, 2, 2)]:
+        with pytest.raises(ValueError, match="registered K"):
+            c._check_factor(0, "U", torch.zeros(*bad), 4)
