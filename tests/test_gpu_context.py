@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from parity import check_update
 import synthetic as S
 
 torch = pytest.importorskip("torch")
@@ -107,11 +108,11 @@ def test_context_sfb_and_ps_world1(pz):
     st = ctx.iteration_end(stats=True)
     assert st["n_layers"] == 2 and st["nccl_bytes_sent"] == 0
     W1, b1 = O.sync_step(W, b, Us, Vs, lr)
-    assert O.update_error_fp32(W, host(Wd), W1) <= 2e-3
-    assert O.update_error_fp32(b, host(bd), b1) <= 1e-5
+    check_update(W, host(Wd), W1, 2e-3)
+    check_update(b, host(bd), b1, 1e-5)
     out = host(flatW)
-    assert O.update_error_fp32(W, out[:M * N].reshape(M, N), W1) <= 1e-5
-    assert O.update_error_fp32(b, out[M * N:n], b1) <= 1e-5
+    check_update(W, out[:M * N].reshape(M, N), W1, 1e-5)
+    check_update(b, out[M * N:n], b1, 1e-5)
     assert np.all(host(flatG) == 0)  # PS_ZERO_GRAD
     ls = ctx.layer_stats(0)
     assert ls["launched"] == 1 and ls["kernel_ms"] > 0
@@ -139,8 +140,8 @@ def test_context_hook_slot_path_and_dwbp_off(pz):
         assert st["n_layers"] == 1
         ctx.wait_layer(3)
         W1, b1 = O.sync_step(W, b, Us, Vs, 0.1)
-        assert O.update_error_fp32(W, host(Wd), W1) <= 2e-3
-        assert O.update_error_fp32(b, host(bd), b1) <= 1e-5
+        check_update(W, host(Wd), W1, 2e-3)
+        check_update(b, host(bd), b1, 1e-5)
         ctx.close()
 
 

@@ -9,6 +9,7 @@ import pytest
 
 import oracle as O
 import synthetic as S
+from parity import check_update, w0_like
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -49,8 +50,8 @@ def test_k2_integer_bit_exact(pz, count):
 
 def test_k2_unaligned_and_random(pz):
     n = 100_001
-    W = S.dense_grads(n + 1, 1, seed=5, scale=1.0)[0]
     gr = S.dense_grads(n + 1, 1, seed=6)[0]
+    W = w0_like(S.dense_grads(n + 1, 1, seed=5, scale=1.0)[0], 0.01 * gr)
     Wd, gd = dev(W), dev(gr)
     # offset by one float -> not 16-byte aligned -> scalar path
     pz.ps_shard_update(gd[1:], Wd[1:], n, -0.01)
@@ -58,7 +59,7 @@ def test_k2_unaligned_and_random(pz):
     ref = W.astype(np.float64)
     ref[1:] += -0.01 * gr[1:].astype(np.float64)
     assert out[0] == W[0]
-    assert O.update_error_fp32(W, out, ref) <= TOL_FP32
+    check_update(W, out, ref, TOL_FP32)
 
 
 def test_k2_stats_warp_reduction(pz):
@@ -104,23 +105,23 @@ def test_ps_simulated_integer_bit_exact(pz, n, P):
     if P in (1, 2, 4, 8):
         assert np.array_equal(out[:n].astype(np.float64), ref)
     else:
-        assert O.update_error_fp32(W[:n], out[:n], ref) <= TOL_FP32
+        check_update(W[:n], out[:n], ref, TOL_FP32)
     assert np.array_equal(out[n:], W[n:])  # padding untouched
 
 
 def test_ps_simulated_random(pz):
     n, P = 1_000_000, 8
     _, _, padded = O.shard_range(n, P, 0)
-    W = np.zeros(padded, np.float32)
-    W[:n] = S.dense_grads(n, 1, seed=1, scale=0.05)[0]
     grads = np.zeros((P, padded), np.float32)
     for p, gp in enumerate(S.dense_grads(n, P, seed=2)):
         grads[p, :n] = gp
+    W = np.zeros(padded, np.float32)
+    W[:n] = w0_like(S.dense_grads(n, 1, seed=1, scale=0.05)[0], 0.01 / P * grads[:, :n].sum(0, dtype=np.float64))
     Wd = dev(W)
     pz.ps_simulated(dev(grads), P, Wd, n, 0.01)
     out = host(Wd)
     ref = O.ps_step_flat(W[:n], [grads[p, :n] for p in range(P)], 0.01)
-    assert O.update_error_fp32(W[:n], out[:n], ref) <= TOL_FP32
+    check_update(W[:n], out[:n], ref, TOL_FP32)
 
 
 # -------------------------------------------------------- SFB simulated ----
@@ -147,9 +148,9 @@ def test_sfb_simulated_vs_oracle(pz, recon, M, N, K, P):
                      recon=pz.RECON_FP32 if recon == "fp32" else pz.RECON_TF32)
     W1, b1 = O.sync_step(W, b, Us, Vs, lr)
     tol = TOL_FP32 if recon == "fp32" else TOL_TF32
-    assert O.update_error_fp32(W, host(Wd), W1) <= tol
+    check_update(W, host(Wd), W1, tol)
     # the bias uses the unrounded fp32 column sums on both paths
-    assert O.update_error_fp32(b, host(bd), b1) <= TOL_FP32
+    check_update(b, host(bd), b1, TOL_FP32)
 
 
 @pytest.mark.parametrize("recon", ["fp32", "tf32"])
@@ -186,9 +187,9 @@ def test_sfb_sfb_equals_ps_on_same_layer(pz):
     W1, _ = O.sync_step(W, None, Us, Vs, lr)
     sfb_out = host(Wd)
     ps_out = host(Wpsd)[:n].reshape(M, N)
-    assert O.update_error_fp32(W, sfb_out, W1) <= TOL_TF32
-    assert O.update_error_fp32(W, ps_out, W1) <= TOL_FP32
-    assert O.update_error_fp32(W, sfb_out, ps_out) <= TOL_TF32
+    check_update(W, sfb_out, W1, TOL_TF32)
+    check_update(W, ps_out, W1, TOL_FP32)
+    check_update(W, sfb_out, ps_out, TOL_TF32)
 
 
 def test_reconstruct_zero_rows_noop(pz):
@@ -263,7 +264,7 @@ def test_sfb_full_size_sampled_rows(pz, M, N, K, P):
     out, outb = host(Wd), host(bd)
     rows = _sampled_rows(M)
     W1r, b1r = O.sync_step_rows(W[rows], b[rows], Us, Vs, lr, rows)
-    assert O.update_error_fp32(W[rows], out[rows], W1r) <= TOL_TF32
-    assert O.update_error_fp32(b[rows], outb[rows], b1r) <= TOL_FP32
+    check_update(W[rows], out[rows], W1r, TOL_TF32)
+    check_update(b[rows], outb[rows], b1r, TOL_FP32)
     # property at any size: rows never sampled still moved only where factors are non-zero
     assert np.all(np.isfinite(out))

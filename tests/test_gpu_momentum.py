@@ -4,6 +4,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from parity import check_update
 import synthetic as S
 
 torch = pytest.importorskip("torch")
@@ -40,8 +41,8 @@ def test_sfb_momentum_three_steps(pz, recon, tol):
         ctx.iteration_end()
         Wr, br, VW, Vb = O.sync_step_momentum(Wr, br, VW, Vb, Us, Vs, lr, mu, wd)
     torch.cuda.synchronize()
-    assert O.update_error_fp32(W, Wd.cpu().numpy(), Wr) <= tol
-    assert O.update_error_fp32(b, bd.cpu().numpy(), br) <= 1e-5
+    check_update(W, Wd.cpu().numpy(), Wr, tol)
+    check_update(b, bd.cpu().numpy(), br, 1e-5)
     # and switching back to plain SGD frees the velocity and follows O4
     ctx.set_momentum(0.0, 0.0, 0)
     W0 = Wd.cpu().numpy()
@@ -50,7 +51,7 @@ def test_sfb_momentum_three_steps(pz, recon, tol):
     ctx.wait_layer(0)
     W1, _ = O.sync_step(W0, None, Us, Vs, lr)
     torch.cuda.synchronize()
-    assert O.update_error_fp32(W0, Wd.cpu().numpy(), W1) <= tol
+    check_update(W0, Wd.cpu().numpy(), W1, tol)
     ctx.close()
 
 
@@ -76,7 +77,7 @@ def test_ps_momentum_three_steps(pz):
         ctx.iteration_end()
         wr, vr = O.ps_step_flat_momentum(wr, vr, [g], lr, mu, wd)
     torch.cuda.synchronize()
-    assert O.update_error_fp32(w0, wflat[:n].cpu().numpy(), wr) <= 1e-5
+    check_update(w0, wflat[:n].cpu().numpy(), wr, 1e-5)
     ctx.close()
 
 

@@ -417,6 +417,73 @@ def test_o4m_ps_equals_definition():
 
 
 
+def _brute_mean_grad(Us, Vs):
+    """(1/P) sum_p sum_k u_k v_k^T and (1/P) sum_p sum_k u_k in exact rationals, element by element."""
+    P, K, M, N = len(Us), Us[0].shape[0], Us[0].shape[1], Vs[0].shape[1]
+    G = [[Fraction(0)] * N for _ in range(M)]
+    gb = [Fraction(0)] * M
+    for p in range(P):
+        for k in range(K):
+            for m in range(M):
+                u = Fraction(float(Us[p][k, m]))
+                gb[m] += u / P
+                for n in range(N):
+                    G[m][n] += u * Fraction(float(Vs[p][k, n])) / P
+    return G, gb
+
+
+def test_o4m_two_steps_momentum_and_decay_closed_form():
+    """mu != 0 AND wd != 0 (pins with only one of them non-zero let a decoupled-decay
+    oracle pass).  Caffe's coupled rule v = mu v + lr (g + wd w), w -= v (P:L141 Lambda, reading Z4b),
+    written out by hand for two steps from v_0 = 0:
+        w_1 = (1 - lr wd) w_0 - lr g_1
+        w_2 = (1 - lr wd)^2 w_0 - (1 - lr wd) lr g_1 - lr g_2 - mu lr (g_1 + wd w_0)
+    A decoupled rule (w -= mu v + lr g + lr wd w) gives the same w_1 but lacks the -mu lr wd w_0 term
+    in w_2.  Dyadic inputs make the fp64 oracle exact, so equality is exact."""
+    M, N, K, P = 3, 4, 2, 2
+    W0, b0, _, _, _ = S.integer_factors(M, N, K, P, seed=31)
+    steps = [S.integer_factors(M, N, K, P, seed=32 + t)[2:4] for t in range(2)]
+    lr, mu, wd = Fraction(1, 8), Fraction(1, 2), Fraction(1, 4)
+    w = [[Fraction(float(W0[m, n])) for n in range(N)] for m in range(M)]
+    bb = [Fraction(float(b0[m])) for m in range(M)]
+    (G1, gb1), (G2, gb2) = (_brute_mean_grad(Us, Vs) for Us, Vs in steps)
+    a = 1 - lr * wd
+
+    def two_steps(w0, g1, g2):
+        return a * a * w0 - a * lr * g1 - lr * g2 - mu * lr * (g1 + wd * w0)
+
+    Wt, bt = W0.astype(np.float64), b0.astype(np.float64)
+    VW, Vb = np.zeros_like(Wt), np.zeros_like(bt)
+    for Us, Vs in steps:
+        Wt, bt, VW, Vb = O.sync_step_momentum(Wt, bt, VW, Vb, Us, Vs, float(lr), float(mu), float(wd))
+    for m in range(M):
+        assert bt[m] == float(two_steps(bb[m], gb1[m], gb2[m]))
+        for n in range(N):
+            assert Wt[m, n] == float(two_steps(w[m][n], G1[m][n], G2[m][n]))
+    # the decoupled variant differs by exactly mu lr wd w_0 (so this pin can tell them apart)
+    assert any(mu * lr * wd * w[m][n] != 0 for m in range(M) for n in range(N))
+    # the PS form with shard-owned velocities gives the same two steps
+    n_ = M * N + M
+    wf, vf = O.flatten_params(W0, b0), np.zeros(n_)
+    for Us, Vs in steps:
+        grads = [O.flatten_params(O.reconstruct(u, v), np.asarray(u, np.float64).sum(0)) for u, v in zip(Us, Vs)]
+        wf, vf = O.ps_step_flat_momentum(wf, vf, grads, float(lr), float(mu), float(wd))
+    assert np.array_equal(wf, O.flatten_params(Wt, bt))
+
+
+def test_ulp_excuse_of_the_fp32_metric():
+    """ulp_excuse = max ulp_fp32(W') / max |dW| (reading Z13b): one ulp of 1.0 is 2^-23; W = 0 leaves
+    only the relative rounding of the update itself."""
+    W0 = np.ones(4, np.float32)
+    ref = W0.astype(np.float64) - 1e-4
+    assert O.ulp_excuse(W0, ref) == pytest.approx(2.0 ** -24 / 1e-4, rel=1e-12)   # ulp(0.9999) = 2^-24
+    ref2 = W0.astype(np.float64) + 0.5
+    assert O.ulp_excuse(W0, ref2) == pytest.approx(2.0 ** -23 / 0.5, rel=1e-12)
+    z = np.zeros(4, np.float32)
+    assert O.ulp_excuse(z, z + 3.0) == pytest.approx(2.0 ** -22 / 3.0, rel=1e-12)
+    assert O.ulp_excuse(z, z) == float("inf")
+
+
 # ---------------------------------------------------------------- O10 SSP ----
 def _ssp_steps(M, N, K, P, T, seed):
     out = []
