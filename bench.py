@@ -215,6 +215,75 @@ def oracle_step_seconds(config: str, P: int, budget_s: float):
     return total, "; ".join(desc), threads
 
 
+def c1_step(pz, dev):
+    """BASELINE.json config C1: one FC layer M=128 (out), N=256 (in), K=8, P=2 simulated workers, one
+    synchronous SGD step, SFB (TF32 K1 and fp32 K1r) and PS on the GPU (CUDA events, median of 50, each
+    launch after a device spin) beside the fp64 oracle's O4 on 1 host thread and on all threads."""
+    import numpy as np
+    import torch
+
+    import oracle as O
+    import synthetic as S
+    from threadpoolctl import threadpool_limits
+
+    M, N, K, P = 128, 256, 8, 2
+    W, b, Us, Vs, lr = S.integer_factors(M, N, K, P, seed=1)
+    Ud = torch.from_numpy(np.concatenate(Us)).to(dev)
+    Vd = torch.from_numpy(np.concatenate(Vs)).to(dev)
+    Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+    n = M * N + M
+    _, _, padded = pz.shard_range(n, P, 0)
+    grads = np.zeros((P, padded), np.float32)
+    for p in range(P):
+        grads[p, :n] = O.flatten_params(O.reconstruct(Us[p], Vs[p]), Us[p].astype(np.float64).sum(0))
+    gd = torch.from_numpy(grads).to(dev)
+    wflat = torch.zeros(padded, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def gpu_ms(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        for _ in range(51):
+            torch.cuda._sleep(20_000)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts[1:])
+
+    out = {"workload": "C1: FC 256->128 (M=128, N=256), K=8, P=2 simulated workers, one sync step"}
+    out["gpu_sfb_tf32_ms"] = gpu_ms(lambda: pz.sfb_simulated(Ud, Vd, P, K, M, N, Wd, bd, lr, recon=pz.RECON_TF32))
+    out["gpu_sfb_fp32_ms"] = gpu_ms(lambda: pz.sfb_simulated(Ud, Vd, P, K, M, N, Wd, bd, lr, recon=pz.RECON_FP32))
+    out["gpu_ps_ms"] = gpu_ms(lambda: pz.ps_simulated(gd, P, wflat, n, lr))
+
+    def cpu_ms(threads):
+        with threadpool_limits(threads):
+            ts = []
+            for _ in range(21):
+                t0 = time.perf_counter()
+                O.sync_step(W, b, Us, Vs, lr)
+                ts.append((time.perf_counter() - t0) * 1e3)
+        return statistics.median(ts)
+
+    out["oracle_1core_ms"] = cpu_ms(1)
+    out["oracle_all_cores_ms"] = cpu_ms(os.cpu_count() or 1)
+    out["host_cores"] = os.cpu_count()
+    return out
+
+
+def oracle_per_config(P: int, budget_s: float = 1.5):
+    """The fp64 oracle's sync step of one iteration of every BASELINE.json network config (C2-C5) at P
+    workers, each on a bounded sample (SFB layers on R rows scaled by M/R): seconds and images/s."""
+    from drivers.cnn import CONFIGS
+    res = {}
+    for name in ("C2", "C3", "C4", "C5"):
+        sec, desc, threads = oracle_step_seconds(name, P, budget_s)
+        res[name] = {"seconds_per_iteration": sec, "images_per_s": P * CONFIGS[name]["batch"] / sec,
+                     "cores": threads, "sample": desc}
+    return res
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -518,6 +587,11 @@ def run_poseidon(args):
                          f"{len(secs)} repetitions ({time.perf_counter() - t_start:.1f} s CPU wall): {desc} "
                          "(SFB layers timed on R rows, scaled by M/R)",
                "seconds_per_iteration": sec}
+        try:
+            cpu["per_config"] = oracle_per_config(world)
+            cpu["c1"] = c1_step(pz, dev)
+        except Exception as e:   # the extra oracle legs are context, never fatal to the bench line
+            cpu["per_config_error"] = repr(e)
 
     if rank == 0:
         line = {
