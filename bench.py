@@ -87,11 +87,25 @@ def measured_peaks():
     if os.path.exists(path):
         with open(path) as f:
             d = json.load(f)
-        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
-                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
-                "source": "measured"}
-    # fallback stated in /opt/skills/guides/B200_PROFILING.md
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+        out = {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+               "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+               "source": "measured (MEASURED_PEAKS.json)"}
+    else:
+        # fallback stated in /opt/skills/guides/B200_PROFILING.md
+        out = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+    # TF32 dense peak measured on a pool B200 with the same protocol (tools/peaks.py, cuBLAS 8192^3 best of
+    # 10 / 4 s sustained); else the bf16 figure x the guide's nominal dense ratio 1.1 / 2.25
+    tp = os.path.join(ROOT, "profiles", "peaks_r2.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            t = json.load(f)
+        out["tf32_tflops"], out["tf32_tflops_sustained"] = t["tf32_tflops"], t["tf32_tflops_sustained"]
+        out["tf32_source"] = "measured (profiles/peaks_r2.json: cuBLAS TF32 8192^3)"
+    else:
+        out["tf32_tflops"] = out["bf16_tflops"] * TF32_OVER_BF16
+        out["tf32_tflops_sustained"] = out["bf16_tflops_sustained"] * TF32_OVER_BF16
+        out["tf32_source"] = "bf16 x 1.1/2.25 (nominal ratio)"
+    return out
 
 
 TF32_OVER_BF16 = 1.1 / 2.25   # nominal dense ratio (B200_PROFILING.md table)
@@ -458,7 +472,7 @@ def run_poseidon(args):
         ldk = (Kf + 3) // 4 * 4
         flops = 2.0 * M * N * Kf * P
         byts = 8.0 * M * N + 4.0 * P * ldk * (M + N)
-        tf32_peak = peaks["bf16_tflops_sustained"] * TF32_OVER_BF16
+        tf32_peak = peaks["tf32_tflops_sustained"]
         ridge = tf32_peak * 1e12 / (peaks["hbm_gbs"] * 1e9)
         if flops / byts >= ridge:
             ach = flops / (kms / 1e3) / 1e12
@@ -471,7 +485,7 @@ def run_poseidon(args):
         roof.update({"kernel": f"K1 recon_tcgen05 ({top.name} {M}x{N}, P*K={P * Kf})" if args.recon == "tf32"
                      else f"K1r recon_simt ({top.name})", "kernel_ms": kms,
                      "algorithmic_flops": flops, "algorithmic_bytes": byts,
-                     "peak_source": f"{peaks['source']} (tf32 = bf16 sustained x 1.1/2.25)"})
+                     "peak_source": f"hbm: {peaks['source']}; tf32 (sustained): {peaks['tf32_source']}"})
         if args.recon == "tf32":
             # context for `frac` (which is the in-step number): the same K1 launch on the same shape ALONE,
             # after the timed region, each launch queued behind a device spin (device time only)
@@ -502,6 +516,19 @@ def run_poseidon(args):
         roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / peaks["hbm_gbs"], "kernel": f"K2 ps_shard_sgd ({top.name})", "kernel_ms": kms,
                 "algorithmic_bytes": byts, "peak_source": peaks["source"]}
+    # K3 (factor pack) of every SFB layer, summed per step: 8 B per packed element (read + write) plus the
+    # column sums; timed by the library's events on the producer stream (layer stats pack_ms)
+    if sfb:
+        pk_ms, pk_bytes = 0.0, 0.0
+        for p in sfb:
+            pk_ms += statistics.mean(ctx.layer_stats(p.layer_id, a)["pack_ms"] for a in range(n_stats))
+            cols = p.M + (0 if early_v else p.N)
+            pk_bytes += 8.0 * p.K * cols + 4.0 * p.M
+        ach = pk_bytes / (pk_ms / 1e3) / 1e9 if pk_ms > 0 else None
+        roof["pack"] = {"kernel": "K3 pack_uv (all SFB layers of one step)", "ms_per_step": pk_ms,
+                        "algorithmic_bytes": pk_bytes, "achieved": ach, "unit": "GB/s",
+                        "frac": (ach / peaks["hbm_gbs"]) if ach else None,
+                        "note": "in-step, on the compute stream; V packed at forward time when early_v"}
     roof["traffic"] = None
     tr_path = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(tr_path):

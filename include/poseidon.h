@@ -122,11 +122,13 @@ typedef struct {
   int32_t iteration;
 } poseidon_iter_stats_t;
 
-/* Per-layer statistics of one iteration (milliseconds, device events). */
+/* Per-layer statistics of one iteration (milliseconds, device events).  pack_ms: the K3 factor pack
+ * of a factor layer on the producer stream (0 for PS layers). */
 typedef struct {
   float ready_to_start_ms, comm_ms, kernel_ms, start_to_done_ms, done_after_bwd_end_ms;
   int32_t scheme;
   int32_t launched;
+  float pack_ms;
 } poseidon_layer_stats_t;
 
 /* ======================= the five named entry points ======================= */
@@ -387,6 +389,18 @@ poseidon_status_t poseidon_reconstruct_sgd(const float* Ug, const float* Vg, int
 poseidon_status_t poseidon_reconstruct_sgd_rows(const float* Ug, const float* Vg, int32_t P, int64_t K,
                                                 int64_t ldk, int64_t M, int64_t m0, int64_t m1, int64_t N,
                                                 float* W, float alpha, int32_t recon, poseidon_stream_t stream);
+
+/* K3 alone (step (1) of SFB: "decouple grad W_p into two vectors u_p and v_p", Eq. 5): pack
+ * worker factors into the gather layout the reconstruction consumes.
+ *   U: K x M (row stride ldU >= M), V: K x N (row stride ldV >= N; NULL -> U only), device, fp32.
+ *   u_dst: M x ldk, v_dst: N x ldk (ldk >= K, multiple of 4), u_dst[m*ldk + k] = U[k*ldU + m] (likewise V);
+ *   columns k in [K, ldk) are NOT written.  round_tf32 != 0: the packed values are rounded to TF32 with
+ *   round-to-nearest, ties away from zero (cvt.rna, reading Z12).  colsum (M floats or NULL): sum_k U[k][m]
+ *   of the UNROUNDED values in fp32 (the bias gradient, reading Z9), in a fixed order (deterministic).
+ * One launch for U and V.  Errors: ERR_INVALID_ARG (NULL U / u_dst, K < 0, ldk < K, ld < cols). */
+poseidon_status_t poseidon_pack_factors(const float* U, int64_t ldU, int64_t M, const float* V, int64_t ldV,
+                                        int64_t N, int64_t K, int64_t ldk, int32_t round_tf32, float* u_dst,
+                                        float* v_dst, float* colsum, poseidon_stream_t stream);
 
 #ifdef __cplusplus
 }

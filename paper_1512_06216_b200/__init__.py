@@ -9,5 +9,5 @@ from .binding import (  # noqa: F401
     FLAG_NO_PRIORITY, FLAG_NVLS_PS, FLAG_SYMM_SFB, FLAG_NVLS_SFB, FLAG_SSP1, FLAG_SFPS, FLAG_EARLY_V, SFB_PATH_NCCL,
     SFB_PATH_NCCL_SYMM, SFB_PATH_NVLS, SFB_PATH_SFPS, PS_ZERO_GRAD, Context, PoseidonError, choose_scheme,
     shard_range, get_unique_id, launch_count, sfb_simulated, ps_simulated, ps_shard_update, reconstruct_sgd,
-    reconstruct_sgd_rows,
+    reconstruct_sgd_rows, pack_factors,
 )

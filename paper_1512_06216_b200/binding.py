@@ -67,7 +67,7 @@ class LayerStats(ctypes.Structure):
     _fields_ = [("ready_to_start_ms", ctypes.c_float), ("comm_ms", ctypes.c_float),
                 ("kernel_ms", ctypes.c_float), ("start_to_done_ms", ctypes.c_float),
                 ("done_after_bwd_end_ms", ctypes.c_float), ("scheme", ctypes.c_int32),
-                ("launched", ctypes.c_int32)]
+                ("launched", ctypes.c_int32), ("pack_ms", ctypes.c_float)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -124,6 +124,7 @@ _SIGS = {
     "poseidon_ps_simulated": (_i32, [_vp, _i32, _vp, _i64, _f, _vp]),
     "poseidon_ps_shard_update": (_i32, [_vp, _vp, _i64, _f, _vp, _vp]),
     "poseidon_reconstruct_sgd": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _f, _i32, _vp]),
+    "poseidon_pack_factors": (_i32, [_vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "poseidon_reconstruct_sgd_rows": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _f, _i32,
                                              _vp]),
 }
@@ -380,6 +381,15 @@ def reconstruct_sgd(Ug, Vg, P, K, ldk, M, N, W, alpha, recon=RECON_TF32, stream=
 def reconstruct_sgd_rows(Ug, Vg, P, K, ldk, M, m0, m1, N, W, alpha, recon=RECON_TF32, stream=None):
     _check(lib.poseidon_reconstruct_sgd_rows(_ptr(Ug), _ptr(Vg), P, K, ldk, M, m0, m1, N, _ptr(W), float(alpha),
                                              recon, _stream(stream)))
+
+
+def pack_factors(U, V, K, ldk, u_dst, v_dst=None, colsum=None, round_tf32=True, stream=None):
+    """K3 alone: U (K x M) -> u_dst (M x ldk), V (K x N) -> v_dst (N x ldk), optional column sums of U."""
+    M = U.shape[1]
+    N = V.shape[1] if V is not None else 0
+    _check(lib.poseidon_pack_factors(_ptr(U), U.stride(0), M, _ptr(V), V.stride(0) if V is not None else 0, N, K,
+                                     ldk, int(bool(round_tf32)), _ptr(u_dst), _ptr(v_dst), _ptr(colsum),
+                                     _stream(stream)))
 
 
 class _CudaArray:

@@ -80,6 +80,9 @@ struct EvSet {
               done = nullptr;
   // early input broadcast (FLAG_EARLY_V): V packed (producer stream), V broadcast done (comm stream)
   cudaEvent_t vready = nullptr, vgath = nullptr;
+  // K3 pack of a factor layer: pstart recorded on the producer stream before the pack (ready after it)
+  cudaEvent_t pstart = nullptr;
+  bool packed = false;
   // The events the statistics read for "collective done", "kernel start" and "kernel end".  An event
   // record costs ~1 us of stream time, so a sync records only the events whose time differs from
   // one already recorded (e.g. the fused NVLS kernel: ready, start, done) and aliases the rest.
@@ -258,7 +261,8 @@ poseidon_status_t ensure_events(Layer& L) {
   if (L.events_created) return POSEIDON_OK;
   for (int i = 0; i < RING; ++i) {
     EvSet& e = L.ev[i];
-    cudaEvent_t* all[] = {&e.ready, &e.start, &e.gathered, &e.kstart, &e.kend, &e.done, &e.vready, &e.vgath};
+    cudaEvent_t* all[] = {&e.ready, &e.start, &e.gathered, &e.kstart, &e.kend, &e.done, &e.vready, &e.vgath,
+                          &e.pstart};
     for (cudaEvent_t* p : all) CU_TRY(cudaEventCreate(p));
   }
   L.events_created = true;
@@ -759,12 +763,13 @@ poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t l
   float* u_slot = g.U + (size_t)c->rank * L.M * L.ldk;
   float* v_slot = g.V + (size_t)c->rank * L.N * L.ldk;
   float* b_slot = g.B + (size_t)c->rank * L.M;
-  cudaError_t err = launch_pack_t(U, ldU, u_slot, L.ldk, L.K, L.M, round, b_slot, producer);
-  if (err != cudaSuccess) return cuda_fail(err, "pack U launch");
-  if (!L.v_posted) {
-    err = launch_pack_t(V, ldV, v_slot, L.ldk, L.K, L.N, round, nullptr, producer);
-    if (err != cudaSuccess) return cuda_fail(err, "pack V launch");
-  }
+  // U (+ bias column sums) and, unless the early input broadcast already packed it, V: one launch
+  EvSet& e = L.ev[c->iter % RING];
+  CU_TRY(cudaEventRecord(e.pstart, producer));
+  e.packed = true;
+  cudaError_t err = launch_pack_uv(U, ldU, u_slot, L.M, b_slot, L.v_posted ? nullptr : V, ldV, v_slot, L.N,
+                                   L.ldk, L.K, round, producer);
+  if (err != cudaSuccess) return cuda_fail(err, "pack U/V launch");
   if ((err = debug_sync(producer, "K3 pack")) != cudaSuccess) return cuda_fail(err, "K3");
   return POSEIDON_OK;
 }
@@ -788,7 +793,7 @@ void free_layer(Layer& L) {
   if (L.events_created) {
     for (int i = 0; i < RING; ++i) {
       EvSet& e = L.ev[i];
-      cudaEvent_t all[] = {e.ready, e.start, e.gathered, e.kstart, e.kend, e.done, e.vready, e.vgath};
+      cudaEvent_t all[] = {e.ready, e.start, e.gathered, e.kstart, e.kend, e.done, e.vready, e.vgath, e.pstart};
       for (cudaEvent_t ev : all)
         if (ev) cudaEventDestroy(ev);
       e = EvSet{};
@@ -1605,6 +1610,7 @@ poseidon_status_t poseidon_get_layer_stats(poseidon_ctx_t c, int32_t ago, int32_
   out->kernel_ms = elapsed(e.ks_eff, e.ke_eff);
   out->start_to_done_ms = elapsed(e.start, e.done);
   out->done_after_bwd_end_ms = elapsed(r.bwd_end, e.done);
+  out->pack_ms = e.packed ? elapsed(e.pstart, e.ready) : 0.f;
   return POSEIDON_OK;
 }
 
@@ -1631,10 +1637,8 @@ poseidon_status_t poseidon_sfb_simulated(const float* U_all, const float* V_all,
   const bool round = recon == POSEIDON_RECON_TF32;
   cudaError_t err = cudaSuccess;
   for (int p = 0; p < P && err == cudaSuccess; ++p) {
-    err = launch_pack_t(U_all + (size_t)p * K * M, M, Ug + (size_t)p * M * ldk, ldk, K, M, round,
-                        Bs + (size_t)p * M, s);
-    if (err == cudaSuccess)
-      err = launch_pack_t(V_all + (size_t)p * K * N, N, Vg + (size_t)p * N * ldk, ldk, K, N, round, nullptr, s);
+    err = launch_pack_uv(U_all + (size_t)p * K * M, M, Ug + (size_t)p * M * ldk, M, Bs + (size_t)p * M,
+                         V_all + (size_t)p * K * N, N, Vg + (size_t)p * N * ldk, N, ldk, K, round, s);
   }
   const float alpha = -lr / (float)P;
   if (err == cudaSuccess) {
@@ -1714,6 +1718,18 @@ poseidon_status_t poseidon_reconstruct_sgd_rows(const float* Ug, const float* Vg
     return fail(POSEIDON_ERR_INVALID_ARG, "bad recon");
   }
   if (err != cudaSuccess) return cuda_fail(err, "reconstruct_sgd_rows launch");
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_pack_factors(const float* U, int64_t ldU, int64_t M, const float* V, int64_t ldV,
+                                        int64_t N, int64_t K, int64_t ldk, int32_t round_tf32, float* u_dst,
+                                        float* v_dst, float* colsum, poseidon_stream_t stream) {
+  if (!U || !u_dst || M <= 0 || K < 0 || ldk < K || ldU < M || (V && (!v_dst || N <= 0 || ldV < N)))
+    return fail(POSEIDON_ERR_INVALID_ARG, "pack_factors: bad arguments");
+  if (K == 0) return POSEIDON_OK;
+  cudaError_t err = launch_pack_uv(U, ldU, u_dst, M, colsum, V, ldV, v_dst, V ? N : 0, ldk, K, round_tf32 != 0,
+                                   reinterpret_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "pack_factors launch");
   return POSEIDON_OK;
 }
 

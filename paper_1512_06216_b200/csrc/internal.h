@@ -39,6 +39,11 @@ cudaError_t launch_ps_sim_update(const float* g, int64_t ld, int32_t P, float* W
 // also writes colsum[c] = sum_k src[k][c] (fp32, fixed order, UNROUNDED values).
 cudaError_t launch_pack_t(const float* src, int64_t ld_src, float* dst, int64_t ldk, int64_t K, int64_t cols,
                           bool round_tf32, float* colsum, cudaStream_t s);
+// K3 for one SFB sync in ONE launch: U (K x M, + column sums) into u_dst [M x ldk] and V (K x N) into
+// v_dst [N x ldk] (V == NULL: U only, the early-V path).
+cudaError_t launch_pack_uv(const float* U, int64_t ldU, float* u_dst, int64_t M, float* colsum, const float* V,
+                           int64_t ldV, float* v_dst, int64_t N, int64_t ldk, int64_t K, bool round_tf32,
+                           cudaStream_t s);
 // Momentum / weight decay (f4, oracle O4m):  v = mu v + lr (g + wd w);  w -= v.
 // PS shard: g = gsum * inv_p.   SFB: K1 already left v_partial = mu v + lr/P * acc in V, so
 // momentum_apply does v += lr*wd*w; w -= v.   Bias: g = inv_p * sum_p bs[p][m].

@@ -12,13 +12,19 @@
 // values) that the bias update needs, so the bias costs M floats on the wire
 // instead of a second pass over the gathered U.
 //
-// Transpose through a 32x33 shared tile: the global reads are coalesced along
-// M (N), the writes along K.  A block owns a 32-column strip and walks all K
-// rows, so the column sums are formed in a fixed order (bit-identical on
-// every rank).
+// Layout of the work (round 2; the round-1 kernel walked all K rows of a 32-column strip in one CTA,
+// only ceil(cols/32) CTAs, 0.19 of HBM): a CTA transposes 32 columns x 64 k per tile through a 64 x 33
+// shared tile (global reads coalesced along the columns, writes along k, 8 loads in flight per thread);
+// the K range is split over a thread-block CLUSTER of up to 8 CTAs along k, and the per-worker column
+// sums are reduced across the cluster through distributed shared memory in a fixed order (CTA rank
+// 0..cs-1), so they are deterministic without atomics.  U (with column sums) and V are packed by ONE
+// launch: the first column blocks are U's, the rest V's.
 #include <algorithm>
+#include <cooperative_groups.h>
 
 #include "internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace poseidon {
 
@@ -30,53 +36,84 @@ __device__ __forceinline__ float tf32_rn(float x) {
   return __uint_as_float(r);
 }
 
-// block (32, 8): x = column within the strip (load) / k within the tile (store)
-template <bool kRound, bool kColsum>
-__global__ void __launch_bounds__(256) pack_t_kernel(const float* __restrict__ src, int64_t ld_src,
-                                                     float* __restrict__ dst, int64_t ldk, int64_t K, int64_t cols,
-                                                     float* __restrict__ colsum) {
-  __shared__ float tile[32][33];
-  __shared__ float part[8][32];
+constexpr int kTileK = 64;   // k rows per tile
+constexpr int kMaxCluster = 8;
+
+struct PackSeg {
+  const float* src;  // K x cols, row stride ld
+  int64_t ld;
+  float* dst;        // cols x ldk
+  int64_t cols;
+  float* colsum;     // cols or NULL
+  int64_t cblocks;   // ceil(cols / 32)
+};
+
+// grid (cblocks(U) + cblocks(V), cs), cluster (1, cs, 1), block (32, 8)
+template <bool kRound>
+__global__ void __launch_bounds__(256) pack_uv_kernel(PackSeg a, PackSeg b, int64_t K, int64_t ldk,
+                                                      int tiles_per_cta) {
+  __shared__ float tile[kTileK][33];
+  __shared__ float part8[8][32];
+  __shared__ float part[32];
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int64_t c0 = (int64_t)blockIdx.x * 32;
+  const bool in_a = (int64_t)blockIdx.x < a.cblocks;
+  const PackSeg& sg = in_a ? a : b;
+  const int64_t c0 = ((int64_t)blockIdx.x - (in_a ? 0 : a.cblocks)) * 32;
   const int64_t c = c0 + tx;
+  const bool want_sum = sg.colsum != nullptr;
   float acc = 0.f;
-  // without column sums the K range is split over gridDim.y (more blocks in flight)
-  const int64_t kspan = kColsum ? K : ((K + 31) / 32 + gridDim.y - 1) / gridDim.y * 32;
-  const int64_t kbeg = kColsum ? 0 : (int64_t)blockIdx.y * kspan;
-  const int64_t kend = kColsum ? K : (kbeg + kspan < K ? kbeg + kspan : K);
-  for (int64_t k0 = kbeg; k0 < kend; k0 += 32) {
+  const int64_t t0 = (int64_t)blockIdx.y * tiles_per_cta;
+  for (int t = 0; t < tiles_per_cta; ++t) {
+    const int64_t k0 = (t0 + t) * kTileK;
+    if (k0 >= K) break;
+    float v[8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 8; ++i) {
       const int64_t k = k0 + ty + 8 * i;
-      float v = 0.f;
-      if (k < kend && c < cols) v = src[k * ld_src + c];
-      if (kColsum) acc += v;
-      tile[ty + 8 * i][tx] = v;
+      v[i] = (k < K && c < sg.cols) ? __ldcs(sg.src + k * sg.ld + c) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      acc += v[i];
+      tile[ty + 8 * i][tx] = v[i];
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t cc = c0 + ty + 8 * i;
-      const int64_t k = k0 + tx;
-      if (cc < cols && k < kend) {
-        float v = tile[tx][ty + 8 * i];
-        if (kRound) v = tf32_rn(v);
-        dst[cc * ldk + k] = v;
+      if (cc < sg.cols) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t k = k0 + tx + 32 * h;
+          if (k < K) {
+            float x = tile[tx + 32 * h][ty + 8 * i];
+            if (kRound) x = tf32_rn(x);
+            sg.dst[cc * ldk + k] = x;   // plain store: K1 / the all-gather read the slot next (L2)
+          }
+        }
       }
     }
     __syncthreads();
   }
-  if (kColsum) {
-    part[ty][tx] = acc;
-    __syncthreads();
-    if (ty == 0 && c < cols) {
-      float s = part[0][tx];
+  if (!want_sum) return;   // uniform over the cluster (one segment per column block)
+  // column sums of the unrounded values: rows of this CTA in a fixed order, then the cluster's CTAs in
+  // rank order through distributed shared memory
+  part8[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0) {
+    float s = part8[0][tx];
 #pragma unroll
-      for (int r = 1; r < 8; ++r) s += part[r][tx];
-      colsum[c] = s;
-    }
+    for (int r = 1; r < 8; ++r) s += part8[r][tx];
+    part[tx] = s;
   }
+  cg::cluster_group cluster = cg::this_cluster();
+  cluster.sync();
+  if (cluster.block_rank() == 0 && ty == 0 && c < sg.cols) {
+    float s = 0.f;
+    for (unsigned r = 0; r < cluster.num_blocks(); ++r) s += cluster.map_shared_rank(part, r)[tx];
+    sg.colsum[c] = s;
+  }
+  cluster.sync();   // keep every CTA's shared memory alive until rank 0 has read it
 }
 
 __global__ void __launch_bounds__(256) bias_update_kernel(const float* __restrict__ bs, int64_t ld, int P,
@@ -111,25 +148,44 @@ cudaError_t launch_bias_momentum(const float* bs, int64_t ld, int32_t P, float* 
   return cudaGetLastError();
 }
 
+static cudaError_t launch_pack(const PackSeg& a, const PackSeg& b, int64_t K, int64_t ldk, bool round_tf32,
+                               cudaStream_t s) {
+  const int64_t tiles_k = (K + kTileK - 1) / kTileK;
+  const int cs = (int)std::min<int64_t>(kMaxCluster, tiles_k);
+  const int tpc = (int)((tiles_k + cs - 1) / cs);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.cblocks + b.cblocks), (unsigned)cs, 1);
+  cfg.blockDim = dim3(32, 8, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = (unsigned)cs;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = round_tf32 ? cudaLaunchKernelEx(&cfg, pack_uv_kernel<true>, a, b, K, ldk, tpc)
+                             : cudaLaunchKernelEx(&cfg, pack_uv_kernel<false>, a, b, K, ldk, tpc);
+  g_launches.fetch_add(1);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+static PackSeg seg(const float* src, int64_t ld, float* dst, int64_t cols, float* colsum) {
+  return PackSeg{src, ld, dst, cols, colsum, cols > 0 ? (cols + 31) / 32 : 0};
+}
+
 cudaError_t launch_pack_t(const float* src, int64_t ld_src, float* dst, int64_t ldk, int64_t K, int64_t cols,
                           bool round_tf32, float* colsum, cudaStream_t s) {
   if (K <= 0 || cols <= 0) return cudaSuccess;
-  const int64_t cblocks = (cols + 31) / 32;
-  int64_t ksplit = 1;
-  if (!colsum) {  // aim for >= 4 blocks per SM
-    const int64_t want = (148 * 4 + cblocks - 1) / cblocks;
-    ksplit = std::max<int64_t>(1, std::min<int64_t>(want, (K + 31) / 32));
-  }
-  const dim3 grid((unsigned)cblocks, (unsigned)ksplit), block(32, 8);
-  if (round_tf32) {
-    if (colsum) pack_t_kernel<true, true><<<grid, block, 0, s>>>(src, ld_src, dst, ldk, K, cols, colsum);
-    else pack_t_kernel<true, false><<<grid, block, 0, s>>>(src, ld_src, dst, ldk, K, cols, nullptr);
-  } else {
-    if (colsum) pack_t_kernel<false, true><<<grid, block, 0, s>>>(src, ld_src, dst, ldk, K, cols, colsum);
-    else pack_t_kernel<false, false><<<grid, block, 0, s>>>(src, ld_src, dst, ldk, K, cols, nullptr);
-  }
-  g_launches.fetch_add(1);
-  return cudaGetLastError();
+  return launch_pack(seg(src, ld_src, dst, cols, colsum), seg(nullptr, 0, nullptr, 0, nullptr), K, ldk, round_tf32, s);
+}
+
+cudaError_t launch_pack_uv(const float* U, int64_t ldU, float* u_dst, int64_t M, float* colsum, const float* V,
+                           int64_t ldV, float* v_dst, int64_t N, int64_t ldk, int64_t K, bool round_tf32,
+                           cudaStream_t s) {
+  if (K <= 0 || (M <= 0 && N <= 0)) return cudaSuccess;
+  return launch_pack(seg(U, ldU, u_dst, M, colsum), seg(V, ldV, v_dst, V ? N : 0, nullptr), K, ldk, round_tf32, s);
 }
 
 cudaError_t launch_bias_update(const float* bs, int64_t ld, int32_t P, float* bias, int64_t M, float alpha,

@@ -268,3 +268,54 @@ def test_sfb_full_size_sampled_rows(pz, M, N, K, P):
     check_update(b[rows], outb[rows], b1r, TOL_FP32)
     # property at any size: rows never sampled still moved only where factors are non-zero
     assert np.all(np.isfinite(out))
+
+
+# ------------------------------------------------------------------ K3 ----
+def _tf32_rna(a):
+    """TF32 round-to-nearest, ties away from zero (cvt.rna): keep 10 mantissa bits, in sign-magnitude."""
+    b = np.ascontiguousarray(a, np.float32).view(np.uint32)
+    return ((b + np.uint32(0x1000)) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
+def _tf32_bits(a):
+    return (np.ascontiguousarray(a, np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 9216, 256), (1000, 4096, 256), (10, 64, 100), (333, 260, 7),
+                                   (21841, 4096, 2048), (5, 3, 513), (128, 256, 8)])
+@pytest.mark.parametrize("round_tf32", [False, True])
+def test_k3_pack_exact(pz, M, N, K, round_tf32):
+    """K3: the packed slot is the exact transpose (and the exact TF32 RNA rounding of it), columns
+    [K, ldk) untouched, U's column sums within fp32 summation error of the fp64 sums (any order), one
+    launch for U and V; cluster split of K (cs = min(8, ceil(K/64))) covers K = 7 ... 2048."""
+    ldk = (K + 3) // 4 * 4 + 4
+    g = S.rng(M + K)
+    U = (g.standard_normal((K, M)) / K).astype(np.float32)
+    V = np.maximum(g.standard_normal((K, N)), 0).astype(np.float32)
+    ud = torch.full((M, ldk), 7.0, device="cuda")
+    vd = torch.full((N, ldk), 7.0, device="cuda")
+    cs = torch.zeros(M, device="cuda")
+    pz.pack_factors(dev(U), dev(V), K, ldk, ud, vd, cs, round_tf32=round_tf32)
+    uo, vo, co = host(ud), host(vd), host(cs)
+    rnd = _tf32_rna if round_tf32 else (lambda a: a)
+    # (TF32 values are compared on their 19 significant bits: the tensor core reads no others)
+    keep = _tf32_bits if round_tf32 else (lambda a: a)
+    assert np.array_equal(keep(uo[:, :K]), rnd(U.T))
+    assert np.array_equal(keep(vo[:, :K]), rnd(V.T))
+    assert np.all(uo[:, K:] == 7.0) and np.all(vo[:, K:] == 7.0)
+    ref = U.astype(np.float64).sum(0)
+    bound = K * np.finfo(np.float32).eps * np.abs(U).astype(np.float64).sum(0) + 1e-30
+    assert np.all(np.abs(co - ref) <= bound)
+
+
+def test_k3_pack_deterministic_and_u_only(pz):
+    K, M = 1024, 3000
+    U = dev(S.rng(5).standard_normal((K, M)).astype(np.float32))
+    outs = []
+    for _ in range(3):
+        ud = torch.zeros(M, K, device="cuda")
+        cs = torch.zeros(M, device="cuda")
+        pz.pack_factors(U, None, K, K, ud, None, cs)
+        outs.append((host(ud).copy(), host(cs).copy()))
+    assert all(np.array_equal(outs[0][1], o[1]) for o in outs[1:])   # fixed-order column sums
+    assert np.array_equal(_tf32_bits(outs[0][0]), _tf32_rna(host(U).T))
