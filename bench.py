@@ -63,6 +63,8 @@ def parse():
                          "many microseconds on its GPU before the forward (a straggler, P:L568)")
     ap.add_argument("--bucket-kb", type=int, default=0,
                     help="sync runs of small PS layers as one bucket of at most this many KB (f1; needs the arena)")
+    ap.add_argument("--override", action="append", default=[], metavar="LAYER=SCHEME",
+                    help="per-layer scheme (auto/ps/sfb/sfps), e.g. fc8=ps: C3's P >= 6 schedule at fewer GPUs")
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--momentum", type=float, default=0.0, help="f4: Lambda momentum (0 = plain SGD hot path)")
     ap.add_argument("--weight-decay", type=float, default=0.0, help="f4: Lambda weight decay")
@@ -385,7 +387,8 @@ def run_poseidon(args):
     if args.memory_format == "channels_last":
         model.to(memory_format=torch.channels_last)   # before PoseidonSync makes params buffer views
     sync = PoseidonSync(model, ctx, K=K, lr=args.lr, scheme=scheme, recon=recon, arena=use_nvls or bool(args.ssp) or bool(args.bucket_kb),
-                        bucket_bytes=args.bucket_kb * 1024)
+                        bucket_bytes=args.bucket_kb * 1024,
+                        overrides=dict(o.split("=", 1) for o in args.override))
     if args.momentum or args.weight_decay:
         ctx.set_momentum(args.momentum, args.weight_decay)
 
@@ -634,7 +637,7 @@ def run_poseidon(args):
                                     ("nccl rs/k2/ag" if world > 1 else "k2 (P=1)")),
                         "nvls_status": ctx.nvls_status(),
                         "sfb_wire": sfb_wire, "ssp": args.ssp, "straggle_us": args.straggle_us,
-                        "bucket_kb": args.bucket_kb,
+                        "bucket_kb": args.bucket_kb, "overrides": args.override,
                         "sfb_paths": sorted({ctx.sfb_path(d["id"]) for d in sync.describe()
                                              if d["scheme"] == "SFB"}) if world > 1 else []},
             "exposed_sync_ms": exposed, "sync_total_ms": sync_total,

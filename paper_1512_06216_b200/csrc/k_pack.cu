@@ -12,13 +12,13 @@
 // values) that the bias update needs, so the bias costs M floats on the wire
 // instead of a second pass over the gathered U.
 //
-// Layout of the work (round 2; the round-1 kernel walked all K rows of a 32-column strip in one CTA,
-// only ceil(cols/32) CTAs, 0.19 of HBM): a CTA transposes 32 columns x 64 k per tile through a 64 x 33
-// shared tile (global reads coalesced along the columns, writes along k, 8 loads in flight per thread);
-// the K range is split over a thread-block CLUSTER of up to 8 CTAs along k, and the per-worker column
-// sums are reduced across the cluster through distributed shared memory in a fixed order (CTA rank
-// 0..cs-1), so they are deterministic without atomics.  U (with column sums) and V are packed by ONE
-// launch: the first column blocks are U's, the rest V's.
+// Layout of the work (round 2; the round-1 kernel walked all K rows of a 32-column strip with 4 loads in
+// flight per thread and launched U and V separately, 0.19 of HBM): a CTA transposes a 32-column x 256-k
+// strip through a 256 x 33 shared tile with all 32 loads per thread in flight at once (global reads
+// coalesced along the columns, writes along k), so C3's layers need one wave; U (with column sums) and V
+// are packed by ONE launch (the first column blocks are U's, the rest V's).  K > 256 is split over a
+// thread-block CLUSTER of up to 8 CTAs along k whose column sums are reduced through distributed shared
+// memory in a fixed order (CTA rank 0..cs-1): deterministic, no atomics.
 #include <algorithm>
 #include <cooperative_groups.h>
 
@@ -36,7 +36,8 @@ __device__ __forceinline__ float tf32_rn(float x) {
   return __uint_as_float(r);
 }
 
-constexpr int kTileK = 64;   // k rows per tile
+constexpr int kTileK = 256;  // k rows per tile: a CTA holds a whole 32-column x 256-k strip in flight
+constexpr int kLoads = kTileK / 8;
 constexpr int kMaxCluster = 8;
 
 struct PackSeg {
@@ -48,7 +49,8 @@ struct PackSeg {
   int64_t cblocks;   // ceil(cols / 32)
 };
 
-// grid (cblocks(U) + cblocks(V), cs), cluster (1, cs, 1), block (32, 8)
+// grid (cblocks(U) + cblocks(V), cs), cluster (1, cs, 1), block (32, 8).  Each tile: 32 loads in flight per
+// thread (the whole 32 x 256 strip, 32 KB per CTA), transposed through a 256 x 33 shared tile, 32 stores.
 template <bool kRound>
 __global__ void __launch_bounds__(256) pack_uv_kernel(PackSeg a, PackSeg b, int64_t K, int64_t ldk,
                                                       int tiles_per_cta) {
@@ -66,14 +68,14 @@ __global__ void __launch_bounds__(256) pack_uv_kernel(PackSeg a, PackSeg b, int6
   for (int t = 0; t < tiles_per_cta; ++t) {
     const int64_t k0 = (t0 + t) * kTileK;
     if (k0 >= K) break;
-    float v[8];
+    float v[kLoads];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kLoads; ++i) {
       const int64_t k = k0 + ty + 8 * i;
       v[i] = (k < K && c < sg.cols) ? __ldcs(sg.src + k * sg.ld + c) : 0.f;
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kLoads; ++i) {
       acc += v[i];
       tile[ty + 8 * i][tx] = v[i];
     }
@@ -82,13 +84,14 @@ __global__ void __launch_bounds__(256) pack_uv_kernel(PackSeg a, PackSeg b, int6
     for (int i = 0; i < 4; ++i) {
       const int64_t cc = c0 + ty + 8 * i;
       if (cc < sg.cols) {
+        float* drow = sg.dst + cc * ldk;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kTileK / 32; ++h) {
           const int64_t k = k0 + tx + 32 * h;
           if (k < K) {
             float x = tile[tx + 32 * h][ty + 8 * i];
             if (kRound) x = tf32_rn(x);
-            sg.dst[cc * ldk + k] = x;   // plain store: K1 / the all-gather read the slot next (L2)
+            drow[k] = x;   // plain store: K1 / the all-gather read the slot next (L2)
           }
         }
       }
@@ -96,8 +99,8 @@ __global__ void __launch_bounds__(256) pack_uv_kernel(PackSeg a, PackSeg b, int6
     __syncthreads();
   }
   if (!want_sum) return;   // uniform over the cluster (one segment per column block)
-  // column sums of the unrounded values: rows of this CTA in a fixed order, then the cluster's CTAs in
-  // rank order through distributed shared memory
+  // column sums of the unrounded values: rows of this CTA in a fixed order, then (K > 256) the cluster's
+  // CTAs in rank order through distributed shared memory
   part8[ty][tx] = acc;
   __syncthreads();
   if (ty == 0) {
@@ -107,6 +110,10 @@ __global__ void __launch_bounds__(256) pack_uv_kernel(PackSeg a, PackSeg b, int6
     part[tx] = s;
   }
   cg::cluster_group cluster = cg::this_cluster();
+  if (cluster.num_blocks() == 1) {
+    if (ty == 0 && c < sg.cols) sg.colsum[c] = part[tx];
+    return;
+  }
   cluster.sync();
   if (cluster.block_rank() == 0 && ty == 0 && c < sg.cols) {
     float s = 0.f;

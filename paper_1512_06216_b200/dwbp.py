@@ -103,7 +103,8 @@ class PoseidonSync:
     per worker per FC layer)."""
 
     def __init__(self, model: nn.Module, ctx: B.Context, K: int, lr: float,
-                 scheme: str = "auto", recon: int = B.RECON_TF32, arena: bool = False, bucket_bytes: int = 0):
+                 scheme: str = "auto", recon: int = B.RECON_TF32, arena: bool = False, bucket_bytes: int = 0,
+                 overrides: Optional[Dict[str, str]] = None):
         self.model = model
         self.ctx = ctx
         self.K = K
@@ -117,11 +118,16 @@ class PoseidonSync:
             raise ValueError("FLAG_SSP1 needs the library arena (arena=True): PS gradients are double-buffered")
         self.arena = arena
         self.nvls_active = False
+        # overrides: layer name -> "auto" / "ps" / "sfb" / "sfps" for that layer only (e.g. the P >= 6 schedule
+        # of C3, fc8 on the server, exercised at fewer GPUs)
+        overrides = dict(overrides or {})
         layer_id = 0
         for name, mod in model.named_modules():
             if isinstance(mod, (nn.Linear, nn.Conv2d)):
-                self._register(layer_id, name, mod, scheme, recon)
+                self._register(layer_id, name, mod, overrides.pop(name, scheme), recon)
                 layer_id += 1
+        if overrides:
+            raise ValueError(f"scheme overrides for unknown layers: {sorted(overrides)}")
         if arena:
             # one library-owned gradient/parameter arena for all PS layers (symmetric NCCL windows
             # with FLAG_NVLS_PS: each PS sync is then one fused multimem kernel); optionally runs of

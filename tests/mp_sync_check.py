@@ -28,6 +28,9 @@ Checks, at world = P:
      kernel's grid stride, several CTAs per layer), four iterations of integer gradients through the
      DWBP hook, bit-exact vs O6 every iteration.  Run with POSEIDON_FUZZ_US set, every CTA sleeps a
      pseudo-random time after the entry barrier (`--race-only` runs just this check).
+  11. C3 with the schedule the rule picks at P >= 6 (fc8 forced to PS) in bench.py's N > 1 launch
+     configuration, one step, every layer vs the oracle (tests/stepcheck.py).
+  `--wire-only` runs only 1b and 9 (the factor broadcast kernel), for POSEIDON_SFB_BCAST_GRID sweeps.
   5. Full size in bench.py's N > 1 configuration: C3 fc6 SFB through the library's broadcast kernel (sampled
      rows vs O4)
      and a 37.7M-parameter PS layer through the fused NVLS kernel (sampled elements vs O6).
@@ -56,6 +59,111 @@ def allsame(t):
     parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
     dist.all_gather(parts, t)
     return all(torch.equal(parts[0], p) for p in parts[1:])
+
+
+def sfb_wire_checks(new_ctx, rank, P, dev):
+    # ---- 1b. SFB on symmetric buffers: NCCL all-gather (SYMM_SFB) and the NVLS multicast broadcast
+    #          (NVLS_SFB); odd M (bias slot not a multiple of 4), ldk padding, 3 iterations in a row
+    #          (the broadcast's entry barrier guards the gather buffers the previous K1 read) ----
+    for flags in (pz.FLAG_SYMM_SFB, pz.FLAG_NVLS_SFB):
+        cs = new_ctx(flags)
+        shapes = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 1000, 4096, 33)]
+        for lid, M_, N_, K_ in shapes:
+            assert cs.register_layer(lid, pz.LAYER_FC, M_, N_, K_) == pz.SCHEME_SFB
+        path = cs.sfb_path(0)
+        assert path >= pz.SFB_PATH_NCCL_SYMM, path
+        if rank == 0:
+            print(f"SFB path flags={flags}: {path}", flush=True)
+        for it in range(3):
+            for lid, M_, N_, K_ in shapes:
+                W, b, Us, Vs, lr = S.integer_factors(M_, N_, K_, P, seed=100 * it + lid)
+                Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+                cs.sync_fc_sfb(lid, torch.from_numpy(Us[rank]).to(dev), torch.from_numpy(Vs[rank]).to(dev), Wd, bd, lr)
+                cs.wait_layer(lid)
+                W1, b1 = O.sync_step(W, b, Us, Vs, lr)
+                torch.cuda.synchronize()
+                assert np.array_equal(Wd.cpu().numpy().astype(np.float64), W1), f"SFB flags={flags} it={it} lid={lid}"
+                assert np.array_equal(bd.cpu().numpy().astype(np.float64), b1)
+                assert allsame(Wd) and allsame(bd)
+            st = cs.iteration_end(stats=True)
+            ldks = [(K_ + 3) // 4 * 4 for _, _, _, K_ in shapes]
+            per = sum((M_ * l + N_ * l + M_) * 4 for (_, M_, N_, _), l in zip(shapes, ldks))
+            assert st["nccl_bytes_recv"] == per * (P - 1), st
+        cs.close()
+
+
+def early_v_checks(new_ctx, rank, P, dev):
+    # ---- 9. early input broadcast (FLAG_EARLY_V): V posted at "forward" time, only U at the sync (whose V
+    #          argument is garbage here); NCCL and broadcast-kernel wires; integer bit-exact vs O4, two
+    #          iterations, and the same NCCL byte total as the plain sync ----
+    for flags in (pz.FLAG_EARLY_V, pz.FLAG_EARLY_V | pz.FLAG_NVLS_SFB):
+        ce = new_ctx(flags)
+        shapes = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 1000, 4096, 33)]
+        for lid, M_, N_, K_ in shapes:
+            assert ce.register_layer(lid, pz.LAYER_FC, M_, N_, K_) == pz.SCHEME_SFB
+        for it in range(2):
+            outs = []
+            for lid, M_, N_, K_ in shapes:   # "forward": every layer posts its input
+                W, b, Us, Vs, lr = S.integer_factors(M_, N_, K_, P, seed=700 + 10 * it + lid)
+                ce.sfb_post_input(lid, torch.from_numpy(Vs[rank]).to(dev))
+                outs.append((W, b, Us, Vs, lr))
+            res = []
+            for lid, (W, b, Us, Vs, lr) in reversed(list(enumerate(outs))):   # "backward": top layer first
+                Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
+                junk = torch.full((Vs[rank].shape[0], Vs[rank].shape[1]), 5.0, device=dev)
+                ce.sync_fc_sfb(lid, torch.from_numpy(Us[rank]).to(dev), junk, Wd, bd, lr)
+                res.append((lid, Wd, bd))
+            st = ce.iteration_end(stats=True)
+            for lid, Wd, bd in res:
+                ce.wait_layer(lid)
+            torch.cuda.synchronize()
+            for lid, Wd, bd in res:
+                W, b, Us, Vs, lr = outs[lid]
+                W1, b1 = O.sync_step(W, b, Us, Vs, lr)
+                assert np.array_equal(Wd.cpu().numpy().astype(np.float64), W1), f"early V flags={flags} lid={lid}"
+                assert np.array_equal(bd.cpu().numpy().astype(np.float64), b1)
+                assert allsame(Wd) and allsame(bd)
+            ldks = [(K_ + 3) // 4 * 4 for _, _, _, K_ in shapes]
+            per = sum((M_ * l + N_ * l + M_) * 4 for (_, M_, N_, _), l in zip(shapes, ldks))
+            assert st["nccl_bytes_recv"] == per * (P - 1), st
+        ce.close()
+
+
+def alexnet_p6_schedule_check(new_ctx, rank, P, dev, world):
+    """Check 11: the schedule the rule picks for C3 at P >= 6 (fc6 / fc7 SFB, fc8 PS, conv PS) on the P GPUs at
+    hand (fc8 forced to PS), in bench.py's N > 1 launch configuration (NVLS PS arena, broadcast wire, early V,
+    channels_last, batch 256 / GPU): one DWBP step, every layer's update vs the oracle from all ranks'
+    captures (O4 on sampled rows for fc6 / fc7, O6 on every element of fc8 and the convs)."""
+    import torch.nn.functional as F
+    from drivers.cnn import AlexNet
+    from stepcheck import StepCapture, oracle_check, safe_lr
+    torch.backends.cudnn.deterministic = True
+    torch.manual_seed(6216)
+    model = AlexNet().to(dev).to(memory_format=torch.channels_last)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1512 + rank)
+    x = torch.rand((256, 3, 227, 227), device=dev, generator=g).contiguous(memory_format=torch.channels_last)
+    y = torch.randint(0, 1000, (256,), device=dev, generator=g)
+    lr = safe_lr(model, lambda m: F.cross_entropy(m(x), y), world)
+    flags = pz.FLAG_NVLS_PS | pz.FLAG_NVLS_SFB | pz.FLAG_EARLY_V if P > 1 else 0
+    c = new_ctx(flags)
+    sync = PoseidonSync(model, c, K=256, lr=lr, arena=P > 1, overrides={"fc8": "ps"})
+    picks = {p.name: p.scheme for p in sync.plans}
+    assert picks["fc6"] == pz.SCHEME_SFB and picks["fc7"] == pz.SCHEME_SFB and picks["fc8"] == pz.SCHEME_PS, picks
+    cap = StepCapture(sync)
+    cap.snapshot()
+    F.cross_entropy(model(x), y).backward()
+    sync.iteration_end()
+    sync.wait_all()
+    torch.cuda.synchronize()
+    errs = oracle_check(cap, lr, world)
+    assert len(errs) == 8, errs
+    flat = torch.cat([p.detach().reshape(-1) for p in model.parameters()])
+    assert allsame(flat)
+    c.close()
+    if rank == 0:
+        print(f"C3 P>=6 schedule (fc8 PS) ok at P={P}: " + ", ".join(f"{k} {v:.1e}" for k, v in errs.items()),
+              flush=True)
 
 
 def nvls_race_check(new_ctx, rank, P, dev):
@@ -128,6 +236,13 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         return pz.Context(rank=rank, world=world, device=local, nccl_id=obj[0], flags=flags)
 
+    if "--wire-only" in sys.argv:   # the factor broadcast kernel alone (e.g. with POSEIDON_SFB_BCAST_GRID set)
+        sfb_wire_checks(new_ctx, rank, P, dev)
+        early_v_checks(new_ctx, rank, P, dev)
+        dist.barrier()
+        print(f"MP_OK {rank}", flush=True)
+        dist.destroy_process_group()
+        return
     if "--race-only" in sys.argv:
         nvls_race_check(new_ctx, rank, P, dev)
         dist.barrier()
@@ -171,34 +286,8 @@ def main():
     check_update(b, bd.cpu().numpy(), b1, 1e-5)
     assert allsame(Wd)
 
-    # ---- 1b. SFB on symmetric buffers: NCCL all-gather (SYMM_SFB) and the NVLS multicast broadcast
-    #          (NVLS_SFB); odd M (bias slot not a multiple of 4), ldk padding, 3 iterations in a row
-    #          (the broadcast's entry barrier guards the gather buffers the previous K1 read) ----
-    for flags in (pz.FLAG_SYMM_SFB, pz.FLAG_NVLS_SFB):
-        cs = new_ctx(flags)
-        shapes = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 1000, 4096, 33)]
-        for lid, M_, N_, K_ in shapes:
-            assert cs.register_layer(lid, pz.LAYER_FC, M_, N_, K_) == pz.SCHEME_SFB
-        path = cs.sfb_path(0)
-        assert path >= pz.SFB_PATH_NCCL_SYMM, path
-        if rank == 0:
-            print(f"SFB path flags={flags}: {path}", flush=True)
-        for it in range(3):
-            for lid, M_, N_, K_ in shapes:
-                W, b, Us, Vs, lr = S.integer_factors(M_, N_, K_, P, seed=100 * it + lid)
-                Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
-                cs.sync_fc_sfb(lid, torch.from_numpy(Us[rank]).to(dev), torch.from_numpy(Vs[rank]).to(dev), Wd, bd, lr)
-                cs.wait_layer(lid)
-                W1, b1 = O.sync_step(W, b, Us, Vs, lr)
-                torch.cuda.synchronize()
-                assert np.array_equal(Wd.cpu().numpy().astype(np.float64), W1), f"SFB flags={flags} it={it} lid={lid}"
-                assert np.array_equal(bd.cpu().numpy().astype(np.float64), b1)
-                assert allsame(Wd) and allsame(bd)
-            st = cs.iteration_end(stats=True)
-            ldks = [(K_ + 3) // 4 * 4 for _, _, _, K_ in shapes]
-            per = sum((M_ * l + N_ * l + M_) * 4 for (_, M_, N_, _), l in zip(shapes, ldks))
-            assert st["nccl_bytes_recv"] == per * (P - 1), st
-        cs.close()
+    sfb_wire_checks(new_ctx, rank, P, dev)
+    alexnet_p6_schedule_check(new_ctx, rank, P, dev, world)
 
     # ---- 2. PS of the same layer ----
     for variant in ("int", "rand"):
@@ -558,41 +647,7 @@ def main():
     assert allsame(Wd) and allsame(bd)
     cp.close()
 
-    # ---- 9. early input broadcast (FLAG_EARLY_V): V posted at "forward" time, only U at the sync (whose V
-    #          argument is garbage here); NCCL and broadcast-kernel wires; integer bit-exact vs O4, two
-    #          iterations, and the same NCCL byte total as the plain sync ----
-    for flags in (pz.FLAG_EARLY_V, pz.FLAG_EARLY_V | pz.FLAG_NVLS_SFB):
-        ce = new_ctx(flags)
-        shapes = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 1000, 4096, 33)]
-        for lid, M_, N_, K_ in shapes:
-            assert ce.register_layer(lid, pz.LAYER_FC, M_, N_, K_) == pz.SCHEME_SFB
-        for it in range(2):
-            outs = []
-            for lid, M_, N_, K_ in shapes:   # "forward": every layer posts its input
-                W, b, Us, Vs, lr = S.integer_factors(M_, N_, K_, P, seed=700 + 10 * it + lid)
-                ce.sfb_post_input(lid, torch.from_numpy(Vs[rank]).to(dev))
-                outs.append((W, b, Us, Vs, lr))
-            res = []
-            for lid, (W, b, Us, Vs, lr) in reversed(list(enumerate(outs))):   # "backward": top layer first
-                Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
-                junk = torch.full((Vs[rank].shape[0], Vs[rank].shape[1]), 5.0, device=dev)
-                ce.sync_fc_sfb(lid, torch.from_numpy(Us[rank]).to(dev), junk, Wd, bd, lr)
-                res.append((lid, Wd, bd))
-            st = ce.iteration_end(stats=True)
-            for lid, Wd, bd in res:
-                ce.wait_layer(lid)
-            torch.cuda.synchronize()
-            for lid, Wd, bd in res:
-                W, b, Us, Vs, lr = outs[lid]
-                W1, b1 = O.sync_step(W, b, Us, Vs, lr)
-                assert np.array_equal(Wd.cpu().numpy().astype(np.float64), W1), f"early V flags={flags} lid={lid}"
-                assert np.array_equal(bd.cpu().numpy().astype(np.float64), b1)
-                assert allsame(Wd) and allsame(bd)
-            ldks = [(K_ + 3) // 4 * 4 for _, _, _, K_ in shapes]
-            per = sum((M_ * l + N_ * l + M_) * 4 for (_, M_, N_, _), l in zip(shapes, ldks))
-            assert st["nccl_bytes_recv"] == per * (P - 1), st
-        ce.close()
-
+    early_v_checks(new_ctx, rank, P, dev)
     # ---- 5. full size in bench.py's N > 1 launch configuration (NVLS_SFB | NVLS_PS): C3 fc6 as SFB
     #          (4096 x 9216, K = 256) and a 37.7M-parameter PS layer in the NVLS arena, sampled against
     #          the oracle (O4 rows / O6 elements) ----

@@ -17,7 +17,7 @@ def timeit(fn, iters=21):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ts = []
     for _ in range(iters):
-        torch.cuda._sleep(100_000)
+        torch.cuda._sleep(2_000_000)
         s.record(); fn(); e.record(); e.synchronize()
         ts.append(s.elapsed_time(e))
     return statistics.median(ts[1:])
