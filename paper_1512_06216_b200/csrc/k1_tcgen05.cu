@@ -229,6 +229,8 @@ struct Params {
   float alpha;
   float beta;   // W' = fmaf(alpha, acc, beta * W): 1 for SGD; mu when the target is a velocity (f4)
   float* dbg;  // debug dump (tile 0 of CTA 0): smem stage 0 of A|B, raw accumulator; NULL in production
+  // diagnostics (POSEIDON_K1_PROF=1): %globaltimer at each CTA's entry and exit, [2 * blockIdx + {0,1}]
+  unsigned long long* prof;
   // fused bias update of the 2-SM kernel (plain SGD): bias[m] = fmaf(alpha, sum_p bs[p*M + m], bias[m]) for
   // m < M, done by the idle lanes of the W-producer warp; NULL when the host runs the separate kernel
   const float* bs;
@@ -453,6 +455,11 @@ __host__ __device__ constexpr uint32_t idesc() {
 }
 }  // namespace k2sm
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -518,6 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  if (p.prof != nullptr && threadIdx.x == 0) p.prof[2 * blockIdx.x] = globaltimer_ns();
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -739,6 +747,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS)
                  : "memory");
   }
+  if (p.prof != nullptr && threadIdx.x == 0) p.prof[2 * blockIdx.x + 1] = globaltimer_ns();
 }
 
 // ------------------------------------------------------------- host side ----
@@ -843,6 +852,22 @@ void map_cache_put(const MapKey& k, const CUtensorMap& a, const CUtensorMap& b, 
 }
 }  // namespace
 
+// POSEIDON_K1_PROF=1 (diagnostics): K1 launches of the largest shape seen so far record per-CTA entry / exit
+// %globaltimer stamps into a device buffer; poseidon_debug_k1_prof copies the latest launch's stamps out.
+unsigned long long* g_prof = nullptr;
+int64_t g_prof_shape = 0;
+unsigned long long* k1_prof_buffer(int64_t M, int64_t N) {
+  static const bool on = [] {
+    const char* v = getenv("POSEIDON_K1_PROF");
+    return v && v[0] == '1';
+  }();
+  if (!on) return nullptr;
+  if (!g_prof && cudaMalloc(&g_prof, 2 * 1024 * sizeof(unsigned long long)) != cudaSuccess) g_prof = nullptr;
+  if (M * N < g_prof_shape) return nullptr;
+  g_prof_shape = M * N;
+  return g_prof;
+}
+
 // A freed and reallocated buffer can come back at the same address with the same shape: its cached
 // maps are then still exact (a tensor map holds only address, shape and strides).
 bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int64_t M, int64_t N, const float* W) {
@@ -895,6 +920,7 @@ have_maps:
   p.alpha = alpha;
   p.beta = beta;
   p.dbg = dbg;
+  p.prof = k1_prof_buffer(M, N);
   p.W = W;
   p.bs = nullptr;
   p.bias = nullptr;
@@ -981,6 +1007,17 @@ have_maps:
 }
 
 }  // namespace poseidon
+
+// Diagnostics entry (not part of include/poseidon.h): copies the per-CTA entry / exit stamps of the latest
+// profiled K1 launch (POSEIDON_K1_PROF=1) into out[2 * n]; returns the number of CTAs copied.
+extern "C" int poseidon_debug_k1_prof(unsigned long long* out, int n) {
+  if (!poseidon::g_prof) return 0;
+  if (n > 1024) n = 1024;
+  if (cudaMemcpy(out, poseidon::g_prof, 2 * (size_t)n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) !=
+      cudaSuccess)
+    return -1;
+  return n;
+}
 
 // Debug entry (not part of include/poseidon.h): runs K1 and dumps stage 0 of tile 0 and its raw
 // accumulator into dbg (STAGE_BYTES/4 + 128*256 floats).
