@@ -306,8 +306,9 @@ poseidon_status_t poseidon_set_lr(poseidon_ctx_t ctx, float lr);
 /* Lambda of Eq. 3 / Alg. 3 line 8, applied once at the aggregation point
  * (oracle O4m):  g = (1/P) sum_p grad_p;  v = mu v + lr (g + weight_decay * w);
  * w -= v, for every parameter (weights and biases).  Velocity buffers are library-owned and
- * zero-initialised on first use: SFB layers keep a replicated M x N (+ M) velocity (K1 updates it
- * in its epilogue, a second elementwise pass applies it); PS layers keep only the velocity of this
+ * zero-initialised on first use: SFB layers keep a replicated M x N (+ M) velocity (on the TF32 path
+ * K1's epilogue streams W and the velocity once and applies both, 16 B / element; the fp32 K1r path
+ * updates the velocity and a second elementwise pass applies it); PS layers keep only the velocity of this
  * rank's shard (the shard owner is the only one that updates it).  layer_id -1 = every registered
  * layer; mu = weight_decay = 0 returns the layer to plain SGD.  0 <= mu < 1, weight_decay >= 0. */
 poseidon_status_t poseidon_set_momentum(poseidon_ctx_t ctx, int32_t layer_id, float mu, float weight_decay);

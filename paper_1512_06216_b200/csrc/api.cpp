@@ -395,18 +395,29 @@ poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, floa
   const float alpha = -lr / (float)P;
   cudaError_t err;
   const bool mom = (L.vel != nullptr);
-  // plain SGD: W = fmaf(-lr/P, acc, W).  Momentum (f4): the velocity is the target,
-  // v_partial = fmaf(lr/P, acc, mu * v), then momentum_apply: v += lr*wd*w, w -= v.
+  bool bias_done = false;   // K1 updates the bias with otherwise idle lanes (no extra launch)
+  bool fused_mom = false;
+  if (mom && L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(g.U, g.V, L.ldk, L.M, L.N, W)) {
+    // f4 fused into K1's epilogue: W and its velocity streamed once, v' = mu v + (lr/P) acc + lr wd w,
+    // w' = w - v' (16 B / element); the bias likewise on idle lanes
+    const K1Momentum km{L.vel, L.vel_b, L.mu, lr, L.wd};
+    err = launch_recon_tcgen05(g.U, g.V, P, L.K, L.ldk, L.M, L.N, W, lr / (float)P, 1.0f, c->recon_stream, nullptr,
+                               0, g.B, bias, &bias_done, &km);
+    fused_mom = (err == cudaSuccess);
+    if (err == cudaErrorNotSupported) err = cudaSuccess;   // fall through to the two-pass form below
+  }
+  // plain SGD: W = fmaf(-lr/P, acc, W).  Momentum, two-pass form (K1r / unsupported layouts): the velocity is
+  // the target, v_partial = fmaf(lr/P, acc, mu * v), then momentum_apply: v += lr*wd*w, w -= v.
   float* target = mom ? L.vel : W;
   const float a1 = mom ? (lr / (float)P) : alpha, b1 = mom ? L.mu : 1.0f;
-  bool bias_done = false;   // plain SGD: K1 updates the bias with otherwise idle lanes (no extra launch)
-  if (L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(g.U, g.V, L.ldk, L.M, L.N, target))
+  if (fused_mom) {
+  } else if (L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(g.U, g.V, L.ldk, L.M, L.N, target))
     err = launch_recon_tcgen05(g.U, g.V, P, L.K, L.ldk, L.M, L.N, target, a1, b1, c->recon_stream, nullptr, 0,
                                mom ? nullptr : g.B, mom ? nullptr : bias, &bias_done);
   else
     err = launch_recon_simt(g.U, g.V, P, L.K, L.ldk, L.M, L.N, target, a1, b1, c->recon_stream);
   if (err != cudaSuccess) return cuda_fail(err, "reconstruct+sgd launch");
-  if (mom) {
+  if (mom && !fused_mom) {
     err = launch_momentum_apply(W, L.vel, L.M * L.N, lr * L.wd, c->recon_stream);
     if (err != cudaSuccess) return cuda_fail(err, "momentum apply launch");
   }

@@ -68,10 +68,17 @@ cudaError_t launch_recon_simt(const float* Ug, const float* Vg, int32_t P, int64
 // K1: the same on tcgen05 (TF32 operands, fp32 TMEM accumulators).  Returns cudaErrorNotSupported
 // when TMA cannot describe the buffers.  Tensor maps are encoded per call (host only, ~us).
 // Both compute W' = fmaf(alpha, acc, beta * W) (beta = 1: SGD; beta = mu: velocity update, f4).
+// f4 momentum fused into K1's epilogue (2-SM kernel): v' = mu v + (lr/P) acc + lr wd w; w' = w - v'
+// (pass alpha = lr/P, beta unused); vel has W's layout; vel_b (M or NULL) takes the bias the same way.
+struct K1Momentum {
+  float* vel;
+  float* vel_b;
+  float mu, lr, wd;
+};
 cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
                                  int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg = nullptr,
                                  int64_t ldm = 0, const float* bs = nullptr, float* bias = nullptr,
-                                 bool* bias_done = nullptr);
+                                 bool* bias_done = nullptr, const K1Momentum* mom = nullptr);
 // (bs, bias, bias_done): optional plain-SGD bias update fused into K1 (bias[m] = fmaf(alpha, sum_p bs[p*M+m],
 // bias[m]), bs [P][M] with M the block's row count); *bias_done tells whether the kernel took it.
 bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int64_t M, int64_t N, const float* W);

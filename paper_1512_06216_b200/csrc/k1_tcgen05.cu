@@ -231,6 +231,11 @@ struct Params {
   float* dbg;  // debug dump (tile 0 of CTA 0): smem stage 0 of A|B, raw accumulator; NULL in production
   // diagnostics (POSEIDON_K1_PROF=1): %globaltimer at each CTA's entry and exit, [2 * blockIdx + {0,1}]
   unsigned long long* prof;
+  // f4 fused momentum + decay (MOM instantiation): vel M x N (same layout as W), vel_b (M or NULL);
+  // v' = mu v + (lr/P) acc + lr wd w, w' = w - v' (alpha = lr/P); bias alike from the gathered column sums
+  float* vel;
+  float* vel_b;
+  float mu, lr_wd, lr, wd, inv_p;
   // fused bias update of the 2-SM kernel (plain SGD): bias[m] = fmaf(alpha, sum_p bs[p*M + m], bias[m]) for
   // m < M, done by the idle lanes of the W-producer warp; NULL when the host runs the separate kernel
   const float* bs;
@@ -448,7 +453,9 @@ constexpr int BN_CTA = 128;             // B rows staged per CTA
 constexpr int A_BYTES = BM_CTA * BK * 4;   // 16 KB
 constexpr int B_BYTES = BN_CTA * BK * 4;   // 16 KB
 constexpr int STAGE = A_BYTES + B_BYTES;   // 32 KB
-constexpr int smem_bytes(int stages, int wslots) { return stages * STAGE + wslots * W_CHUNK_BYTES + 1024 + 1024; }
+constexpr int smem_bytes(int stages, int wslots, bool mom = false) {
+  return stages * STAGE + wslots * (mom ? 2 : 1) * W_CHUNK_BYTES + 1024 + 1024;
+}
 
 __host__ __device__ constexpr uint32_t idesc() {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
@@ -504,15 +511,20 @@ __device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
                : "memory");
 }
 
-template <int NST, int NWS>
+// MOM (f4, fused momentum): every W slot carries the matching velocity chunk right after the W chunk
+// (2 x 16 KB); the epilogue reads both, writes both (16 B per element instead of K1-on-the-velocity + a
+// separate pass, 24 B).
+template <int NST, int NWS, bool MOM = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     recon_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                             const __grid_constant__ CUtensorMap tmW, const Params p) {
+                             const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmV,
+                             const Params p) {
+  constexpr int SLOT = (MOM ? 2 : 1) * W_CHUNK_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_ops = smem;
   uint8_t* smem_w = smem + NST * k2sm::STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_w + NWS * W_CHUNK_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_w + NWS * SLOT);
   uint64_t* full = bars;
   uint64_t* empty = full + NST;
   uint64_t* tfull = empty + NST;
@@ -541,6 +553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    if (MOM) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmV) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_smem)),
@@ -622,7 +635,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
       for (int m = (int)blockIdx.x * 31 + (lane - 1); m < p.M; m += (int)gridDim.x * 31) {
         float sum = 0.f;
         for (int w = 0; w < p.nP; ++w) sum += p.bs[(size_t)w * p.M + m];
-        p.bias[m] = fmaf(p.alpha, sum, p.bias[m]);
+        if (MOM) {   // Lambda on the bias (O4m): v = mu v + lr (g + wd b), b -= v
+          const float b = p.bias[m];
+          const float v = fmaf(p.mu, p.vel_b[m], p.lr * fmaf(p.wd, b, sum * p.inv_p));
+          p.vel_b[m] = v;
+          p.bias[m] = b - v;
+        } else {
+          p.bias[m] = fmaf(p.alpha, sum, p.bias[m]);
+        }
       }
     }
     if (lane == 0 && p.mode != 7) {
@@ -638,8 +658,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
         for (int c = 0; c < nch; ++c, ++g) {
           const uint32_t slot = g % NWS, ph = (g / NWS) & 1;
           mbar_wait(&wempty[slot], ph ^ 1);
-          mbar_expect_tx(&wfull[slot], W_CHUNK_BYTES);
-          tma_load_2d(&tmW, &wfull[slot], smem_w + slot * W_CHUNK_BYTES, n0 + c * W_CHUNK_COLS, m0, pol);
+          mbar_expect_tx(&wfull[slot], (uint32_t)SLOT);
+          tma_load_2d(&tmW, &wfull[slot], smem_w + slot * SLOT, n0 + c * W_CHUNK_COLS, m0, pol);
+          if (MOM) tma_load_2d(&tmV, &wfull[slot], smem_w + slot * SLOT + W_CHUNK_BYTES, n0 + c * W_CHUNK_COLS, m0, pol);
         }
       }
     }
@@ -706,7 +727,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
           continue;
         }
         mbar_wait(&wfull[slot], ph);
-        const uint32_t sbase = smem_w_u32 + slot * W_CHUNK_BYTES;
+        const uint32_t sbase = smem_w_u32 + slot * SLOT;
         const int col_base = n0 + c * W_CHUNK_COLS;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -720,9 +741,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
               const int cl = 8 * j + 2 * t0;                 // column within the 32-column chunk
               const uint32_t a8 = sbase + row * 128 + ((((cl >> 2) ^ (row & 7))) << 4) + ((cl & 3) << 2);
               float2 w = lds64(a8);
+              const float a0 = __uint_as_float(r[h][4 * j + 2 * k + 0]), a1 = __uint_as_float(r[h][4 * j + 2 * k + 1]);
+              if (MOM) {
+                float2 v = lds64(a8 + W_CHUNK_BYTES);
+                v.x = fmaf(p.mu, v.x, fmaf(p.alpha, a0, p.lr_wd * w.x));
+                v.y = fmaf(p.mu, v.y, fmaf(p.alpha, a1, p.lr_wd * w.y));
+                w.x -= v.x;
+                w.y -= v.y;
+                if (row_ok && col_base + cl < p.N) {
+                  stg64_na(grow + col_base + cl, w);
+                  stg64_na(p.vel + (size_t)(m0 + row) * p.N + col_base + cl, v);
+                }
+                continue;
+              }
               if (p.mode != 2) {
-                w.x = fmaf(p.alpha, __uint_as_float(r[h][4 * j + 2 * k + 0]), p.beta * w.x);
-                w.y = fmaf(p.alpha, __uint_as_float(r[h][4 * j + 2 * k + 1]), p.beta * w.y);
+                w.x = fmaf(p.alpha, a0, p.beta * w.x);
+                w.y = fmaf(p.alpha, a1, p.beta * w.y);
               }
               if (p.mode != 3 && row_ok && col_base + cl < p.N) stg64_na(grow + col_base + cl, w);
             }
@@ -818,21 +852,22 @@ int sm_count_k1() {
 
 namespace {
 struct MapKey {
-  const void *u, *v, *w;
+  const void *u, *v, *w, *vel;
   int64_t P, K, ldk, M, N, ldm;
   bool operator==(const MapKey& o) const {
-    return u == o.u && v == o.v && w == o.w && P == o.P && K == o.K && ldk == o.ldk && M == o.M && N == o.N &&
-           ldm == o.ldm;
+    return u == o.u && v == o.v && w == o.w && vel == o.vel && P == o.P && K == o.K && ldk == o.ldk && M == o.M &&
+           N == o.N && ldm == o.ldm;
   }
 };
 struct MapEntry {
   MapKey key;
-  CUtensorMap a, b, w, b2;
+  CUtensorMap a, b, w, b2, vm;
 };
 std::mutex g_map_mu;
 std::vector<MapEntry> g_maps;   // small FIFO: one entry per SFB layer (and per gather set)
 constexpr size_t kMapCap = 256;
-bool map_cache_get(const MapKey& k, CUtensorMap* a, CUtensorMap* b, CUtensorMap* w, CUtensorMap* b2) {
+bool map_cache_get(const MapKey& k, CUtensorMap* a, CUtensorMap* b, CUtensorMap* w, CUtensorMap* b2,
+                   CUtensorMap* vm) {
   std::lock_guard<std::mutex> lock(g_map_mu);
   for (const auto& e : g_maps)
     if (e.key == k) {
@@ -840,15 +875,16 @@ bool map_cache_get(const MapKey& k, CUtensorMap* a, CUtensorMap* b, CUtensorMap*
       *b = e.b;
       *w = e.w;
       *b2 = e.b2;
+      *vm = e.vm;
       return true;
     }
   return false;
 }
 void map_cache_put(const MapKey& k, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& w,
-                   const CUtensorMap& b2) {
+                   const CUtensorMap& b2, const CUtensorMap& vm) {
   std::lock_guard<std::mutex> lock(g_map_mu);
   if (g_maps.size() >= kMapCap) g_maps.erase(g_maps.begin());
-  g_maps.push_back(MapEntry{k, a, b, w, b2});
+  g_maps.push_back(MapEntry{k, a, b, w, b2, vm});
 }
 }  // namespace
 
@@ -877,18 +913,19 @@ bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int6
 
 cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
                                  int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg,
-                                 int64_t ldm, const float* bs, float* bias, bool* bias_done) {
+                                 int64_t ldm, const float* bs, float* bias, bool* bias_done, const K1Momentum* mom) {
   if (bias_done) *bias_done = false;
   if (M <= 0 || N <= 0 || K <= 0 || P <= 0) return cudaSuccess;
   if (ldm <= 0) ldm = M;
   if (ldm < M) return cudaErrorInvalidValue;
   if (!recon_tcgen05_supported(Ug, Vg, ldk, M, N, W) || ldk < K) return cudaErrorNotSupported;
-  CUtensorMap tmA, tmB, tmW, tmB2;
   const int variant = knobs().variant;
+  if (mom != nullptr && (variant != 2 || dbg != nullptr || !aligned16(mom->vel))) return cudaErrorNotSupported;
+  CUtensorMap tmA, tmB, tmW, tmB2, tmV;
   // Tensor maps are cached per (buffers, shape): encoding four of them costs ~10 us of host time per
   // launch, which lands on the step whenever the GPU is not far behind the host (small layers).
-  const MapKey key{Ug, Vg, W, P, K, ldk, M, N, ldm};
-  if (dbg == nullptr && map_cache_get(key, &tmA, &tmB, &tmW, &tmB2)) goto have_maps;
+  const MapKey key{Ug, Vg, W, mom ? mom->vel : nullptr, P, K, ldk, M, N, ldm};
+  if (dbg == nullptr && map_cache_get(key, &tmA, &tmB, &tmW, &tmB2, &tmV)) goto have_maps;
   {
   const uint64_t dA[3] = {(uint64_t)ldk, (uint64_t)M, (uint64_t)P};
   // rows [M, ldm) of a worker block belong to other masters (SF-PS): outside the map, so TMA
@@ -906,7 +943,9 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   // the 2-SM kernel stages 128 rows of B per CTA (half of the 256-wide N tile)
   const uint32_t bB2[3] = {BK, (uint32_t)k2sm::BN_CTA, 1};
   if (!encode(&tmB2, Vg, 3, dB, sB, bB2)) return cudaErrorNotSupported;
-  if (dbg == nullptr) map_cache_put(key, tmA, tmB, tmW, tmB2);
+  tmV = tmW;
+  if (mom != nullptr && !encode(&tmV, mom->vel, 2, dW, sW, bW)) return cudaErrorNotSupported;
+  if (dbg == nullptr) map_cache_put(key, tmA, tmB, tmW, tmB2, tmV);
   }
 have_maps:
   Params p;
@@ -921,6 +960,13 @@ have_maps:
   p.beta = beta;
   p.dbg = dbg;
   p.prof = k1_prof_buffer(M, N);
+  p.vel = mom ? mom->vel : nullptr;
+  p.vel_b = mom ? mom->vel_b : nullptr;
+  p.mu = mom ? mom->mu : 0.f;
+  p.lr = mom ? mom->lr : 0.f;
+  p.wd = mom ? mom->wd : 0.f;
+  p.lr_wd = mom ? mom->lr * mom->wd : 0.f;
+  p.inv_p = 1.0f / (float)P;
   p.W = W;
   p.bs = nullptr;
   p.bias = nullptr;
@@ -939,7 +985,8 @@ have_maps:
   p.mode = knobs().mode;
   if (variant == 2 && dbg == nullptr) {
     tmB = tmB2;
-    if (knobs().fbias && bias != nullptr && bs != nullptr && bias_done != nullptr && M < (1 << 30)) {
+    if (knobs().fbias && bias != nullptr && bs != nullptr && bias_done != nullptr && M < (1 << 30) &&
+        (mom == nullptr || mom->vel_b != nullptr)) {
       p.bs = bs;
       p.bias = bias;
       *bias_done = true;
@@ -956,6 +1003,31 @@ have_maps:
     static bool attr_a = false, attr_b = false;
     const int pairs = std::min(p.num_tiles, sm_count_k1() / 2);
     cudaError_t e = cudaSuccess;
+    if (mom != nullptr) {
+      // f4: W and velocity chunks share a slot (2 x 16 KB): <3 stages, 4 slots> when the W stream dominates
+      // (<= 8 factor slabs per tile), else <4, 3>; both 224 KB of shared memory
+      if (p.num_kb <= 8) {
+        constexpr int SM_ = k2sm::smem_bytes(3, 4, true);
+        static bool attr_m1 = false;
+        if (!attr_m1) {
+          e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<3, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
+          if (e != cudaSuccess) return e;
+          attr_m1 = true;
+        }
+        recon_tcgen05_2sm_kernel<3, 4, true><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, tmV, p);
+      } else {
+        constexpr int SM_ = k2sm::smem_bytes(4, 3, true);
+        static bool attr_m2 = false;
+        if (!attr_m2) {
+          e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<4, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
+          if (e != cudaSuccess) return e;
+          attr_m2 = true;
+        }
+        recon_tcgen05_2sm_kernel<4, 3, true><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, tmV, p);
+      }
+      g_launches.fetch_add(1);
+      return cudaGetLastError();
+    }
     if (cfg == 0) {
       constexpr int SM_ = k2sm::smem_bytes(3, 8);
       if (!attr_a) {
@@ -963,7 +1035,7 @@ have_maps:
         if (e != cudaSuccess) return e;
         attr_a = true;
       }
-      recon_tcgen05_2sm_kernel<3, 8><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, p);
+      recon_tcgen05_2sm_kernel<3, 8><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, tmW, p);
     } else if (cfg == 3) {
       constexpr int SM_ = k2sm::smem_bytes(5, 4);
       static bool attr_d = false;
@@ -972,7 +1044,7 @@ have_maps:
         if (e != cudaSuccess) return e;
         attr_d = true;
       }
-      recon_tcgen05_2sm_kernel<5, 4><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, p);
+      recon_tcgen05_2sm_kernel<5, 4><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, tmW, p);
     } else if (cfg == 2) {
       constexpr int SM_ = k2sm::smem_bytes(2, 8);
       static bool attr_c = false;
@@ -981,7 +1053,7 @@ have_maps:
         if (e != cudaSuccess) return e;
         attr_c = true;
       }
-      recon_tcgen05_2sm_kernel<2, 8><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, p);
+      recon_tcgen05_2sm_kernel<2, 8><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, tmW, p);
     } else {
       constexpr int SM_ = k2sm::smem_bytes(4, 5);
       if (!attr_b) {
@@ -989,7 +1061,7 @@ have_maps:
         if (e != cudaSuccess) return e;
         attr_b = true;
       }
-      recon_tcgen05_2sm_kernel<4, 5><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, p);
+      recon_tcgen05_2sm_kernel<4, 5><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, tmW, p);
     }
     g_launches.fetch_add(1);
     return cudaGetLastError();
