@@ -9,12 +9,12 @@ import subprocess
 import sys
 from collections import OrderedDict
 
-OURS = ("poseidon", "recon_tcgen05", "recon_simt", "ps_shard_sgd", "pack_t_kernel", "bias_update", "ps_sim")
+OURS = ("poseidon", "recon_tcgen05", "recon_simt", "ps_shard_sgd", "pack_t_kernel", "pack_uv_kernel", "bias_update", "ps_sim")
 
 
 def short(name):
     for key in ("recon_tcgen05_2sm_kernel", "recon_tcgen05_kernel", "recon_simt_kernel", "ps_shard_sgd_kernel", "ps_shard_sgd_scalar",
-                "pack_t_kernel", "bias_update_kernel", "bias_momentum_kernel", "ps_sim_kernel", "ps_nvls_kernel",
+                "pack_t_kernel", "pack_uv_kernel", "bias_update_kernel", "bias_momentum_kernel", "ps_sim_kernel", "ps_nvls_kernel",
                 "sfb_bcast_kernel", "ps_momentum_kernel", "momentum_apply_kernel"):
         if key in name:
             return key + (" [libposeidon]")

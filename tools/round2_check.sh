@@ -7,6 +7,7 @@ NG=$(nvidia-smi -L | wc -l)
 python paper_1512_06216_b200/build.py --force > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
 (echo "HEAD=$SHA GPUs=$NG"; timeout -s KILL 1500 python -m pytest tests -x -q -m gpu -p no:cacheprovider) > gpurun_out/pytest_gpu_r2.log 2>&1
 POSEIDON_K1_PROF=1 CUDA_VISIBLE_DEVICES=0 timeout -s KILL 300 python tools/k1_prof.py > gpurun_out/k1_prof_r2.txt 2>&1
+CUDA_VISIBLE_DEVICES=0 timeout -s KILL 120 python tools/peaks.py > gpurun_out/peaks_r2.json 2> gpurun_out/peaks_r2.err
 echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu_r2.log
 for P in 2 4; do
   [ "$NG" -ge "$P" ] || continue
