@@ -192,6 +192,24 @@ __device__ __forceinline__ void stg128_na(float* ptr, float4 v) {
                "f"(v.w)
                : "memory");
 }
+// register-path W stream (RW epilogue): W is read once, so loads bypass L1 and are first out of L2
+__device__ __forceinline__ void ldg256_ef(const float* ptr, float4& a, float4& b, uint64_t pol) {
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+               : "l"(ptr), "l"(pol));
+}
+__device__ __forceinline__ float4 ldg128_ef(const float* ptr, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stg256_na(float* ptr, float4 a, float4 b) {
+  asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(ptr), "f"(a.x), "f"(a.y),
+               "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+               : "memory");
+}
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -511,10 +529,129 @@ __device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t mask) {
                : "memory");
 }
 
+// RW epilogue (round 2; production for plain SGD): W never passes through shared memory.  Each epilogue
+// warp owns its 32 TMEM lanes (= 32 rows of W) and, of every tile, the 32-column chunks c = e, e+2, ...
+// (e = its group); thread t holds row t of the chunk: one tcgen05.ld 32x32b.x32 gives it 32 consecutive
+// accumulator columns, and its 32 W values are four 256-bit loads (each warp instruction = 32 rows x one
+// full 32-B sector).  W is loaded D chunks ahead of the accumulator into registers (a load cursor running
+// through the same chunk sequence), so 8 warps x D x 4 KB of W reads are in flight per SM while the
+// MMAs run; the smem-ring pattern (TMA W boxes + LDS) capped the W stream at ~5.4 TB/s
+// (profiles/w_stream_probe_r1.txt).  The TMEM buffer is released right after the warp's last TMEM load
+// of the tile, before its W stores.
+template <int D>
+__device__ __forceinline__ void rw_epilogue(const Params& p, uint32_t tmem_base, uint64_t* tfull,
+                                            uint64_t* tempty_local, int pair, int npairs, uint32_t rank, int warp,
+                                            int lane) {
+  const int e = (warp - 4) >> 2, q = warp & 3;
+  const uint64_t pol = policy_evict_first();
+  const bool v8ok = (p.N & 7) == 0;   // 32-B aligned rows
+  auto chunks = [&](int tile, int& m0, int& n0) {
+    int mt, nt;
+    tile_coords(p, tile, mt, nt);
+    n0 = nt * k2sm::BN;
+    m0 = mt * k2sm::BM + (int)rank * k2sm::BM_CTA;
+    int n = (p.N - n0 + W_CHUNK_COLS - 1) / W_CHUNK_COLS;
+    if (n > CHUNKS_PER_TILE) n = CHUNKS_PER_TILE;
+    return m0 >= p.M ? 0 : n;
+  };
+  // load cursor: (lt, lc), D chunks of this warp's sequence ahead of the consumer
+  int lt = pair, lc = e;
+  auto lnorm = [&]() {
+    int m0, n0;
+    while (lt < p.num_tiles && lc >= chunks(lt, m0, n0)) {
+      lt += npairs;
+      lc = e;
+    }
+  };
+  auto load = [&](float4 (&b)[8]) {
+    if (lt >= p.num_tiles) return;
+    int m0, n0;
+    chunks(lt, m0, n0);
+    const int row = m0 + q * 32 + lane, col = n0 + lc * W_CHUNK_COLS;
+    if (row < p.M) {
+      const float* src = p.W + (size_t)row * p.N + col;
+      const int ncol = p.N - col;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (v8ok && 8 * j + 8 <= ncol) {
+          ldg256_ef(src + 8 * j, b[2 * j], b[2 * j + 1], pol);
+        } else {
+          if (8 * j + 4 <= ncol) b[2 * j] = ldg128_ef(src + 8 * j, pol);
+          if (8 * j + 8 <= ncol) b[2 * j + 1] = ldg128_ef(src + 8 * j + 4, pol);
+        }
+      }
+    }
+    lc += 2;
+    lnorm();
+  };
+  float4 buf[D][8];
+  lnorm();
+#pragma unroll
+  for (int d = 0; d < D; ++d) load(buf[d]);
+  int slot = 0, it = 0;
+  for (int tile = pair; tile < p.num_tiles; tile += npairs, ++it) {
+    int m0, n0;
+    const int nc = chunks(tile, m0, n0);
+    const int acc = it & 1;
+    mbar_wait(&tfull[acc], (it >> 1) & 1);
+    tc_fence_after();
+    bool released = false;
+    const int row = m0 + q * 32 + lane;
+    for (int c = e; c < nc; c += 2) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * k2sm::BN + c * W_CHUNK_COLS), r);
+      tmem_ld_wait();
+      if (c + 2 >= nc) {   // this warp's last TMEM read of the tile: hand the accumulator back early
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_local[acc]);
+        released = true;
+      }
+      const int col = n0 + c * W_CHUNK_COLS, ncol = p.N - col;
+      float* dst = p.W + (size_t)row * p.N + col;
+      auto consume = [&](float4 (&b)[8]) {
+        if (row < p.M) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 w = b[j];
+            w.x = fmaf(p.alpha, __uint_as_float(r[4 * j + 0]), p.beta * w.x);
+            w.y = fmaf(p.alpha, __uint_as_float(r[4 * j + 1]), p.beta * w.y);
+            w.z = fmaf(p.alpha, __uint_as_float(r[4 * j + 2]), p.beta * w.z);
+            w.w = fmaf(p.alpha, __uint_as_float(r[4 * j + 3]), p.beta * w.w);
+            b[j] = w;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (v8ok && 8 * j + 8 <= ncol) {
+              stg256_na(dst + 8 * j, b[2 * j], b[2 * j + 1]);
+            } else {
+              if (8 * j + 4 <= ncol) stg128_na(dst + 8 * j, b[2 * j]);
+              if (8 * j + 8 <= ncol) stg128_na(dst + 8 * j + 4, b[2 * j + 1]);
+            }
+          }
+        }
+        load(b);   // the slot's next chunk (D ahead)
+      };
+      // static register indexing: one unrolled body per ring slot
+      if (D == 1 || slot == 0) consume(buf[0]);
+      else if (D >= 2 && slot == 1) consume(buf[D >= 2 ? 1 : 0]);
+      else if (D >= 3 && slot == 2) consume(buf[D >= 3 ? 2 : 0]);
+      else if (D >= 4) consume(buf[D >= 4 ? 3 : 0]);
+      slot = (slot + 1 == D) ? 0 : slot + 1;
+    }
+    if (!released) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_local[acc]);
+    }
+  }
+}
+
 // MOM (f4, fused momentum): every W slot carries the matching velocity chunk right after the W chunk
 // (2 x 16 KB); the epilogue reads both, writes both (16 B per element instead of K1-on-the-velocity + a
 // separate pass, 24 B).
-template <int NST, int NWS, bool MOM = false>
+// RWD > 0: the RW epilogue with RWD chunks of W in flight per warp (NWS = 0: no W slots, no W TMA).
+template <int NST, int NWS, bool MOM = false, int RWD = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     recon_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmV,
@@ -645,7 +782,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
         }
       }
     }
-    if (lane == 0 && p.mode != 7) {
+    if (RWD == 0 && lane == 0 && p.mode != 7) {
       const uint64_t pol = p.w_policy ? policy_evict_normal() : policy_evict_first();
       uint32_t g = 0;
       for (int tile = pair; tile < p.num_tiles; tile += npairs) {
@@ -679,6 +816,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
         mbar_arrive_cluster_release(acc == 0 ? tl0 : tl1);
       }
     }
+  } else if (RWD > 0) {
+    if constexpr (RWD > 0) rw_epilogue<RWD>(p, tmem_base, tfull, tempty_local, pair, npairs, rank, warp, lane);
   } else if (warp >= 4) {
     // ===================== epilogue: 2 groups x 4 warps =====================
     // Group e processes the chunks g with g % 2 == e (g = global chunk counter shared with the W
@@ -793,12 +932,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
 //   POSEIDON_K1_MODE=5|6    TMEM loads without MMA / MMA + accumulator handshake without TMEM loads
 //   POSEIDON_K1_MODE=7      operands + MMA + TMEM loads, no W traffic
 //   POSEIDON_K1_FUSE_BIAS=0 bias update as a separate kernel after K1 (A/B of the fused update)
+//   POSEIDON_K1_RW=0|1      force the TMA W ring (0) or the RW epilogue (1) for plain SGD (default: by regime)
+//   POSEIDON_K1_RWD=2|3|4   W chunks in flight per epilogue warp (RW epilogue);  POSEIDON_K1_RWS=4|5|6  stages
 struct K1Knobs {
-  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0, fbias = 1;
+  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0, fbias = 1, rw = -1, rwd = 3, rws = 6;
   K1Knobs() {
+    if (const char* v = getenv("POSEIDON_K1_RW")) rw = v[0] - '0';
+    if (const char* v = getenv("POSEIDON_K1_RWD")) rwd = v[0] - '0';
+    if (const char* v = getenv("POSEIDON_K1_RWS")) rws = v[0] - '0';
     if (const char* v = getenv("POSEIDON_K1_VARIANT")) variant = (v[0] == '1') ? 1 : 2;
     if (const char* r = getenv("POSEIDON_K1_RASTER")) raster = (r[0] == 'm') ? 1 : 0;
-    if (const char* c = getenv("POSEIDON_K1_CFG")) cfg = (c[0] == 'a') ? 0 : (c[0] == 'c') ? 2 : (c[0] == 'd') ? 3 : 1;
+    // a <3,8>  b <4,5>  c <2,8>  d <5,4>  e <2,10>  f <3,7>  g <4,6>  h <2,9>
+    if (const char* c = getenv("POSEIDON_K1_CFG")) cfg = (c[0] >= 'a' && c[0] <= 'h') ? c[0] - 'a' : 1;
     if (const char* e = getenv("POSEIDON_K1_EPI")) epi = (e[0] == '1') ? 1 : 2;
     if (const char* w = getenv("POSEIDON_K1_WPOL")) wpol = w[0] - '0';
     if (const char* m = getenv("POSEIDON_K1_MODE")) mode = m[0] - '0';
@@ -996,10 +1141,11 @@ have_maps:
     p.num_tiles = p.m_tiles * p.n_tiles;
     // Regime: with few factor rows per tile the kernel is bound by the W
     // read-modify-write, so more W chunks in flight beat deeper operand staging.
-    // Stage / W-slot split (tools/k1_sweep*.sh): with <= 8 factor slabs per tile the W stream
-    // dominates and <4 stages, 5 W slots> wins; with more slabs deeper operand staging <5, 4> wins
-    // (fc6 P*K=2048: 686 -> 743 TFLOP/s).  0: <3,8>, 1: <4,5>, 2: <2,8>, 3: <5,4>.
-    const int cfg = knobs().cfg >= 0 ? knobs().cfg : (p.num_kb <= 8 ? 1 : 3);
+    // Stage / W-slot split (tools/k1_sweep*.sh, tools/k1_cfg_bench.sh): with <= 8 factor slabs per tile the
+    // W stream dominates and <4 stages, 6 W slots> wins (round 2: fc6 P*K=256 in the C3 step 84 -> 69 us,
+    // alone 67.6 us either way; <4,5> was the round-1 pick); with more slabs deeper operand staging <5, 4>
+    // wins (fc6 P*K=2048: 686 -> 743 TFLOP/s).  Letters of POSEIDON_K1_CFG in K1Knobs.
+    const int cfg = knobs().cfg >= 0 ? knobs().cfg : (p.num_kb <= 8 ? 6 : 3);
     static bool attr_a = false, attr_b = false;
     const int pairs = std::min(p.num_tiles, sm_count_k1() / 2);
     cudaError_t e = cudaSuccess;
@@ -1028,43 +1174,52 @@ have_maps:
       g_launches.fetch_add(1);
       return cudaGetLastError();
     }
-    if (cfg == 0) {
-      constexpr int SM_ = k2sm::smem_bytes(3, 8);
-      if (!attr_a) {
-        e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
-        if (e != cudaSuccess) return e;
-        attr_a = true;
-      }
-      recon_tcgen05_2sm_kernel<3, 8><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, tmW, p);
-    } else if (cfg == 3) {
-      constexpr int SM_ = k2sm::smem_bytes(5, 4);
-      static bool attr_d = false;
-      if (!attr_d) {
-        e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<5, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
-        if (e != cudaSuccess) return e;
-        attr_d = true;
-      }
-      recon_tcgen05_2sm_kernel<5, 4><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, tmW, p);
-    } else if (cfg == 2) {
-      constexpr int SM_ = k2sm::smem_bytes(2, 8);
-      static bool attr_c = false;
-      if (!attr_c) {
-        e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
-        if (e != cudaSuccess) return e;
-        attr_c = true;
-      }
-      recon_tcgen05_2sm_kernel<2, 8><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, tmW, p);
-    } else {
-      constexpr int SM_ = k2sm::smem_bytes(4, 5);
-      if (!attr_b) {
-        e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
-        if (e != cudaSuccess) return e;
-        attr_b = true;
-      }
-      recon_tcgen05_2sm_kernel<4, 5><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, tmW, p);
+    // RW epilogue (no W slots: the shared memory goes to 6 operand stages) where the tensor pipe is the
+    // bound, i.e. >= 32 factor slabs per tile (P*K >= 1024): tools/k1_ab.py, profiles/r2/k1_rw_r2.md
+    // (fc6 P*K = 1024: 117.6 -> 109.3 us, P*K = 2048: 192.5 -> 186.4 us, bit-identical W); the TMA W ring
+    // stays where the W read-modify-write is the bound (fc6 P*K = 256: 67.6 vs 79.9 us).
+    const bool rw = knobs().rw >= 0 ? knobs().rw == 1 : p.num_kb >= 32;
+    if (rw && p.mode == 0 && p.epi_groups == 2) {
+      auto go = [&](auto kern, int smem, bool& attr) -> cudaError_t {
+        if (!attr) {
+          cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+          if (ea != cudaSuccess) return ea;
+          attr = true;
+        }
+        kern<<<2 * pairs, NUM_THREADS_2SM, smem, s>>>(tmA, tmB, tmW, tmW, p);
+        g_launches.fetch_add(1);
+        return cudaGetLastError();
+      };
+      static bool a62 = false, a63 = false, a64 = false, a43 = false, a53 = false;
+      const int d = knobs().rwd, st = knobs().rws;
+      if (st == 4) return go(recon_tcgen05_2sm_kernel<4, 0, false, 3>, k2sm::smem_bytes(4, 0), a43);
+      if (st == 5) return go(recon_tcgen05_2sm_kernel<5, 0, false, 3>, k2sm::smem_bytes(5, 0), a53);
+      if (d == 2) return go(recon_tcgen05_2sm_kernel<6, 0, false, 2>, k2sm::smem_bytes(6, 0), a62);
+      if (d == 4) return go(recon_tcgen05_2sm_kernel<6, 0, false, 4>, k2sm::smem_bytes(6, 0), a64);
+      return go(recon_tcgen05_2sm_kernel<6, 0, false, 3>, k2sm::smem_bytes(6, 0), a63);
     }
-    g_launches.fetch_add(1);
-    return cudaGetLastError();
+    // the TMA W ring: <operand stages, W slots>
+    auto ring = [&](auto kern, int smem, bool& attr) -> cudaError_t {
+      if (!attr) {
+        cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (ea != cudaSuccess) return ea;
+        attr = true;
+      }
+      kern<<<2 * pairs, NUM_THREADS_2SM, smem, s>>>(tmA, tmB, tmW, tmW, p);
+      g_launches.fetch_add(1);
+      return cudaGetLastError();
+    };
+    static bool at[8] = {};
+    switch (cfg) {
+      case 0: return ring(recon_tcgen05_2sm_kernel<3, 8>, k2sm::smem_bytes(3, 8), at[0]);
+      case 2: return ring(recon_tcgen05_2sm_kernel<2, 8>, k2sm::smem_bytes(2, 8), at[2]);
+      case 3: return ring(recon_tcgen05_2sm_kernel<5, 4>, k2sm::smem_bytes(5, 4), at[3]);
+      case 4: return ring(recon_tcgen05_2sm_kernel<2, 10>, k2sm::smem_bytes(2, 10), at[4]);
+      case 5: return ring(recon_tcgen05_2sm_kernel<3, 7>, k2sm::smem_bytes(3, 7), at[5]);
+      case 6: return ring(recon_tcgen05_2sm_kernel<4, 6>, k2sm::smem_bytes(4, 6), at[6]);
+      case 7: return ring(recon_tcgen05_2sm_kernel<2, 9>, k2sm::smem_bytes(2, 9), at[7]);
+      default: return ring(recon_tcgen05_2sm_kernel<4, 5>, k2sm::smem_bytes(4, 5), at[1]);
+    }
   }
   static bool attr_set = false;
   if (!attr_set) {

@@ -22,6 +22,12 @@ struct Cfg {
 
 // byte offset of element (mn, k) of an MN-major operand with MN extent `mn_ext` (K = 8)
 __device__ uint32_t mn_off(int mn, int k, int layout, uint32_t lbo, uint32_t sbo) {
+  if (layout == 1) {                  // SWIZZLE_128B_BASE32B (CUTLASS Layout_MN_SW128_32B_Atom: the only MN-major
+                                      // tf32 layout): 128-B rows (one per k), 32-B chunks XOR (k mod 4); MN
+                                      // chunks of 32 at LBO, groups of 4 k rows at SBO
+    int j = mn / 32, s = (mn % 32) / 8, t = mn % 8;
+    return j * lbo + (k / 4) * sbo + (k % 4) * 128 + ((s ^ (k % 4)) << 5) + t * 4;
+  }
   if (layout == 2) {                  // 32 tf32 per 128-B row; chunk j = mn / 32 at j * LBO; row k at 128 k
     int j = mn / 32, s = (mn % 32) / 4, t = mn % 4;
     return j * lbo + k * 128 + ((s ^ (k & 7)) << 4) + t * 4;
@@ -117,6 +123,11 @@ int main() {
     for (uint32_t l : sw_lbo)
       for (uint32_t s : sw_sbo)
         for (int lm = 0; lm < 2; ++lm) cfgs.push_back({ab & 1, (ab >> 1) & 1, 2, l, s, lm});
+  // SWIZZLE_128B_BASE32B (layout type 1): packed LBO = 8 k rows x 128 B = 1024, SBO = 4 rows = 512
+  const uint32_t b32_pairs[][2] = {{1024, 512}, {512, 1024}, {4096, 512}, {1024, 128}, {128, 512}, {2048, 512}};
+  for (int ab = 1; ab <= 3; ++ab)
+    for (auto& pr : b32_pairs)
+      for (int lm = 0; lm < 2; ++lm) cfgs.push_back({ab & 1, (ab >> 1) & 1, 1, pr[0], pr[1], lm});
   // INTERLEAVE: core matrices 128 B; MN groups at SBO (= 128 when packed), K groups at LBO (one group here)
   for (int ab = 1; ab <= 3; ++ab)
     for (int lm = 0; lm < 2; ++lm) {
@@ -137,7 +148,7 @@ int main() {
         nz += D[m * 256 + n] != 0.f;
       }
     printf("A %s B %s layout %s lbo %5u sbo %5u lbo_mode %d: %s maxerr %g nonzero %d%s\n", cf.a_mn ? "MN" : "K ",
-           cf.b_mn ? "MN" : "K ", cf.layout == 2 ? "SW128" : "INTLV", cf.lbo, cf.sbo, cf.lbo_mode, cudaGetErrorString(e),
+           cf.b_mn ? "MN" : "K ", cf.layout == 2 ? "SW128" : cf.layout == 1 ? "SW128_32B" : "INTLV", cf.lbo, cf.sbo, cf.lbo_mode, cudaGetErrorString(e),
            maxerr, nz, maxerr == 0 ? "   <== EXACT" : "");
     if (e != cudaSuccess) return 1;
   }
