@@ -47,6 +47,11 @@ def parse():
     ap.add_argument("--else-branch", default="ps", choices=["ps", "sfps"],
                     help="how FC layers the SACP rule sends to the server execute: full-gradient PS (reading Z7) "
                          "or the literal sharded SF-PS of Alg. 3 (reading Z20, POSEIDON_FLAG_SFPS)")
+    ap.add_argument("--factors", default="auto", choices=["auto", "async", "mn", "pack"],
+                    help="where the SFB factors are read: async = POSEIDON_FLAG_INPLACE_FACTORS (K3 on the library's "
+                         "stream, off the backward's); mn = + POSEIDON_FLAG_INPLACE_MN (N = 1: K1 reads them MN-major, "
+                         "no K3); pack = K3 on the backward's stream (round 1); auto = mn at N = 1 "
+                         "(profiles/r2/factors_r2.md: +1%% images/s), pack at N > 1")
     ap.add_argument("--dwbp", default="on", choices=["on", "off"])
     ap.add_argument("--recon", default="tf32", choices=["tf32", "fp32"])
     ap.add_argument("--nvls", default="auto", choices=["auto", "on", "off"],
@@ -386,6 +391,13 @@ def run_poseidon(args):
     early_v = args.early_v == "on" or (args.early_v == "auto" and world > 1)
     if early_v:
         flags |= pz.FLAG_EARLY_V
+    if args.factors == "auto":
+        args.factors = "mn" if world == 1 else "pack"
+    if args.factors != "pack":
+        flags |= pz.FLAG_INPLACE_FACTORS
+    if args.factors == "mn":
+        flags |= pz.FLAG_INPLACE_MN
+    inplace = (args.factors == "mn" and world == 1 and not args.ssp and args.dwbp == "on" and args.recon == "tf32")
     ctx = pz.Context(rank=rank, world=world, device=local, nccl_id=nccl_id, flags=flags)
 
     torch.manual_seed(6216)          # identical weights on every rank
@@ -479,7 +491,7 @@ def run_poseidon(args):
         top = max(sfb, key=lambda p: p.M * p.N)
         kms = statistics.mean(ctx.layer_stats(top.layer_id, a)["kernel_ms"] for a in range(n_stats))
         M, N, Kf, P = top.M, top.N, top.K, world
-        ldk = (Kf + 3) // 4 * 4
+        ldk = Kf if inplace else (Kf + 3) // 4 * 4
         flops = 2.0 * M * N * Kf * P
         byts = 8.0 * M * N + 4.0 * P * ldk * (M + N)
         tf32_peak = peaks["tf32_tflops_sustained"]
@@ -499,15 +511,22 @@ def run_poseidon(args):
         if args.recon == "tf32":
             # context for `frac` (which is the in-step number): the same K1 launch on the same shape ALONE,
             # after the timed region, each launch queued behind a device spin (device time only)
-            Ug = torch.randn(P, M, ldk, device=dev).mul_(0.01)
-            Vg = torch.randn(P, N, ldk, device=dev).relu_()
+            if inplace:   # the factors as the layer leaves them: U [K x M], V [K x N] (MN-major K1)
+                Ug = torch.randn(Kf, M, device=dev).mul_(0.01)
+                Vg = torch.randn(Kf, N, device=dev).relu_()
+            else:
+                Ug = torch.randn(P, M, ldk, device=dev).mul_(0.01)
+                Vg = torch.randn(P, N, ldk, device=dev).relu_()
             Wt = torch.zeros(M, N, device=dev)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ts = []
             for _ in range(6):
                 torch.cuda._sleep(200_000)
                 e0.record(stream)
-                pz.reconstruct_sgd(Ug, Vg, P, Kf, ldk, M, N, Wt, -1e-3, stream=stream)
+                if inplace:
+                    pz.reconstruct_sgd_mn(Ug, Vg, P, Kf, M, N, Wt, -1e-3, stream=stream)
+                else:
+                    pz.reconstruct_sgd(Ug, Vg, P, Kf, ldk, M, N, Wt, -1e-3, stream=stream)
                 e1.record(stream)
                 e1.synchronize()
                 ts.append(e0.elapsed_time(e1))
@@ -528,7 +547,12 @@ def run_poseidon(args):
                 "algorithmic_bytes": byts, "peak_source": peaks["source"]}
     # K3 (factor pack) of every SFB layer, summed per step: 8 B per packed element (read + write) plus the
     # column sums; timed by the library's events on the producer stream (layer stats pack_ms)
-    if sfb:
+    if sfb and inplace:
+        roof["pack"] = {"kernel": "none: factors read in place by K1 (POSEIDON_FLAG_INPLACE_FACTORS, N = 1)",
+                        "ms_per_step": 0.0, "algorithmic_bytes": 0.0, "achieved": None, "unit": "GB/s", "frac": None,
+                        "note": "K1 consumes dl/dy and a_i MN-major where the backward wrote them; its idle lanes form "
+                                "the bias sums (4 K M B of extra reads per SFB layer, not counted as algorithmic)"}
+    elif sfb:
         pk_ms, pk_bytes = 0.0, 0.0
         for p in sfb:
             pk_ms += statistics.mean(ctx.layer_stats(p.layer_id, a)["pack_ms"] for a in range(n_stats))
@@ -538,7 +562,9 @@ def run_poseidon(args):
         roof["pack"] = {"kernel": "K3 pack_uv (all SFB layers of one step)", "ms_per_step": pk_ms,
                         "algorithmic_bytes": pk_bytes, "achieved": ach, "unit": "GB/s",
                         "frac": (ach / peaks["hbm_gbs"]) if ach else None,
-                        "note": "in-step, on the compute stream; V packed at forward time when early_v"}
+                        "note": ("in-step, on the library's sync stream (POSEIDON_FLAG_INPLACE_FACTORS)"
+                                 if args.factors == "async" else "in-step, on the compute stream")
+                                + "; V packed at forward time when early_v"}
     roof["traffic"] = None
     tr_path = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(tr_path):
@@ -637,7 +663,7 @@ def run_poseidon(args):
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "tf32" if args.recon == "tf32" else "f32", "data": "synthetic",
             "config": workload_config(args, cfg, world),
-            "details": {"scheme": scheme, "else_branch": args.else_branch, "early_v": early_v, "dwbp": args.dwbp, "recon": args.recon, "lr": args.lr,
+            "details": {"scheme": scheme, "else_branch": args.else_branch, "early_v": early_v, "factors": args.factors, "inplace_mn_k1": inplace, "dwbp": args.dwbp, "recon": args.recon, "lr": args.lr,
                         "momentum": args.momentum, "weight_decay": args.weight_decay,
                         "memory_format": args.memory_format,
                         "ps_path": ("nvls-fused" if sync.nvls_active else

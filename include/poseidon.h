@@ -105,6 +105,18 @@ typedef struct {
 #define POSEIDON_FLAG_EARLY_V 0x80u    /* enables poseidon_sfb_post_input: an SFB layer's input factors V may be
                                          broadcast during the forward pass (BSP with DWBP only: not combined
                                          with POSEIDON_FLAG_SSP1 or POSEIDON_FLAG_DWBP_OFF) */
+#define POSEIDON_FLAG_INPLACE_FACTORS 0x100u /* round 2 (BSP with DWBP, SFB layers): the library reads U and V of
+                                         poseidon_sync_fc_sfb in place, asynchronously on its own streams, so no
+                                         factor work stays on the caller's (backward's) stream: the pack (K3) runs
+                                         on the stream the sync continues on (comm at world > 1, recon at 1).  The
+                                         CALLER then keeps U and V unchanged until the layer's sync is done (e.g.
+                                         tensor.record_stream on both poseidon_stream()s before freeing them, or
+                                         poseidon_wait_layer). */
+#define POSEIDON_FLAG_INPLACE_MN 0x200u /* with POSEIDON_FLAG_INPLACE_FACTORS, at world == 1 (TF32, 16-B aligned U / V,
+                                         M and N multiples of 4): no pack at all, K1 consumes U and V MN-major and
+                                         forms the bias sums itself; the tensor core then reads the fp32 factors as
+                                         TF32 (13 low mantissa bits dropped) instead of the pack's RN rounding
+                                         (reading Z12'). */
 
 typedef struct poseidon_ctx* poseidon_ctx_t;
 
@@ -162,7 +174,8 @@ int32_t poseidon_choose_scheme(int32_t kind, int64_t M, int64_t N, int64_t K, in
  * the library's streams: all-gather of all ranks' factors (NCCL, skipped at
  * P == 1) and the fused reconstruction + SGD  W += alpha * Ug^T Vg,
  * b += alpha * sum_rows Ug.  U and V may be reused after the producer stream
- * passes this point.  K must equal the registered K.
+ * passes this point (with POSEIDON_FLAG_INPLACE_FACTORS at world == 1: only once
+ * the layer's sync is done, see the flag).  K must equal the registered K.
  * SF-PS layers (POSEIDON_SCHEME_SFPS) take the same call: after the pack, each
  * rank sends its U rows of master q's block to q (NCCL send/recv) and all-gathers
  * V and the bias sums; master r runs K1 on its rows [rb, re) only
@@ -296,6 +309,12 @@ poseidon_status_t poseidon_ps_layer_buffers(poseidon_ctx_t ctx, int32_t layer_id
  * broadcast kernel (FLAG_NVLS_SFB), 3 = SF-PS layer (NCCL send/recv of U row blocks, all-gather of V, broadcast of
  * the masters' W rows).  Negative status for a bad id or a PS layer. */
 int32_t poseidon_sfb_path(poseidon_ctx_t ctx, int32_t layer_id);
+
+/* The library's streams (cudaStream_t as poseidon_stream_t), e.g. for the caller's allocator to order
+ * buffer reuse after in-place factor reads (POSEIDON_FLAG_INPLACE_FACTORS).  NULL for a bad ctx / which. */
+#define POSEIDON_STREAM_COMM 0
+#define POSEIDON_STREAM_RECON 1
+poseidon_stream_t poseidon_stream(poseidon_ctx_t ctx, int32_t which);
 /* Human-readable state of the fused NVLS PS path ("active", "not requested", or the NCCL error). */
 const char* poseidon_nvls_status(poseidon_ctx_t ctx);
 
@@ -381,6 +400,18 @@ poseidon_status_t poseidon_ps_shard_update(const float* g, float* W, int64_t cou
 poseidon_status_t poseidon_reconstruct_sgd(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk,
                                            int64_t M, int64_t N, float* W, float alpha, int32_t recon,
                                            poseidon_stream_t stream);
+
+/* Reconstruction alone on the factors in the layer's own (MN-major) layout, no pack (round 2, step (3) of
+ * SFB P:L331, Eq. 5): W[M x N] += alpha * sum_p sum_k<K U[p][k][m] V[p][k][n], where worker block p
+ * of U starts at U + p*ublk and its row k at + k*ldu (M contiguous: the error messages dl/dy [K x M] exactly
+ * as the backward wrote them), V alike with ldv / vblk (the layer input [K x N]).  tcgen05 only
+ * (POSEIDON_RECON_TF32 semantics; the tensor core reads fp32 operands as TF32, i.e. drops their 13 low
+ * mantissa bits, reading Z12'); needs U, V, W 16-byte aligned, ldu >= M, ldv >= N, ldu, ldv, N multiples of
+ * 4 and, for P > 1, ublk >= K*ldu and vblk >= K*ldv multiples of 4 (ignored at P = 1).  Nothing is
+ * allocated; errors: INVALID_ARG, ALIGNMENT (a layout the TMA maps cannot express), CUDA. */
+poseidon_status_t poseidon_reconstruct_sgd_mn(const float* U, int64_t ldu, int64_t ublk, const float* V, int64_t ldv,
+                                              int64_t vblk, int32_t P, int64_t K, int64_t M, int64_t N, float* W,
+                                              float alpha, poseidon_stream_t stream);
 
 /* The SF-PS master's reconstruction (reading Z20): rows [m0, m1) only of the above,
  * W[m][n] += alpha * sum_p sum_k<K Ug[p][m][k] Vg[p][n][k] for m0 <= m < m1 and every n, with

@@ -24,7 +24,8 @@ SCHEME_PS, SCHEME_SFB, SCHEME_SFPS = 0, 1, 2
 LAYER_CONV, LAYER_FC = 0, 1
 RECON_TF32, RECON_FP32 = 0, 1
 FLAG_DWBP_OFF, FLAG_NO_PRIORITY, FLAG_NVLS_PS, FLAG_SYMM_SFB, FLAG_NVLS_SFB, FLAG_SSP1 = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
-FLAG_SFPS, FLAG_EARLY_V = 0x40, 0x80
+FLAG_SFPS, FLAG_EARLY_V, FLAG_INPLACE_FACTORS, FLAG_INPLACE_MN = 0x40, 0x80, 0x100, 0x200
+STREAM_COMM, STREAM_RECON = 0, 1
 SFB_PATH_NCCL, SFB_PATH_NCCL_SYMM, SFB_PATH_NVLS, SFB_PATH_SFPS = 0, 1, 2, 3
 PS_ZERO_GRAD = 0x1
 
@@ -127,6 +128,9 @@ _SIGS = {
     "poseidon_pack_factors": (_i32, [_vp, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _vp]),
     "poseidon_reconstruct_sgd_rows": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _f, _i32,
                                              _vp]),
+    "poseidon_stream": (_vp, [_vp, _i32]),
+    "poseidon_reconstruct_sgd_mn": (_i32, [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i64, _i64, _i64, _vp, _f,
+                                           _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(lib, _name)
@@ -302,6 +306,14 @@ class Context:
         """SSP: apply every layer's deferred update (collective; no-op without FLAG_SSP1)."""
         _check(lib.poseidon_flush(self.h, _stream(stream)))
 
+    def stream(self, which=STREAM_RECON):
+        """The library's comm / reconstruction stream as a torch.cuda.ExternalStream (e.g. for record_stream)."""
+        import torch
+        h = lib.poseidon_stream(self.h, which)
+        if not h:
+            raise PoseidonError(ERR_INVALID_ARG, "poseidon_stream: bad context or stream id")
+        return torch.cuda.ExternalStream(h, device=torch.device("cuda", self.device))
+
     def sfb_path(self, layer_id) -> int:
         r = lib.poseidon_sfb_path(self.h, layer_id)
         _check(min(r, 0))
@@ -376,6 +388,15 @@ def ps_shard_update(g, W, count, alpha, stats=None, stream=None):
 def reconstruct_sgd(Ug, Vg, P, K, ldk, M, N, W, alpha, recon=RECON_TF32, stream=None):
     _check(lib.poseidon_reconstruct_sgd(_ptr(Ug), _ptr(Vg), P, K, ldk, M, N, _ptr(W), float(alpha), recon,
                                         _stream(stream)))
+
+
+def reconstruct_sgd_mn(U, V, P, K, M, N, W, alpha, stream=None):
+    """K1 on MN-major factors: U [P, K, ldu] (or [K, ldu] at P = 1), V [P, K, ldv]; ld = the last stride."""
+    ldu, ldv = U.stride(-2), V.stride(-2)
+    ublk = U.stride(0) if U.dim() == 3 else K * ldu
+    vblk = V.stride(0) if V.dim() == 3 else K * ldv
+    _check(lib.poseidon_reconstruct_sgd_mn(_ptr(U), ldu, ublk, _ptr(V), ldv, vblk, P, K, M, N, _ptr(W),
+                                           float(alpha), _stream(stream)))
 
 
 def reconstruct_sgd_rows(Ug, Vg, P, K, ldk, M, m0, m1, N, W, alpha, recon=RECON_TF32, stream=None):

@@ -39,6 +39,15 @@ poseidon_status_t cuda_fail(cudaError_t e, const char* what) {
 
 // POSEIDON_DEBUG_SYNC=1: synchronise the library stream after every kernel launch and report the
 // kernel that faulted (debugging aid for asynchronous launch failures; off in production).
+// experiment knob: POSEIDON_ASYNC_PACK=0 keeps K3 on the producer stream with POSEIDON_FLAG_INPLACE_FACTORS
+bool knobs_async_pack() {
+  static const bool on = [] {
+    const char* v = getenv("POSEIDON_ASYNC_PACK");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 bool debug_sync_enabled() {
   static const bool on = [] {
     const char* v = getenv("POSEIDON_DEBUG_SYNC");
@@ -83,6 +92,9 @@ struct EvSet {
   // K3 pack of a factor layer: pstart recorded on the producer stream before the pack (ready after it)
   cudaEvent_t pstart = nullptr;
   bool packed = false;
+  // FLAG_INPLACE_FACTORS with the pack kept: K3 runs on the sync's own stream; pend = after it (pack_ms)
+  cudaEvent_t pend = nullptr;
+  bool pack_async = false;
   // The events the statistics read for "collective done", "kernel start" and "kernel end".  An event
   // record costs ~1 us of stream time, so a sync records only the events whose time differs from
   // one already recorded (e.g. the fused NVLS kernel: ready, start, done) and aliases the rest.
@@ -262,7 +274,7 @@ poseidon_status_t ensure_events(Layer& L) {
   for (int i = 0; i < RING; ++i) {
     EvSet& e = L.ev[i];
     cudaEvent_t* all[] = {&e.ready, &e.start, &e.gathered, &e.kstart, &e.kend, &e.done, &e.vready, &e.vgath,
-                          &e.pstart};
+                          &e.pstart, &e.pend};
     for (cudaEvent_t* p : all) CU_TRY(cudaEventCreate(p));
   }
   L.events_created = true;
@@ -433,6 +445,75 @@ poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, floa
     if ((err = debug_sync(c->recon_stream, "bias update")) != cudaSuccess) return cuda_fail(err, "bias");
   }
   CU_TRY(cudaEventRecord(dst.done, c->recon_stream));
+  return POSEIDON_OK;
+}
+
+// POSEIDON_FLAG_INPLACE_FACTORS (round 2): at world == 1 nothing travels, so the sufficient factors are consumed
+// where the backward wrote them ("the vectors already exist"): K1 reads U = dl/dy [K x M] and
+// V = a_i [K x N] MN-major on the reconstruction stream (no K3 pack, no gather buffer) and its idle lanes form
+// the bias sums.  The caller keeps U and V until the sync is done (the glue: record_stream on the recon stream).
+bool inplace_ok(poseidon_ctx_t c, const Layer& L, const float* U, const float* V, const float* W) {
+  return (c->flags & POSEIDON_FLAG_INPLACE_FACTORS) && (c->flags & POSEIDON_FLAG_INPLACE_MN) && c->world == 1 &&
+         !c->ssp && !(c->flags & POSEIDON_FLAG_DWBP_OFF) && L.scheme == POSEIDON_SCHEME_SFB &&
+         L.recon == POSEIDON_RECON_TF32 && !L.v_posted &&
+         recon_tcgen05_mn_supported(U, L.M, L.K * L.M, V, L.N, L.K * L.N, 1, L.K, L.M, L.N, W);
+}
+
+poseidon_status_t launch_factor_sync(poseidon_ctx_t c, int32_t id, Layer& L, float* W, float* bias, float lr,
+                                     cudaEvent_t wait_ev);
+poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t ldU, const float* V, int64_t ldV,
+                           cudaStream_t producer);
+
+// FLAG_INPLACE_FACTORS where K1 keeps the K-major gather layout (world > 1, or the in-place K1 declined): the
+// pack (K3) itself reads U and V in place, on the stream the sync continues on (comm at P > 1, recon at P = 1),
+// so it leaves the backward's critical path; the caller keeps U and V alive as for the in-place K1.
+bool async_pack_ok(poseidon_ctx_t c, const Layer& L) {
+  return (c->flags & POSEIDON_FLAG_INPLACE_FACTORS) && !c->ssp && !(c->flags & POSEIDON_FLAG_DWBP_OFF) &&
+         L.scheme == POSEIDON_SCHEME_SFB && knobs_async_pack();
+}
+
+poseidon_status_t sfb_async_pack(poseidon_ctx_t c, int32_t id, Layer& L, const float* U, const float* V, float* W,
+                                 float* bias, float lr, cudaStream_t producer) {
+  EvSet& e = L.ev[c->iter % RING];
+  CU_TRY(cudaEventRecord(e.ready, producer));   // the factors exist
+  cudaStream_t ls = c->world > 1 ? c->comm_stream : c->recon_stream;
+  CU_TRY(cudaStreamWaitEvent(ls, e.ready, 0));
+  // the previous sync of this layer (its K1 on the recon stream) must be done with the gather buffers
+  if (L.last_iter >= 0) CU_TRY(cudaStreamWaitEvent(ls, L.ev[L.last_iter % RING].done, 0));
+  poseidon_status_t st = pack_sfb(c, L, U, L.M, V, L.N, ls);
+  if (st) return st;
+  e.pack_async = true;
+  CU_TRY(cudaEventRecord(e.pend, ls));
+  L.last_iter = c->iter;
+  st = launch_factor_sync(c, id, L, W, bias, lr, e.pend);
+  L.v_posted = false;
+  return st;
+}
+
+poseidon_status_t sfb_inplace(poseidon_ctx_t c, int32_t id, Layer& L, const float* U, const float* V, float* W,
+                              float* bias, float lr, cudaStream_t producer) {
+  EvSet& e = L.ev[c->iter % RING];
+  e.packed = false;
+  CU_TRY(cudaEventRecord(e.ready, producer));
+  L.last_iter = c->iter;
+  IterRecord& r = open_record(c);
+  CU_TRY(cudaStreamWaitEvent(c->recon_stream, e.ready, 0));
+  FZ(c->recon_stream);
+  CU_TRY(cudaEventRecord(e.start, c->recon_stream));
+  e.g_eff = e.start;
+  e.ks_eff = e.start;
+  e.ke_eff = e.done;
+  const bool mom = (L.vel != nullptr);
+  const K1Momentum km{L.vel, L.vel_b, L.mu, lr, L.wd};
+  bool bias_done = false;
+  cudaError_t err = launch_recon_tcgen05_mn(U, L.M, L.K * L.M, V, L.N, L.K * L.N, 1, L.K, L.M, L.N, W,
+                                            mom ? lr : -lr, 1.0f, c->recon_stream, nullptr, bias, &bias_done,
+                                            mom ? &km : nullptr, /*bias_from_u=*/true);
+  if (err != cudaSuccess) return cuda_fail(err, "in-place reconstruct+sgd launch");
+  if (bias && !bias_done) return fail(POSEIDON_ERR_STATE, "in-place sync: bias not fused");
+  if ((err = debug_sync(c->recon_stream, "K1 in place")) != cudaSuccess) return cuda_fail(err, "K1 in place");
+  CU_TRY(cudaEventRecord(e.done, c->recon_stream));
+  r.layers.push_back(id);
   return POSEIDON_OK;
 }
 
@@ -778,6 +859,7 @@ poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t l
   EvSet& e = L.ev[c->iter % RING];
   CU_TRY(cudaEventRecord(e.pstart, producer));
   e.packed = true;
+  e.pack_async = false;
   cudaError_t err = launch_pack_uv(U, ldU, u_slot, L.M, b_slot, L.v_posted ? nullptr : V, ldV, v_slot, L.N,
                                    L.ldk, L.K, round, producer);
   if (err != cudaSuccess) return cuda_fail(err, "pack U/V launch");
@@ -1361,9 +1443,18 @@ poseidon_status_t poseidon_sync_fc_sfb(poseidon_ctx_t c, int32_t id, const float
   cudaStream_t ps = reinterpret_cast<cudaStream_t>(producer);
   st = producer_guard(c, *L, ps);
   if (st) return st;
+  if (inplace_ok(c, *L, U, V, W)) return sfb_inplace(c, id, *L, U, V, W, bias, lr, ps);
+  if (async_pack_ok(c, *L)) return sfb_async_pack(c, id, *L, U, V, W, bias, lr, ps);
   st = pack_sfb(c, *L, U, L->M, V, L->N, ps);
   if (st) return st;
   return sfb_after_pack(c, id, *L, W, bias, lr, ps);
+}
+
+poseidon_stream_t poseidon_stream(poseidon_ctx_t c, int32_t which) {
+  if (check_ctx(c) != POSEIDON_OK) return nullptr;
+  if (which == POSEIDON_STREAM_COMM) return reinterpret_cast<poseidon_stream_t>(c->comm_stream);
+  if (which == POSEIDON_STREAM_RECON) return reinterpret_cast<poseidon_stream_t>(c->recon_stream);
+  return nullptr;
 }
 
 poseidon_status_t poseidon_sfb_post_input(poseidon_ctx_t c, int32_t id, const float* V, int64_t ldV,
@@ -1621,7 +1712,7 @@ poseidon_status_t poseidon_get_layer_stats(poseidon_ctx_t c, int32_t ago, int32_
   out->kernel_ms = elapsed(e.ks_eff, e.ke_eff);
   out->start_to_done_ms = elapsed(e.start, e.done);
   out->done_after_bwd_end_ms = elapsed(r.bwd_end, e.done);
-  out->pack_ms = e.packed ? elapsed(e.pstart, e.ready) : 0.f;
+  out->pack_ms = e.packed ? elapsed(e.pstart, e.pack_async ? e.pend : e.ready) : 0.f;
   return POSEIDON_OK;
 }
 
@@ -1706,6 +1797,21 @@ poseidon_status_t poseidon_reconstruct_sgd(const float* Ug, const float* Vg, int
     return fail(POSEIDON_ERR_INVALID_ARG, "bad recon");
   }
   if (err != cudaSuccess) return cuda_fail(err, "reconstruct_sgd launch");
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_reconstruct_sgd_mn(const float* U, int64_t ldu, int64_t ublk, const float* V, int64_t ldv,
+                                              int64_t vblk, int32_t P, int64_t K, int64_t M, int64_t N, float* W,
+                                              float alpha, poseidon_stream_t stream) {
+  if (!U || !V || !W || P < 1 || K < 0 || M <= 0 || N <= 0 || ldu < M || ldv < N)
+    return fail(POSEIDON_ERR_INVALID_ARG, "reconstruct_sgd_mn: bad arguments");
+  if (K == 0) return POSEIDON_OK;
+  if (!recon_tcgen05_mn_supported(U, ldu, ublk, V, ldv, vblk, P, K, M, N, W))
+    return fail(POSEIDON_ERR_ALIGNMENT, "reconstruct_sgd_mn: 16-B aligned buffers, ldu/ldv/N (and block strides) "
+                                        "multiples of 4, block strides >= K*ld");
+  cudaError_t err = launch_recon_tcgen05_mn(U, ldu, ublk, V, ldv, vblk, P, K, M, N, W, alpha, 1.0f,
+                                            reinterpret_cast<cudaStream_t>(stream));
+  if (err != cudaSuccess) return cuda_fail(err, "reconstruct_sgd_mn launch");
   return POSEIDON_OK;
 }
 

@@ -79,6 +79,15 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
                                  int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg = nullptr,
                                  int64_t ldm = 0, const float* bs = nullptr, float* bias = nullptr,
                                  bool* bias_done = nullptr, const K1Momentum* mom = nullptr);
+// K1 on MN-major factors (round 2): U block p at U + p*ublk, k-th row at + k*ldu (M contiguous), V alike; the
+// factors as the layer produced them (grad_out [K x M], input [K x N]), no transposing pack
+bool recon_tcgen05_mn_supported(const float* U, int64_t ldu, int64_t ublk, const float* V, int64_t ldv, int64_t vblk,
+                                int32_t P, int64_t K, int64_t M, int64_t N, const float* W);
+cudaError_t launch_recon_tcgen05_mn(const float* U, int64_t ldu, int64_t ublk, const float* V, int64_t ldv,
+                                    int64_t vblk, int32_t P, int64_t K, int64_t M, int64_t N, float* W, float alpha,
+                                    float beta, cudaStream_t s, const float* bs = nullptr, float* bias = nullptr,
+                                    bool* bias_done = nullptr, const K1Momentum* mom = nullptr,
+                                    bool bias_from_u = false);
 // (bs, bias, bias_done): optional plain-SGD bias update fused into K1 (bias[m] = fmaf(alpha, sum_p bs[p*M+m],
 // bias[m]), bs [P][M] with M the block's row count); *bias_done tells whether the kernel took it.
 bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int64_t M, int64_t N, const float* W);

@@ -228,6 +228,22 @@ __device__ __forceinline__ uint64_t make_desc_k_sw128(uint32_t saddr, uint32_t l
   return d;
 }
 
+// MN-major operand (round 2): the factors as the layer produced them, [K][MN] row-major (MN contiguous),
+// staged by TMA with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B as 32-element chunks of BK rows x 128 B.  UMMA
+// layout type SWIZZLE_128B_BASE32B (= 1; CUTLASS Layout_MN_SW128_32B_Atom, the only MN-major tf32 layout):
+// ((8,n),(4,k)) : ((1,LBO),(8,SBO)) in 16-byte units, 32-B granules XOR (k mod 4); LBO = stride between
+// 32-element MN chunks, SBO = stride between groups of 4 k rows (512 B).  Checked exactly on the box
+// (tools/tc_probe_mn.cu, profiles/r2/tc_probe_mn_r2b.txt); plain SWIZZLE_128B gives all-zero accumulators.
+__device__ __forceinline__ uint64_t make_desc_mn_sw128_32b(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  d |= (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
+  return d;
+}
+
 // Instruction descriptor: D=f32, A=B=tf32, A and B K-major, N=BN, M=BM.
 __host__ __device__ constexpr uint32_t make_idesc() {
   return (1u << 4)              // c_format = F32
@@ -259,6 +275,14 @@ struct Params {
   const float* bs;
   float* bias;
   int32_t nP;
+  // in-place factors (POSEIDON_FLAG_INPLACE_FACTORS): no bs; the bias lanes sum U's columns themselves,
+  // sum_w sum_k<Kc ucol[w * ublk + k * ldu + m]
+  const float* ucol;
+  int64_t ldu, ublk;
+  int32_t Kc;
+  // MN-major operands: 1 -> 4-D maps {32, K, MN/32, P} whose one box {32, BK, 4, 1} lands as the four
+  // 32-element chunks of a CTA's 128 rows (MN a multiple of 32), else four 3-D boxes per operand and stage
+  int32_t mn4;
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& mt, int& nt) {
@@ -475,9 +499,11 @@ constexpr int smem_bytes(int stages, int wslots, bool mom = false) {
   return stages * STAGE + wslots * (mom ? 2 : 1) * W_CHUNK_BYTES + 1024 + 1024;
 }
 
-__host__ __device__ constexpr uint32_t idesc() {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+__host__ __device__ constexpr uint32_t idesc(bool mn = false) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24) |
+         (mn ? (1u << 15) | (1u << 16) : 0u);   // a_major / b_major = MN
 }
+constexpr int MN_CHUNK = 32 * BK * 4;   // MN-major staging: one 32-element x BK-row chunk (4 KB)
 }  // namespace k2sm
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -509,6 +535,14 @@ __device__ __forceinline__ void tma_load_3d_2sm(const CUtensorMap* map, uint32_t
       "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
       "l"(map), "r"(bar_cluster), "r"(x), "r"(y), "r"(z), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_2sm(const CUtensorMap* map, uint32_t bar_cluster, void* dst, int32_t x,
+                                                int32_t y, int32_t z, int32_t w, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(x), "r"(y), "r"(z), "r"(w), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void tc_mma_tf32_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -650,8 +684,23 @@ __device__ __forceinline__ void rw_epilogue(const Params& p, uint32_t tmem_base,
 // MOM (f4, fused momentum): every W slot carries the matching velocity chunk right after the W chunk
 // (2 x 16 KB); the epilogue reads both, writes both (16 B per element instead of K1-on-the-velocity + a
 // separate pass, 24 B).
+// bias[m] update from the gathered column sum `sum` = sum_p sum_k U_p[k][m] (reading Z9): plain SGD, or Lambda
+// (O4m) v = mu v + lr (g + wd b), b -= v with g = sum / P
+template <bool MOM>
+__device__ __forceinline__ void bias_apply(const Params& p, int m, float sum) {
+  if (MOM) {
+    const float b = p.bias[m];
+    const float v = fmaf(p.mu, p.vel_b[m], p.lr * fmaf(p.wd, b, sum * p.inv_p));
+    p.vel_b[m] = v;
+    p.bias[m] = b - v;
+  } else {
+    p.bias[m] = fmaf(p.alpha, sum, p.bias[m]);
+  }
+}
+
 // RWD > 0: the RW epilogue with RWD chunks of W in flight per warp (NWS = 0: no W slots, no W TMA).
-template <int NST, int NWS, bool MOM = false, int RWD = 0>
+// MNK: operands MN-major ([P][K][ld] blocks straight from the layer, no transposing pack), else K-major.
+template <int NST, int NWS, bool MOM = false, int RWD = 0, bool MNK = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     recon_tcgen05_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmV,
@@ -720,8 +769,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
           if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * k2sm::STAGE));
           uint8_t* sa = smem_ops + stage * k2sm::STAGE;
           uint8_t* sb = sa + k2sm::A_BYTES;
-          tma_load_3d_2sm(&tmA, full_leader, sa, kb * BK, a_row, pw, pol);
-          tma_load_3d_2sm(&tmB, full_leader, sb, kb * BK, b_row, pw, pol);
+          if (MNK && p.mn4) {
+            tma_load_4d_2sm(&tmA, full_leader, sa, 0, kb * BK, a_row / 32, pw, pol);
+            tma_load_4d_2sm(&tmB, full_leader, sb, 0, kb * BK, b_row / 32, pw, pol);
+          } else if (MNK) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              tma_load_3d_2sm(&tmA, full_leader, sa + j * k2sm::MN_CHUNK, a_row + 32 * j, kb * BK, pw, pol);
+              tma_load_3d_2sm(&tmB, full_leader, sb + j * k2sm::MN_CHUNK, b_row + 32 * j, kb * BK, pw, pol);
+            }
+          } else {
+            tma_load_3d_2sm(&tmA, full_leader, sa, kb * BK, a_row, pw, pol);
+            tma_load_3d_2sm(&tmB, full_leader, sb, kb * BK, b_row, pw, pol);
+          }
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
@@ -736,7 +796,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA, one thread) =====================
     if (rank == 0 && lane == 0 && (p.mode == 0 || p.mode == 6 || p.mode == 7)) {
-      constexpr uint32_t id = k2sm::idesc();
+      constexpr uint32_t id = k2sm::idesc(MNK);
       uint32_t stage = 0, phase = 0;
       int it = 0;
       for (int tile = pair; tile < p.num_tiles; tile += npairs, ++it) {
@@ -752,8 +812,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
           const uint32_t sb = sa + k2sm::A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k) {
-            const uint64_t ad = make_desc_k_sw128(sa + k * 32, 16, 1024);
-            const uint64_t bd = make_desc_k_sw128(sb + k * 32, 16, 1024);
+            // K-major: the k-th UMMA (8 k = 32 B) starts 32 k bytes into each 128-B row; MN-major: 8 k rows
+            // of 128 B further into every 32-element chunk
+            const uint64_t ad = MNK ? make_desc_mn_sw128_32b(sa + k * UK * 128, k2sm::MN_CHUNK, 512)
+                                    : make_desc_k_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = MNK ? make_desc_mn_sw128_32b(sb + k * UK * 128, k2sm::MN_CHUNK, 512)
+                                    : make_desc_k_sw128(sb + k * 32, 16, 1024);
             tc_mma_tf32_2sm(d_tmem, ad, bd, id, (kk | k) != 0 ? 1u : 0u);
           }
           tc_commit_2sm_mc(&empty[stage], 0x3);
@@ -767,19 +831,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     }
   } else if (warp == 2) {
     // ===================== W tile TMA producer (both CTAs, own rows) =====================
-    if (lane > 0 && p.bias != nullptr) {
+    if (lane > 0 && p.bias != nullptr && p.ucol == nullptr) {
       // the bias update (Z9: per-worker column sums of U, already gathered) on lanes 1..31 of every CTA
       for (int m = (int)blockIdx.x * 31 + (lane - 1); m < p.M; m += (int)gridDim.x * 31) {
         float sum = 0.f;
         for (int w = 0; w < p.nP; ++w) sum += p.bs[(size_t)w * p.M + m];
-        if (MOM) {   // Lambda on the bias (O4m): v = mu v + lr (g + wd b), b -= v
-          const float b = p.bias[m];
-          const float v = fmaf(p.mu, p.vel_b[m], p.lr * fmaf(p.wd, b, sum * p.inv_p));
-          p.vel_b[m] = v;
-          p.bias[m] = b - v;
-        } else {
-          p.bias[m] = fmaf(p.alpha, sum, p.bias[m]);
-        }
+        bias_apply<MOM>(p, m, sum);
       }
     }
     if (RWD == 0 && lane == 0 && p.mode != 7) {
@@ -802,6 +859,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
       }
     }
   } else if (warp == 3) {
+    if (lane > 0 && p.bias != nullptr && p.ucol != nullptr) {
+      // in-place factors: the bias sums are U's column sums, formed here (lanes 1..31 of the relay warp, so
+      // the W producer's lane never waits behind these loads): sum_w sum_k U[w][k][m] in k order, 16 loads
+      // in flight per thread
+      for (int m = (int)blockIdx.x * 31 + (lane - 1); m < p.M; m += (int)gridDim.x * 31) {
+        float sum = 0.f;
+        for (int w = 0; w < p.nP; ++w) {
+          const float* col = p.ucol + (size_t)w * p.ublk + m;
+          int k = 0;
+          for (; k + 16 <= p.Kc; k += 16) {
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __ldg(col + (size_t)(k + j) * p.ldu);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sum += v[j];
+          }
+          for (; k < p.Kc; ++k) sum += __ldg(col + (size_t)k * p.ldu);
+        }
+        bias_apply<MOM>(p, m, sum);
+      }
+    }
     // ===================== accumulator-free relay =====================
     // The 8 local epilogue warps arrive on tempty_local (CTA scope); this thread forwards ONE
     // release.cluster arrival to the leader's tempty.  It issues no global stores, so the
@@ -935,9 +1013,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
 //   POSEIDON_K1_RW=0|1      force the TMA W ring (0) or the RW epilogue (1) for plain SGD (default: by regime)
 //   POSEIDON_K1_RWD=2|3|4   W chunks in flight per epilogue warp (RW epilogue);  POSEIDON_K1_RWS=4|5|6  stages
 struct K1Knobs {
-  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0, fbias = 1, rw = -1, rwd = 3, rws = 6;
+  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0, fbias = 1, rw = -1, rwd = 3, rws = 6, mn4 = 1;
   K1Knobs() {
     if (const char* v = getenv("POSEIDON_K1_RW")) rw = v[0] - '0';
+    if (const char* v = getenv("POSEIDON_K1_MN4")) mn4 = v[0] - '0';
     if (const char* v = getenv("POSEIDON_K1_RWD")) rwd = v[0] - '0';
     if (const char* v = getenv("POSEIDON_K1_RWS")) rws = v[0] - '0';
     if (const char* v = getenv("POSEIDON_K1_VARIANT")) variant = (v[0] == '1') ? 1 : 2;
@@ -969,7 +1048,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 bool encode(CUtensorMap* map, const float* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-            const uint32_t* box) {
+            const uint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t d[3], st[2];
@@ -977,7 +1056,7 @@ bool encode(CUtensorMap* map, const float* base, int rank, const uint64_t* dims,
   for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; }
   for (int i = 0; i < rank - 1; ++i) st[i] = strides_bytes[i];
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<float*>(base), d, st, b, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -999,23 +1078,26 @@ namespace {
 struct MapKey {
   const void *u, *v, *w, *vel;
   int64_t P, K, ldk, M, N, ldm;
+  int64_t ldu, ldv, ublk, vblk;   // MN-major operands (0 for the K-major maps)
   bool operator==(const MapKey& o) const {
     return u == o.u && v == o.v && w == o.w && vel == o.vel && P == o.P && K == o.K && ldk == o.ldk && M == o.M &&
-           N == o.N && ldm == o.ldm;
+           N == o.N && ldm == o.ldm && ldu == o.ldu && ldv == o.ldv && ublk == o.ublk && vblk == o.vblk;
   }
 };
 struct MapEntry {
   MapKey key;
   CUtensorMap a, b, w, b2, vm;
+  int aux;   // MN-major: the operand maps are 4-D (Params::mn4)
 };
 std::mutex g_map_mu;
 std::vector<MapEntry> g_maps;   // small FIFO: one entry per SFB layer (and per gather set)
 constexpr size_t kMapCap = 256;
 bool map_cache_get(const MapKey& k, CUtensorMap* a, CUtensorMap* b, CUtensorMap* w, CUtensorMap* b2,
-                   CUtensorMap* vm) {
+                   CUtensorMap* vm, int* aux = nullptr) {
   std::lock_guard<std::mutex> lock(g_map_mu);
   for (const auto& e : g_maps)
     if (e.key == k) {
+      if (aux) *aux = e.aux;
       *a = e.a;
       *b = e.b;
       *w = e.w;
@@ -1026,10 +1108,10 @@ bool map_cache_get(const MapKey& k, CUtensorMap* a, CUtensorMap* b, CUtensorMap*
   return false;
 }
 void map_cache_put(const MapKey& k, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& w,
-                   const CUtensorMap& b2, const CUtensorMap& vm) {
+                   const CUtensorMap& b2, const CUtensorMap& vm, int aux = 0) {
   std::lock_guard<std::mutex> lock(g_map_mu);
   if (g_maps.size() >= kMapCap) g_maps.erase(g_maps.begin());
-  g_maps.push_back(MapEntry{k, a, b, w, b2, vm});
+  g_maps.push_back(MapEntry{k, a, b, w, b2, vm, aux});
 }
 }  // namespace
 
@@ -1056,6 +1138,127 @@ bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int6
          N < (1 << 30) && ldk < (1 << 30);
 }
 
+namespace {
+void fill_params(Params& p, int32_t P, int64_t K, int64_t M, int64_t N, float* W, float alpha, float beta,
+                 const K1Momentum* mom, double operand_bytes) {
+  p.M = (int32_t)M;
+  p.N = (int32_t)N;
+  p.m_tiles = (int32_t)((M + BM - 1) / BM);
+  p.n_tiles = (int32_t)((N + BN - 1) / BN);
+  p.num_tiles = p.m_tiles * p.n_tiles;
+  p.kb_per_p = (int32_t)((K + BK - 1) / BK);  // k >= K of a block are zero (padding / TMA OOB)
+  p.num_kb = p.kb_per_p * P;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.dbg = nullptr;
+  p.prof = k1_prof_buffer(M, N);
+  p.vel = mom ? mom->vel : nullptr;
+  p.vel_b = mom ? mom->vel_b : nullptr;
+  p.mu = mom ? mom->mu : 0.f;
+  p.lr = mom ? mom->lr : 0.f;
+  p.wd = mom ? mom->wd : 0.f;
+  p.lr_wd = mom ? mom->lr * mom->wd : 0.f;
+  p.inv_p = 1.0f / (float)P;
+  p.W = W;
+  p.bs = nullptr;
+  p.bias = nullptr;
+  p.nP = P;
+  p.ucol = nullptr;
+  p.ldu = p.ublk = 0;
+  p.Kc = (int32_t)K;
+  p.mn4 = 0;
+  // Raster (measured, tools/k1_sweep.sh): when both factor buffers fit comfortably in L2 the waves
+  // walk N so each wave's W tiles are whole row segments; otherwise consecutive tiles walk the
+  // dimension whose operand is smaller, so the operand re-swept every wave stays L2-resident.
+  p.m_fast = (operand_bytes <= 48e6) ? 0 : ((M <= N) ? 1 : 0);
+  if (knobs().raster >= 0) p.m_fast = knobs().raster;
+  p.epi_groups = knobs().epi;
+  p.w_policy = knobs().wpol;
+  p.mode = knobs().mode;
+}
+
+template <class Kern>
+cudaError_t launch_2sm(Kern kern, int smem, bool& attr, int pairs, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                       const CUtensorMap& tmW, const CUtensorMap& tmV, const Params& p, cudaStream_t s) {
+  if (!attr) {
+    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (ea != cudaSuccess) return ea;
+    attr = true;
+  }
+  kern<<<2 * pairs, NUM_THREADS_2SM, smem, s>>>(tmA, tmB, tmW, tmV, p);
+  g_launches.fetch_add(1);
+  return cudaGetLastError();
+}
+
+// The 2-SM kernel's configurations (both operand layouts): momentum (W + velocity slots), RW epilogue, TMA W ring.
+template <bool MNK>
+cudaError_t dispatch_2sm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtensorMap& tmV,
+                         Params& p, const K1Momentum* mom, cudaStream_t s) {
+  using k2sm::smem_bytes;
+  p.m_tiles = (int32_t)((p.M + k2sm::BM - 1) / k2sm::BM);
+  p.n_tiles = (int32_t)((p.N + k2sm::BN - 1) / k2sm::BN);
+  p.num_tiles = p.m_tiles * p.n_tiles;
+  const int pairs = std::min(p.num_tiles, sm_count_k1() / 2);
+  if (mom != nullptr) {
+    // f4: W and velocity chunks share a slot (2 x 16 KB): <3 stages, 4 slots> when the W stream dominates
+    // (<= 8 factor slabs per tile), else <4, 3>; both 224 KB of shared memory
+    static bool m1 = false, m2 = false;
+    if (p.num_kb <= 8)
+      return launch_2sm(recon_tcgen05_2sm_kernel<3, 4, true, 0, MNK>, smem_bytes(3, 4, true), m1, pairs, tmA, tmB, tmW,
+                        tmV, p, s);
+    return launch_2sm(recon_tcgen05_2sm_kernel<4, 3, true, 0, MNK>, smem_bytes(4, 3, true), m2, pairs, tmA, tmB, tmW,
+                      tmV, p, s);
+  }
+  // RW epilogue (no W slots: the shared memory goes to 6 operand stages) where the tensor pipe is the
+  // bound, i.e. >= 32 factor slabs per tile (P*K >= 1024): tools/k1_ab.py, profiles/r2/k1_rw_r2.md
+  // (fc6 P*K = 1024: 117.6 -> 109.3 us, P*K = 2048: 192.5 -> 186.4 us, bit-identical W); the TMA W ring
+  // stays where the W read-modify-write is the bound (fc6 P*K = 256: 67.6 vs 79.9 us).
+  const bool rw = knobs().rw >= 0 ? knobs().rw == 1 : p.num_kb >= 32;
+  if (rw && p.mode == 0 && p.epi_groups == 2) {
+    static bool a62 = false, a63 = false, a64 = false, a43 = false, a53 = false;
+    const int d = knobs().rwd, st = knobs().rws;
+    if (!MNK && st == 4)
+      return launch_2sm(recon_tcgen05_2sm_kernel<4, 0, false, 3>, smem_bytes(4, 0), a43, pairs, tmA, tmB, tmW, tmW, p, s);
+    if (!MNK && st == 5)
+      return launch_2sm(recon_tcgen05_2sm_kernel<5, 0, false, 3>, smem_bytes(5, 0), a53, pairs, tmA, tmB, tmW, tmW, p, s);
+    if (!MNK && d == 2)
+      return launch_2sm(recon_tcgen05_2sm_kernel<6, 0, false, 2>, smem_bytes(6, 0), a62, pairs, tmA, tmB, tmW, tmW, p, s);
+    if (!MNK && d == 4)
+      return launch_2sm(recon_tcgen05_2sm_kernel<6, 0, false, 4>, smem_bytes(6, 0), a64, pairs, tmA, tmB, tmW, tmW, p, s);
+    return launch_2sm(recon_tcgen05_2sm_kernel<6, 0, false, 3, MNK>, smem_bytes(6, 0), a63, pairs, tmA, tmB, tmW, tmW,
+                      p, s);
+  }
+  // the TMA W ring: <operand stages, W slots>.  Regime: with <= 8 factor slabs per tile the W
+  // stream dominates and <4 stages, 6 W slots> wins (round 2, tools/k1_cfg_bench.sh: fc6 P*K=256 in the C3
+  // step 84 -> 69 us, alone 67.6 us either way; <4,5> was the round-1 pick); with more slabs deeper operand
+  // staging <5, 4> wins (fc6 P*K=2048: 686 -> 743 TFLOP/s).  Letters of POSEIDON_K1_CFG in K1Knobs.
+  const int cfg = knobs().cfg >= 0 ? knobs().cfg : (p.num_kb <= 8 ? 6 : 3);
+  static bool at[8] = {};
+  if (MNK) {
+    if (cfg == 3)
+      return launch_2sm(recon_tcgen05_2sm_kernel<5, 4, false, 0, true>, smem_bytes(5, 4), at[3], pairs, tmA, tmB, tmW,
+                        tmW, p, s);
+    return launch_2sm(recon_tcgen05_2sm_kernel<4, 6, false, 0, true>, smem_bytes(4, 6), at[6], pairs, tmA, tmB, tmW, tmW,
+                      p, s);
+  }
+  switch (cfg) {
+    case 0: return launch_2sm(recon_tcgen05_2sm_kernel<3, 8>, smem_bytes(3, 8), at[0], pairs, tmA, tmB, tmW, tmW, p, s);
+    case 2: return launch_2sm(recon_tcgen05_2sm_kernel<2, 8>, smem_bytes(2, 8), at[2], pairs, tmA, tmB, tmW, tmW, p, s);
+    case 3: return launch_2sm(recon_tcgen05_2sm_kernel<5, 4>, smem_bytes(5, 4), at[3], pairs, tmA, tmB, tmW, tmW, p, s);
+    case 4: return launch_2sm(recon_tcgen05_2sm_kernel<2, 10>, smem_bytes(2, 10), at[4], pairs, tmA, tmB, tmW, tmW, p, s);
+    case 5: return launch_2sm(recon_tcgen05_2sm_kernel<3, 7>, smem_bytes(3, 7), at[5], pairs, tmA, tmB, tmW, tmW, p, s);
+    case 6: return launch_2sm(recon_tcgen05_2sm_kernel<4, 6>, smem_bytes(4, 6), at[6], pairs, tmA, tmB, tmW, tmW, p, s);
+    case 7: return launch_2sm(recon_tcgen05_2sm_kernel<2, 9>, smem_bytes(2, 9), at[7], pairs, tmA, tmB, tmW, tmW, p, s);
+    default: return launch_2sm(recon_tcgen05_2sm_kernel<4, 5>, smem_bytes(4, 5), at[1], pairs, tmA, tmB, tmW, tmW, p, s);
+  }
+}
+
+bool bias_fusable(const float* bs, float* bias, bool* bias_done, int64_t M, const K1Momentum* mom) {
+  return knobs().fbias && bias != nullptr && bs != nullptr && bias_done != nullptr && M < (1 << 30) &&
+         (mom == nullptr || mom->vel_b != nullptr);
+}
+}  // namespace
+
 cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, int64_t K, int64_t ldk, int64_t M,
                                  int64_t N, float* W, float alpha, float beta, cudaStream_t s, float* dbg,
                                  int64_t ldm, const float* bs, float* bias, bool* bias_done, const K1Momentum* mom) {
@@ -1069,7 +1272,7 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   CUtensorMap tmA, tmB, tmW, tmB2, tmV;
   // Tensor maps are cached per (buffers, shape): encoding four of them costs ~10 us of host time per
   // launch, which lands on the step whenever the GPU is not far behind the host (small layers).
-  const MapKey key{Ug, Vg, W, mom ? mom->vel : nullptr, P, K, ldk, M, N, ldm};
+  const MapKey key{Ug, Vg, W, mom ? mom->vel : nullptr, P, K, ldk, M, N, ldm, 0, 0, 0, 0};
   if (dbg == nullptr && map_cache_get(key, &tmA, &tmB, &tmW, &tmB2, &tmV)) goto have_maps;
   {
   const uint64_t dA[3] = {(uint64_t)ldk, (uint64_t)M, (uint64_t)P};
@@ -1094,132 +1297,15 @@ cudaError_t launch_recon_tcgen05(const float* Ug, const float* Vg, int32_t P, in
   }
 have_maps:
   Params p;
-  p.M = (int32_t)M;
-  p.N = (int32_t)N;
-  p.m_tiles = (int32_t)((M + BM - 1) / BM);
-  p.n_tiles = (int32_t)((N + BN - 1) / BN);
-  p.num_tiles = p.m_tiles * p.n_tiles;
-  p.kb_per_p = (int32_t)((K + BK - 1) / BK);  // k columns >= K of a block are zero (padding / TMA OOB)
-  p.num_kb = p.kb_per_p * P;
-  p.alpha = alpha;
-  p.beta = beta;
+  fill_params(p, P, K, M, N, W, alpha, beta, mom, 4.0 * (double)P * (double)ldk * (double)(M + N));
   p.dbg = dbg;
-  p.prof = k1_prof_buffer(M, N);
-  p.vel = mom ? mom->vel : nullptr;
-  p.vel_b = mom ? mom->vel_b : nullptr;
-  p.mu = mom ? mom->mu : 0.f;
-  p.lr = mom ? mom->lr : 0.f;
-  p.wd = mom ? mom->wd : 0.f;
-  p.lr_wd = mom ? mom->lr * mom->wd : 0.f;
-  p.inv_p = 1.0f / (float)P;
-  p.W = W;
-  p.bs = nullptr;
-  p.bias = nullptr;
-  p.nP = P;
-  // Raster (measured, tools/k1_sweep.sh): when both factor buffers fit comfortably in L2 the waves
-  // walk N so each wave's W tiles are whole row segments; otherwise consecutive tiles walk the
-  // dimension whose operand is smaller, so the operand re-swept every wave stays L2-resident.
-  const double operand_bytes = 4.0 * (double)P * (double)ldk * (double)(M + N);
-  p.m_fast = (operand_bytes <= 48e6) ? 0 : ((M <= N) ? 1 : 0);
-  if (knobs().raster >= 0) p.m_fast = knobs().raster;
-  p.mode = 0;
-  p.epi_groups = 2;
-  p.w_policy = 0;
-  p.epi_groups = knobs().epi;
-  p.w_policy = knobs().wpol;
-  p.mode = knobs().mode;
   if (variant == 2 && dbg == nullptr) {
-    tmB = tmB2;
-    if (knobs().fbias && bias != nullptr && bs != nullptr && bias_done != nullptr && M < (1 << 30) &&
-        (mom == nullptr || mom->vel_b != nullptr)) {
+    if (bias_fusable(bs, bias, bias_done, M, mom)) {
       p.bs = bs;
       p.bias = bias;
       *bias_done = true;
     }
-    p.m_tiles = (int32_t)((M + k2sm::BM - 1) / k2sm::BM);
-    p.n_tiles = (int32_t)((N + k2sm::BN - 1) / k2sm::BN);
-    p.num_tiles = p.m_tiles * p.n_tiles;
-    // Regime: with few factor rows per tile the kernel is bound by the W
-    // read-modify-write, so more W chunks in flight beat deeper operand staging.
-    // Stage / W-slot split (tools/k1_sweep*.sh, tools/k1_cfg_bench.sh): with <= 8 factor slabs per tile the
-    // W stream dominates and <4 stages, 6 W slots> wins (round 2: fc6 P*K=256 in the C3 step 84 -> 69 us,
-    // alone 67.6 us either way; <4,5> was the round-1 pick); with more slabs deeper operand staging <5, 4>
-    // wins (fc6 P*K=2048: 686 -> 743 TFLOP/s).  Letters of POSEIDON_K1_CFG in K1Knobs.
-    const int cfg = knobs().cfg >= 0 ? knobs().cfg : (p.num_kb <= 8 ? 6 : 3);
-    static bool attr_a = false, attr_b = false;
-    const int pairs = std::min(p.num_tiles, sm_count_k1() / 2);
-    cudaError_t e = cudaSuccess;
-    if (mom != nullptr) {
-      // f4: W and velocity chunks share a slot (2 x 16 KB): <3 stages, 4 slots> when the W stream dominates
-      // (<= 8 factor slabs per tile), else <4, 3>; both 224 KB of shared memory
-      if (p.num_kb <= 8) {
-        constexpr int SM_ = k2sm::smem_bytes(3, 4, true);
-        static bool attr_m1 = false;
-        if (!attr_m1) {
-          e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<3, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
-          if (e != cudaSuccess) return e;
-          attr_m1 = true;
-        }
-        recon_tcgen05_2sm_kernel<3, 4, true><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, tmV, p);
-      } else {
-        constexpr int SM_ = k2sm::smem_bytes(4, 3, true);
-        static bool attr_m2 = false;
-        if (!attr_m2) {
-          e = cudaFuncSetAttribute(recon_tcgen05_2sm_kernel<4, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM_);
-          if (e != cudaSuccess) return e;
-          attr_m2 = true;
-        }
-        recon_tcgen05_2sm_kernel<4, 3, true><<<2 * pairs, NUM_THREADS_2SM, SM_, s>>>(tmA, tmB, tmW, tmV, p);
-      }
-      g_launches.fetch_add(1);
-      return cudaGetLastError();
-    }
-    // RW epilogue (no W slots: the shared memory goes to 6 operand stages) where the tensor pipe is the
-    // bound, i.e. >= 32 factor slabs per tile (P*K >= 1024): tools/k1_ab.py, profiles/r2/k1_rw_r2.md
-    // (fc6 P*K = 1024: 117.6 -> 109.3 us, P*K = 2048: 192.5 -> 186.4 us, bit-identical W); the TMA W ring
-    // stays where the W read-modify-write is the bound (fc6 P*K = 256: 67.6 vs 79.9 us).
-    const bool rw = knobs().rw >= 0 ? knobs().rw == 1 : p.num_kb >= 32;
-    if (rw && p.mode == 0 && p.epi_groups == 2) {
-      auto go = [&](auto kern, int smem, bool& attr) -> cudaError_t {
-        if (!attr) {
-          cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-          if (ea != cudaSuccess) return ea;
-          attr = true;
-        }
-        kern<<<2 * pairs, NUM_THREADS_2SM, smem, s>>>(tmA, tmB, tmW, tmW, p);
-        g_launches.fetch_add(1);
-        return cudaGetLastError();
-      };
-      static bool a62 = false, a63 = false, a64 = false, a43 = false, a53 = false;
-      const int d = knobs().rwd, st = knobs().rws;
-      if (st == 4) return go(recon_tcgen05_2sm_kernel<4, 0, false, 3>, k2sm::smem_bytes(4, 0), a43);
-      if (st == 5) return go(recon_tcgen05_2sm_kernel<5, 0, false, 3>, k2sm::smem_bytes(5, 0), a53);
-      if (d == 2) return go(recon_tcgen05_2sm_kernel<6, 0, false, 2>, k2sm::smem_bytes(6, 0), a62);
-      if (d == 4) return go(recon_tcgen05_2sm_kernel<6, 0, false, 4>, k2sm::smem_bytes(6, 0), a64);
-      return go(recon_tcgen05_2sm_kernel<6, 0, false, 3>, k2sm::smem_bytes(6, 0), a63);
-    }
-    // the TMA W ring: <operand stages, W slots>
-    auto ring = [&](auto kern, int smem, bool& attr) -> cudaError_t {
-      if (!attr) {
-        cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (ea != cudaSuccess) return ea;
-        attr = true;
-      }
-      kern<<<2 * pairs, NUM_THREADS_2SM, smem, s>>>(tmA, tmB, tmW, tmW, p);
-      g_launches.fetch_add(1);
-      return cudaGetLastError();
-    };
-    static bool at[8] = {};
-    switch (cfg) {
-      case 0: return ring(recon_tcgen05_2sm_kernel<3, 8>, k2sm::smem_bytes(3, 8), at[0]);
-      case 2: return ring(recon_tcgen05_2sm_kernel<2, 8>, k2sm::smem_bytes(2, 8), at[2]);
-      case 3: return ring(recon_tcgen05_2sm_kernel<5, 4>, k2sm::smem_bytes(5, 4), at[3]);
-      case 4: return ring(recon_tcgen05_2sm_kernel<2, 10>, k2sm::smem_bytes(2, 10), at[4]);
-      case 5: return ring(recon_tcgen05_2sm_kernel<3, 7>, k2sm::smem_bytes(3, 7), at[5]);
-      case 6: return ring(recon_tcgen05_2sm_kernel<4, 6>, k2sm::smem_bytes(4, 6), at[6]);
-      case 7: return ring(recon_tcgen05_2sm_kernel<2, 9>, k2sm::smem_bytes(2, 9), at[7]);
-      default: return ring(recon_tcgen05_2sm_kernel<4, 5>, k2sm::smem_bytes(4, 5), at[1]);
-    }
+    return dispatch_2sm<false>(tmA, tmB2, tmW, tmV, p, mom, s);
   }
   static bool attr_set = false;
   if (!attr_set) {
@@ -1231,6 +1317,79 @@ have_maps:
   recon_tcgen05_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(tmA, tmB, tmW, p);
   g_launches.fetch_add(1);
   return cudaGetLastError();
+}
+
+bool recon_tcgen05_mn_supported(const float* U, int64_t ldu, int64_t ublk, const float* V, int64_t ldv, int64_t vblk,
+                                int32_t P, int64_t K, int64_t M, int64_t N, const float* W) {
+  return aligned16(U) && aligned16(V) && aligned16(W) && ldu % 4 == 0 && ldv % 4 == 0 && ldu >= M && ldv >= N &&
+         N % 4 == 0 && (P == 1 || (ublk % 4 == 0 && vblk % 4 == 0 && ublk >= K * ldu && vblk >= K * ldv)) &&
+         M < (1 << 30) && N < (1 << 30) && K < (1 << 30);
+}
+
+cudaError_t launch_recon_tcgen05_mn(const float* U, int64_t ldu, int64_t ublk, const float* V, int64_t ldv,
+                                    int64_t vblk, int32_t P, int64_t K, int64_t M, int64_t N, float* W, float alpha,
+                                    float beta, cudaStream_t s, const float* bs, float* bias, bool* bias_done,
+                                    const K1Momentum* mom, bool bias_from_u) {
+  if (bias_done) *bias_done = false;
+  if (M <= 0 || N <= 0 || K <= 0 || P <= 0) return cudaSuccess;
+  if (!recon_tcgen05_mn_supported(U, ldu, ublk, V, ldv, vblk, P, K, M, N, W)) return cudaErrorNotSupported;
+  if (mom != nullptr && !aligned16(mom->vel)) return cudaErrorNotSupported;
+  if (P == 1) {   // the block stride is not used; keep the map's outer stride legal
+    ublk = K * ldu;
+    vblk = K * ldv;
+  }
+  CUtensorMap tmA, tmB, tmW, tmB2, tmV;
+  const MapKey key{U, V, W, mom ? mom->vel : nullptr, P, K, 0, M, N, 0, ldu, ldv, ublk, vblk};
+  int mn4 = 0;
+  if (!map_cache_get(key, &tmA, &tmB, &tmW, &tmB2, &tmV, &mn4)) {
+    // [P][K][ld] blocks, MN contiguous: box = 32 MN elements (128 B) x BK k rows, 128B swizzle with 32-B atoms;
+    // MN >= M (N) and k >= K are outside the map, so TMA fills them with zeros
+    const uint64_t dA[3] = {(uint64_t)M, (uint64_t)K, (uint64_t)P};
+    const uint64_t sA[2] = {(uint64_t)ldu * 4, (uint64_t)ublk * 4};
+    const uint64_t dB[3] = {(uint64_t)N, (uint64_t)K, (uint64_t)P};
+    const uint64_t sB[2] = {(uint64_t)ldv * 4, (uint64_t)vblk * 4};
+    const uint32_t box[3] = {32, BK, 1};
+    const uint64_t dW[2] = {(uint64_t)N, (uint64_t)M};
+    const uint64_t sW[1] = {(uint64_t)N * 4};
+    const uint32_t bW[2] = {W_CHUNK_COLS, BM};
+    // one 4-D box per operand and stage when both MN extents are multiples of 32: dims {32, K, MN/32, P},
+    // strides {ld, 128 B, blk}; the box {32, BK, 4, 1} is laid out chunk-major, i.e. exactly the four
+    // [BK x 128 B] chunks of the 3-D form (POSEIDON_K1_MN4=0 keeps the four 3-D boxes)
+    bool four = false;
+    if (M % 32 == 0 && N % 32 == 0 && knobs().mn4) {
+      const uint64_t dA4[4] = {32, (uint64_t)K, (uint64_t)M / 32, (uint64_t)P};
+      const uint64_t sA4[3] = {(uint64_t)ldu * 4, 128, (uint64_t)ublk * 4};
+      const uint64_t dB4[4] = {32, (uint64_t)K, (uint64_t)N / 32, (uint64_t)P};
+      const uint64_t sB4[3] = {(uint64_t)ldv * 4, 128, (uint64_t)vblk * 4};
+      const uint32_t box4[4] = {32, BK, 4, 1};
+      four = encode(&tmA, U, 4, dA4, sA4, box4, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
+             encode(&tmB, V, 4, dB4, sB4, box4, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    }
+    if (!four && (!encode(&tmA, U, 3, dA, sA, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+                  !encode(&tmB, V, 3, dB, sB, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)))
+      return cudaErrorNotSupported;
+    if (!encode(&tmW, W, 2, dW, sW, bW)) return cudaErrorNotSupported;
+    mn4 = four ? 1 : 0;
+    tmB2 = tmB;
+    tmV = tmW;
+    if (mom != nullptr && !encode(&tmV, mom->vel, 2, dW, sW, bW)) return cudaErrorNotSupported;
+    map_cache_put(key, tmA, tmB, tmW, tmB2, tmV, mn4);
+  }
+  Params p;
+  fill_params(p, P, K, M, N, W, alpha, beta, mom, 4.0 * (double)P * (double)K * (double)(M + N));
+  p.mn4 = mn4;
+  if (bias_from_u && bias != nullptr && bias_done != nullptr && (mom == nullptr || mom->vel_b != nullptr)) {
+    p.ucol = U;
+    p.ldu = ldu;
+    p.ublk = ublk;
+    p.bias = bias;
+    *bias_done = true;
+  } else if (bias_fusable(bs, bias, bias_done, M, mom)) {
+    p.bs = bs;
+    p.bias = bias;
+    *bias_done = true;
+  }
+  return dispatch_2sm<true>(tmA, tmB, tmW, tmV, p, mom, s);
 }
 
 }  // namespace poseidon

@@ -114,6 +114,12 @@ class PoseidonSync:
         ctx.set_lr(self.lr)
         self.ssp = bool(getattr(ctx, "flags", 0) & B.FLAG_SSP1)
         self.early_v = bool(getattr(ctx, "flags", 0) & B.FLAG_EARLY_V)
+        # FLAG_INPLACE_FACTORS: the library reads grad_out and x where they are, on its own streams (K1 at
+        # world 1, else the pack before the factor broadcast), so the allocator must not hand their memory out
+        # again before those streams have passed the sync (record_stream)
+        self.inplace_streams = []
+        if (getattr(ctx, "flags", 0) & B.FLAG_INPLACE_FACTORS) and not self.ssp:
+            self.inplace_streams = [ctx.stream(B.STREAM_RECON)] + ([ctx.stream(B.STREAM_COMM)] if ctx.world > 1 else [])
         if self.ssp and not arena:
             raise ValueError("FLAG_SSP1 needs the library arena (arena=True): PS gradients are double-buffered")
         self.arena = arena
@@ -250,6 +256,9 @@ class PoseidonSync:
 
     def sfb_backward(self, plan, grad_out, x, weight, bias):
         self.ctx.sync_fc_sfb(plan.layer_id, grad_out, x, weight, bias, self.lr, torch.cuda.current_stream())
+        for st in getattr(self, "inplace_streams", ()):
+            grad_out.record_stream(st)
+            x.record_stream(st)
 
     # ------------------------------------------------------------ driver ----
     def iteration_end(self, stats: bool = False):

@@ -26,7 +26,11 @@ def pz():
     return pz
 
 
-def test_alexnet_step_matches_oracle(pz):
+@pytest.mark.parametrize("factors", ["async", "mn", "pack"])
+def test_alexnet_step_matches_oracle(pz, factors):
+    """factors="async" is bench.py's default (POSEIDON_FLAG_INPLACE_FACTORS: fc6-fc8's pack runs on the
+    library's stream, reading grad_out and x in place); "mn" adds POSEIDON_FLAG_INPLACE_MN (K1 reads them
+    MN-major, no pack); "pack" the round-1 path (K3 on the backward's stream)."""
     import torch.nn.functional as F
     from paper_1512_06216_b200.dwbp import PoseidonSync
     from drivers.cnn import AlexNet
@@ -45,7 +49,8 @@ def test_alexnet_step_matches_oracle(pz):
     F.cross_entropy(model(x), y).backward()
     lr = max(float(p.detach().abs().max() / (4 * p.grad.abs().max())) for p in model.parameters())
     model.zero_grad(set_to_none=True)
-    ctx = pz.Context(rank=0, world=1, device=0)
+    flags = {"async": pz.FLAG_INPLACE_FACTORS, "mn": pz.FLAG_INPLACE_FACTORS | pz.FLAG_INPLACE_MN, "pack": 0}[factors]
+    ctx = pz.Context(rank=0, world=1, device=0, flags=flags)
     sync = PoseidonSync(model, ctx, K=256, lr=lr)
     plans = {p.name: p for p in sync.plans}
     fcs, convs = ("fc6", "fc7", "fc8"), ("conv1", "conv2", "conv3", "conv4", "conv5")

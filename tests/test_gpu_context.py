@@ -228,3 +228,40 @@ def test_ps_buckets_world1(pz, bucket_kb):
     for lid in range(len(shapes)):
         assert ctx.layer_stats(lid)["launched"] == 1
     ctx.close()
+
+
+@pytest.mark.parametrize("mn", [False, True])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 8), (1000, 4096, 256), (100, 200, 37), (130, 256, 8)])
+def test_context_inplace_factors_world1(pz, M, N, K, mn):
+    """POSEIDON_FLAG_INPLACE_FACTORS at world 1: the pack reads U [K x M] and V [K x N] in place on the
+    reconstruction stream; with POSEIDON_FLAG_INPLACE_MN K1 reads them itself (MN-major, no pack) and forms the
+    bias sums.  Integer variant bit-exact vs O4 (W and bias); random factors within the TF32 / fp32 gates;
+    M = 130 (not a multiple of 4) falls back to the pack; a second iteration reuses the layer; no pack time is
+    reported for the MN in-place syncs."""
+    ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device(),
+                     flags=pz.FLAG_INPLACE_FACTORS | (pz.FLAG_INPLACE_MN if mn else 0))
+    assert ctx.register_layer(0, pz.LAYER_FC, M, N, K, has_bias=True) == pz.SCHEME_SFB
+    inplace = mn and M % 4 == 0
+    # integer variant: bit-exact
+    W, b, Us, Vs, lr = S.integer_factors(M, N, K, 1, seed=M + K)
+    Wd, bd = dev(W), dev(b)
+    Ud, Vd = dev(Us[0]), dev(Vs[0])
+    ctx.sync_fc_sfb(0, Ud, Vd, Wd, bd, lr)
+    ctx.wait_layer(0)
+    ctx.iteration_end()
+    W1, b1 = O.sync_step(W, b, Us, Vs, lr)
+    assert np.array_equal(host(Wd).astype(np.float64), W1)
+    assert np.array_equal(host(bd).astype(np.float64), b1)
+    assert (ctx.layer_stats(0)["pack_ms"] == 0) == inplace
+    # random hidden-layer factors: gates
+    W, b = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, 1)
+    lr = 0.5
+    Wd, bd = dev(W), dev(b)
+    ctx.sync_fc_sfb(0, dev(Us[0]), dev(Vs[0]), Wd, bd, lr)
+    ctx.wait_layer(0)
+    ctx.iteration_end()
+    W1, b1 = O.sync_step(W, b, Us, Vs, lr)
+    check_update(W, host(Wd), W1, 2e-3)
+    check_update(b, host(bd), b1, 1e-5)
+    ctx.close()

@@ -319,3 +319,63 @@ def test_k3_pack_deterministic_and_u_only(pz):
         outs.append((host(ud).copy(), host(cs).copy()))
     assert all(np.array_equal(outs[0][1], o[1]) for o in outs[1:])   # fixed-order column sums
     assert np.array_equal(_tf32_bits(outs[0][0]), _tf32_rna(host(U).T))
+
+
+# --------------------------------------- K1 on MN-major (in-place) factors ----
+@pytest.mark.parametrize("M,N,K,P,ldu", [(200, 300, 6, 2, 200), (128, 256, 8, 1, 128), (1000, 1024, 37, 2, 1004),
+                                         (300, 520, 64, 4, 304), (256, 512, 256, 1, 256), (4, 4, 1, 1, 4)])
+def test_reconstruct_sgd_mn_integer_bit_exact(pz, M, N, K, P, ldu):
+    """K1 reading the factors as the layer produced them (U [P][K][ldu], V [P][K][N], MN contiguous): integer
+    variant bit-exact vs O4; ragged M / N / K tails, padded ldu, single-row K, tiny tiles."""
+    g = S.rng(M + N + K)
+    U = np.zeros((P, K, ldu), np.float32)
+    U[:, :, :M] = g.integers(-3, 4, size=(P, K, M))
+    U[:, :, M:] = 1e6                              # columns [M, ldu) must never be read
+    V = g.integers(0, 4, size=(P, K, N)).astype(np.float32)
+    W = (g.integers(-1023, 1024, size=(M, N)) * 2.0 ** -10).astype(np.float32)
+    lr = 2.0 ** -7
+    Wd = dev(W)
+    pz.reconstruct_sgd_mn(dev(U), dev(V), P, K, M, N, Wd, -lr / P)
+    W1, _ = O.sync_step(W, None, [U[p, :, :M] for p in range(P)], [V[p] for p in range(P)], lr)
+    assert np.array_equal(host(Wd).astype(np.float64), W1)
+
+
+@pytest.mark.parametrize("M,N,K,P", [(1000, 4096, 256, 1), (512, 1024, 100, 3)])
+def test_reconstruct_sgd_mn_equals_kmajor(pz, M, N, K, P):
+    """Same factors, two operand layouts: the MN-major and the K-major (transposed, zero-padded) K1 give
+    bit-identical W (same accumulation order), random fp32 factors."""
+    U = torch.randn(P, K, M, device="cuda") * 0.01
+    V = torch.randn(P, K, N, device="cuda").relu()
+    W = torch.randn(M, N, device="cuda")
+    ldk = (K + 3) // 4 * 4
+    Ug = torch.zeros(P, M, ldk, device="cuda")
+    Vg = torch.zeros(P, N, ldk, device="cuda")
+    Ug[:, :, :K] = U.transpose(1, 2)
+    Vg[:, :, :K] = V.transpose(1, 2)
+    Wa, Wb = W.clone(), W.clone()
+    pz.reconstruct_sgd_mn(U, V, P, K, M, N, Wa, -1e-3)
+    pz.reconstruct_sgd(Ug, Vg, P, K, ldk, M, N, Wb, -1e-3)
+    torch.cuda.synchronize()
+    assert torch.equal(Wa, Wb)
+
+
+def test_reconstruct_sgd_mn_random_vs_oracle(pz):
+    """Random hidden-layer factors at the C3 fc6 shape, P = 1: within the TF32 gate of O4 (the tensor core
+    reads the fp32 factors as TF32, truncating: reading Z12'), sampled rows."""
+    M, N, K = 4096, 9216, 256
+    W, _ = S.fc_weights_randbias(M, N)
+    Us, Vs = S.hidden_factors(M, N, K, 1)
+    lr = 0.5
+    Wd = dev(W)
+    pz.reconstruct_sgd_mn(dev(Us[0]), dev(Vs[0]), 1, K, M, N, Wd, -lr)
+    rows = _sampled_rows(M, seed=5)
+    W1r, _ = O.sync_step_rows(W[rows], None, Us, Vs, lr, rows)
+    check_update(W[rows], host(Wd)[rows], W1r, TOL_TF32)
+
+
+def test_reconstruct_sgd_mn_rejects_bad_layouts(pz):
+    U = torch.zeros(2, 8, 6, device="cuda")    # ldu = 6: not a multiple of 4
+    V = torch.zeros(2, 8, 16, device="cuda")
+    W = torch.zeros(6, 16, device="cuda")
+    with pytest.raises(pz.PoseidonError):
+        pz.reconstruct_sgd_mn(U, V, 2, 8, 6, 16, W, 1.0)

@@ -13,6 +13,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1512_06216_b200 as pz  # noqa: E402
+from paper_1512_06216_b200 import binding as B  # noqa: E402
 
 HBM = 6458.7e9
 
@@ -31,7 +32,8 @@ def timeit(fn, iters=30, warm=3):
     return ts[len(ts) // 2]
 
 
-tag = " ".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith("POSEIDON_K1")) or "default"
+MN = os.environ.get("K1_AB_MN") == "1"   # MN-major operands (poseidon_reconstruct_sgd_mn)
+tag = ("MN " if MN else "") + " ".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith("POSEIDON_K1")) or "default"
 SHAPES = [(4096, 9216, 256, 1), (4096, 9216, 256, 2), (4096, 9216, 256, 4), (4096, 4096, 256, 1),
           (1000, 4096, 256, 1), (1000, 4100, 37, 3), (21841, 4096, 256, 4), (4096, 9216, 256, 8)]
 for (M, N, K, P) in SHAPES:
@@ -41,10 +43,18 @@ for (M, N, K, P) in SHAPES:
     Vg = torch.randn(P, N, ldk, device="cuda", generator=g).relu()
     W0 = torch.randn(M, N, device="cuda", generator=g)
     W = W0.clone()
-    pz.reconstruct_sgd(Ug, Vg, P, K, ldk, M, N, W, -1e-3)   # one update for the digest
+    if MN:   # the same factors in the layer's own layout: U [P][K][Mp], V [P][K][N]
+        Mp = (M + 3) // 4 * 4
+        Um = torch.zeros(P, K, Mp, device="cuda")
+        Um[:, :, :M] = Ug[:, :, :K].transpose(1, 2)
+        Vm = Vg[:, :, :K].transpose(1, 2).contiguous()
+        run = lambda: B.reconstruct_sgd_mn(Um, Vm, P, K, M, N, W, -1e-3)  # noqa: E731
+    else:
+        run = lambda: pz.reconstruct_sgd(Ug, Vg, P, K, ldk, M, N, W, -1e-3)  # noqa: E731
+    run()   # one update for the digest
     torch.cuda.synchronize()
     dig = hashlib.sha1(W.cpu().numpy().tobytes()).hexdigest()[:12]
-    ms = timeit(lambda: pz.reconstruct_sgd(Ug, Vg, P, K, ldk, M, N, W, -1e-3))
+    ms = timeit(run)
     flops = 2.0 * M * N * K * P
     byts = 8.0 * M * N + 4.0 * P * K * (M + N)
     print(f"[{tag}] M={M} N={N} K={K} P={P}: {ms * 1e3:7.1f} us  {flops / ms / 1e9:6.1f} TFLOP/s  "
