@@ -17,6 +17,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "internal.h"
@@ -195,6 +196,11 @@ struct poseidon_ctx {
   std::vector<Layer> buckets; // pseudo-layers, addressed as MAX_LAYERS + index in records
   NvlsState* nvls = nullptr;
   std::string nvls_error;
+  // CUDA-graph capture (round 2): id of the stream-capture sequence the caller is in (0 = eager), and per event
+  // the internal twin the captured waits use plus the capture id of its last record (evrec / evwait)
+  unsigned long long cap_id = 0;
+  std::unordered_map<cudaEvent_t, std::pair<cudaEvent_t, unsigned long long>> evmeta;
+  cudaEvent_t join_ev[2] = {nullptr, nullptr};   // capture: the comm / recon streams' tails, joined at iteration_end
 };
 
 namespace {
@@ -202,6 +208,46 @@ namespace {
 poseidon_status_t check_ctx(poseidon_ctx_t c) {
   if (!c) return fail(POSEIDON_ERR_NOT_INITIALIZED, "context is NULL");
   return POSEIDON_OK;
+}
+
+// ---- CUDA-graph capture of a training step (round 2) ----
+// An event recorded on a stream that is being captured becomes a capture-internal dependency, not a timestamp.
+// While the caller captures, every event the library records is recorded twice: an internal twin (the waits use
+// it, so the library's streams fork from and join the capture) and the event itself as an external event-record
+// node (each replay stamps it, so the statistics stay valid).  A wait on an event last recorded outside the
+// current capture (an earlier iteration) is dropped: graph launches into one stream are ordered as a whole.
+void note_capture(poseidon_ctx_t c, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  if (cudaStreamGetCaptureInfo(s, &st, &id) != cudaSuccess) {
+    cudaGetLastError();
+    st = cudaStreamCaptureStatusNone;
+  }
+  c->cap_id = (st == cudaStreamCaptureStatusActive) ? id : 0;
+}
+cudaError_t make_twin(poseidon_ctx_t c, cudaEvent_t ev) {
+  if (!ev || c->evmeta.count(ev)) return cudaSuccess;
+  cudaEvent_t tw = nullptr;
+  cudaError_t e = cudaEventCreateWithFlags(&tw, cudaEventDisableTiming);
+  if (e == cudaSuccess) c->evmeta[ev] = {tw, 0ull};
+  return e;
+}
+cudaError_t evrec(poseidon_ctx_t c, cudaEvent_t ev, cudaStream_t s) {
+  auto it = c->evmeta.find(ev);
+  if (c->cap_id == 0 || it == c->evmeta.end()) {
+    if (it != c->evmeta.end()) it->second.second = 0;
+    return cudaEventRecord(ev, s);
+  }
+  cudaError_t e = cudaEventRecord(it->second.first, s);
+  if (e != cudaSuccess) return e;
+  it->second.second = c->cap_id;
+  return cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+}
+cudaError_t evwait(poseidon_ctx_t c, cudaStream_t s, cudaEvent_t ev) {
+  auto it = c->evmeta.find(ev);
+  if (c->cap_id == 0 || it == c->evmeta.end()) return cudaStreamWaitEvent(s, ev, 0);
+  if (it->second.second != c->cap_id) return cudaSuccess;   // recorded before this capture: already ordered
+  return cudaStreamWaitEvent(s, it->second.first, 0);
 }
 
 // Asynchronous NCCL failures are sticky; they surface at the next wait_layer / iteration_end /
@@ -269,13 +315,16 @@ Layer& resolve(poseidon_ctx_t c, int32_t id) {
   return id >= MAX_LAYERS ? c->buckets[(size_t)(id - MAX_LAYERS)] : c->layers[(size_t)id];
 }
 
-poseidon_status_t ensure_events(Layer& L) {
+poseidon_status_t ensure_events(poseidon_ctx_t c, Layer& L) {
   if (L.events_created) return POSEIDON_OK;
   for (int i = 0; i < RING; ++i) {
     EvSet& e = L.ev[i];
     cudaEvent_t* all[] = {&e.ready, &e.start, &e.gathered, &e.kstart, &e.kend, &e.done, &e.vready, &e.vgath,
                           &e.pstart, &e.pend};
-    for (cudaEvent_t* p : all) CU_TRY(cudaEventCreate(p));
+    for (cudaEvent_t* p : all) {
+      CU_TRY(cudaEventCreate(p));
+      CU_TRY(make_twin(c, *p));   // created now: nothing is created while a caller captures
+    }
   }
   L.events_created = true;
   return POSEIDON_OK;
@@ -326,7 +375,7 @@ poseidon_status_t fuzz(cudaStream_t s) {
 // Producer-side prologue shared by both schemes: the previous sync of this
 // layer must be finished before its buffers are rewritten.
 poseidon_status_t producer_guard(poseidon_ctx_t c, Layer& L, cudaStream_t producer) {
-  if (L.last_iter >= 0) CU_TRY(cudaStreamWaitEvent(producer, L.ev[L.last_iter % RING].done, 0));
+  if (L.last_iter >= 0) CU_TRY(evwait(c, producer, L.ev[L.last_iter % RING].done));
   return POSEIDON_OK;
 }
 
@@ -345,15 +394,15 @@ poseidon_status_t sfb_comm(poseidon_ctx_t c, Layer& L, int set, EvSet& e, cudaEv
   const int P = c->world;
   const GatherSet g = gather_set(L, set);
   if (P <= 1) {   // nothing to gather: the sync starts on the reconstruction stream (one stream hop less)
-    CU_TRY(cudaStreamWaitEvent(c->recon_stream, wait_ev, 0));
+    CU_TRY(evwait(c, c->recon_stream, wait_ev));
     FZ(c->recon_stream);
-    CU_TRY(cudaEventRecord(e.start, c->recon_stream));
+    CU_TRY(evrec(c, e.start, c->recon_stream));
     e.g_eff = e.start;
     return POSEIDON_OK;
   }
-  CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
+  CU_TRY(evwait(c, c->comm_stream, wait_ev));
   FZ(c->comm_stream);
-  CU_TRY(cudaEventRecord(e.start, c->comm_stream));
+  CU_TRY(evrec(c, e.start, c->comm_stream));
   e.g_eff = e.start;
   const size_t ucount = (size_t)(L.M * L.ldk), vfull = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
   const size_t vcount = L.v_posted ? 0 : vfull;   // early V: already broadcast during the forward pass
@@ -379,7 +428,7 @@ poseidon_status_t sfb_comm(poseidon_ctx_t c, Layer& L, int set, EvSet& e, cudaEv
     r.sent += per;  // handed to NCCL once; NCCL forwards it to P-1 peers
   }
   r.recv += per * (uint64_t)(P - 1);
-  CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+  CU_TRY(evrec(c, e.gathered, c->comm_stream));
   e.g_eff = e.gathered;
   return POSEIDON_OK;
 }
@@ -391,16 +440,16 @@ poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, floa
                              cudaEvent_t extra, EvSet& dst) {
   const int P = c->world;
   const GatherSet g = gather_set(L, set);
-  CU_TRY(cudaStreamWaitEvent(c->recon_stream, src_g, 0));
-  if (extra) CU_TRY(cudaStreamWaitEvent(c->recon_stream, extra, 0));
-  if (L.v_posted) CU_TRY(cudaStreamWaitEvent(c->recon_stream, L.ev[L.v_iter % RING].vgath, 0));
+  CU_TRY(evwait(c, c->recon_stream, src_g));
+  if (extra) CU_TRY(evwait(c, c->recon_stream, extra));
+  if (L.v_posted) CU_TRY(evwait(c, c->recon_stream, L.ev[L.v_iter % RING].vgath));
   FZ(c->recon_stream);
   // an event record costs ~1 us of stream time: record only the events whose times differ (BSP at P = 1
   // the sync's start was just recorded on this stream; with nothing after K1, its end is `done`)
   if (P <= 1 && src_g == dst.start && !extra) {
     dst.ks_eff = dst.start;
   } else {
-    CU_TRY(cudaEventRecord(dst.kstart, c->recon_stream));
+    CU_TRY(evrec(c, dst.kstart, c->recon_stream));
     dst.ks_eff = dst.kstart;
   }
   dst.ke_eff = dst.kend;
@@ -435,7 +484,7 @@ poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, floa
   }
   if ((err = debug_sync(c->recon_stream, "K1/K1r reconstruct+sgd")) != cudaSuccess) return cuda_fail(err, "K1");
   if (bias && !bias_done)
-    CU_TRY(cudaEventRecord(dst.kend, c->recon_stream));  // kernel_ms = K1/K1r alone
+    CU_TRY(evrec(c, dst.kend, c->recon_stream));  // kernel_ms = K1/K1r alone
   else
     dst.ke_eff = dst.done;
   if (bias && !bias_done) {
@@ -444,7 +493,7 @@ poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, floa
     if (err != cudaSuccess) return cuda_fail(err, "bias update launch");
     if ((err = debug_sync(c->recon_stream, "bias update")) != cudaSuccess) return cuda_fail(err, "bias");
   }
-  CU_TRY(cudaEventRecord(dst.done, c->recon_stream));
+  CU_TRY(evrec(c, dst.done, c->recon_stream));
   return POSEIDON_OK;
 }
 
@@ -475,15 +524,15 @@ bool async_pack_ok(poseidon_ctx_t c, const Layer& L) {
 poseidon_status_t sfb_async_pack(poseidon_ctx_t c, int32_t id, Layer& L, const float* U, const float* V, float* W,
                                  float* bias, float lr, cudaStream_t producer) {
   EvSet& e = L.ev[c->iter % RING];
-  CU_TRY(cudaEventRecord(e.ready, producer));   // the factors exist
+  CU_TRY(evrec(c, e.ready, producer));   // the factors exist
   cudaStream_t ls = c->world > 1 ? c->comm_stream : c->recon_stream;
-  CU_TRY(cudaStreamWaitEvent(ls, e.ready, 0));
+  CU_TRY(evwait(c, ls, e.ready));
   // the previous sync of this layer (its K1 on the recon stream) must be done with the gather buffers
-  if (L.last_iter >= 0) CU_TRY(cudaStreamWaitEvent(ls, L.ev[L.last_iter % RING].done, 0));
+  if (L.last_iter >= 0) CU_TRY(evwait(c, ls, L.ev[L.last_iter % RING].done));
   poseidon_status_t st = pack_sfb(c, L, U, L.M, V, L.N, ls);
   if (st) return st;
   e.pack_async = true;
-  CU_TRY(cudaEventRecord(e.pend, ls));
+  CU_TRY(evrec(c, e.pend, ls));
   L.last_iter = c->iter;
   st = launch_factor_sync(c, id, L, W, bias, lr, e.pend);
   L.v_posted = false;
@@ -494,12 +543,12 @@ poseidon_status_t sfb_inplace(poseidon_ctx_t c, int32_t id, Layer& L, const floa
                               float* bias, float lr, cudaStream_t producer) {
   EvSet& e = L.ev[c->iter % RING];
   e.packed = false;
-  CU_TRY(cudaEventRecord(e.ready, producer));
+  CU_TRY(evrec(c, e.ready, producer));
   L.last_iter = c->iter;
   IterRecord& r = open_record(c);
-  CU_TRY(cudaStreamWaitEvent(c->recon_stream, e.ready, 0));
+  CU_TRY(evwait(c, c->recon_stream, e.ready));
   FZ(c->recon_stream);
-  CU_TRY(cudaEventRecord(e.start, c->recon_stream));
+  CU_TRY(evrec(c, e.start, c->recon_stream));
   e.g_eff = e.start;
   e.ks_eff = e.start;
   e.ke_eff = e.done;
@@ -512,7 +561,7 @@ poseidon_status_t sfb_inplace(poseidon_ctx_t c, int32_t id, Layer& L, const floa
   if (err != cudaSuccess) return cuda_fail(err, "in-place reconstruct+sgd launch");
   if (bias && !bias_done) return fail(POSEIDON_ERR_STATE, "in-place sync: bias not fused");
   if ((err = debug_sync(c->recon_stream, "K1 in place")) != cudaSuccess) return cuda_fail(err, "K1 in place");
-  CU_TRY(cudaEventRecord(e.done, c->recon_stream));
+  CU_TRY(evrec(c, e.done, c->recon_stream));
   r.layers.push_back(id);
   return POSEIDON_OK;
 }
@@ -538,9 +587,9 @@ poseidon_status_t launch_sfb_comm(poseidon_ctx_t c, int32_t id, Layer& L, float*
 // per-worker bias sums.  Records e.start and e.gathered.
 poseidon_status_t sfps_comm(poseidon_ctx_t c, Layer& L, EvSet& e, cudaEvent_t wait_ev, IterRecord& r) {
   const int P = c->world;
-  CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
+  CU_TRY(evwait(c, c->comm_stream, wait_ev));
   FZ(c->comm_stream);
-  CU_TRY(cudaEventRecord(e.start, c->comm_stream));
+  CU_TRY(evrec(c, e.start, c->comm_stream));
   e.g_eff = e.start;
   if (P <= 1) return POSEIDON_OK;
   const size_t ucount = (size_t)(L.M * L.ldk), vcount = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
@@ -570,7 +619,7 @@ poseidon_status_t sfps_comm(poseidon_ctx_t c, Layer& L, EvSet& e, cudaEvent_t wa
   NC_TRY(ncclGroupEnd());
   r.sent += sent;
   r.recv += recv;
-  CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+  CU_TRY(evrec(c, e.gathered, c->comm_stream));
   e.g_eff = e.gathered;
   return POSEIDON_OK;
 }
@@ -582,9 +631,9 @@ poseidon_status_t sfps_comm(poseidon_ctx_t c, Layer& L, EvSet& e, cudaEvent_t wa
 poseidon_status_t sfps_update(poseidon_ctx_t c, Layer& L, float* W, float* bias, float lr, cudaEvent_t src_g,
                               EvSet& dst, IterRecord& r) {
   const int P = c->world;
-  CU_TRY(cudaStreamWaitEvent(c->recon_stream, src_g, 0));
+  CU_TRY(evwait(c, c->recon_stream, src_g));
   FZ(c->recon_stream);
-  CU_TRY(cudaEventRecord(dst.kstart, c->recon_stream));
+  CU_TRY(evrec(c, dst.kstart, c->recon_stream));
   dst.ks_eff = dst.kstart;
   dst.ke_eff = dst.kend;
   const float alpha = -lr / (float)P;
@@ -607,8 +656,8 @@ poseidon_status_t sfps_update(poseidon_ctx_t c, Layer& L, float* W, float* bias,
     }
     if ((err = debug_sync(c->recon_stream, "SF-PS K1")) != cudaSuccess) return cuda_fail(err, "SF-PS K1");
   }
-  CU_TRY(cudaEventRecord(dst.kend, c->recon_stream));
-  CU_TRY(cudaStreamWaitEvent(c->comm_stream, dst.kend, 0));
+  CU_TRY(evrec(c, dst.kend, c->recon_stream));
+  CU_TRY(evwait(c, c->comm_stream, dst.kend));
   FZ(c->comm_stream);
   int64_t S0b, S0e, S0pad;
   poseidon_shard_range(L.M, P, 0, &S0b, &S0e, &S0pad);
@@ -638,7 +687,7 @@ poseidon_status_t sfps_update(poseidon_ctx_t c, Layer& L, float* W, float* bias,
               : launch_bias_update(L.Bs, L.M, P, bias, L.M, alpha, c->comm_stream);
     if (err != cudaSuccess) return cuda_fail(err, "bias update launch");
   }
-  CU_TRY(cudaEventRecord(dst.done, c->comm_stream));
+  CU_TRY(evrec(c, dst.done, c->comm_stream));
   return POSEIDON_OK;
 }
 
@@ -663,16 +712,16 @@ bool ps_fused(poseidon_ctx_t c, const Layer& L) { return c->world > 1 && c->ps_n
 // kernel, so nothing is launched here.  Records e.start (and e.gathered).
 poseidon_status_t ps_comm(poseidon_ctx_t c, Layer& L, float* grad, EvSet& e, cudaEvent_t wait_ev, IterRecord& r) {
   const int P = c->world;
-  CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
+  CU_TRY(evwait(c, c->comm_stream, wait_ev));
   FZ(c->comm_stream);
-  CU_TRY(cudaEventRecord(e.start, c->comm_stream));
+  CU_TRY(evrec(c, e.start, c->comm_stream));
   e.g_eff = e.ks_eff = e.start;
   if (ps_fused(c, L) || P <= 1) return POSEIDON_OK;
   NC_TRY(ncclReduceScatter(grad, grad + (size_t)c->rank * L.S, (size_t)L.S, ncclFloat32, ncclSum, c->comm,
                            c->comm_stream));
   r.sent += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
   r.recv += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
-  CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+  CU_TRY(evrec(c, e.gathered, c->comm_stream));
   e.g_eff = e.ks_eff = e.gathered;
   return POSEIDON_OK;
 }
@@ -688,7 +737,7 @@ poseidon_status_t ps_update(poseidon_ctx_t c, Layer& L, float* grad, float* W, f
                                      L.end, L.padded, -lr / (float)P, (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0,
                                      kNvlsBlocks, L.S, L.vel, 1.0f / (float)P, lr, L.mu, L.wd, c->comm_stream);
     if (err != cudaSuccess) return cuda_fail(err, "fused NVLS PS launch");
-    CU_TRY(cudaEventRecord(dst.done, c->comm_stream));
+    CU_TRY(evrec(c, dst.done, c->comm_stream));
     // bytes through NVLink per rank: the switch reads this rank's gradient for the other P-1
     // shards and writes the other ranks' updated shards here; this rank reads its reduced shard
     // and writes its updated shard once into the switch
@@ -712,7 +761,7 @@ poseidon_status_t ps_update(poseidon_ctx_t c, Layer& L, float* grad, float* W, f
   if (err != cudaSuccess) return cuda_fail(err, "ps shard update launch");
   if ((err = debug_sync(c->comm_stream, "K2 ps shard update")) != cudaSuccess) return cuda_fail(err, "K2");
   if (P > 1) {
-    CU_TRY(cudaEventRecord(dst.kend, c->comm_stream));
+    CU_TRY(evrec(c, dst.kend, c->comm_stream));
     dst.ke_eff = dst.kend;
     NC_TRY(ncclAllGather(W + (size_t)c->rank * L.S, W, (size_t)L.S, ncclFloat32, c->comm, c->comm_stream));
     r.sent += (uint64_t)L.S * 4u * (uint64_t)(P - 1);
@@ -722,12 +771,12 @@ poseidon_status_t ps_update(poseidon_ctx_t c, Layer& L, float* grad, float* W, f
   }
   if (zero && !fused_zero) {
     if (P == 1) {  // kernel_ms must not include the memset
-      CU_TRY(cudaEventRecord(dst.kend, c->comm_stream));
+      CU_TRY(evrec(c, dst.kend, c->comm_stream));
       dst.ke_eff = dst.kend;
     }
     CU_TRY(cudaMemsetAsync(grad, 0, (size_t)L.padded * 4u, c->comm_stream));
   }
-  CU_TRY(cudaEventRecord(dst.done, c->comm_stream));
+  CU_TRY(evrec(c, dst.done, c->comm_stream));
   return POSEIDON_OK;
 }
 
@@ -751,16 +800,16 @@ poseidon_status_t launch_ps_comm(poseidon_ctx_t c, int32_t id, Layer& L, float* 
 poseidon_status_t ps_comm_allreduce(poseidon_ctx_t c, Layer& L, float* grad, EvSet& e, cudaEvent_t wait_ev,
                                     IterRecord& r) {
   const int P = c->world;
-  CU_TRY(cudaStreamWaitEvent(c->comm_stream, wait_ev, 0));
+  CU_TRY(evwait(c, c->comm_stream, wait_ev));
   FZ(c->comm_stream);
-  CU_TRY(cudaEventRecord(e.start, c->comm_stream));
+  CU_TRY(evrec(c, e.start, c->comm_stream));
   e.g_eff = e.start;
   if (P <= 1) return POSEIDON_OK;
   NC_TRY(ncclAllReduce(grad, grad, (size_t)L.padded, ncclFloat32, ncclSum, c->comm, c->comm_stream));
   const uint64_t wire = 2u * (uint64_t)L.S * 4u * (uint64_t)(P - 1);
   r.sent += wire;
   r.recv += wire;
-  CU_TRY(cudaEventRecord(e.gathered, c->comm_stream));
+  CU_TRY(evrec(c, e.gathered, c->comm_stream));
   e.g_eff = e.gathered;
   return POSEIDON_OK;
 }
@@ -771,10 +820,10 @@ poseidon_status_t ps_comm_allreduce(poseidon_ctx_t c, Layer& L, float* grad, EvS
 poseidon_status_t ps_update_local(poseidon_ctx_t c, Layer& L, float* grad, float* W, float lr, cudaEvent_t src_g,
                                   cudaEvent_t extra, EvSet& dst) {
   const int P = c->world;
-  CU_TRY(cudaStreamWaitEvent(c->recon_stream, src_g, 0));
-  if (extra) CU_TRY(cudaStreamWaitEvent(c->recon_stream, extra, 0));
+  CU_TRY(evwait(c, c->recon_stream, src_g));
+  if (extra) CU_TRY(evwait(c, c->recon_stream, extra));
   FZ(c->recon_stream);
-  CU_TRY(cudaEventRecord(dst.kstart, c->recon_stream));
+  CU_TRY(evrec(c, dst.kstart, c->recon_stream));
   dst.ks_eff = dst.kstart;
   dst.ke_eff = dst.done;
   const bool zero = (L.ps_flags & POSEIDON_PS_ZERO_GRAD) != 0;
@@ -788,7 +837,7 @@ poseidon_status_t ps_update_local(poseidon_ctx_t c, Layer& L, float* grad, float
   }
   if (err != cudaSuccess) return cuda_fail(err, "SSP PS local update launch");
   if ((err = debug_sync(c->recon_stream, "SSP PS update")) != cudaSuccess) return cuda_fail(err, "SSP PS update");
-  CU_TRY(cudaEventRecord(dst.done, c->recon_stream));
+  CU_TRY(evrec(c, dst.done, c->recon_stream));
   return POSEIDON_OK;
 }
 
@@ -812,8 +861,8 @@ poseidon_status_t ssp_hook(poseidon_ctx_t c, int32_t id, Layer& L, float* W, flo
     if (st) return st;
   } else {
     // first sync: nothing to apply yet; done only orders after this backward
-    CU_TRY(cudaStreamWaitEvent(c->recon_stream, e.ready, 0));
-    CU_TRY(cudaEventRecord(e.done, c->recon_stream));
+    CU_TRY(evwait(c, c->recon_stream, e.ready));
+    CU_TRY(evrec(c, e.done, c->recon_stream));
     e.ks_eff = e.ke_eff = e.done;
   }
   L.ssp_pend = true;
@@ -831,7 +880,7 @@ poseidon_status_t ssp_hook(poseidon_ctx_t c, int32_t id, Layer& L, float* W, flo
 poseidon_status_t sfb_after_pack(poseidon_ctx_t c, int32_t id, Layer& L, float* W, float* bias, float lr,
                                  cudaStream_t producer) {
   EvSet& e = L.ev[c->iter % RING];
-  CU_TRY(cudaEventRecord(e.ready, producer));
+  CU_TRY(evrec(c, e.ready, producer));
   L.last_iter = c->iter;
   if (c->ssp) return ssp_hook(c, id, L, W, bias, nullptr, lr);
   if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
@@ -857,7 +906,7 @@ poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t l
   float* b_slot = g.B + (size_t)c->rank * L.M;
   // U (+ bias column sums) and, unless the early input broadcast already packed it, V: one launch
   EvSet& e = L.ev[c->iter % RING];
-  CU_TRY(cudaEventRecord(e.pstart, producer));
+  CU_TRY(evrec(c, e.pstart, producer));
   e.packed = true;
   e.pack_async = false;
   cudaError_t err = launch_pack_uv(U, ldU, u_slot, L.M, b_slot, L.v_posted ? nullptr : V, ldV, v_slot, L.N,
@@ -867,7 +916,7 @@ poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t l
   return POSEIDON_OK;
 }
 
-void free_layer(Layer& L) {
+void free_layer(poseidon_ctx_t c, Layer& L) {
   if (L.symm) {
     if (L.win) ncclCommWindowDeregister(L.win_comm, L.win);  // collective: every rank frees the layer
     ncclMemFree(L.symm);
@@ -886,9 +935,17 @@ void free_layer(Layer& L) {
   if (L.events_created) {
     for (int i = 0; i < RING; ++i) {
       EvSet& e = L.ev[i];
-      cudaEvent_t all[] = {e.ready, e.start, e.gathered, e.kstart, e.kend, e.done, e.vready, e.vgath, e.pstart};
-      for (cudaEvent_t ev : all)
-        if (ev) cudaEventDestroy(ev);
+      cudaEvent_t all[] = {e.ready, e.start, e.gathered, e.kstart, e.kend, e.done, e.vready, e.vgath, e.pstart,
+                           e.pend};
+      for (cudaEvent_t ev : all) {
+        if (!ev) continue;
+        auto it = c->evmeta.find(ev);
+        if (it != c->evmeta.end()) {
+          cudaEventDestroy(it->second.first);
+          c->evmeta.erase(it);
+        }
+        cudaEventDestroy(ev);
+      }
       e = EvSet{};
     }
     L.events_created = false;
@@ -957,7 +1014,13 @@ poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, 
     return cuda_fail(e1 != cudaSuccess ? e1 : e2, "stream create");
   }
   for (auto& r : c->rec) {
-    if (cudaEventCreate(&r.bwd_end) != cudaSuccess) {
+    if (cudaEventCreate(&r.bwd_end) != cudaSuccess || make_twin(c, r.bwd_end) != cudaSuccess) {
+      delete c;
+      return fail(POSEIDON_ERR_CUDA, "event create");
+    }
+  }
+  for (auto& j : c->join_ev) {
+    if (cudaEventCreateWithFlags(&j, cudaEventDisableTiming) != cudaSuccess) {
       delete c;
       return fail(POSEIDON_ERR_CUDA, "event create");
     }
@@ -990,10 +1053,10 @@ poseidon_status_t poseidon_finalize(poseidon_ctx_t c) {
   cudaSetDevice(c->device);
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->recon_stream) cudaStreamSynchronize(c->recon_stream);
-  for (auto& L : c->layers) free_layer(L);
+  for (auto& L : c->layers) free_layer(c, L);
   for (auto& B : c->buckets) {
     B.grad = B.Wps = nullptr;   // views into the arena
-    free_layer(B);
+    free_layer(c, B);
   }
   if (c->nvls) nvls_destroy(c->comm, c->nvls);
   if (c->win_g) ncclCommWindowDeregister(c->comm, c->win_g);
@@ -1006,6 +1069,9 @@ poseidon_status_t poseidon_finalize(poseidon_ctx_t c) {
     }
   for (auto& r : c->rec)
     if (r.bwd_end) cudaEventDestroy(r.bwd_end);
+  for (auto& kv : c->evmeta) cudaEventDestroy(kv.second.first);
+  for (auto& j : c->join_ev)
+    if (j) cudaEventDestroy(j);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->recon_stream) cudaStreamDestroy(c->recon_stream);
@@ -1040,7 +1106,7 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
     // re-registration: wait for the layer to be idle
     cudaEventSynchronize(L.ev[L.last_iter % RING].done);
   }
-  free_layer(L);
+  free_layer(c, L);
   L = Layer{};
   L.kind = kind;
   L.M = M;
@@ -1106,7 +1172,7 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
     CU_TRY(cudaMemset(L.Vg, 0, vb));
     CU_TRY(cudaMemset(L.Bs, 0, bb));
   }
-  st = ensure_events(L);
+  st = ensure_events(c, L);
   if (st) return st;
   L.registered = true;
   if (chosen_scheme) *chosen_scheme = scheme;
@@ -1315,7 +1381,7 @@ poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
     B.S = padded / c->world;
     B.ps_flags = POSEIDON_PS_ZERO_GRAD;
     B.in_arena = true;
-    st = ensure_events(B);
+    st = ensure_events(c, B);
     if (st) return st;
     // momentum already set on the members carries over to the bucket (all members share mu, wd)
     const Layer& M0 = c->layers[(size_t)B.members[0]];
@@ -1441,6 +1507,7 @@ poseidon_status_t poseidon_sync_fc_sfb(poseidon_ctx_t c, int32_t id, const float
   if (bias && !L->has_bias) return fail(POSEIDON_ERR_INVALID_ARG, "layer registered without bias");
   if (!aligned16(W)) return fail(POSEIDON_ERR_ALIGNMENT, "W must be 16-byte aligned");
   cudaStream_t ps = reinterpret_cast<cudaStream_t>(producer);
+  note_capture(c, ps);
   st = producer_guard(c, *L, ps);
   if (st) return st;
   if (inplace_ok(c, *L, U, V, W)) return sfb_inplace(c, id, *L, U, V, W, bias, lr, ps);
@@ -1467,6 +1534,7 @@ poseidon_status_t poseidon_sfb_post_input(poseidon_ctx_t c, int32_t id, const fl
   if (!V || ldV < L->N) return fail(POSEIDON_ERR_INVALID_ARG, "V is NULL or ldV < N");
   if (L->v_posted) return fail(POSEIDON_ERR_STATE, "V already posted for this sync");
   cudaStream_t ps = reinterpret_cast<cudaStream_t>(stream);
+  note_capture(c, ps);
   st = producer_guard(c, *L, ps);   // the previous sync's K1 no longer reads the gather buffers
   if (st) return st;
   const int P = c->world;
@@ -1475,11 +1543,11 @@ poseidon_status_t poseidon_sfb_post_input(poseidon_ctx_t c, int32_t id, const fl
   cudaError_t err = launch_pack_t(V, ldV, v_slot, L->ldk, L->K, L->N, round, nullptr, ps);
   if (err != cudaSuccess) return cuda_fail(err, "pack V launch");
   EvSet& e = L->ev[c->iter % RING];
-  CU_TRY(cudaEventRecord(e.vready, ps));
+  CU_TRY(evrec(c, e.vready, ps));
   if (P > 1) {
     IterRecord& r = open_record(c);
     const size_t vcount = (size_t)(L->N * L->ldk);
-    CU_TRY(cudaStreamWaitEvent(c->comm_stream, e.vready, 0));
+    CU_TRY(evwait(c, c->comm_stream, e.vready));
     FZ(c->comm_stream);
     if (L->bcast) {
       const size_t vb = (size_t)((char*)L->Vg - (char*)L->symm);
@@ -1491,9 +1559,9 @@ poseidon_status_t poseidon_sfb_post_input(poseidon_ctx_t c, int32_t id, const fl
     }
     r.sent += (uint64_t)vcount * 4u;
     r.recv += (uint64_t)vcount * 4u * (uint64_t)(P - 1);
-    CU_TRY(cudaEventRecord(e.vgath, c->comm_stream));
+    CU_TRY(evrec(c, e.vgath, c->comm_stream));
   } else {
-    CU_TRY(cudaEventRecord(e.vgath, ps));
+    CU_TRY(evrec(c, e.vgath, ps));
   }
   L->v_posted = true;
   L->v_iter = c->iter;
@@ -1517,10 +1585,11 @@ poseidon_status_t poseidon_sync_ps(poseidon_ctx_t c, int32_t id, float* grad, fl
     }
   }
   if (!L->grad) return fail(POSEIDON_ERR_STATE, "no PS buffers given or bound");
+  note_capture(c, reinterpret_cast<cudaStream_t>(producer));
   if (n != L->n) return fail(POSEIDON_ERR_SHAPE, "n does not match the bound buffers");
   cudaStream_t ps = reinterpret_cast<cudaStream_t>(producer);
   EvSet& e = L->ev[c->iter % RING];
-  CU_TRY(cudaEventRecord(e.ready, ps));
+  CU_TRY(evrec(c, e.ready, ps));
   L->last_iter = c->iter;
   if (c->ssp) {
     float* g = (L->in_arena && L->gsets[1]) ? L->gsets[next_set(c, *L)] : L->grad;
@@ -1534,8 +1603,8 @@ poseidon_status_t poseidon_sync_ps(poseidon_ctx_t c, int32_t id, float* grad, fl
     B.members_ready = 0;
     const int32_t bid = MAX_LAYERS + L->bucket;
     for (int32_t m : B.members)
-      if (m != id) CU_TRY(cudaStreamWaitEvent(c->comm_stream, c->layers[(size_t)m].ev[c->iter % RING].ready, 0));
-    CU_TRY(cudaEventRecord(B.ev[c->iter % RING].ready, ps));
+      if (m != id) CU_TRY(evwait(c, c->comm_stream, c->layers[(size_t)m].ev[c->iter % RING].ready));
+    CU_TRY(evrec(c, B.ev[c->iter % RING].ready, ps));
     B.last_iter = c->iter;
     if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
       B.pending = true;
@@ -1569,6 +1638,7 @@ poseidon_status_t poseidon_backprop_hook(poseidon_ctx_t c, int32_t id, poseidon_
   if (!L->W) return fail(POSEIDON_ERR_STATE, "SFB layer has no bound W (poseidon_bind_sfb_params)");
   if (!L->stU) return fail(POSEIDON_ERR_STATE, "SFB layer has no staging slot (call poseidon_sfb_slot first)");
   cudaStream_t ps = reinterpret_cast<cudaStream_t>(stream);
+  note_capture(c, ps);
   st = producer_guard(c, *L, ps);
   if (st) return st;
   st = pack_sfb(c, *L, L->stU, L->M, L->stV, L->N, ps);
@@ -1581,14 +1651,15 @@ poseidon_status_t poseidon_flush(poseidon_ctx_t c, poseidon_stream_t stream) {
   if (st) return st;
   if (!c->ssp) return POSEIDON_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  note_capture(c, s);
   IterRecord& r = open_record(c);
   for (int32_t id = 0; id < (int32_t)c->layers.size(); ++id) {   // same order on every rank
     Layer& L = c->layers[id];
     if (!L.registered || !L.ssp_pend) continue;
     EvSet& e = L.ev[c->iter % RING];
-    CU_TRY(cudaEventRecord(e.ready, s));
-    CU_TRY(cudaStreamWaitEvent(c->comm_stream, e.ready, 0));
-    CU_TRY(cudaEventRecord(e.start, c->comm_stream));
+    CU_TRY(evrec(c, e.ready, s));
+    CU_TRY(evwait(c, c->comm_stream, e.ready));
+    CU_TRY(evrec(c, e.start, c->comm_stream));
     e.g_eff = e.ks_eff = e.start;
     const EvSet& src = L.ev[L.pend_iter % RING];
     st = (L.scheme == POSEIDON_SCHEME_SFB)
@@ -1601,7 +1672,7 @@ poseidon_status_t poseidon_flush(poseidon_ctx_t c, poseidon_stream_t stream) {
   }
   // the flush is an iteration of its own (its events live in ring slot c->iter): close and advance,
   // so hooks that follow a flush record into a fresh slot and the statistics never count a sync twice
-  CU_TRY(cudaEventRecord(r.bwd_end, s));
+  CU_TRY(evrec(c, r.bwd_end, s));
   r.closed = true;
   c->iter += 1;
   return POSEIDON_OK;
@@ -1613,15 +1684,16 @@ poseidon_status_t poseidon_wait_layer(poseidon_ctx_t c, int32_t id, poseidon_str
   if (st) return st;
   if ((st = check_async(c)) != POSEIDON_OK) return st;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(consumer);
+  note_capture(c, cs);
   if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
     // traditional BP (Fig. dwbp (a)): the next iteration waits for every layer
     const IterRecord& r = c->rec[(c->iter + RING - 1) % RING];
     if (r.iter == c->iter - 1)
-      for (int32_t lid : r.layers) CU_TRY(cudaStreamWaitEvent(cs, resolve(c, lid).ev[r.iter % RING].done, 0));
+      for (int32_t lid : r.layers) CU_TRY(evwait(c, cs, resolve(c, lid).ev[r.iter % RING].done));
     return POSEIDON_OK;
   }
   const Layer& D = (L->bucket >= 0) ? c->buckets[(size_t)L->bucket] : *L;
-  if (D.last_iter >= 0) CU_TRY(cudaStreamWaitEvent(cs, D.ev[D.last_iter % RING].done, 0));
+  if (D.last_iter >= 0) CU_TRY(evwait(c, cs, D.ev[D.last_iter % RING].done));
   return POSEIDON_OK;
 }
 
@@ -1630,8 +1702,9 @@ poseidon_status_t poseidon_iteration_end(poseidon_ctx_t c, poseidon_stream_t com
   if (st) return st;
   if ((st = check_async(c)) != POSEIDON_OK) return st;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(compute);
+  note_capture(c, cs);
   IterRecord& r = open_record(c);
-  CU_TRY(cudaEventRecord(r.bwd_end, cs));
+  CU_TRY(evrec(c, r.bwd_end, cs));
   if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
     // deferred syncs in the order the hooks fired, all after the whole backward
     for (int32_t id : c->pending_order) {
@@ -1645,8 +1718,23 @@ poseidon_status_t poseidon_iteration_end(poseidon_ctx_t c, poseidon_stream_t com
     }
     c->pending_order.clear();
   }
+  if (c->cap_id) {
+    // captured step: the library's streams that joined the capture rejoin the caller's stream here (a graph
+    // launch then covers every sync of the iteration; the next launch is ordered after all of them)
+    cudaStream_t lib[2] = {c->comm_stream, c->recon_stream};
+    for (int k = 0; k < 2; ++k) {
+      cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+      unsigned long long id = 0;
+      if (cudaStreamGetCaptureInfo(lib[k], &cst, &id) == cudaSuccess && cst == cudaStreamCaptureStatusActive &&
+          id == c->cap_id) {
+        CU_TRY(cudaEventRecord(c->join_ev[k], lib[k]));
+        CU_TRY(cudaStreamWaitEvent(cs, c->join_ev[k], 0));
+      }
+    }
+  }
   r.closed = true;
   c->iter += 1;
+  if (out && c->cap_id) return fail(POSEIDON_ERR_STATE, "statistics of a captured iteration: read them after a replay");
   if (out) return poseidon_get_iter_stats(c, 0, out);
   return POSEIDON_OK;
 }

@@ -65,20 +65,23 @@ def sfb_wire_checks(new_ctx, rank, P, dev):
     # ---- 1b. SFB on symmetric buffers: NCCL all-gather (SYMM_SFB) and the NVLS multicast broadcast
     #          (NVLS_SFB); odd M (bias slot not a multiple of 4), ldk padding, 3 iterations in a row
     #          (the broadcast's entry barrier guards the gather buffers the previous K1 read) ----
-    for flags in (pz.FLAG_SYMM_SFB, pz.FLAG_NVLS_SFB):
+    # (+ FLAG_INPLACE_FACTORS: the pack reads U / V in place on the comm stream; the caller keeps them alive)
+    for flags in (pz.FLAG_SYMM_SFB, pz.FLAG_NVLS_SFB, pz.FLAG_NVLS_SFB | pz.FLAG_INPLACE_FACTORS,
+                  pz.FLAG_INPLACE_FACTORS):
         cs = new_ctx(flags)
         shapes = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 1000, 4096, 33)]
         for lid, M_, N_, K_ in shapes:
             assert cs.register_layer(lid, pz.LAYER_FC, M_, N_, K_) == pz.SCHEME_SFB
         path = cs.sfb_path(0)
-        assert path >= pz.SFB_PATH_NCCL_SYMM, path
+        assert path >= pz.SFB_PATH_NCCL_SYMM or not (flags & (pz.FLAG_SYMM_SFB | pz.FLAG_NVLS_SFB)), path
         if rank == 0:
             print(f"SFB path flags={flags}: {path}", flush=True)
         for it in range(3):
             for lid, M_, N_, K_ in shapes:
                 W, b, Us, Vs, lr = S.integer_factors(M_, N_, K_, P, seed=100 * it + lid)
                 Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
-                cs.sync_fc_sfb(lid, torch.from_numpy(Us[rank]).to(dev), torch.from_numpy(Vs[rank]).to(dev), Wd, bd, lr)
+                Ud, Vd = torch.from_numpy(Us[rank]).to(dev), torch.from_numpy(Vs[rank]).to(dev)
+                cs.sync_fc_sfb(lid, Ud, Vd, Wd, bd, lr)
                 cs.wait_layer(lid)
                 W1, b1 = O.sync_step(W, b, Us, Vs, lr)
                 torch.cuda.synchronize()
@@ -96,8 +99,10 @@ def early_v_checks(new_ctx, rank, P, dev):
     # ---- 9. early input broadcast (FLAG_EARLY_V): V posted at "forward" time, only U at the sync (whose V
     #          argument is garbage here); NCCL and broadcast-kernel wires; integer bit-exact vs O4, two
     #          iterations, and the same NCCL byte total as the plain sync ----
-    for flags in (pz.FLAG_EARLY_V, pz.FLAG_EARLY_V | pz.FLAG_NVLS_SFB):
+    for flags in (pz.FLAG_EARLY_V, pz.FLAG_EARLY_V | pz.FLAG_NVLS_SFB,
+                  pz.FLAG_EARLY_V | pz.FLAG_NVLS_SFB | pz.FLAG_INPLACE_FACTORS):
         ce = new_ctx(flags)
+        keep = []   # FLAG_INPLACE_FACTORS: the factors stay alive until the syncs are done
         shapes = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 1000, 4096, 33)]
         for lid, M_, N_, K_ in shapes:
             assert ce.register_layer(lid, pz.LAYER_FC, M_, N_, K_) == pz.SCHEME_SFB
@@ -111,7 +116,9 @@ def early_v_checks(new_ctx, rank, P, dev):
             for lid, (W, b, Us, Vs, lr) in reversed(list(enumerate(outs))):   # "backward": top layer first
                 Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
                 junk = torch.full((Vs[rank].shape[0], Vs[rank].shape[1]), 5.0, device=dev)
-                ce.sync_fc_sfb(lid, torch.from_numpy(Us[rank]).to(dev), junk, Wd, bd, lr)
+                Ud = torch.from_numpy(Us[rank]).to(dev)
+                keep += [Ud, junk]
+                ce.sync_fc_sfb(lid, Ud, junk, Wd, bd, lr)
                 res.append((lid, Wd, bd))
             st = ce.iteration_end(stats=True)
             for lid, Wd, bd in res:
