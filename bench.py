@@ -52,6 +52,10 @@ def parse():
                          "stream, off the backward's); mn = + POSEIDON_FLAG_INPLACE_MN (N = 1: K1 reads them MN-major, "
                          "no K3); pack = K3 on the backward's stream (round 1); auto = mn at N = 1 "
                          "(profiles/r2/factors_r2.md: +1%% images/s), pack at N > 1")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="capture one training step (forward, backward with every layer's DWBP sync, iteration_end) "
+                         "in a CUDA graph after the warm-up and replay it per step; auto = on for C2, whose step is "
+                         "bound by host launch latency (profiles/r2/graph_r2.md)")
     ap.add_argument("--dwbp", default="on", choices=["on", "off"])
     ap.add_argument("--recon", default="tf32", choices=["tf32", "fp32"])
     ap.add_argument("--nvls", default="auto", choices=["auto", "on", "off"],
@@ -443,6 +447,34 @@ def run_poseidon(args):
         step(x, y)
     sync.wait_all()
     barrier()
+    use_graph = args.graph == "on" or (args.graph == "auto" and args.config == "C2")
+    if use_graph and (args.ssp or args.straggle_us or args.dwbp == "off"):
+        raise SystemExit("--graph: BSP with DWBP only (no --ssp, --straggle-us, --dwbp off)")
+    run_step, graph_launches = step, None
+    if use_graph:
+        # One captured step: the library sees the capture on the caller's stream, forks its comm / recon streams
+        # from it, records its statistics events as graph nodes and rejoins at iteration_end, so one replay is
+        # the whole iteration (Alg. 2) with no host launches; x, y are the graph's static inputs.
+        gs = torch.cuda.Stream(device=dev)
+        gs.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        lc0 = pz.launch_count()
+        with torch.cuda.graph(graph, stream=gs):
+            static_loss = step(x, y)
+        graph_launches = pz.launch_count() - lc0
+        torch.cuda.current_stream().wait_stream(gs)
+
+        def run_step(xb, yb):
+            if xb is not x:
+                x.copy_(xb, non_blocking=True)
+                y.copy_(yb, non_blocking=True)
+            graph.replay()
+            return static_loss
+
+        for _ in range(2):
+            run_step(x, y)
+        sync.wait_all()
+        barrier()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.25)  # let the sampler start
@@ -454,12 +486,13 @@ def run_poseidon(args):
     nvtx_id = torch.cuda.nvtx.range_start("timed")
     ev0.record(stream)
     for _ in range(args.steps):
-        step(x, y)
+        run_step(x, y)
     sync.wait_all()
     ev1.record(stream)
     torch.cuda.nvtx.range_end(nvtx_id)
     ev1.synchronize()
-    launches = pz.launch_count() - l0
+    # graph mode: the host launches nothing per step; every replay runs the captured launches
+    launches = pz.launch_count() - l0 if graph_launches is None else graph_launches * args.steps
     clk = clocks.stop()
     barrier()
     ms = ev0.elapsed_time(ev1)
@@ -472,7 +505,7 @@ def run_poseidon(args):
     value = images / (ms / 1e3)
 
     # per-iteration sync statistics (device events kept by the library)
-    n_stats = min(args.steps, 7)
+    n_stats = 1 if use_graph else min(args.steps, 7)   # graph: the captured iteration's events (last replay)
     its = [ctx.iter_stats(a) for a in range(n_stats)]
     exposed = statistics.mean(i["exposed_ms"] for i in its)
     sync_total = statistics.mean(i["sync_total_ms"] for i in its)
@@ -609,7 +642,7 @@ def run_poseidon(args):
             for i in range(n):
                 b = i % 2
                 stream.wait_event(copied[b])
-                loss = step(xd[b], yd[b])
+                loss = run_step(xd[b], yd[b])
                 consumed[b].record(stream)
                 if i + 1 < n:
                     h2d(i + 1)
@@ -663,7 +696,7 @@ def run_poseidon(args):
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "tf32" if args.recon == "tf32" else "f32", "data": "synthetic",
             "config": workload_config(args, cfg, world),
-            "details": {"scheme": scheme, "else_branch": args.else_branch, "early_v": early_v, "factors": args.factors, "inplace_mn_k1": inplace, "dwbp": args.dwbp, "recon": args.recon, "lr": args.lr,
+            "details": {"scheme": scheme, "else_branch": args.else_branch, "early_v": early_v, "factors": args.factors, "cuda_graph": use_graph, "inplace_mn_k1": inplace, "dwbp": args.dwbp, "recon": args.recon, "lr": args.lr,
                         "momentum": args.momentum, "weight_decay": args.weight_decay,
                         "memory_format": args.memory_format,
                         "ps_path": ("nvls-fused" if sync.nvls_active else

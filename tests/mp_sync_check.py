@@ -136,6 +136,61 @@ def early_v_checks(new_ctx, rank, P, dev):
         ce.close()
 
 
+def graph_checks(new_ctx, rank, P, dev, batch, lr, Kc):
+    """Check 12 (round 2): one CIFAR-quick DWBP step captured in a CUDA graph (bench.py --graph) on the bench's
+    N > 1 paths -- the fused NVLS PS kernel, the SFB broadcast wire with early V, NCCL RS/AG -- replayed twice
+    after two eager steps, equals four eager steps bit for bit on every rank (cuDNN deterministic)."""
+    from paper_1512_06216_b200.dwbp import PoseidonSync
+    det, bench_ = torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark
+    torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = True, False
+    variants = [("ps", pz.FLAG_NVLS_PS, True), ("auto", pz.FLAG_NVLS_PS | pz.FLAG_NVLS_SFB | pz.FLAG_EARLY_V, True),
+                ("auto", 0, False)]
+    for scheme, flags, arena in variants:
+        out = []
+        for graph in (False, True):
+            cg = new_ctx(flags)
+            torch.manual_seed(1234)
+            model = CifarQuick().to(dev)
+            sync = PoseidonSync(model, cg, K=Kc, lr=lr, scheme=scheme, recon=pz.RECON_TF32, arena=arena)
+            x = torch.empty(Kc, 3, 32, 32, device=dev)
+            y = torch.empty(Kc, dtype=torch.long, device=dev)
+
+            def step():
+                F.cross_entropy(model(x), y).backward()
+                sync.iteration_end()
+
+            for it in range(4):
+                xb, yb = batch(it)
+                x.copy_(xb)
+                y.copy_(yb)
+                if graph and it == 2:
+                    sync.wait_all()
+                    torch.cuda.synchronize()
+                    gs = torch.cuda.Stream(device=dev)
+                    gs.wait_stream(torch.cuda.current_stream())
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=gs):
+                        step()
+                    torch.cuda.current_stream().wait_stream(gs)
+                if graph and it >= 2:
+                    g.replay()
+                else:
+                    step()
+            sync.wait_all()
+            torch.cuda.synchronize()
+            flat = torch.cat([p.detach().reshape(-1) for p in model.parameters()])
+            assert allsame(flat), f"graph check: ranks differ ({scheme}, flags {flags}, graph {graph})"
+            if graph:
+                st = cg.iter_stats(0)
+                assert st["n_layers"] == 5 and st["sync_total_ms"] > 0, st
+            out.append(flat.cpu())
+            cg.close()
+        assert torch.equal(out[0], out[1]), f"graph replay != eager ({scheme}, flags {flags})"
+    torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = det, bench_
+    if rank == 0:
+        print(f"graph check ok ({len(variants)} variants: 2 eager + 2 replays == 4 eager)", flush=True)
+
+
 def alexnet_p6_schedule_check(new_ctx, rank, P, dev, world):
     """Check 11: the schedule the rule picks for C3 at P >= 6 (fc6 / fc7 SFB, fc8 PS, conv PS) on the P GPUs at
     hand (fc8 forced to PS), in bench.py's N > 1 launch configuration (NVLS PS arena, broadcast wire, early V,
@@ -494,6 +549,7 @@ def main():
     for scheme, nv in [(sc, nv) for sc in ("auto", "ps") for nv in (False, True)] + [("sfps", False)]:
         assert torch.equal(results[(scheme, "on", nv)], results[(scheme, "off", nv)]), \
             f"DWBP on/off differ ({scheme}, nvls {nv})"
+    graph_checks(new_ctx, rank, P, dev, batch, lr_c, Kc)
     # ---- 6. SSP with staleness 1 (FLAG_SSP1, reading Z19): SFB + PS (arena) over 4 iterations and a
     #          flush, integer variant bit-exact vs O10, on the NCCL paths and on the NVLS paths ----
     from paper_1512_06216_b200.binding import device_view
