@@ -714,6 +714,9 @@ def run_poseidon(args):
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
+    if use_graph:
+        del graph   # captured NCCL work holds the communicator: release the graph before ncclCommDestroy
+        torch.cuda.synchronize()
     ctx.close()
     if world > 1:
         dist.destroy_process_group()

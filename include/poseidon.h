@@ -349,7 +349,14 @@ poseidon_status_t poseidon_wait_layer(poseidon_ctx_t ctx, int32_t layer_id, pose
 
 /* Mark the end of backward on `compute` (records bwd_end; under DWBP_OFF
  * launches the deferred syncs), close the iteration and, if out != NULL,
- * block until its syncs are done and fill the statistics. */
+ * block until its syncs are done and fill the statistics.
+ * CUDA graphs (round 2): a whole training step may be captured by stream capture on the caller's stream
+ * (BSP with DWBP; e.g. torch.cuda.graph around forward, backward and this call).  Every entry point that
+ * takes a stream notices the capture; the library's streams then fork from and join the capture through
+ * internal event twins, its statistics events become event-record nodes (valid after each replay:
+ * poseidon_get_iter_stats(ago = 0) describes the latest replay), waits on earlier iterations are dropped
+ * (graph launches on one stream are ordered as a whole), and here the library's streams rejoin `compute`,
+ * so one replay is one complete iteration.  out must be NULL while capturing (POSEIDON_ERR_STATE). */
 poseidon_status_t poseidon_iteration_end(poseidon_ctx_t ctx, poseidon_stream_t compute, poseidon_iter_stats_t* out);
 
 /* Statistics of a finished iteration, `ago` iterations back (0 = the last one
@@ -361,6 +368,9 @@ poseidon_status_t poseidon_get_layer_stats(poseidon_ctx_t ctx, int32_t ago, int3
 /* Number of library kernels launched so far by this process (all contexts). */
 uint64_t poseidon_launch_count(void);
 
+/* Frees everything the context owns (collective at world > 1: ncclCommDestroy).  A CUDA graph that captured
+ * this context's NCCL collectives (stream capture of a step, see poseidon_iteration_end) must be destroyed
+ * first: NCCL keeps the communicator's persistent resources alive for it, and the destroy would wait. */
 poseidon_status_t poseidon_finalize(poseidon_ctx_t ctx);
 const char* poseidon_last_error(void);
 int32_t poseidon_version(void);

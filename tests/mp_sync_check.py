@@ -145,9 +145,13 @@ def graph_checks(new_ctx, rank, P, dev, batch, lr, Kc):
     torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = True, False
     variants = [("ps", pz.FLAG_NVLS_PS, True), ("auto", pz.FLAG_NVLS_PS | pz.FLAG_NVLS_SFB | pz.FLAG_EARLY_V, True),
                 ("auto", 0, False)]
+    if os.environ.get("MP_GRAPH_VARIANT"):
+        variants = [variants[int(os.environ["MP_GRAPH_VARIANT"])]]
     for scheme, flags, arena in variants:
         out = []
         for graph in (False, True):
+            if rank == 0 and os.environ.get("MP_VERBOSE"):
+                print(f"graph check: {scheme} flags {flags} graph {graph}", flush=True)
             cg = new_ctx(flags)
             torch.manual_seed(1234)
             model = CifarQuick().to(dev)
@@ -172,8 +176,13 @@ def graph_checks(new_ctx, rank, P, dev, batch, lr, Kc):
                     with torch.cuda.graph(g, stream=gs):
                         step()
                     torch.cuda.current_stream().wait_stream(gs)
+                    if os.environ.get("MP_VERBOSE"):
+                        print(f"[rank {rank}] captured", flush=True)
                 if graph and it >= 2:
                     g.replay()
+                    if os.environ.get("MP_VERBOSE"):
+                        torch.cuda.synchronize()
+                        print(f"[rank {rank}] replay {it} done", flush=True)
                 else:
                     step()
             sync.wait_all()
@@ -184,6 +193,11 @@ def graph_checks(new_ctx, rank, P, dev, batch, lr, Kc):
                 st = cg.iter_stats(0)
                 assert st["n_layers"] == 5 and st["sync_total_ms"] > 0, st
             out.append(flat.cpu())
+            if graph:
+                # a graph with captured NCCL work keeps the communicator's persistent plans alive: release it
+                # before ncclCommDestroy (poseidon_finalize would otherwise wait for it forever)
+                del g
+                torch.cuda.synchronize()
             cg.close()
         assert torch.equal(out[0], out[1]), f"graph replay != eager ({scheme}, flags {flags})"
     torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = det, bench_
@@ -301,6 +315,20 @@ def main():
     if "--wire-only" in sys.argv:   # the factor broadcast kernel alone (e.g. with POSEIDON_SFB_BCAST_GRID set)
         sfb_wire_checks(new_ctx, rank, P, dev)
         early_v_checks(new_ctx, rank, P, dev)
+        dist.barrier()
+        print(f"MP_OK {rank}", flush=True)
+        dist.destroy_process_group()
+        return
+    if "--graph-only" in sys.argv:   # check 12 alone
+        Kc = 16
+
+        def batch(it):
+            gen = torch.Generator().manual_seed(100 + it)
+            xall = torch.rand(P * Kc, 3, 32, 32, generator=gen).to(dev)
+            yall = torch.randint(0, 10, (P * Kc,), generator=gen).to(dev)
+            return xall[rank * Kc:(rank + 1) * Kc], yall[rank * Kc:(rank + 1) * Kc]
+
+        graph_checks(new_ctx, rank, P, dev, batch, 0.05, Kc)
         dist.barrier()
         print(f"MP_OK {rank}", flush=True)
         dist.destroy_process_group()

@@ -73,6 +73,8 @@ def _run(pz, scheme, flags, graph):
         it = ctx.iter_stats(0)
         stats["_iter"] = it
     flat = torch.cat([p.detach().reshape(-1) for p in model.parameters()]).cpu()
+    if graph:
+        del g   # release the graph before the context (its NCCL work, if any, holds the communicator)
     ctx.close()
     return flat, stats
 
