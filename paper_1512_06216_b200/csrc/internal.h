@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <utility>
 #include <stdint.h>
 
 #include <atomic>
@@ -91,5 +93,25 @@ cudaError_t launch_recon_tcgen05_mn(const float* U, int64_t ldu, int64_t ublk, c
 // (bs, bias, bias_done): optional plain-SGD bias update fused into K1 (bias[m] = fmaf(alpha, sum_p bs[p*M+m],
 // bias[m]), bs [P][M] with M the block's row count); *bias_done tells whether the kernel took it.
 bool recon_tcgen05_supported(const float* Ug, const float* Vg, int64_t ldk, int64_t M, int64_t N, const float* W);
+
+// Launch with the stream's priority as a launch attribute: a kernel node captured into a CUDA graph keeps it
+// (stream priorities are not part of a captured graph), so the sync kernels still take SMs ahead of the
+// backward's kernels when a whole step is replayed (bench.py --graph).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_prio(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  int prio = 0;
+  cudaStreamGetPriority(s, &prio);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributePriority;
+  la[0].val.priority = prio;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace poseidon

@@ -1185,9 +1185,23 @@ cudaError_t launch_2sm(Kern kern, int smem, bool& attr, int pairs, const CUtenso
     if (ea != cudaSuccess) return ea;
     attr = true;
   }
-  kern<<<2 * pairs, NUM_THREADS_2SM, smem, s>>>(tmA, tmB, tmW, tmV, p);
+  // the stream's priority travels with the launch as an attribute, so a kernel node captured into a CUDA graph
+  // keeps it (bench.py --graph): K1 of a DWBP sync is meant to take SMs ahead of the backward's kernels
+  int prio = 0;
+  cudaStreamGetPriority(s, &prio);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  cfg.blockDim = dim3(NUM_THREADS_2SM);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributePriority;
+  la[0].val.priority = prio;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmW, tmV, p);
   g_launches.fetch_add(1);
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // The 2-SM kernel's configurations (both operand layouts): momentum (W + velocity slots), RW epilogue, TMA W ring.

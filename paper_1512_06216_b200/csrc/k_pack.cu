@@ -165,13 +165,17 @@ static cudaError_t launch_pack(const PackSeg& a, const PackSeg& b, int64_t K, in
   cfg.blockDim = dim3(32, 8, 1);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  int prio = 0;
+  cudaStreamGetPriority(s, &prio);
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = (unsigned)cs;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributePriority;   // kept by a captured graph node (internal.h launch_prio)
+  attr[1].val.priority = prio;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaError_t e = round_tf32 ? cudaLaunchKernelEx(&cfg, pack_uv_kernel<true>, a, b, K, ldk, tpc)
                              : cudaLaunchKernelEx(&cfg, pack_uv_kernel<false>, a, b, K, ldk, tpc);
   g_launches.fetch_add(1);

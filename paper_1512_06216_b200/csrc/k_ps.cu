@@ -217,12 +217,13 @@ cudaError_t launch_ps_shard_update(const float* g, float* W, int64_t count, floa
     const int64_t per_block = (int64_t)threads * 4;
     const int64_t blocks = n4 > 0 ? (n4 + per_block - 1) / per_block : 1;
     const dim3 grid((unsigned)blocks);
-    if (stats)
-      ps_shard_sgd_kernel<true, false><<<grid, threads, 0, s>>>(const_cast<float*>(g), W, count, alpha, stats,
-                                                                nullptr, 0, 0, 0);
-    else
-      ps_shard_sgd_kernel<false, false><<<grid, threads, 0, s>>>(const_cast<float*>(g), W, count, alpha, nullptr,
-                                                                 nullptr, 0, 0, 0);
+    cudaError_t e = stats ? launch_prio(ps_shard_sgd_kernel<true, false>, grid, dim3(threads), 0, s,
+                                        const_cast<float*>(g), W, count, alpha, stats, (float*)nullptr, (int64_t)0,
+                                        (int64_t)0, (int64_t)0)
+                          : launch_prio(ps_shard_sgd_kernel<false, false>, grid, dim3(threads), 0, s,
+                                        const_cast<float*>(g), W, count, alpha, (float*)nullptr, (float*)nullptr,
+                                        (int64_t)0, (int64_t)0, (int64_t)0);
+    if (e != cudaSuccess) return e;
   }
   g_launches.fetch_add(1);
   return cudaGetLastError();
@@ -242,10 +243,10 @@ cudaError_t launch_ps_shard_update_zero(float* gbase, float* Wbase, int64_t b, i
   const int64_t zero_blocks = ((padded - count) / 4 + per_block * 4 - 1) / (per_block * 4);  // ~16 float4 / thread
   if (blocks < zero_blocks) blocks = zero_blocks;
   if (blocks < 1) blocks = 1;
-  ps_shard_sgd_kernel<false, true><<<(unsigned)blocks, threads, 0, s>>>(gbase + b, Wbase + b, count, alpha, nullptr,
-                                                                       gbase, b, b + count, padded);
+  cudaError_t err = launch_prio(ps_shard_sgd_kernel<false, true>, dim3((unsigned)blocks), dim3(threads), 0, s,
+                                gbase + b, Wbase + b, count, alpha, (float*)nullptr, gbase, b, b + count, padded);
   g_launches.fetch_add(1);
-  return cudaGetLastError();
+  return err != cudaSuccess ? err : cudaGetLastError();
 }
 
 cudaError_t launch_ps_momentum(const float* gsum, float* W, float* V, int64_t count, float inv_p, float lr,

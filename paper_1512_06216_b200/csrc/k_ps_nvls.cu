@@ -270,14 +270,11 @@ cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww
   NvlsMomentum mom{vel, inv_p, lr, mu, wd};
   const uint32_t fz = fuzz_bound_ns(), seed = fz ? next_fuzz_seed() : 0u;
   const int zg = zero_grad ? 1 : 0;
-  if (env_u == 8)
-    ps_nvls_kernel<8><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, shard, nranks, alpha, zg, mom, fz, seed);
-  else if (env_u == 2)
-    ps_nvls_kernel<2><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, shard, nranks, alpha, zg, mom, fz, seed);
-  else
-    ps_nvls_kernel<4><<<blocks, 256, 0, s>>>(st->dev, wg, ww, off_g, off_w, b, e, shard, nranks, alpha, zg, mom, fz, seed);
+  auto kern = env_u == 8 ? ps_nvls_kernel<8> : env_u == 2 ? ps_nvls_kernel<2> : ps_nvls_kernel<4>;
+  cudaError_t err = launch_prio(kern, dim3(blocks), dim3(256), 0, s, st->dev, wg, ww, off_g, off_w, b, e, shard, nranks,
+                                alpha, zg, mom, fz, seed);
   g_launches.fetch_add(1);
-  return cudaGetLastError();
+  return err != cudaSuccess ? err : cudaGetLastError();
 }
 
 cudaError_t launch_sfb_bcast_nvls(const NvlsState* st, ncclWindow_t win, size_t off_u, int64_t n_u, size_t off_v,
@@ -304,14 +301,11 @@ cudaError_t launch_sfb_bcast_nvls(const NvlsState* st, ncclWindow_t win, size_t 
   if (cap < max_blocks) max_blocks = cap;
   if (blocks > max_blocks) blocks = max_blocks;
   const uint32_t fz = fuzz_bound_ns(), seed = fz ? next_fuzz_seed() : 0u;
-  if (p2p)
-    sfb_bcast_kernel<4, true><<<blocks, 256, 0, s>>>(st->dev, win, BcastSeg{off_u, n_u}, BcastSeg{off_v, n_v},
-                                                     BcastSeg{off_b, n_b}, fz, seed);
-  else
-    sfb_bcast_kernel<4, false><<<blocks, 256, 0, s>>>(st->dev, win, BcastSeg{off_u, n_u}, BcastSeg{off_v, n_v},
-                                                      BcastSeg{off_b, n_b}, fz, seed);
+  cudaError_t err = launch_prio(p2p ? sfb_bcast_kernel<4, true> : sfb_bcast_kernel<4, false>, dim3(blocks), dim3(256),
+                                0, s, st->dev, win, BcastSeg{off_u, n_u}, BcastSeg{off_v, n_v}, BcastSeg{off_b, n_b},
+                                fz, seed);
   g_launches.fetch_add(1);
-  return cudaGetLastError();
+  return err != cudaSuccess ? err : cudaGetLastError();
 }
 
 NvlsState* nvls_create(ncclComm_t comm, int barriers, std::string* err) {
