@@ -392,11 +392,14 @@ def run_poseidon(args):
         flags |= pz.FLAG_SSP1
     if args.else_branch == "sfps":
         flags |= pz.FLAG_SFPS
-    early_v = args.early_v == "on" or (args.early_v == "auto" and world > 1)
+    # early V: BSP with DWBP only (the library refuses it with DWBP off or SSP)
+    early_v = args.early_v == "on" or (args.early_v == "auto" and world > 1 and args.dwbp == "on" and not args.ssp)
     if early_v:
         flags |= pz.FLAG_EARLY_V
     if args.factors == "auto":
         args.factors = "mn" if world == 1 else "pack"
+    if args.dwbp == "off" or args.ssp:
+        args.factors = "pack"   # in-place factor reads are a BSP + DWBP feature (the library ignores the flags)
     if args.factors != "pack":
         flags |= pz.FLAG_INPLACE_FACTORS
     if args.factors == "mn":

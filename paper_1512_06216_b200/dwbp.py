@@ -118,7 +118,8 @@ class PoseidonSync:
         # world 1, else the pack before the factor broadcast), so the allocator must not hand their memory out
         # again before those streams have passed the sync (record_stream)
         self.inplace_streams = []
-        if (getattr(ctx, "flags", 0) & B.FLAG_INPLACE_FACTORS) and not self.ssp:
+        if (getattr(ctx, "flags", 0) & B.FLAG_INPLACE_FACTORS) and not self.ssp and \
+                not (getattr(ctx, "flags", 0) & B.FLAG_DWBP_OFF):
             self.inplace_streams = [ctx.stream(B.STREAM_RECON)] + ([ctx.stream(B.STREAM_COMM)] if ctx.world > 1 else [])
         if self.ssp and not arena:
             raise ValueError("FLAG_SSP1 needs the library arena (arena=True): PS gradients are double-buffered")

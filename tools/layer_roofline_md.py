@@ -15,7 +15,8 @@ alpha = the 8-byte NCCL all-gather measured in the same run; T_LAUNCH = 2 us.
 import json
 import sys
 
-TC_TF32, BW_HBM, BW_NVL, T_LAUNCH = 794e12, 6543.7e9, 900e9, 2e-6
+# round 2: TF32 = max(bf16 burst x 1.1/2.25, measured cuBLAS TF32) and HBM from MEASURED_PEAKS.json (bench.py)
+TC_TF32, BW_HBM, BW_NVL, T_LAUNCH = 807.9e12, 6458.7e9, 900e9, 2e-6
 
 
 def bounds(d, P, alpha, bw_nvl=BW_NVL):
