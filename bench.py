@@ -54,8 +54,9 @@ def parse():
                          "(profiles/r2/factors_r2.md: +1%% images/s), pack at N > 1")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="capture one training step (forward, backward with every layer's DWBP sync, iteration_end) "
-                         "in a CUDA graph after the warm-up and replay it per step; auto = on for C2, whose step is "
-                         "bound by host launch latency (profiles/r2/graph_r2.md)")
+                         "in a CUDA graph after the warm-up and replay it per step; auto = on for C2 (host-bound: "
+                         "2.4x) and at N > 1 (+1.3-1.9%%); off for C3-C5 at N = 1, where the replay packs K1 deeper "
+                         "into the conv backward (in-step fraction 0.66 -> 0.48-0.60 for +1.3%%; DESIGN §6d)")
     ap.add_argument("--dwbp", default="on", choices=["on", "off"])
     ap.add_argument("--recon", default="tf32", choices=["tf32", "fp32"])
     ap.add_argument("--nvls", default="auto", choices=["auto", "on", "off"],
@@ -450,7 +451,8 @@ def run_poseidon(args):
         step(x, y)
     sync.wait_all()
     barrier()
-    use_graph = args.graph == "on" or (args.graph == "auto" and args.config == "C2")
+    use_graph = args.graph == "on" or (args.graph == "auto" and (args.config == "C2" or world > 1)
+                                         and not args.ssp and not args.straggle_us and args.dwbp == "on")
     if use_graph and (args.ssp or args.straggle_us or args.dwbp == "off"):
         raise SystemExit("--graph: BSP with DWBP only (no --ssp, --straggle-us, --dwbp off)")
     run_step, graph_launches = step, None
