@@ -522,3 +522,34 @@ def test_ssp_one_reads_exactly_updates_up_to_t_minus_2():
     # iterations 0 and 1 both read the initial parameters; the flushed end state equals BSP's
     assert np.array_equal(vis[0][0], vis[1][0])
     assert np.array_equal(vis[-1][0], O.ssp_visible_weights(W, b, steps, lr, s=0)[-1][0])
+
+
+def _round_mantissa(x, keep_bits, mode):
+    """fp32 -> fp32 with only `keep_bits` explicit mantissa bits: 'rn' = round half away from zero (cvt.rna),
+    'rz' = truncate (what the tensor core does to fp32 operands read as TF32)."""
+    b = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    drop = 23 - keep_bits
+    if mode == "rn":
+        b = b + (1 << (drop - 1))
+    b = b & ~np.uint64((1 << drop) - 1) & 0xFFFFFFFF
+    return b.astype(np.uint32).view(np.float32)
+
+
+def test_wire_precision_readings_against_the_gate():
+    """DESIGN §9 / reading Z12': on the hidden-layer factor recipe, a bf16 wire (7 mantissa bits, RN) exceeds the
+    2e-3 gate of the Z13 metric while TF32 (10 bits) stays inside it, rounded (the pack) or truncated (the
+    in-place MN-major K1 at P = 1) -- the arithmetic behind rejecting the compact wire and accepting truncation."""
+    errs = {}
+    for (M, N, K, P) in [(256, 512, 8, 2), (1024, 2048, 256, 1), (1000, 1024, 128, 4)]:
+        W, _ = S.fc_weights_randbias(M, N)
+        Us, Vs = S.hidden_factors(M, N, K, P)
+        W1, _ = O.sync_step(W, None, Us, Vs, 0.5)
+        for name, bits, mode in (("bf16", 7, "rn"), ("tf32_rn", 10, "rn"), ("tf32_rz", 10, "rz")):
+            Ur = [_round_mantissa(u, bits, mode) for u in Us]
+            Vr = [_round_mantissa(v, bits, mode) for v in Vs]
+            Wt, _ = O.sync_step(W, None, Ur, Vr, 0.5)
+            errs.setdefault(name, []).append(O.update_error(W, Wt, W1))
+    assert min(errs["bf16"]) > 2e-3, errs
+    assert max(errs["tf32_rn"]) < 6e-4, errs
+    assert max(errs["tf32_rz"]) < 1.5e-3, errs   # 0.79e-3 .. 1.28e-3 (small K: fewer products average out)
+    assert min(errs["tf32_rz"]) > max(errs["tf32_rn"]), errs   # truncation is the worse of the two TF32 roundings
