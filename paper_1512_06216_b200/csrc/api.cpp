@@ -216,7 +216,9 @@ poseidon_status_t check_ctx(poseidon_ctx_t c) {
 // it, so the library's streams fork from and join the capture) and the event itself as an external event-record
 // node (each replay stamps it, so the statistics stay valid).  A wait on an event last recorded outside the
 // current capture (an earlier iteration) is dropped: graph launches into one stream are ordered as a whole.
-void note_capture(poseidon_ctx_t c, cudaStream_t s) {
+// SSP keeps host-side state across iterations (which gather / gradient set a sync uses, the pending update of
+// the previous iteration): a captured step would replay one fixed assignment, so SSP refuses capture.
+poseidon_status_t note_capture(poseidon_ctx_t c, cudaStream_t s) {
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
   unsigned long long id = 0;
   if (cudaStreamGetCaptureInfo(s, &st, &id) != cudaSuccess) {
@@ -224,6 +226,9 @@ void note_capture(poseidon_ctx_t c, cudaStream_t s) {
     st = cudaStreamCaptureStatusNone;
   }
   c->cap_id = (st == cudaStreamCaptureStatusActive) ? id : 0;
+  if (c->cap_id && c->ssp)
+    return fail(POSEIDON_ERR_UNSUPPORTED, "POSEIDON_FLAG_SSP1 steps cannot be captured into a CUDA graph");
+  return POSEIDON_OK;
 }
 cudaError_t make_twin(poseidon_ctx_t c, cudaEvent_t ev) {
   if (!ev || c->evmeta.count(ev)) return cudaSuccess;
@@ -1507,7 +1512,7 @@ poseidon_status_t poseidon_sync_fc_sfb(poseidon_ctx_t c, int32_t id, const float
   if (bias && !L->has_bias) return fail(POSEIDON_ERR_INVALID_ARG, "layer registered without bias");
   if (!aligned16(W)) return fail(POSEIDON_ERR_ALIGNMENT, "W must be 16-byte aligned");
   cudaStream_t ps = reinterpret_cast<cudaStream_t>(producer);
-  note_capture(c, ps);
+  if ((st = note_capture(c, ps)) != POSEIDON_OK) return st;
   st = producer_guard(c, *L, ps);
   if (st) return st;
   if (inplace_ok(c, *L, U, V, W)) return sfb_inplace(c, id, *L, U, V, W, bias, lr, ps);
@@ -1534,7 +1539,7 @@ poseidon_status_t poseidon_sfb_post_input(poseidon_ctx_t c, int32_t id, const fl
   if (!V || ldV < L->N) return fail(POSEIDON_ERR_INVALID_ARG, "V is NULL or ldV < N");
   if (L->v_posted) return fail(POSEIDON_ERR_STATE, "V already posted for this sync");
   cudaStream_t ps = reinterpret_cast<cudaStream_t>(stream);
-  note_capture(c, ps);
+  if ((st = note_capture(c, ps)) != POSEIDON_OK) return st;
   st = producer_guard(c, *L, ps);   // the previous sync's K1 no longer reads the gather buffers
   if (st) return st;
   const int P = c->world;
@@ -1585,7 +1590,7 @@ poseidon_status_t poseidon_sync_ps(poseidon_ctx_t c, int32_t id, float* grad, fl
     }
   }
   if (!L->grad) return fail(POSEIDON_ERR_STATE, "no PS buffers given or bound");
-  note_capture(c, reinterpret_cast<cudaStream_t>(producer));
+  if ((st = note_capture(c, reinterpret_cast<cudaStream_t>(producer))) != POSEIDON_OK) return st;
   if (n != L->n) return fail(POSEIDON_ERR_SHAPE, "n does not match the bound buffers");
   cudaStream_t ps = reinterpret_cast<cudaStream_t>(producer);
   EvSet& e = L->ev[c->iter % RING];
@@ -1638,7 +1643,7 @@ poseidon_status_t poseidon_backprop_hook(poseidon_ctx_t c, int32_t id, poseidon_
   if (!L->W) return fail(POSEIDON_ERR_STATE, "SFB layer has no bound W (poseidon_bind_sfb_params)");
   if (!L->stU) return fail(POSEIDON_ERR_STATE, "SFB layer has no staging slot (call poseidon_sfb_slot first)");
   cudaStream_t ps = reinterpret_cast<cudaStream_t>(stream);
-  note_capture(c, ps);
+  if ((st = note_capture(c, ps)) != POSEIDON_OK) return st;
   st = producer_guard(c, *L, ps);
   if (st) return st;
   st = pack_sfb(c, *L, L->stU, L->M, L->stV, L->N, ps);
@@ -1651,7 +1656,7 @@ poseidon_status_t poseidon_flush(poseidon_ctx_t c, poseidon_stream_t stream) {
   if (st) return st;
   if (!c->ssp) return POSEIDON_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  note_capture(c, s);
+  if ((st = note_capture(c, s)) != POSEIDON_OK) return st;
   IterRecord& r = open_record(c);
   for (int32_t id = 0; id < (int32_t)c->layers.size(); ++id) {   // same order on every rank
     Layer& L = c->layers[id];
@@ -1684,7 +1689,7 @@ poseidon_status_t poseidon_wait_layer(poseidon_ctx_t c, int32_t id, poseidon_str
   if (st) return st;
   if ((st = check_async(c)) != POSEIDON_OK) return st;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(consumer);
-  note_capture(c, cs);
+  if ((st = note_capture(c, cs)) != POSEIDON_OK) return st;
   if (c->flags & POSEIDON_FLAG_DWBP_OFF) {
     // traditional BP (Fig. dwbp (a)): the next iteration waits for every layer
     const IterRecord& r = c->rec[(c->iter + RING - 1) % RING];
@@ -1702,7 +1707,7 @@ poseidon_status_t poseidon_iteration_end(poseidon_ctx_t c, poseidon_stream_t com
   if (st) return st;
   if ((st = check_async(c)) != POSEIDON_OK) return st;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(compute);
-  note_capture(c, cs);
+  if ((st = note_capture(c, cs)) != POSEIDON_OK) return st;
   IterRecord& r = open_record(c);
   CU_TRY(evrec(c, r.bwd_end, cs));
   if (c->flags & POSEIDON_FLAG_DWBP_OFF) {

@@ -91,3 +91,32 @@ def test_graph_replay_equals_eager(pz, scheme, flags):
         assert st["start_to_done_ms"] > 0, (name, st)
         if name != "conv1":   # DWBP: the sync of every layer above the first overlaps the backward below it
             assert st["done_after_bwd_end_ms"] - st["start_to_done_ms"] < 0, (name, st)
+
+
+def test_ssp_refuses_capture(pz):
+    """SSP (staleness 1) carries host-side state from one iteration to the next (which gather / gradient set a
+    sync uses): a captured step would replay one fixed assignment, so the library refuses the capture."""
+    import torch.nn.functional as F
+    from paper_1512_06216_b200.dwbp import PoseidonSync
+    from drivers.cnn import CifarQuick
+
+    dev = torch.device("cuda", 0)
+    ctx = pz.Context(rank=0, world=1, device=0, flags=pz.FLAG_SSP1)
+    torch.manual_seed(6216)
+    model = CifarQuick().to(dev)
+    sync = PoseidonSync(model, ctx, K=100, lr=0.05, arena=True)
+    x, y = _batches(dev, 1)[0]
+    F.cross_entropy(model(x), y).backward()
+    sync.iteration_end()
+    sync.wait_all()
+    torch.cuda.synchronize()
+    gs = torch.cuda.Stream(device=dev)
+    gs.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(Exception):
+        with torch.cuda.graph(g, stream=gs):
+            F.cross_entropy(model(x), y).backward()
+            sync.iteration_end()
+    torch.cuda.synchronize()
+    del g
+    ctx.close()

@@ -49,6 +49,31 @@ constexpr int M = 4096, N = 9216, TM = 128, TN = 256;
 #endif
 constexpr int SLOTS = SLOTS_, CH = 16384;
 
+__device__ int g_raster = 0;   // 0: tile t -> (t / NT, t % NT) (K1's N walk); 1: M walk; 2: contiguous tiles per CTA
+__device__ __forceinline__ void tile_of(int i, int& mt, int& nt) {
+  constexpr int NT = N / TN, MT = M / TM;
+  if (g_raster == 1) {
+    const int t = blockIdx.x + i * gridDim.x;
+    mt = t % MT; nt = t / MT;
+  } else if (g_raster == 2) {
+    const int per = (MT * NT + gridDim.x - 1) / gridDim.x;
+    const int t = blockIdx.x * per + i;
+    mt = t / NT; nt = t % NT;
+  } else {
+    const int t = blockIdx.x + i * gridDim.x;
+    mt = t / NT; nt = t % NT;
+  }
+}
+__device__ __forceinline__ int tiles_of_cta() {
+  constexpr int T = (M / TM) * (N / TN);
+  if (g_raster == 2) {
+    const int per = (T + gridDim.x - 1) / gridDim.x;
+    const int lo = blockIdx.x * per;
+    return lo >= T ? 0 : (T - lo < per ? T - lo : per);
+  }
+  return (T - (int)blockIdx.x + gridDim.x - 1) / gridDim.x;
+}
+
 template <int V>
 __global__ void __launch_bounds__(160, 1) probe(const __grid_constant__ CUtensorMap map, float* W) {
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -61,12 +86,13 @@ __global__ void __launch_bounds__(160, 1) probe(const __grid_constant__ CUtensor
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
-  const int ntiles = (M / TM) * (N / TN);
+  const int my_tiles = tiles_of_cta();
   if (warp == 4) {  // loader
     if (lane == 0) {
       uint32_t g = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int mt = t / (N / TN), nt = t % (N / TN);
+      for (int i = 0; i < my_tiles; ++i) {
+        int mt, nt;
+        tile_of(i, mt, nt);
         for (int c = 0; c < 8; ++c, ++g) {
           const uint32_t slot = g % SLOTS, ph = (g / SLOTS) & 1;
           mbar_wait(&empty[slot], ph ^ 1);
@@ -80,8 +106,9 @@ __global__ void __launch_bounds__(160, 1) probe(const __grid_constant__ CUtensor
   }
   const int t = threadIdx.x;  // 0..127
   uint32_t g = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int mt = tile / (N / TN), nt = tile % (N / TN);
+  for (int i = 0; i < my_tiles; ++i) {
+    int mt, nt;
+    tile_of(i, mt, nt);
     for (int c = 0; c < 8; ++c, ++g) {
       const uint32_t slot = g % SLOTS, ph = (g / SLOTS) & 1;
       mbar_wait(&full[slot], ph);
@@ -169,6 +196,9 @@ int main() {
   cudaEventCreate(&b);
   const double bytes = 8.0 * M * N;
   const int grid = getenv("GRID") ? atoi(getenv("GRID")) : 148;
+  const int raster = getenv("RASTER") ? atoi(getenv("RASTER")) : 0;
+  cudaMemcpyToSymbol(g_raster, &raster, sizeof(int));
+  printf("RASTER=%d GRID=%d SLOTS=%d\n", raster, grid, SLOTS);
   for (int v = 1; v <= 4; ++v) {
     float best = 1e9;
     for (int it = 0; it < 6; ++it) {
