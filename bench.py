@@ -532,7 +532,8 @@ def run_poseidon(args):
         top = max(sfb, key=lambda p: p.M * p.N)
         kms = statistics.mean(ctx.layer_stats(top.layer_id, a)["kernel_ms"] for a in range(n_stats))
         M, N, Kf, P = top.M, top.N, top.K, world
-        ldk = Kf if inplace else (Kf + 3) // 4 * 4
+        top_inplace = inplace and M % 4 == 0 and N % 4 == 0   # else the library packed this layer (K-major)
+        ldk = Kf if top_inplace else (Kf + 3) // 4 * 4
         flops = 2.0 * M * N * Kf * P
         byts = 8.0 * M * N + 4.0 * P * ldk * (M + N)
         tf32_peak = peaks["tf32_tflops_sustained"]
@@ -552,7 +553,7 @@ def run_poseidon(args):
         if args.recon == "tf32":
             # context for `frac` (which is the in-step number): the same K1 launch on the same shape ALONE,
             # after the timed region, each launch queued behind a device spin (device time only)
-            if inplace:   # the factors as the layer leaves them: U [K x M], V [K x N] (MN-major K1)
+            if top_inplace:   # the factors as the layer leaves them: U [K x M], V [K x N] (MN-major K1)
                 Ug = torch.randn(Kf, M, device=dev).mul_(0.01)
                 Vg = torch.randn(Kf, N, device=dev).relu_()
             else:
@@ -564,7 +565,7 @@ def run_poseidon(args):
             for _ in range(6):
                 torch.cuda._sleep(200_000)
                 e0.record(stream)
-                if inplace:
+                if top_inplace:
                     pz.reconstruct_sgd_mn(Ug, Vg, P, Kf, M, N, Wt, -1e-3, stream=stream)
                 else:
                     pz.reconstruct_sgd(Ug, Vg, P, Kf, ldk, M, N, Wt, -1e-3, stream=stream)
@@ -588,14 +589,15 @@ def run_poseidon(args):
                 "algorithmic_bytes": byts, "peak_source": peaks["source"]}
     # K3 (factor pack) of every SFB layer, summed per step: 8 B per packed element (read + write) plus the
     # column sums; timed by the library's events on the producer stream (layer stats pack_ms)
-    if sfb and inplace:
+    packed_layers = [p for p in sfb if not (inplace and p.M % 4 == 0 and p.N % 4 == 0)]
+    if sfb and not packed_layers:
         roof["pack"] = {"kernel": "none: factors read in place by K1 (POSEIDON_FLAG_INPLACE_FACTORS, N = 1)",
                         "ms_per_step": 0.0, "algorithmic_bytes": 0.0, "achieved": None, "unit": "GB/s", "frac": None,
                         "note": "K1 consumes dl/dy and a_i MN-major where the backward wrote them; its idle lanes form "
                                 "the bias sums (4 K M B of extra reads per SFB layer, not counted as algorithmic)"}
     elif sfb:
         pk_ms, pk_bytes = 0.0, 0.0
-        for p in sfb:
+        for p in packed_layers:
             pk_ms += statistics.mean(ctx.layer_stats(p.layer_id, a)["pack_ms"] for a in range(n_stats))
             cols = p.M + (0 if early_v else p.N)
             pk_bytes += 8.0 * p.K * cols + 4.0 * p.M
@@ -605,7 +607,9 @@ def run_poseidon(args):
                         "frac": (ach / peaks["hbm_gbs"]) if ach else None,
                         "note": ("in-step, on the library's sync stream (POSEIDON_FLAG_INPLACE_FACTORS)"
                                  if args.factors == "async" else "in-step, on the compute stream")
-                                + "; V packed at forward time when early_v"}
+                                + "; V packed at forward time when early_v"
+                                + ("; layers packed: " + ", ".join(p.name for p in packed_layers)
+                                   + " (M or N not a multiple of 4: no in-place K1)" if inplace else "")}
     roof["traffic"] = None
     tr_path = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(tr_path):
