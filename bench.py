@@ -65,7 +65,7 @@ def parse():
                     help="SFB factor broadcast: NCCL all-gather on plain buffers, on NCCL symmetric windows, "
                          "or the library's broadcast kernel on symmetric windows (peer stores over NVLink; "
                          "POSEIDON_SFB_BCAST=mc for the multicast variant); auto = nvls when N > 1")
-    ap.add_argument("--ssp", type=int, default=0, choices=[0, 1],
+    ap.add_argument("--ssp", type=int, default=0, choices=[0, 1, 2, 3, 4, 5],
                     help="staleness s of the SSP consistency model (P:L399-402, E11); 0 = BSP (the paper's "
                          "headline setting)")
     ap.add_argument("--straggle-us", type=float, default=0.0,
@@ -409,6 +409,8 @@ def run_poseidon(args):
         flags |= pz.FLAG_INPLACE_MN
     inplace = (args.factors == "mn" and world == 1 and not args.ssp and args.dwbp == "on" and args.recon == "tf32")
     ctx = pz.Context(rank=rank, world=world, device=local, nccl_id=nccl_id, flags=flags)
+    if args.ssp > 1:
+        ctx.set_staleness(args.ssp)
 
     torch.manual_seed(6216)          # identical weights on every rank
     model = cfg["model"]().to(dev)

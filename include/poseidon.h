@@ -343,6 +343,14 @@ poseidon_status_t poseidon_set_recon(poseidon_ctx_t ctx, int32_t layer_id /* -1:
  * poseidon_get_iter_stats(ago = 0)), so training may continue after it.  No-op without SSP. */
 poseidon_status_t poseidon_flush(poseidon_ctx_t ctx, poseidon_stream_t stream);
 
+/* SSP staleness s ("a worker at iteration t reads parameters that contain all updates of iterations
+ * <= t - s - 1"), round 2: a context created with POSEIDON_FLAG_SSP1 runs s = 1; this call sets
+ * 1 <= s <= 5 before any layer is registered and before poseidon_ps_arena.  Each layer then keeps s + 1 gather /
+ * gradient sets used round robin, and the update of iteration t - s is applied at the layer's hook of
+ * iteration t (poseidon_flush applies every deferred one).  Errors: STATE (no SSP context, layers or arena
+ * already set up), INVALID_ARG (s out of range). */
+poseidon_status_t poseidon_set_staleness(poseidon_ctx_t ctx, int32_t s);
+
 /* Next-forward barrier: `consumer` waits until layer_id's latest sync is done
  * (under DWBP_OFF: until every layer's sync of the last iteration is done). */
 poseidon_status_t poseidon_wait_layer(poseidon_ctx_t ctx, int32_t layer_id, poseidon_stream_t consumer);

@@ -129,6 +129,7 @@ _SIGS = {
     "poseidon_reconstruct_sgd_rows": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _f, _i32,
                                              _vp]),
     "poseidon_stream": (_vp, [_vp, _i32]),
+    "poseidon_set_staleness": (_i32, [_vp, _i32]),
     "poseidon_reconstruct_sgd_mn": (_i32, [_vp, _i64, _i64, _vp, _i64, _i64, _i32, _i64, _i64, _i64, _vp, _f,
                                            _vp]),
 }
@@ -301,6 +302,10 @@ class Context:
     def set_ps_buckets(self, bucket_bytes: int):
         """Sync runs of small PS layers as one flat buffer (call before ps_arena, same on every rank)."""
         _check(lib.poseidon_set_ps_buckets(self.h, int(bucket_bytes)))
+
+    def set_staleness(self, s: int):
+        """SSP staleness s (context created with FLAG_SSP1; before registering layers and before ps_arena)."""
+        _check(lib.poseidon_set_staleness(self.h, int(s)))
 
     def flush(self, stream=None):
         """SSP: apply every layer's deferred update (collective; no-op without FLAG_SSP1)."""

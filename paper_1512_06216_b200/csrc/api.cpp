@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include <cstdio>
+#include <deque>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -113,7 +114,8 @@ struct Layer {
   float *Ug = nullptr, *Vg = nullptr, *Bs = nullptr;
   // POSEIDON_FLAG_SSP1: a second gather set (sync t packs/gathers into set t % 2 while the deferred
   // update of sync t-1 still reads set (t-1) % 2)
-  float *Ug2 = nullptr, *Vg2 = nullptr, *Bs2 = nullptr;
+  // sets 1..s (staleness s): xU[i], xV[i], xB[i] is gather set i + 1
+  std::vector<float*> xU, xV, xB;
   // POSEIDON_FLAG_SYMM_SFB: Ug|Vg|Bs are one ncclMemAlloc buffer registered as a symmetric window
   void* symm = nullptr;
   ncclWindow_t win = nullptr;
@@ -136,19 +138,22 @@ struct Layer {
   float mu = 0.f, wd = 0.f;
   float *vel = nullptr, *vel_b = nullptr;
   size_t arena_off = 0;      // byte offset of this layer in both arenas
-  float* gsets[2] = {nullptr, nullptr};  // arena gradient buffers (SSP: two, alternating per sync)
+  std::vector<float*> gsets;   // arena gradient buffers (SSP: s + 1, used round robin per sync)
   // PS bucketing (poseidon_set_ps_buckets): a member layer points at its bucket; a bucket is a hidden
   // pseudo-layer over the members' contiguous arena span, synced once all members are ready
   int32_t bucket = -1;
   std::vector<int32_t> members;
   size_t members_ready = 0;
   int64_t nsync = 0;         // syncs issued so far (SSP set parity)
-  // SSP (s = 1): the sync whose update is deferred to this layer's next hook (or poseidon_flush)
-  bool ssp_pend = false;
-  int64_t pend_iter = -1;
-  int pend_set = 0;
-  float pend_lr = 0.f;
-  float *pend_W2 = nullptr, *pend_bias2 = nullptr, *pend_grad2 = nullptr;
+  // SSP (staleness s): the syncs whose updates are deferred, oldest first; the one of iteration t - s is applied
+  // at this layer's hook of iteration t (or by poseidon_flush)
+  struct Pend {
+    int64_t iter;
+    int set;
+    float lr;
+    float *W, *bias, *grad;
+  };
+  std::deque<Pend> pend;
   EvSet ev[RING];
   bool events_created = false;
   int64_t last_iter = -1;  // iteration of the latest sync
@@ -187,11 +192,13 @@ struct poseidon_ctx {
   bool ps_nvls = false;        // PS arena is symmetric and the device communicator exists
   std::string devcomm_error;
   float *arena_g = nullptr, *arena_w = nullptr;
-  float* arena_g2 = nullptr;  // SSP: second gradient arena
   size_t arena_bytes = 0;
   bool arena_nccl_mem = false;
-  ncclWindow_t win_g = nullptr, win_w = nullptr, win_g2 = nullptr;
+  ncclWindow_t win_g = nullptr, win_w = nullptr;
+  std::vector<float*> arena_gx;          // SSP: gradient sets 1..s of the arena
+  std::vector<ncclWindow_t> win_gx;
   bool ssp = false;           // FLAG_SSP1
+  int stale = 0;              // SSP staleness s (1 with FLAG_SSP1; poseidon_set_staleness)
   int64_t bucket_bytes = 0;   // poseidon_set_ps_buckets
   std::vector<Layer> buckets; // pseudo-layers, addressed as MAX_LAYERS + index in records
   NvlsState* nvls = nullptr;
@@ -388,10 +395,11 @@ struct GatherSet {
   float *U, *V, *B;
 };
 GatherSet gather_set(const Layer& L, int set) {
-  return set ? GatherSet{L.Ug2, L.Vg2, L.Bs2} : GatherSet{L.Ug, L.Vg, L.Bs};
+  return set ? GatherSet{L.xU[(size_t)set - 1], L.xV[(size_t)set - 1], L.xB[(size_t)set - 1]}
+             : GatherSet{L.Ug, L.Vg, L.Bs};
 }
 // the gather set the next sync of this layer packs into (always 0 without SSP)
-int next_set(poseidon_ctx_t c, const Layer& L) { return c->ssp ? (int)(L.nsync & 1) : 0; }
+int next_set(poseidon_ctx_t c, const Layer& L) { return c->ssp ? (int)(L.nsync % (c->stale + 1)) : 0; }
 
 // SFB step 2: broadcast every worker's factors = all-gather of gather set `set`, on the
 // comm stream after `wait_ev`.  Records e.start and e.gathered.
@@ -858,25 +866,21 @@ poseidon_status_t ssp_hook(poseidon_ctx_t c, int32_t id, Layer& L, float* W, flo
   poseidon_status_t st = (L.scheme == POSEIDON_SCHEME_SFB) ? sfb_comm(c, L, set, e, e.ready, r)
                                                            : ps_comm_allreduce(c, L, grad, e, e.ready, r);
   if (st) return st;
-  if (L.ssp_pend) {
-    const EvSet& src = L.ev[L.pend_iter % RING];
-    st = (L.scheme == POSEIDON_SCHEME_SFB)
-             ? sfb_update(c, L, L.pend_set, L.pend_W2, L.pend_bias2, L.pend_lr, src.g_eff, e.ready, e)
-             : ps_update_local(c, L, L.pend_grad2, L.Wps, L.pend_lr, src.g_eff, e.ready, e);
+  L.pend.push_back(Layer::Pend{c->iter, set, lr, W, bias, grad});
+  if ((int)L.pend.size() > c->stale) {
+    // apply the update of iteration t - s (its collective is ordered before this one on the comm stream)
+    const Layer::Pend q = L.pend.front();
+    L.pend.pop_front();
+    const EvSet& src = L.ev[q.iter % RING];
+    st = (L.scheme == POSEIDON_SCHEME_SFB) ? sfb_update(c, L, q.set, q.W, q.bias, q.lr, src.g_eff, e.ready, e)
+                                           : ps_update_local(c, L, q.grad, L.Wps, q.lr, src.g_eff, e.ready, e);
     if (st) return st;
   } else {
-    // first sync: nothing to apply yet; done only orders after this backward
+    // the first s syncs: nothing to apply yet; done only orders after this backward
     CU_TRY(evwait(c, c->recon_stream, e.ready));
     CU_TRY(evrec(c, e.done, c->recon_stream));
     e.ks_eff = e.ke_eff = e.done;
   }
-  L.ssp_pend = true;
-  L.pend_iter = c->iter;
-  L.pend_set = set;
-  L.pend_lr = lr;
-  L.pend_W2 = W;
-  L.pend_bias2 = bias;
-  L.pend_grad2 = grad;
   L.nsync += 1;
   r.layers.push_back(id);
   return POSEIDON_OK;
@@ -928,10 +932,15 @@ void free_layer(poseidon_ctx_t c, Layer& L) {
     L.symm = nullptr;
     L.win = nullptr;
   } else {
-    for (float* q : {L.Ug, L.Vg, L.Bs, L.Ug2, L.Vg2, L.Bs2})
+    for (float* q : {L.Ug, L.Vg, L.Bs})
       if (q) cudaFree(q);
+    for (auto* vec : {&L.xU, &L.xV, &L.xB})
+      for (float* q : *vec)
+        if (q) cudaFree(q);
   }
-  L.Ug2 = L.Vg2 = L.Bs2 = nullptr;
+  L.xU.clear();
+  L.xV.clear();
+  L.xB.clear();
   if (L.stU) cudaFree(L.stU);
   if (L.stV) cudaFree(L.stV);
   if (L.vel) cudaFree(L.vel);
@@ -1008,6 +1017,7 @@ poseidon_status_t poseidon_init(int32_t world, const poseidon_topology_t* topo, 
   c->want_nvls = (topo->flags & POSEIDON_FLAG_NVLS_PS) != 0 && world > 1;
   c->want_nvls_sfb = (topo->flags & POSEIDON_FLAG_NVLS_SFB) != 0 && world > 1;
   c->ssp = (topo->flags & POSEIDON_FLAG_SSP1) != 0;
+  c->stale = c->ssp ? 1 : 0;
   c->layers.resize(64);
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -1065,9 +1075,12 @@ poseidon_status_t poseidon_finalize(poseidon_ctx_t c) {
   }
   if (c->nvls) nvls_destroy(c->comm, c->nvls);
   if (c->win_g) ncclCommWindowDeregister(c->comm, c->win_g);
-  if (c->win_g2) ncclCommWindowDeregister(c->comm, c->win_g2);
+  for (ncclWindow_t wg : c->win_gx)
+    if (wg) ncclCommWindowDeregister(c->comm, wg);
   if (c->win_w) ncclCommWindowDeregister(c->comm, c->win_w);
-  for (float* q : {c->arena_g, c->arena_g2, c->arena_w})
+  std::vector<float*> arenas = {c->arena_g, c->arena_w};
+  arenas.insert(arenas.end(), c->arena_gx.begin(), c->arena_gx.end());
+  for (float* q : arenas)
     if (q) {
       if (c->arena_nccl_mem) ncclMemFree(q);
       else cudaFree(q);
@@ -1127,7 +1140,7 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
     L.ldk = round_up(K, 4);
     const size_t P = (size_t)c->world;
     const size_t ub = P * (size_t)(M * L.ldk) * 4, vb = P * (size_t)(N * L.ldk) * 4, bb = P * (size_t)M * 4;
-    const int nsets = c->ssp ? 2 : 1;
+    const int nsets = c->ssp ? c->stale + 1 : 1;
     bool placed = false;
     if (c->world > 1 && (c->flags & (POSEIDON_FLAG_SYMM_SFB | POSEIDON_FLAG_NVLS_SFB))) {
       // one symmetric window for the layer's gather buffers: NCCL then runs the factor all-gather
@@ -1146,10 +1159,10 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
           L.Ug = reinterpret_cast<float*>(b0);
           L.Vg = reinterpret_cast<float*>(b0 + ua);
           L.Bs = reinterpret_cast<float*>(b0 + ua + va);
-          if (nsets == 2) {
-            L.Ug2 = reinterpret_cast<float*>(b0 + one);
-            L.Vg2 = reinterpret_cast<float*>(b0 + one + ua);
-            L.Bs2 = reinterpret_cast<float*>(b0 + one + ua + va);
+          for (int k = 1; k < nsets; ++k) {
+            L.xU.push_back(reinterpret_cast<float*>(b0 + k * one));
+            L.xV.push_back(reinterpret_cast<float*>(b0 + k * one + ua));
+            L.xB.push_back(reinterpret_cast<float*>(b0 + k * one + ua + va));
           }
           placed = true;
           L.bcast = scheme == POSEIDON_SCHEME_SFB && c->want_nvls_sfb && ensure_devcomm(c);
@@ -1162,16 +1175,20 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
       CU_TRY(cudaMalloc(&L.Ug, ub));
       CU_TRY(cudaMalloc(&L.Vg, vb));
       CU_TRY(cudaMalloc(&L.Bs, bb));
-      if (nsets == 2) {
-        CU_TRY(cudaMalloc(&L.Ug2, ub));
-        CU_TRY(cudaMalloc(&L.Vg2, vb));
-        CU_TRY(cudaMalloc(&L.Bs2, bb));
+      for (int k = 1; k < nsets; ++k) {
+        float *u = nullptr, *v = nullptr, *b = nullptr;
+        CU_TRY(cudaMalloc(&u, ub));
+        CU_TRY(cudaMalloc(&v, vb));
+        CU_TRY(cudaMalloc(&b, bb));
+        L.xU.push_back(u);
+        L.xV.push_back(v);
+        L.xB.push_back(b);
       }
     }
-    if (nsets == 2) {
-      CU_TRY(cudaMemset(L.Ug2, 0, ub));
-      CU_TRY(cudaMemset(L.Vg2, 0, vb));
-      CU_TRY(cudaMemset(L.Bs2, 0, bb));
+    for (int k = 0; k + 1 < nsets; ++k) {
+      CU_TRY(cudaMemset(L.xU[(size_t)k], 0, ub));
+      CU_TRY(cudaMemset(L.xV[(size_t)k], 0, vb));
+      CU_TRY(cudaMemset(L.xB[(size_t)k], 0, bb));
     }
     CU_TRY(cudaMemset(L.Ug, 0, ub));  // k columns in [K, ldk) stay zero forever
     CU_TRY(cudaMemset(L.Vg, 0, vb));
@@ -1318,13 +1335,18 @@ poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
   c->arena_bytes = total;
   bool symmetric = false;
   if (c->want_nvls && c->comm) {
-    void *g = nullptr, *w = nullptr, *g2 = nullptr;
+    void *g = nullptr, *w = nullptr;
+    std::vector<void*> gx((size_t)(c->ssp ? c->stale : 0), nullptr);
     ncclResult_t r = ncclMemAlloc(&g, total);
     if (r == ncclSuccess) r = ncclMemAlloc(&w, total);
-    if (r == ncclSuccess && c->ssp) r = ncclMemAlloc(&g2, total);
+    for (size_t k = 0; k < gx.size() && r == ncclSuccess; ++k) r = ncclMemAlloc(&gx[k], total);
     if (r == ncclSuccess) r = ncclCommWindowRegister(c->comm, g, total, &c->win_g, NCCL_WIN_COLL_SYMMETRIC);
     if (r == ncclSuccess) r = ncclCommWindowRegister(c->comm, w, total, &c->win_w, NCCL_WIN_COLL_SYMMETRIC);
-    if (r == ncclSuccess && c->ssp) r = ncclCommWindowRegister(c->comm, g2, total, &c->win_g2, NCCL_WIN_COLL_SYMMETRIC);
+    for (size_t k = 0; k < gx.size() && r == ncclSuccess; ++k) {
+      ncclWindow_t wk = nullptr;
+      r = ncclCommWindowRegister(c->comm, gx[k], total, &wk, NCCL_WIN_COLL_SYMMETRIC);
+      if (r == ncclSuccess) c->win_gx.push_back(wk);
+    }
     if (r == ncclSuccess) {
       c->ps_nvls = ensure_devcomm(c);
       if (!c->ps_nvls) c->nvls_error = c->devcomm_error;
@@ -1332,23 +1354,31 @@ poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
       c->arena_nccl_mem = true;
       c->arena_g = static_cast<float*>(g);
       c->arena_w = static_cast<float*>(w);
-      c->arena_g2 = static_cast<float*>(g2);
+      for (void* q : gx) c->arena_gx.push_back(static_cast<float*>(q));
     } else {
       c->nvls_error = std::string("symmetric window: ") + ncclGetErrorString(r);
       if (c->win_g) { ncclCommWindowDeregister(c->comm, c->win_g); c->win_g = nullptr; }
       if (c->win_w) { ncclCommWindowDeregister(c->comm, c->win_w); c->win_w = nullptr; }
-      for (void* q : {g, w, g2})
+      for (ncclWindow_t wk : c->win_gx) ncclCommWindowDeregister(c->comm, wk);
+      c->win_gx.clear();
+      gx.push_back(g);
+      gx.push_back(w);
+      for (void* q : gx)
         if (q) ncclMemFree(q);
     }
   }
   if (!symmetric) {
     CU_TRY(cudaMalloc(&c->arena_g, total));
     CU_TRY(cudaMalloc(&c->arena_w, total));
-    if (c->ssp) CU_TRY(cudaMalloc(&c->arena_g2, total));
+    for (int k = 0; k < (c->ssp ? c->stale : 0); ++k) {
+      float* q = nullptr;
+      CU_TRY(cudaMalloc(&q, total));
+      c->arena_gx.push_back(q);
+    }
   }
   CU_TRY(cudaMemset(c->arena_g, 0, total));
   CU_TRY(cudaMemset(c->arena_w, 0, total));
-  if (c->arena_g2) CU_TRY(cudaMemset(c->arena_g2, 0, total));
+  for (float* q : c->arena_gx) CU_TRY(cudaMemset(q, 0, total));
   CU_TRY(cudaDeviceSynchronize());
   auto at = [](float* base, size_t off) {
     return base ? reinterpret_cast<float*>(reinterpret_cast<char*>(base) + off) : nullptr;
@@ -1371,8 +1401,8 @@ poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
       if (st) return st;
     }
     L.in_arena = true;
-    L.gsets[0] = g;
-    L.gsets[1] = at(c->arena_g2, L.arena_off);
+    L.gsets.assign(1, g);
+    for (float* q : c->arena_gx) L.gsets.push_back(at(q, L.arena_off));
   }
   for (auto& B : c->buckets) {
     B.grad = at(c->arena_g, B.arena_off);
@@ -1405,7 +1435,7 @@ poseidon_status_t poseidon_ps_layer_buffers(poseidon_ctx_t c, int32_t id, float*
   if (st) return st;
   if (!L->in_arena) return fail(POSEIDON_ERR_STATE, "layer has no arena buffers (call poseidon_ps_arena)");
   // the gradient buffer the layer's NEXT sync reduces (SSP alternates two)
-  if (grad) *grad = (c->ssp && L->gsets[1]) ? L->gsets[next_set(c, *L)] : L->grad;
+  if (grad) *grad = (c->ssp && L->gsets.size() > 1) ? L->gsets[(size_t)next_set(c, *L)] : L->grad;
   if (W) *W = L->Wps;
   if (padded) *padded = L->padded;
   return POSEIDON_OK;
@@ -1454,6 +1484,18 @@ static poseidon_status_t set_momentum_one(poseidon_ctx_t c, Layer& L, float mu, 
   }
   CU_TRY(cudaMalloc(&L.vel, count * 4));
   CU_TRY(cudaMemset(L.vel, 0, count * 4));
+  return POSEIDON_OK;
+}
+
+poseidon_status_t poseidon_set_staleness(poseidon_ctx_t c, int32_t s) {
+  poseidon_status_t st = check_ctx(c);
+  if (st) return st;
+  if (!c->ssp) return fail(POSEIDON_ERR_STATE, "staleness needs a context created with POSEIDON_FLAG_SSP1");
+  if (s < 1 || s > RING - 3) return fail(POSEIDON_ERR_INVALID_ARG, "staleness must be in [1, 5]");
+  for (const Layer& L : c->layers)
+    if (L.registered) return fail(POSEIDON_ERR_STATE, "set the staleness before registering layers");
+  if (c->arena_g) return fail(POSEIDON_ERR_STATE, "set the staleness before poseidon_ps_arena");
+  c->stale = s;
   return POSEIDON_OK;
 }
 
@@ -1597,7 +1639,7 @@ poseidon_status_t poseidon_sync_ps(poseidon_ctx_t c, int32_t id, float* grad, fl
   CU_TRY(evrec(c, e.ready, ps));
   L->last_iter = c->iter;
   if (c->ssp) {
-    float* g = (L->in_arena && L->gsets[1]) ? L->gsets[next_set(c, *L)] : L->grad;
+    float* g = (L->in_arena && L->gsets.size() > 1) ? L->gsets[(size_t)next_set(c, *L)] : L->grad;
     return ssp_hook(c, id, *L, L->Wps, nullptr, g, lr);
   }
   if (L->bucket >= 0) {
@@ -1660,18 +1702,20 @@ poseidon_status_t poseidon_flush(poseidon_ctx_t c, poseidon_stream_t stream) {
   IterRecord& r = open_record(c);
   for (int32_t id = 0; id < (int32_t)c->layers.size(); ++id) {   // same order on every rank
     Layer& L = c->layers[id];
-    if (!L.registered || !L.ssp_pend) continue;
+    if (!L.registered || L.pend.empty()) continue;
     EvSet& e = L.ev[c->iter % RING];
     CU_TRY(evrec(c, e.ready, s));
     CU_TRY(evwait(c, c->comm_stream, e.ready));
     CU_TRY(evrec(c, e.start, c->comm_stream));
     e.g_eff = e.ks_eff = e.start;
-    const EvSet& src = L.ev[L.pend_iter % RING];
-    st = (L.scheme == POSEIDON_SCHEME_SFB)
-             ? sfb_update(c, L, L.pend_set, L.pend_W2, L.pend_bias2, L.pend_lr, src.g_eff, e.ready, e)
-             : ps_update_local(c, L, L.pend_grad2, L.Wps, L.pend_lr, src.g_eff, e.ready, e);
-    if (st) return st;
-    L.ssp_pend = false;
+    while (!L.pend.empty()) {   // oldest first: every deferred update, in iteration order
+      const Layer::Pend q = L.pend.front();
+      L.pend.pop_front();
+      const EvSet& src = L.ev[q.iter % RING];
+      st = (L.scheme == POSEIDON_SCHEME_SFB) ? sfb_update(c, L, q.set, q.W, q.bias, q.lr, src.g_eff, e.ready, e)
+                                             : ps_update_local(c, L, q.grad, L.Wps, q.lr, src.g_eff, e.ready, e);
+      if (st) return st;
+    }
     L.last_iter = c->iter;
     r.layers.push_back(id);
   }

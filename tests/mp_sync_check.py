@@ -581,9 +581,13 @@ def main():
     # ---- 6. SSP with staleness 1 (FLAG_SSP1, reading Z19): SFB + PS (arena) over 4 iterations and a
     #          flush, integer variant bit-exact vs O10, on the NCCL paths and on the NVLS paths ----
     from paper_1512_06216_b200.binding import device_view
-    for flags in (pz.FLAG_SSP1 | pz.FLAG_SYMM_SFB, pz.FLAG_SSP1 | pz.FLAG_NVLS_PS | pz.FLAG_NVLS_SFB):
+    #          (+ staleness 2, poseidon_set_staleness, on the NVLS paths) ----
+    for flags, stale in ((pz.FLAG_SSP1 | pz.FLAG_SYMM_SFB, 1), (pz.FLAG_SSP1 | pz.FLAG_NVLS_PS | pz.FLAG_NVLS_SFB, 1),
+                         (pz.FLAG_SSP1 | pz.FLAG_NVLS_PS | pz.FLAG_NVLS_SFB, 2)):
         cs = new_ctx(flags)
-        M, N, K, T = 40, 72, 4, 4
+        if stale != 1:
+            cs.set_staleness(stale)
+        M, N, K, T = 40, 72, 4, 5
         cs.register_layer(0, pz.LAYER_FC, M, N, K)
         cs.register_layer(1, pz.LAYER_CONV, M, N, K, True, pz.SCHEME_PS)
         cs.ps_arena()
@@ -592,7 +596,7 @@ def main():
         for t in range(T):
             _, _, Us, Vs, _ = S.integer_factors(M, N, K, P, seed=80 + t)
             steps.append((Us, Vs))
-        vis = O.ssp_visible_weights(W, b, steps, lr, s=1)
+        vis = O.ssp_visible_weights(W, b, steps, lr, s=stale)
         Wd, bd = torch.from_numpy(W).to(dev), torch.from_numpy(b).to(dev)
         n = M * N + M
         _, wp, padded = cs.ps_layer_buffers(1)
@@ -619,12 +623,12 @@ def main():
         cs.wait_layer(0)
         cs.wait_layer(1)
         torch.cuda.synchronize()
-        Wf, bf = vis[T + 1]
+        Wf, bf = vis[T + stale]
         assert np.array_equal(Wd.cpu().numpy().astype(np.float64), Wf)
         assert np.array_equal(wflat[:n].cpu().numpy().astype(np.float64), O.flatten_params(Wf, bf))
         assert allsame(Wd) and allsame(wflat)
         if rank == 0:
-            print(f"SSP flags={flags}: PS {cs.nvls_status()}, SFB path {cs.sfb_path(0)}", flush=True)
+            print(f"SSP flags={flags} s={stale}: PS {cs.nvls_status()}, SFB path {cs.sfb_path(0)}", flush=True)
         cs.close()
 
     # ---- 7. PS buckets (f1): small PS layers synced as one flat buffer, NCCL and fused NVLS paths;

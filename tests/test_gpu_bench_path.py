@@ -26,22 +26,24 @@ def pz():
     return pz
 
 
-@pytest.mark.parametrize("factors", ["async", "mn", "pack"])
-def test_alexnet_step_matches_oracle(pz, factors):
-    """factors="async" is bench.py's default (POSEIDON_FLAG_INPLACE_FACTORS: fc6-fc8's pack runs on the
-    library's stream, reading grad_out and x in place); "mn" adds POSEIDON_FLAG_INPLACE_MN (K1 reads them
-    MN-major, no pack); "pack" the round-1 path (K3 on the backward's stream)."""
+@pytest.mark.parametrize("cfg,factors", [("C3", "async"), ("C3", "mn"), ("C3", "pack"), ("C5", "mn")])
+def test_alexnet_step_matches_oracle(pz, cfg, factors):
+    """factors="mn" is bench.py's N = 1 default (POSEIDON_FLAG_INPLACE_FACTORS | _INPLACE_MN: K1 reads grad_out
+    and x in place, MN-major, no pack); "async" keeps the pack but runs it on the library's stream; "pack" the
+    round-1 path (K3 on the backward's stream).  C5 = the ImageNet-22K AlexNet: its 21841-way fc8 (M not a
+    multiple of 4) is packed even under "mn", fc6 / fc7 are read in place."""
     import torch.nn.functional as F
     from paper_1512_06216_b200.dwbp import PoseidonSync
     from drivers.cnn import AlexNet
 
     dev = torch.device("cuda", 0)
     torch.manual_seed(6216)
-    model = AlexNet().to(dev)
+    classes = 21841 if cfg == "C5" else 1000
+    model = AlexNet(n_classes=classes).to(dev)
     g = torch.Generator(device=dev)
     g.manual_seed(1512)
     x = torch.rand((256, 3, 227, 227), device=dev, generator=g)
-    y = torch.randint(0, 1000, (256,), device=dev, generator=g)
+    y = torch.randint(0, classes, (256,), device=dev, generator=g)
     # lr large enough that every layer's update is at least a quarter of its weights, so the fp32 gate
     # tests the update and not the storage rounding of W' (tests/parity.py: at lr = 0.05 the conv updates
     # are ~1e-4 of W and one ulp of W' would be most of the 1e-5 gate).  A plain torch backward of the same

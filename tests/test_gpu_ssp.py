@@ -25,11 +25,16 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-@pytest.mark.parametrize("recon", ["tf32", "fp32"])
-def test_ssp1_sfb_and_ps_integer_exact(pz, recon):
+@pytest.mark.parametrize("recon,s", [("tf32", 1), ("fp32", 1), ("tf32", 2), ("tf32", 3), ("fp32", 3)])
+def test_ssp_sfb_and_ps_integer_exact(pz, recon, s):
+    """Staleness s (poseidon_set_staleness; s = 1 is FLAG_SSP1's default): after the hook of iteration t the
+    parameters hold exactly the updates of iterations <= t - s (O10), for SFB and PS; s + 1 gradient sets used
+    round robin; flush applies the rest."""
     from paper_1512_06216_b200.binding import device_view
-    M, N, K, T = 72, 136, 8, 4
+    M, N, K, T = 72, 136, 8, 7
     ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device(), flags=pz.FLAG_SSP1)
+    if s != 1:
+        ctx.set_staleness(s)
     ctx.register_layer(0, pz.LAYER_FC, M, N, K)                          # SFB
     ctx.register_layer(1, pz.LAYER_CONV, M, N, K, True, pz.SCHEME_PS)    # PS (arena)
     ctx.set_recon(pz.RECON_TF32 if recon == "tf32" else pz.RECON_FP32, 0)
@@ -39,7 +44,7 @@ def test_ssp1_sfb_and_ps_integer_exact(pz, recon):
     for t in range(T):
         _, _, Us, Vs, _ = S.integer_factors(M, N, K, 1, seed=50 + t)
         steps.append((Us, Vs))
-    vis = O.ssp_visible_weights(W, b, steps, lr, s=1)
+    vis = O.ssp_visible_weights(W, b, steps, lr, s=s)
     Wd, bd = dev(W), dev(b)
     n = M * N + M
     _, wp, padded = ctx.ps_layer_buffers(1)
@@ -59,16 +64,16 @@ def test_ssp1_sfb_and_ps_integer_exact(pz, recon):
         ctx.wait_layer(1)
         ctx.iteration_end()
         torch.cuda.synchronize()
-        Wv, bv = vis[t + 1]                       # after hook t: updates of iterations <= t-1
+        Wv, bv = vis[t + 1]                       # after hook t: updates of iterations <= t-s
         assert np.array_equal(Wd.cpu().numpy().astype(np.float64), Wv), f"SFB step {t}"
         assert np.array_equal(bd.cpu().numpy().astype(np.float64), bv)
         assert np.array_equal(wflat[:n].cpu().numpy().astype(np.float64), O.flatten_params(Wv, bv)), f"PS step {t}"
-    assert len(seen_g) == 2                        # the two gradient buffers alternate
+    assert len(seen_g) == s + 1                    # the s + 1 gradient buffers are used round robin
     ctx.flush()
     ctx.wait_layer(0)
     ctx.wait_layer(1)
     torch.cuda.synchronize()
-    Wf, bf = vis[T + 1]
+    Wf, bf = vis[T + s]
     assert np.array_equal(Wd.cpu().numpy().astype(np.float64), Wf)
     assert np.array_equal(bd.cpu().numpy().astype(np.float64), bf)
     assert np.array_equal(wflat[:n].cpu().numpy().astype(np.float64), O.flatten_params(Wf, bf))
@@ -83,9 +88,25 @@ def test_ssp1_flag_validation(pz):
                    flags=pz.FLAG_SSP1 | pz.FLAG_DWBP_OFF)
 
 
-def test_ssp1_cifar_training_matches_delayed_sgd(pz):
-    """Three DWBP steps of CIFAR-10 quick with FLAG_SSP1 (SFB for ip1/ip2, PS for the convs) + flush
-    equal single-GPU SGD where the gradient of iteration t is applied after the backward of t+1."""
+def test_set_staleness_validation(pz):
+    c0 = pz.Context(rank=0, world=1, device=torch.cuda.current_device())
+    with pytest.raises(pz.PoseidonError):
+        c0.set_staleness(2)                       # no SSP context
+    c0.close()
+    c1 = pz.Context(rank=0, world=1, device=torch.cuda.current_device(), flags=pz.FLAG_SSP1)
+    for bad in (0, 6):
+        with pytest.raises(pz.PoseidonError):
+            c1.set_staleness(bad)
+    c1.register_layer(0, pz.LAYER_FC, 8, 8, 4)
+    with pytest.raises(pz.PoseidonError):
+        c1.set_staleness(2)                       # after a registration
+    c1.close()
+
+
+@pytest.mark.parametrize("s", [1, 2])
+def test_ssp_cifar_training_matches_delayed_sgd(pz, s):
+    """DWBP steps of CIFAR-10 quick with SSP staleness s (SFB for ip1/ip2, PS for the convs) + flush equal
+    single-GPU SGD where the gradient of iteration t is applied after the backward of t+s."""
     import torch.nn.functional as F
     from paper_1512_06216_b200.dwbp import PoseidonSync
     from drivers.cnn import CifarQuick
@@ -94,28 +115,30 @@ def test_ssp1_cifar_training_matches_delayed_sgd(pz):
     torch.manual_seed(3)
     model = CifarQuick().cuda()
     ref = copy.deepcopy(model)
-    lr, T, B = 0.05, 3, 16
+    lr, T, B = 0.05, 4, 16
     ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device(), flags=pz.FLAG_SSP1)
+    if s != 1:
+        ctx.set_staleness(s)
     sync = PoseidonSync(model, ctx, K=B, lr=lr, arena=True)
     g = torch.Generator(device="cuda").manual_seed(11)
     batches = [(torch.rand(B, 3, 32, 32, device="cuda", generator=g),
                 torch.randint(0, 10, (B,), device="cuda", generator=g)) for _ in range(T)]
-    pending = None
+    pending = []
     for x, y in batches:
         F.cross_entropy(model(x), y).backward()
         sync.iteration_end()
         ref.zero_grad()
         F.cross_entropy(ref(x), y).backward()
-        grads = [p.grad.detach().clone() for p in ref.parameters()]
+        pending.append([p.grad.detach().clone() for p in ref.parameters()])
         with torch.no_grad():
-            if pending is not None:
-                for p, gr in zip(ref.parameters(), pending):
+            if len(pending) > s:                  # after the backward of t: apply the gradient of t - s
+                for p, gr in zip(ref.parameters(), pending.pop(0)):
                     p -= lr * gr
-        pending = grads
     sync.flush()
     with torch.no_grad():
-        for p, gr in zip(ref.parameters(), pending):
-            p -= lr * gr
+        for grads in pending:
+            for p, gr in zip(ref.parameters(), grads):
+                p -= lr * gr
     torch.cuda.synchronize()
     for (name, p), (_, q) in zip(model.named_parameters(), ref.named_parameters()):
         w0 = q.detach().cpu().numpy()
