@@ -6,7 +6,9 @@ the library (tests/stepcheck.py): PS layers element by element (O6, 1e-5), facto
 
   C2 cifar10_quick, batch 100, PS-only (BJ): 5 layers
   C4 bvlc_googlenet, batch 128, SACP auto: 57 conv layers PS + the 1024 x 1000 FC (SFB at P = 1)
-  C3 is covered by test_gpu_bench_path.py; C5 (22K-way fc8) by test_gpu_kernels' full-size rows.
+  C3 and C5 (22K-way fc8) are covered by test_gpu_bench_path.py.  The context has bench.py's N = 1 flags
+  (POSEIDON_FLAG_INPLACE_FACTORS | _INPLACE_MN: GoogLeNet's FC reads its factors in place); C2's CUDA-graph
+  step equals the eager one bit for bit (test_gpu_graph.py).
 """
 import pytest
 
@@ -40,7 +42,7 @@ def test_config_step_matches_oracle(pz, config, n_layers):
     x = torch.rand((K, 3, cfg["hw"], cfg["hw"]), device=dev, generator=g).contiguous(memory_format=torch.channels_last)
     y = torch.randint(0, cfg["classes"], (K,), device=dev, generator=g)
     lr = safe_lr(model, lambda m: F.cross_entropy(m(x), y))
-    ctx = pz.Context(rank=0, world=1, device=0)
+    ctx = pz.Context(rank=0, world=1, device=0, flags=pz.FLAG_INPLACE_FACTORS | pz.FLAG_INPLACE_MN)
     sync = PoseidonSync(model, ctx, K=K, lr=lr, scheme=cfg["scheme"])
     assert len(sync.plans) == n_layers
     cap = StepCapture(sync)
