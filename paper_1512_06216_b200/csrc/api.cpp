@@ -41,6 +41,16 @@ poseidon_status_t cuda_fail(cudaError_t e, const char* what) {
 
 // POSEIDON_DEBUG_SYNC=1: synchronise the library stream after every kernel launch and report the
 // kernel that faulted (debugging aid for asynchronous launch failures; off in production).
+// K2o (one-shot small-layer PS sync): largest layer it takes (floats), POSEIDON_ONESHOT=0 disables it
+constexpr int64_t kOneShotMax = 65536;
+bool knobs_oneshot() {
+  static const bool on = [] {
+    const char* v = getenv("POSEIDON_ONESHOT");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 // experiment knob: POSEIDON_ASYNC_PACK=0 keeps K3 on the producer stream with POSEIDON_FLAG_INPLACE_FACTORS
 bool knobs_async_pack() {
   static const bool on = [] {
@@ -139,6 +149,7 @@ struct Layer {
   float *vel = nullptr, *vel_b = nullptr;
   size_t arena_off = 0;      // byte offset of this layer in both arenas
   std::vector<float*> gsets;   // arena gradient buffers (SSP: s + 1, used round robin per sync)
+  int64_t os_off = -1;         // K2o one-shot sync: byte offset of this layer's [P][np] slot in the scratch window
   // PS bucketing (poseidon_set_ps_buckets): a member layer points at its bucket; a bucket is a hidden
   // pseudo-layer over the members' contiguous arena span, synced once all members are ready
   int32_t bucket = -1;
@@ -196,6 +207,8 @@ struct poseidon_ctx {
   bool arena_nccl_mem = false;
   ncclWindow_t win_g = nullptr, win_w = nullptr;
   std::vector<float*> arena_gx;          // SSP: gradient sets 1..s of the arena
+  void* os_buf = nullptr;                // K2o one-shot scratch (symmetric window win_s)
+  ncclWindow_t win_s = nullptr;
   std::vector<ncclWindow_t> win_gx;
   bool ssp = false;           // FLAG_SSP1
   int stale = 0;              // SSP staleness s (1 with FLAG_SSP1; poseidon_set_staleness)
@@ -743,6 +756,17 @@ poseidon_status_t ps_comm(poseidon_ctx_t c, Layer& L, float* grad, EvSet& e, cud
 // gradient buffer `grad`, then the gradient clear (the fused NVLS kernel does all of it).
 poseidon_status_t ps_update(poseidon_ctx_t c, Layer& L, float* grad, float* W, float lr, EvSet& dst, IterRecord& r) {
   const int P = c->world;
+  if (ps_fused(c, L) && L.os_off >= 0 && c->win_s && !L.vel && (L.ps_flags & POSEIDON_PS_ZERO_GRAD)) {
+    // K2o: one-shot sync of a small layer (peer stores, one barrier, replicated update, clear)
+    dst.ke_eff = dst.done;
+    cudaError_t err = launch_ps_oneshot(c->nvls, c->win_s, (size_t)L.os_off, L.grad, L.Wps, L.n, -lr / (float)P,
+                                        c->comm_stream);
+    if (err != cudaSuccess) return cuda_fail(err, "one-shot PS launch");
+    CU_TRY(evrec(c, dst.done, c->comm_stream));
+    r.sent += (uint64_t)L.n * 4u * (uint64_t)(P - 1);
+    r.recv += (uint64_t)L.n * 4u * (uint64_t)(P - 1);
+    return POSEIDON_OK;
+  }
   if (ps_fused(c, L)) {
     // fused one-kernel PS over NVLink SHARP (reduce-scatter + K2 + all-gather + zero-grad)
     dst.ke_eff = dst.done;
@@ -1077,6 +1101,8 @@ poseidon_status_t poseidon_finalize(poseidon_ctx_t c) {
   if (c->win_g) ncclCommWindowDeregister(c->comm, c->win_g);
   for (ncclWindow_t wg : c->win_gx)
     if (wg) ncclCommWindowDeregister(c->comm, wg);
+  if (c->win_s) ncclCommWindowDeregister(c->comm, c->win_s);
+  if (c->os_buf) ncclMemFree(c->os_buf);
   if (c->win_w) ncclCommWindowDeregister(c->comm, c->win_w);
   std::vector<float*> arenas = {c->arena_g, c->arena_w};
   arenas.insert(arenas.end(), c->arena_gx.begin(), c->arena_gx.end());
@@ -1423,6 +1449,33 @@ poseidon_status_t poseidon_ps_arena(poseidon_ctx_t c, int32_t* nvls_active) {
     if (M0.vel) {
       st = set_momentum_one(c, B, M0.mu, M0.wd);
       if (st) return st;
+    }
+  }
+  // K2o: layers whose fused sync is latency-bound (n <= kOneShotMax floats, no bucket, no SSP) get a slot in a
+  // symmetric scratch window and sync with one barrier instead of two -- when at least two barrier-synced
+  // layers exist (the slot reuse argument of k_ps_nvls.cu) and POSEIDON_ONESHOT is not 0
+  if (c->ps_nvls && !c->ssp && knobs_oneshot()) {
+    int barrier_layers = (int)c->buckets.size();
+    for (const Layer& L : c->layers)
+      if (L.registered && L.scheme == POSEIDON_SCHEME_PS && L.in_arena && L.bucket < 0) ++barrier_layers;
+    size_t total = 0;
+    if (barrier_layers >= 2)
+      for (Layer& L : c->layers)
+        if (L.registered && L.scheme == POSEIDON_SCHEME_PS && L.in_arena && L.bucket < 0 && L.n <= kOneShotMax) {
+          L.os_off = (int64_t)total;
+          total += (size_t)round_up((int64_t)c->world * round_up(L.n, 4) * 4, 4096);
+        }
+    if (total > 0) {
+      void* buf = nullptr;
+      ncclWindow_t w = nullptr;
+      if (ncclMemAlloc(&buf, total) == ncclSuccess &&
+          ncclCommWindowRegister(c->comm, buf, total, &w, NCCL_WIN_COLL_SYMMETRIC) == ncclSuccess) {
+        c->os_buf = buf;
+        c->win_s = w;
+      } else {
+        if (buf) ncclMemFree(buf);
+        for (Layer& L : c->layers) L.os_off = -1;
+      }
     }
   }
   if (nvls_active) *nvls_active = c->ps_nvls ? 1 : 0;

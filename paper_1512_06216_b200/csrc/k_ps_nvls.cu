@@ -145,6 +145,76 @@ __global__ void __launch_bounds__(256) ps_nvls_kernel(const __grid_constant__ nc
   }
 }
 
+// K2o — one-shot PS sync of a small layer (round 2): ONE LSA barrier instead of K2n's two, for layers whose
+// sync is latency-bound (a few microseconds of barrier round trips dominate; C2, C4's small convolutions).
+// Every rank owns a slot [P][np] (np = roundup(n, 4)) in a symmetric scratch window, reused every iteration:
+//   1. block j stores its float4 range of this rank's whole gradient into slot[rank] of every rank (peer
+//      stores over NVLink, itself included);
+//   2. LSA barrier j (acq_rel): block j of every rank has stored the same range;
+//   3. block j sums slot[0..P-1] of its range in rank order -- the same arithmetic on every rank, so every
+//      replica gets the same W -- applies W = fmaf(alpha, sum, W) to the whole layer (the update is
+//      replicated, no all-gather) and clears its range of the local gradient, which only step 1 read.
+// The slot of iteration t+1 is written only after the writing rank has passed another barrier kernel that
+// every rank reaches only after finishing iteration t's reads (the host enables K2o only when at least two
+// barrier-synced layers exist, and every rank issues the syncs in the same order).
+template <int U>
+__global__ void __launch_bounds__(256) ps_oneshot_kernel(const __grid_constant__ ncclDevComm comm, ncclWindow_t ws,
+                                                         size_t off_s, float* __restrict__ g, float* __restrict__ W,
+                                                         int64_t n, int64_t np, float alpha, uint32_t fuzz_ns,
+                                                         uint32_t fuzz_seed) {
+  const ncclTeam lsa = ncclTeamLsa(comm);
+  const int64_t n4 = n >> 2;
+  const int64_t per = (int64_t)blockDim.x * U;             // float4 per block
+  const int64_t lo = (int64_t)blockIdx.x * per;
+  const int64_t hi = lo + per < n4 ? lo + per : n4;
+  const bool tail_block = blockIdx.x == gridDim.x - 1;     // also owns the scalar tail n % 4
+  // 1. this rank's gradient range -> slot[rank] of every rank
+  float4 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = lo + u * blockDim.x + threadIdx.x;
+    if (i < hi) v[u] = reinterpret_cast<const float4*>(g)[i];
+  }
+  for (int d = 0; d < lsa.nRanks; ++d) {
+    const int q = (lsa.rank + d) % lsa.nRanks;
+    float* dst = static_cast<float*>(ncclGetLsaPointer(ws, off_s + (size_t)lsa.rank * np * 4, q));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = lo + u * blockDim.x + threadIdx.x;
+      if (i < hi) reinterpret_cast<float4*>(dst)[i] = v[u];
+    }
+    if (tail_block && threadIdx.x < (n & 3)) dst[4 * n4 + threadIdx.x] = g[4 * n4 + threadIdx.x];
+  }
+  ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamTagLsa(), blockIdx.x, /*multimem=*/true);
+  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  cta_fuzz(fuzz_ns, fuzz_seed, lsa.rank);
+  // 3. sum in rank order, update, clear
+  const float* slot = static_cast<const float*>(ncclGetLocalPointer(ws, off_s));
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = lo + u * blockDim.x + threadIdx.x;
+    if (i < hi) {
+      float4 sum = reinterpret_cast<const float4*>(slot)[i];
+      for (int p = 1; p < lsa.nRanks; ++p) {
+        const float4 x = reinterpret_cast<const float4*>(slot + (size_t)p * np)[i];
+        sum.x += x.x; sum.y += x.y; sum.z += x.z; sum.w += x.w;
+      }
+      float4 w = reinterpret_cast<float4*>(W)[i];
+      w.x = fmaf(alpha, sum.x, w.x); w.y = fmaf(alpha, sum.y, w.y);
+      w.z = fmaf(alpha, sum.z, w.z); w.w = fmaf(alpha, sum.w, w.w);
+      reinterpret_cast<float4*>(W)[i] = w;
+      reinterpret_cast<float4*>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  if (tail_block && threadIdx.x < (n & 3)) {
+    const int64_t k = 4 * n4 + threadIdx.x;
+    float sum = slot[k];
+    for (int p = 1; p < lsa.nRanks; ++p) sum += slot[(size_t)p * np + k];
+    W[k] = fmaf(alpha, sum, W[k]);
+    g[k] = 0.f;
+  }
+}
+
 struct BcastSeg {
   size_t off;   // byte offset of this rank's slot within the layer's window
   int64_t n;    // floats
@@ -273,6 +343,21 @@ cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww
   auto kern = env_u == 8 ? ps_nvls_kernel<8> : env_u == 2 ? ps_nvls_kernel<2> : ps_nvls_kernel<4>;
   cudaError_t err = launch_prio(kern, dim3(blocks), dim3(256), 0, s, st->dev, wg, ww, off_g, off_w, b, e, shard, nranks,
                                 alpha, zg, mom, fz, seed);
+  g_launches.fetch_add(1);
+  return err != cudaSuccess ? err : cudaGetLastError();
+}
+
+cudaError_t launch_ps_oneshot(const NvlsState* st, ncclWindow_t ws, size_t off_s, float* g, float* W, int64_t n,
+                              float alpha, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  constexpr int U = 4;
+  const int64_t n4 = n >> 2;
+  int blocks = (int)((n4 + 256 * U - 1) / (256 * U));
+  if (blocks < 1) blocks = 1;   // identical on every rank (n is)
+  if (blocks > 128) return cudaErrorInvalidValue;   // one LSA barrier per block
+  const uint32_t fz = fuzz_bound_ns(), seed = fz ? next_fuzz_seed() : 0u;
+  cudaError_t err = launch_prio(ps_oneshot_kernel<U>, dim3(blocks), dim3(256), 0, s, st->dev, ws, off_s, g, W, n,
+                                (n + 3) / 4 * 4, alpha, fz, seed);
   g_launches.fetch_add(1);
   return err != cudaSuccess ? err : cudaGetLastError();
 }

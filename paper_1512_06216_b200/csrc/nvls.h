@@ -15,6 +15,12 @@ cudaError_t launch_ps_nvls(const NvlsState* st, ncclWindow_t wg, ncclWindow_t ww
                            int64_t b, int64_t e, int64_t padded, float alpha, bool zero_grad, int max_blocks,
                            int64_t shard, float* vel, float inv_p, float lr, float mu, float wd, cudaStream_t s);
 
+// One-shot PS sync of a small layer (K2o): peer stores of the local gradient into slot [P][roundup(n,4)] of
+// every rank (byte offset off_s in the scratch window ws), one LSA barrier, rank-ordered sum, replicated update
+// of W[0,n) and clear of g[0,n) (both local arena pointers).
+cudaError_t launch_ps_oneshot(const NvlsState* st, ncclWindow_t ws, size_t off_s, float* g, float* W, int64_t n,
+                              float alpha, cudaStream_t s);
+
 // NVLS factor broadcast (SFB step 2 done by the switch): barrier; multimem.st of this rank's three
 // slots (byte offsets within the layer's window, float counts); barrier.
 cudaError_t launch_sfb_bcast_nvls(const NvlsState* st, ncclWindow_t win, size_t off_u, int64_t n_u, size_t off_v,
