@@ -41,12 +41,12 @@ poseidon_status_t cuda_fail(cudaError_t e, const char* what) {
 
 // POSEIDON_DEBUG_SYNC=1: synchronise the library stream after every kernel launch and report the
 // kernel that faulted (debugging aid for asynchronous launch failures; off in production).
-// K2o (one-shot small-layer PS sync): largest layer it takes (floats), POSEIDON_ONESHOT=0 disables it
+// K2o (one-shot small-layer PS sync): largest layer it takes (floats); POSEIDON_ONESHOT=1 enables it
 constexpr int64_t kOneShotMax = 65536;
 bool knobs_oneshot() {
   static const bool on = [] {
     const char* v = getenv("POSEIDON_ONESHOT");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
   return on;
 }

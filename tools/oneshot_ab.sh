@@ -2,7 +2,7 @@
 # K2o one-shot small-layer PS sync (round 2): multi-GPU parity, then C2 / C4 with and without it (POSEIDON_ONESHOT).
 python paper_1512_06216_b200/build.py --force > gpurun_out/build.log 2>&1 || exit 1
 NG=$(nvidia-smi -L | wc -l)
-timeout -s KILL 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$NG --master-addr 127.0.0.1 --master-port 29811 tests/mp_sync_check.py > gpurun_out/mp_oneshot_p$NG.log 2>&1; echo "mp P=$NG rc=$?"
+POSEIDON_ONESHOT=1 timeout -s KILL 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$NG --master-addr 127.0.0.1 --master-port 29811 tests/mp_sync_check.py > gpurun_out/mp_oneshot_p$NG.log 2>&1; echo "mp P=$NG rc=$?"
 grep -c MP_OK gpurun_out/mp_oneshot_p$NG.log
 for rep in 1 2; do for cfg in C2 C4; do for os in 1 0; do
   POSEIDON_ONESHOT=$os timeout -s KILL 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$NG --master-addr 127.0.0.1 \
