@@ -706,6 +706,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
                              const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmV,
                              const Params p) {
   constexpr int SLOT = (MOM ? 2 : 1) * W_CHUNK_BYTES;
+  // The two epilogue groups take alternate W chunks (g % 2) and chunk g lives in slot g % NWS: with an even
+  // slot count every slot belongs to one group, so each group waits on consecutive phases of its own slots.
+  // With an odd count a slot alternates between the groups and a group could test a full barrier two phases
+  // ahead, whose parity matches an already-completed phase (round 2: the <5,3> probe failed this way).
+  static_assert(NWS % 2 == 0, "W slot count must be even (two epilogue groups alternate chunks)");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_ops = smem;
@@ -1021,8 +1026,9 @@ struct K1Knobs {
     if (const char* v = getenv("POSEIDON_K1_RWS")) rws = v[0] - '0';
     if (const char* v = getenv("POSEIDON_K1_VARIANT")) variant = (v[0] == '1') ? 1 : 2;
     if (const char* r = getenv("POSEIDON_K1_RASTER")) raster = (r[0] == 'm') ? 1 : 0;
-    // a <3,8>  b <4,5>  c <2,8>  d <5,4>  e <2,10>  f <3,7>  g <4,6>  h <2,9>
-    if (const char* c = getenv("POSEIDON_K1_CFG")) cfg = (c[0] >= 'a' && c[0] <= 'h') ? c[0] - 'a' : 1;
+    // a <3,8>  c <2,8>  d <5,4>  e <2,10>  g <4,6>  i <6,2>  (even W-slot counts only; b / f / h / j = the
+    // round-1 <4,5> and the odd probes <3,7>, <2,9>, <5,3> are gone: see the kernel's static_assert)
+    if (const char* c = getenv("POSEIDON_K1_CFG")) cfg = (c[0] >= 'a' && c[0] <= 'j') ? c[0] - 'a' : 1;
     if (const char* e = getenv("POSEIDON_K1_EPI")) epi = (e[0] == '1') ? 1 : 2;
     if (const char* w = getenv("POSEIDON_K1_WPOL")) wpol = w[0] - '0';
     if (const char* m = getenv("POSEIDON_K1_MODE")) mode = m[0] - '0';
@@ -1215,12 +1221,12 @@ cudaError_t dispatch_2sm(const CUtensorMap& tmA, const CUtensorMap& tmB, const C
   const int pairs = std::min(p.num_tiles, sm_count_k1() / 2);
   if (mom != nullptr) {
     // f4: W and velocity chunks share a slot (2 x 16 KB): <3 stages, 4 slots> when the W stream dominates
-    // (<= 8 factor slabs per tile), else <4, 3>; both 224 KB of shared memory
+    // (<= 8 factor slabs per tile), else <4, 2> (an even slot count: see the kernel's static_assert)
     static bool m1 = false, m2 = false;
     if (p.num_kb <= 8)
       return launch_2sm(recon_tcgen05_2sm_kernel<3, 4, true, 0, MNK>, smem_bytes(3, 4, true), m1, pairs, tmA, tmB, tmW,
                         tmV, p, s);
-    return launch_2sm(recon_tcgen05_2sm_kernel<4, 3, true, 0, MNK>, smem_bytes(4, 3, true), m2, pairs, tmA, tmB, tmW,
+    return launch_2sm(recon_tcgen05_2sm_kernel<4, 2, true, 0, MNK>, smem_bytes(4, 2, true), m2, pairs, tmA, tmB, tmW,
                       tmV, p, s);
   }
   // RW epilogue (no W slots: the shared memory goes to 6 operand stages) where the tensor pipe is the
@@ -1247,7 +1253,7 @@ cudaError_t dispatch_2sm(const CUtensorMap& tmA, const CUtensorMap& tmB, const C
   // step 84 -> 69 us, alone 67.6 us either way; <4,5> was the round-1 pick); with more slabs deeper operand
   // staging <5, 4> wins (fc6 P*K=2048: 686 -> 743 TFLOP/s).  Letters of POSEIDON_K1_CFG in K1Knobs.
   const int cfg = knobs().cfg >= 0 ? knobs().cfg : (p.num_kb <= 8 ? 6 : 3);
-  static bool at[8] = {};
+  static bool at[10] = {};
   if (MNK) {
     if (cfg == 3)
       return launch_2sm(recon_tcgen05_2sm_kernel<5, 4, false, 0, true>, smem_bytes(5, 4), at[3], pairs, tmA, tmB, tmW,
@@ -1260,10 +1266,9 @@ cudaError_t dispatch_2sm(const CUtensorMap& tmA, const CUtensorMap& tmB, const C
     case 2: return launch_2sm(recon_tcgen05_2sm_kernel<2, 8>, smem_bytes(2, 8), at[2], pairs, tmA, tmB, tmW, tmW, p, s);
     case 3: return launch_2sm(recon_tcgen05_2sm_kernel<5, 4>, smem_bytes(5, 4), at[3], pairs, tmA, tmB, tmW, tmW, p, s);
     case 4: return launch_2sm(recon_tcgen05_2sm_kernel<2, 10>, smem_bytes(2, 10), at[4], pairs, tmA, tmB, tmW, tmW, p, s);
-    case 5: return launch_2sm(recon_tcgen05_2sm_kernel<3, 7>, smem_bytes(3, 7), at[5], pairs, tmA, tmB, tmW, tmW, p, s);
     case 6: return launch_2sm(recon_tcgen05_2sm_kernel<4, 6>, smem_bytes(4, 6), at[6], pairs, tmA, tmB, tmW, tmW, p, s);
-    case 7: return launch_2sm(recon_tcgen05_2sm_kernel<2, 9>, smem_bytes(2, 9), at[7], pairs, tmA, tmB, tmW, tmW, p, s);
-    default: return launch_2sm(recon_tcgen05_2sm_kernel<4, 5>, smem_bytes(4, 5), at[1], pairs, tmA, tmB, tmW, tmW, p, s);
+    case 8: return launch_2sm(recon_tcgen05_2sm_kernel<6, 2>, smem_bytes(6, 2), at[8], pairs, tmA, tmB, tmW, tmW, p, s);
+    default: return launch_2sm(recon_tcgen05_2sm_kernel<4, 6>, smem_bytes(4, 6), at[6], pairs, tmA, tmB, tmW, tmW, p, s);
   }
 }
 

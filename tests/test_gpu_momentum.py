@@ -23,9 +23,12 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-@pytest.mark.parametrize("recon,tol", [("tf32", 2e-3), ("fp32", 1e-5)])
-def test_sfb_momentum_three_steps(pz, recon, tol):
-    M, N, K, steps, lr, mu, wd = 300, 520, 16, 3, 0.5, 0.9, 1e-2
+@pytest.mark.parametrize("recon,tol,M,N,K", [("tf32", 2e-3, 300, 520, 16), ("fp32", 1e-5, 300, 520, 16),
+                                             ("tf32", 2e-3, 4096, 4096, 384)])
+def test_sfb_momentum_three_steps(pz, recon, tol, M, N, K):
+    """Lambda fused into K1's epilogue (f4, O4m).  K = 384: 12 factor slabs per tile, the <4 stages, 2 W+V slots>
+    configuration, and 256 tiles over 74 CTA pairs, so W slots are reused across tiles by both epilogue groups."""
+    steps, lr, mu, wd = 3, 0.5, 0.9, 1e-2
     ctx = pz.Context(rank=0, world=1, device=torch.cuda.current_device())
     ctx.register_layer(0, pz.LAYER_FC, M, N, K)
     ctx.set_recon(pz.RECON_TF32 if recon == "tf32" else pz.RECON_FP32, 0)
