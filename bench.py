@@ -459,7 +459,7 @@ def run_poseidon(args):
                                          and not args.ssp and not args.straggle_us and args.dwbp == "on")
     if use_graph and (args.ssp or args.straggle_us or args.dwbp == "off"):
         raise SystemExit("--graph: BSP with DWBP only (no --ssp, --straggle-us, --dwbp off)")
-    run_step, graph_launches = step, None
+    run_step, graph_launches, graph_fallback = step, None, None
     if use_graph:
         # One captured step: the library sees the capture on the caller's stream, forks its comm / recon streams
         # from it, records its statistics events as graph nodes and rejoins at iteration_end, so one replay is
@@ -468,11 +468,27 @@ def run_poseidon(args):
         gs.wait_stream(torch.cuda.current_stream())
         graph = torch.cuda.CUDAGraph()
         lc0 = pz.launch_count()
-        with torch.cuda.graph(graph, stream=gs):
-            static_loss = step(x, y)
-        graph_launches = pz.launch_count() - lc0
+        try:
+            with torch.cuda.graph(graph, stream=gs):
+                static_loss = step(x, y)
+            graph_launches = pz.launch_count() - lc0
+        except Exception as exc:   # e.g. an untested topology: fall back to the eager loop, say so in the line
+            graph_fallback = f"{type(exc).__name__}: {exc}"[:200]
+            sys.stderr.write(f"bench: CUDA-graph capture failed, eager steps instead ({graph_fallback})\n")
+            use_graph = False
         torch.cuda.current_stream().wait_stream(gs)
+        if world > 1:   # every rank replays, or none does
+            ok = torch.tensor([1.0 if use_graph else 0.0], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if use_graph and float(ok) < 1.0:
+                graph_fallback = graph_fallback or "another rank's capture failed"
+                use_graph = False
+        if not use_graph:
+            del graph
+            sync.wait_all()
+            barrier()
 
+    if use_graph:
         def run_step(xb, yb):
             if xb is not x:
                 x.copy_(xb, non_blocking=True)
@@ -723,7 +739,7 @@ def run_poseidon(args):
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "tf32" if args.recon == "tf32" else "f32", "data": "synthetic",
             "config": workload_config(args, cfg, world),
-            "details": {"scheme": scheme, "else_branch": args.else_branch, "early_v": early_v, "factors": args.factors, "cuda_graph": use_graph, "inplace_mn_k1": inplace, "dwbp": args.dwbp, "recon": args.recon, "lr": args.lr,
+            "details": {"scheme": scheme, "else_branch": args.else_branch, "early_v": early_v, "factors": args.factors, "cuda_graph": use_graph, "graph_fallback": graph_fallback, "inplace_mn_k1": inplace, "dwbp": args.dwbp, "recon": args.recon, "lr": args.lr,
                         "momentum": args.momentum, "weight_decay": args.weight_decay,
                         "memory_format": args.memory_format,
                         "ps_path": ("nvls-fused" if sync.nvls_active else
