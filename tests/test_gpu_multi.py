@@ -19,7 +19,8 @@ def test_multi_gpu_sync(nproc):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(29611 + nproc),
            os.path.join(ROOT, "tests", "mp_sync_check.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    # every check creates its own communicators; NCCL bring-up grows with the rank count
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300 + 150 * nproc, cwd=ROOT)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     for rank in range(nproc):
