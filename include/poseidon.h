@@ -109,9 +109,9 @@ typedef struct {
                                          poseidon_sync_fc_sfb in place, asynchronously on its own streams, so no
                                          factor work stays on the caller's (backward's) stream: the pack (K3) runs
                                          on the stream the sync continues on (comm at world > 1, recon at 1).  The
-                                         CALLER then keeps U and V unchanged until the layer's sync is done (e.g.
-                                         tensor.record_stream on both poseidon_stream()s before freeing them, or
-                                         poseidon_wait_layer). */
+                                         CALLER then keeps U and V unchanged until the layer's sync is done: e.g.
+                                         it holds them until poseidon_wait_layer has ordered its stream after the
+                                         sync (what the glue does), or record_stream on both poseidon_stream()s. */
 #define POSEIDON_FLAG_INPLACE_MN 0x200u /* with POSEIDON_FLAG_INPLACE_FACTORS, at world == 1 (TF32, 16-B aligned U / V,
                                          M and N multiples of 4): no pack at all, K1 consumes U and V MN-major and
                                          forms the bias sums itself; the tensor core then reads the fp32 factors as

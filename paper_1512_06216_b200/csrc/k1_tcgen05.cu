@@ -174,6 +174,11 @@ __device__ __forceinline__ float2 lds64(uint32_t a) {
   asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
   return v;
 }
+__device__ __forceinline__ void stg64_na_hint(float* ptr, float2 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f32 [%0], {%1,%2}, %3;" ::"l"(ptr), "f"(v.x), "f"(v.y),
+               "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void stg64_na(float* ptr, float2 v) {
   asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1,%2};" ::"l"(ptr), "f"(v.x), "f"(v.y) : "memory");
 }
@@ -283,6 +288,7 @@ struct Params {
   // MN-major operands: 1 -> 4-D maps {32, K, MN/32, P} whose one box {32, BK, 4, 1} lands as the four
   // 32-element chunks of a CTA's 128 rows (MN a multiple of 32), else four 3-D boxes per operand and stage
   int32_t mn4;
+  int32_t wst_hint;   // experiment (POSEIDON_K1_WSTORE=1): W stores carry an L2 evict_first policy
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& mt, int& nt) {
@@ -927,6 +933,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
     const int q = (warp - 4) & 3;
     const int t0 = lane & 3, tr = lane >> 2;   // column pair / row within a 16-lane slab
     const uint32_t smem_w_u32 = smem_u32(smem_w);
+    const uint64_t wst_pol = policy_evict_first();
     uint32_t g = 0;
     int it = 0;
     for (int tile = pair; tile < p.num_tiles; tile += npairs, ++it) {
@@ -994,7 +1001,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
                 w.x = fmaf(p.alpha, a0, p.beta * w.x);
                 w.y = fmaf(p.alpha, a1, p.beta * w.y);
               }
-              if (p.mode != 3 && row_ok && col_base + cl < p.N) stg64_na(grow + col_base + cl, w);
+              if (p.mode != 3 && row_ok && col_base + cl < p.N) {
+                if (p.wst_hint) stg64_na_hint(grow + col_base + cl, w, wst_pol);
+                else stg64_na(grow + col_base + cl, w);
+              }
             }
           }
         }
@@ -1032,10 +1042,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
 //   POSEIDON_K1_RW=0|1      force the TMA W ring (0) or the RW epilogue (1) for plain SGD (default: by regime)
 //   POSEIDON_K1_RWD=2|3|4   W chunks in flight per epilogue warp (RW epilogue);  POSEIDON_K1_RWS=4|5|6  stages
 struct K1Knobs {
-  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0, fbias = 1, rw = -1, rwd = 3, rws = 6, mn4 = 1;
+  int variant = 2, raster = -1, cfg = -1, epi = 2, wpol = 0, mode = 0, fbias = 1, rw = -1, rwd = 3, rws = 6, mn4 = 1,
+      wst = 0;
   K1Knobs() {
     if (const char* v = getenv("POSEIDON_K1_RW")) rw = v[0] - '0';
     if (const char* v = getenv("POSEIDON_K1_MN4")) mn4 = v[0] - '0';
+    if (const char* v = getenv("POSEIDON_K1_WSTORE")) wst = v[0] - '0';
     if (const char* v = getenv("POSEIDON_K1_RWD")) rwd = v[0] - '0';
     if (const char* v = getenv("POSEIDON_K1_RWS")) rws = v[0] - '0';
     if (const char* v = getenv("POSEIDON_K1_VARIANT")) variant = (v[0] == '1') ? 1 : 2;
@@ -1187,6 +1199,7 @@ void fill_params(Params& p, int32_t P, int64_t K, int64_t M, int64_t N, float* W
   p.ldu = p.ublk = 0;
   p.Kc = (int32_t)K;
   p.mn4 = 0;
+  p.wst_hint = knobs().wst;
   // Raster (measured, tools/k1_sweep.sh): when both factor buffers fit comfortably in L2 the waves
   // walk N so each wave's W tiles are whole row segments; otherwise consecutive tiles walk the
   // dimension whose operand is smaller, so the operand re-swept every wave stays L2-resident.

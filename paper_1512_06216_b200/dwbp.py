@@ -115,12 +115,15 @@ class PoseidonSync:
         self.ssp = bool(getattr(ctx, "flags", 0) & B.FLAG_SSP1)
         self.early_v = bool(getattr(ctx, "flags", 0) & B.FLAG_EARLY_V)
         # FLAG_INPLACE_FACTORS: the library reads grad_out and x where they are, on its own streams (K1 at
-        # world 1, else the pack before the factor broadcast), so the allocator must not hand their memory out
-        # again before those streams have passed the sync (record_stream)
-        self.inplace_streams = []
-        if (getattr(ctx, "flags", 0) & B.FLAG_INPLACE_FACTORS) and not self.ssp and \
-                not (getattr(ctx, "flags", 0) & B.FLAG_DWBP_OFF):
-            self.inplace_streams = [ctx.stream(B.STREAM_RECON)] + ([ctx.stream(B.STREAM_COMM)] if ctx.world > 1 else [])
+        # world 1, else the pack before the factor broadcast), so their memory must not be handed out again
+        # before the sync is done.  The glue holds the two tensors until the layer's next forward has waited
+        # for the sync (poseidon_wait_layer in the pre-forward hook) and only then drops them: the allocator
+        # then reuses the blocks on the compute stream, already ordered after the sync.  (record_stream on the
+        # library's streams did the same job but made the caching allocator defer and re-allocate blocks: 1 in
+        # ~5 C3 runs lost half its images/s, profiles/r2/factors_r2.md.)
+        self.hold_factors = bool(getattr(ctx, "flags", 0) & B.FLAG_INPLACE_FACTORS) and not self.ssp and \
+            not (getattr(ctx, "flags", 0) & B.FLAG_DWBP_OFF)
+        self.held: Dict[int, tuple] = {}
         if self.ssp and not arena:
             raise ValueError("FLAG_SSP1 needs the library arena (arena=True): PS gradients are double-buffered")
         self.arena = arena
@@ -245,6 +248,8 @@ class PoseidonSync:
     def _pre_forward(self, plan):
         def hook(_mod, _inp):
             self.ctx.wait_layer(plan.layer_id, torch.cuda.current_stream())
+            # the stream is ordered after the layer's sync now: its factors may be released
+            getattr(self, "held", {}).pop(plan.layer_id, None)
         return hook
 
     def _post_accumulate(self, plan):
@@ -257,9 +262,8 @@ class PoseidonSync:
 
     def sfb_backward(self, plan, grad_out, x, weight, bias):
         self.ctx.sync_fc_sfb(plan.layer_id, grad_out, x, weight, bias, self.lr, torch.cuda.current_stream())
-        for st in getattr(self, "inplace_streams", ()):
-            grad_out.record_stream(st)
-            x.record_stream(st)
+        if getattr(self, "hold_factors", False):
+            self.held[plan.layer_id] = (grad_out, x)
 
     # ------------------------------------------------------------ driver ----
     def iteration_end(self, stats: bool = False):
@@ -285,6 +289,7 @@ class PoseidonSync:
         s = stream or torch.cuda.current_stream()
         for p in self.plans:
             self.ctx.wait_layer(p.layer_id, s)
+        getattr(self, "held", {}).clear()   # ordered after every sync: the held factors may go
 
     def describe(self):
         out = []
