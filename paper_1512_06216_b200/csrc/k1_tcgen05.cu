@@ -551,14 +551,6 @@ __device__ __forceinline__ void tma_load_4d_2sm(const CUtensorMap* map, uint32_t
       "l"(map), "r"(bar_cluster), "r"(x), "r"(y), "r"(z), "r"(w), "l"(policy)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_5d_2sm(const CUtensorMap* map, uint32_t bar_cluster, void* dst, int32_t c0,
-                                                int32_t c1, int32_t c2, int32_t c3, int32_t c4, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "l"(policy)
-      : "memory");
-}
 __device__ __forceinline__ void tc_mma_tf32_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                                 uint32_t accumulate) {
   asm volatile(
@@ -788,10 +780,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
           if (rank == 0) mbar_expect_tx(&full[stage], (uint32_t)(2 * k2sm::STAGE));
           uint8_t* sa = smem_ops + stage * k2sm::STAGE;
           uint8_t* sb = sa + k2sm::A_BYTES;
-          if (MNK && p.mn4 == 2) {   // k-group-major: [BK/4 k-groups][4 chunks][4 k rows x 128 B]
-            tma_load_5d_2sm(&tmA, full_leader, sa, 0, 0, a_row / 32, kb * BK / 4, pw, pol);
-            tma_load_5d_2sm(&tmB, full_leader, sb, 0, 0, b_row / 32, kb * BK / 4, pw, pol);
-          } else if (MNK && p.mn4) {
+          if (MNK && p.mn4) {
             tma_load_4d_2sm(&tmA, full_leader, sa, 0, kb * BK, a_row / 32, pw, pol);
             tma_load_4d_2sm(&tmB, full_leader, sb, 0, kb * BK, b_row / 32, pw, pol);
           } else if (MNK) {
@@ -836,13 +825,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS_2SM, 1)
           for (int k = 0; k < BK / UK; ++k) {
             // K-major: the k-th UMMA (8 k = 32 B) starts 32 k bytes into each 128-B row; MN-major: 8 k rows
             // of 128 B further into every 32-element chunk
-            // (MN-major, k-group-major stage (mn4 == 2): chunks 512 B apart, k-groups 2 KB apart)
-            const uint64_t ad = !MNK ? make_desc_k_sw128(sa + k * 32, 16, 1024)
-                                : p.mn4 == 2 ? make_desc_mn_sw128_32b(sa + k * (UK / 4) * 2048, 512, 2048)
-                                             : make_desc_mn_sw128_32b(sa + k * UK * 128, k2sm::MN_CHUNK, 512);
-            const uint64_t bd = !MNK ? make_desc_k_sw128(sb + k * 32, 16, 1024)
-                                : p.mn4 == 2 ? make_desc_mn_sw128_32b(sb + k * (UK / 4) * 2048, 512, 2048)
-                                             : make_desc_mn_sw128_32b(sb + k * UK * 128, k2sm::MN_CHUNK, 512);
+            const uint64_t ad = MNK ? make_desc_mn_sw128_32b(sa + k * UK * 128, k2sm::MN_CHUNK, 512)
+                                    : make_desc_k_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bd = MNK ? make_desc_mn_sw128_32b(sb + k * UK * 128, k2sm::MN_CHUNK, 512)
+                                    : make_desc_k_sw128(sb + k * 32, 16, 1024);
             tc_mma_tf32_2sm(d_tmem, ad, bd, id, (kk | k) != 0 ? 1u : 0u);
           }
           tc_commit_2sm_mc(&empty[stage], 0x3);
@@ -1401,18 +1387,8 @@ cudaError_t launch_recon_tcgen05_mn(const float* U, int64_t ldu, int64_t ublk, c
     // one 4-D box per operand and stage when both MN extents are multiples of 32: dims {32, K, MN/32, P},
     // strides {ld, 128 B, blk}; the box {32, BK, 4, 1} is laid out chunk-major, i.e. exactly the four
     // [BK x 128 B] chunks of the 3-D form (POSEIDON_K1_MN4=0 keeps the four 3-D boxes)
-    bool four = false, five = false;
-    if (M % 32 == 0 && N % 32 == 0 && K % 4 == 0 && knobs().mn4 == 2) {
-      // POSEIDON_K1_MN4=2 (experiment): k-group-major stages, dims {32, 4, MN/32, K/4, P}
-      const uint64_t dA5[5] = {32, 4, (uint64_t)M / 32, (uint64_t)K / 4, (uint64_t)P};
-      const uint64_t sA5[4] = {(uint64_t)ldu * 4, 128, (uint64_t)ldu * 16, (uint64_t)ublk * 4};
-      const uint64_t dB5[5] = {32, 4, (uint64_t)N / 32, (uint64_t)K / 4, (uint64_t)P};
-      const uint64_t sB5[4] = {(uint64_t)ldv * 4, 128, (uint64_t)ldv * 16, (uint64_t)vblk * 4};
-      const uint32_t box5[5] = {32, 4, 4, BK / 4, 1};
-      five = encode(&tmA, U, 5, dA5, sA5, box5, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
-             encode(&tmB, V, 5, dB5, sB5, box5, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    }
-    if (!five && M % 32 == 0 && N % 32 == 0 && knobs().mn4) {
+    bool four = false;
+    if (M % 32 == 0 && N % 32 == 0 && knobs().mn4) {
       const uint64_t dA4[4] = {32, (uint64_t)K, (uint64_t)M / 32, (uint64_t)P};
       const uint64_t sA4[3] = {(uint64_t)ldu * 4, 128, (uint64_t)ublk * 4};
       const uint64_t dB4[4] = {32, (uint64_t)K, (uint64_t)N / 32, (uint64_t)P};
@@ -1421,11 +1397,11 @@ cudaError_t launch_recon_tcgen05_mn(const float* U, int64_t ldu, int64_t ublk, c
       four = encode(&tmA, U, 4, dA4, sA4, box4, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
              encode(&tmB, V, 4, dB4, sB4, box4, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     }
-    if (!four && !five && (!encode(&tmA, U, 3, dA, sA, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+    if (!four && (!encode(&tmA, U, 3, dA, sA, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
                   !encode(&tmB, V, 3, dB, sB, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)))
       return cudaErrorNotSupported;
     if (!encode(&tmW, W, 2, dW, sW, bW)) return cudaErrorNotSupported;
-    mn4 = five ? 2 : four ? 1 : 0;
+    mn4 = four ? 1 : 0;
     tmB2 = tmB;
     tmV = tmW;
     if (mom != nullptr && !encode(&tmV, mom->vel, 2, dW, sW, bW)) return cudaErrorNotSupported;
