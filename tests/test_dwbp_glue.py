@@ -174,3 +174,35 @@ def test_binding_refuses_factor_shapes_other_than_registered():
     for bad in [(4, 4), (5, 5), (6, 4), (5, 2, 2)]:
         with pytest.raises(ValueError, match="registered K"):
             c._check_factor(0, "U", torch.zeros(*bad), 4)
+
+
+def test_inplace_factors_are_held_until_the_next_wait(monkeypatch):
+    """POSEIDON_FLAG_INPLACE_FACTORS: the library reads an SFB layer's grad_out and input where they are, on its
+    own streams, so the glue keeps both tensors alive from the layer's backward until the layer's next
+    pre-forward hook has called wait_layer (or until wait_all), and drops them right after (no record_stream:
+    plain stream-ordered reuse).  Without the flag, or with DWBP off, nothing is held."""
+    from drivers.cnn import CifarQuick
+    monkeypatch.setattr(torch.cuda, "current_stream", lambda *a, **k: None)
+    for flags, expect in ((B.FLAG_INPLACE_FACTORS, True), (0, False),
+                          (B.FLAG_INPLACE_FACTORS | B.FLAG_DWBP_OFF, False)):
+        torch.manual_seed(0)
+        model = CifarQuick()
+        ctx = _FakeContext(flags)
+        sync = PoseidonSync(model, ctx, K=4, lr=0.1)
+        sfb = {p.layer_id for p in sync.plans if p.scheme == B.SCHEME_SFB}
+        x, y = torch.rand(4, 3, 32, 32), torch.randint(0, 10, (4,))
+        torch.nn.functional.cross_entropy(model(x), y).backward()
+        sync.iteration_end()
+        assert set(sync.held) == (sfb if expect else set())
+        if expect:
+            for lid in sfb:
+                g, a = sync.held[lid]
+                assert g.shape[0] == 4 and a.shape[0] == 4          # (K x M) error messages, (K x N) inputs
+        # the next forward: each layer's hold ends at its own pre-forward hook, after its wait_layer
+        waits_before = len([c for c in ctx.calls if c[0] == "wait"])
+        model(x)
+        assert sync.held == {}
+        assert len([c for c in ctx.calls if c[0] == "wait"]) == waits_before + len(sync.plans)
+        torch.nn.functional.cross_entropy(model(x), y).backward()
+        sync.wait_all()
+        assert sync.held == {}
