@@ -526,7 +526,7 @@ poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, floa
 // POSEIDON_FLAG_INPLACE_FACTORS (round 2): at world == 1 nothing travels, so the sufficient factors are consumed
 // where the backward wrote them ("the vectors already exist"): K1 reads U = dl/dy [K x M] and
 // V = a_i [K x N] MN-major on the reconstruction stream (no K3 pack, no gather buffer) and its idle lanes form
-// the bias sums.  The caller keeps U and V until the sync is done (the glue: record_stream on the recon stream).
+// the bias sums.  The caller keeps U and V until the sync is done (the glue holds them until the layer's next wait).
 bool inplace_ok(poseidon_ctx_t c, const Layer& L, const float* U, const float* V, const float* W) {
   return (c->flags & POSEIDON_FLAG_INPLACE_FACTORS) && (c->flags & POSEIDON_FLAG_INPLACE_MN) && c->world == 1 &&
          !c->ssp && !(c->flags & POSEIDON_FLAG_DWBP_OFF) && L.scheme == POSEIDON_SCHEME_SFB &&
