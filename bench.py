@@ -407,7 +407,9 @@ def run_poseidon(args):
         flags |= pz.FLAG_INPLACE_FACTORS
     if args.factors == "mn":
         flags |= pz.FLAG_INPLACE_MN
-    inplace = (args.factors == "mn" and world == 1 and not args.ssp and args.dwbp == "on" and args.recon == "tf32")
+    # MN-major K1 on the SFB layers whose M, N are multiples of 4: in place at N = 1, on the MN-major gather
+    # buffers (slot filled by a copy-engine memcpy, no K3) at N > 1
+    inplace = (args.factors == "mn" and not args.ssp and args.dwbp == "on" and args.recon == "tf32")
     ctx = pz.Context(rank=rank, world=world, device=local, nccl_id=nccl_id, flags=flags)
     if args.ssp > 1:
         ctx.set_staleness(args.ssp)
@@ -571,9 +573,9 @@ def run_poseidon(args):
         if args.recon == "tf32":
             # context for `frac` (which is the in-step number): the same K1 launch on the same shape ALONE,
             # after the timed region, each launch queued behind a device spin (device time only)
-            if top_inplace:   # the factors as the layer leaves them: U [K x M], V [K x N] (MN-major K1)
-                Ug = torch.randn(Kf, M, device=dev).mul_(0.01)
-                Vg = torch.randn(Kf, N, device=dev).relu_()
+            if top_inplace:   # the factors as the layers leave them: U [P][K][M], V [P][K][N] (MN-major K1)
+                Ug = torch.randn(P, Kf, M, device=dev).mul_(0.01)
+                Vg = torch.randn(P, Kf, N, device=dev).relu_()
             else:
                 Ug = torch.randn(P, M, ldk, device=dev).mul_(0.01)
                 Vg = torch.randn(P, N, ldk, device=dev).relu_()
@@ -609,7 +611,9 @@ def run_poseidon(args):
     # column sums; timed by the library's events on the producer stream (layer stats pack_ms)
     packed_layers = [p for p in sfb if not (inplace and p.M % 4 == 0 and p.N % 4 == 0)]
     if sfb and not packed_layers:
-        roof["pack"] = {"kernel": "none: factors read in place by K1 (POSEIDON_FLAG_INPLACE_FACTORS, N = 1)",
+        roof["pack"] = {"kernel": ("none: factors read in place by K1 (POSEIDON_FLAG_INPLACE_MN, N = 1)" if world == 1
+                                   else "none: copy-engine memcpy of the factors into the MN-major gather slot "
+                                        "(POSEIDON_FLAG_INPLACE_MN, N > 1)"),
                         "ms_per_step": 0.0, "algorithmic_bytes": 0.0, "achieved": None, "unit": "GB/s", "frac": None,
                         "note": "K1 consumes dl/dy and a_i MN-major where the backward wrote them; its idle lanes form "
                                 "the bias sums (4 K M B of extra reads per SFB layer, not counted as algorithmic)"}

@@ -131,6 +131,10 @@ struct Layer {
   ncclWindow_t win = nullptr;
   ncclComm_t win_comm = nullptr;
   bool bcast = false;   // POSEIDON_FLAG_NVLS_SFB: factors broadcast by the multicast kernel
+  // POSEIDON_FLAG_INPLACE_MN at world > 1 (round 2): MN-major gather layout Ug [P][K][M], Vg [P][K][N] -- the
+  // factors exactly as the layer wrote them; this rank's slot is filled by a copy-engine memcpy (no K3), K1
+  // reads MN-major and forms the bias sums from Ug (no Bs travels)
+  bool mn = false;
   // SF-PS (scheme 2, reading Z20): output rows [rb, re) this rank is the master of (O2 on the rows)
   int64_t rb = 0, re = 0;
   // FLAG_EARLY_V: this sync's V was packed and broadcast by poseidon_sfb_post_input (events in ev[v_iter])
@@ -411,6 +415,11 @@ GatherSet gather_set(const Layer& L, int set) {
   return set ? GatherSet{L.xU[(size_t)set - 1], L.xV[(size_t)set - 1], L.xB[(size_t)set - 1]}
              : GatherSet{L.Ug, L.Vg, L.Bs};
 }
+// floats of one rank's U / V / bias-sum slot in the gather buffers (K-major or, L.mn, MN-major)
+size_t slot_u(const Layer& L) { return L.mn ? (size_t)(L.K * L.M) : (size_t)(L.M * L.ldk); }
+size_t slot_v(const Layer& L) { return L.mn ? (size_t)(L.K * L.N) : (size_t)(L.N * L.ldk); }
+size_t slot_b(const Layer& L) { return L.mn ? 0 : (size_t)L.M; }
+
 // the gather set the next sync of this layer packs into (always 0 without SSP)
 int next_set(poseidon_ctx_t c, const Layer& L) { return c->ssp ? (int)(L.nsync % (c->stale + 1)) : 0; }
 
@@ -430,7 +439,7 @@ poseidon_status_t sfb_comm(poseidon_ctx_t c, Layer& L, int set, EvSet& e, cudaEv
   FZ(c->comm_stream);
   CU_TRY(evrec(c, e.start, c->comm_stream));
   e.g_eff = e.start;
-  const size_t ucount = (size_t)(L.M * L.ldk), vfull = (size_t)(L.N * L.ldk), bcount = (size_t)L.M;
+  const size_t ucount = slot_u(L), vfull = slot_v(L), bcount = slot_b(L);
   const size_t vcount = L.v_posted ? 0 : vfull;   // early V: already broadcast during the forward pass
   const uint64_t per = (uint64_t)(ucount + vcount + bcount) * 4u;
   if (L.bcast) {
@@ -449,7 +458,8 @@ poseidon_status_t sfb_comm(poseidon_ctx_t c, Layer& L, int set, EvSet& e, cudaEv
     NC_TRY(ncclAllGather(g.U + (size_t)c->rank * ucount, g.U, ucount, ncclFloat32, c->comm, c->comm_stream));
     if (vcount)
       NC_TRY(ncclAllGather(g.V + (size_t)c->rank * vcount, g.V, vcount, ncclFloat32, c->comm, c->comm_stream));
-    NC_TRY(ncclAllGather(g.B + (size_t)c->rank * bcount, g.B, bcount, ncclFloat32, c->comm, c->comm_stream));
+    if (bcount)
+      NC_TRY(ncclAllGather(g.B + (size_t)c->rank * bcount, g.B, bcount, ncclFloat32, c->comm, c->comm_stream));
     NC_TRY(ncclGroupEnd());
     r.sent += per;  // handed to NCCL once; NCCL forwards it to P-1 peers
   }
@@ -484,6 +494,19 @@ poseidon_status_t sfb_update(poseidon_ctx_t c, Layer& L, int set, float* W, floa
   const bool mom = (L.vel != nullptr);
   bool bias_done = false;   // K1 updates the bias with otherwise idle lanes (no extra launch)
   bool fused_mom = false;
+  if (L.mn) {
+    // MN-major gather (round 2): K1 on the factors as the layers wrote them; bias sums from Ug on idle lanes
+    const K1Momentum km{L.vel, L.vel_b, L.mu, lr, L.wd};
+    err = launch_recon_tcgen05_mn(g.U, L.M, L.K * L.M, g.V, L.N, L.K * L.N, P, L.K, L.M, L.N, W,
+                                  mom ? lr / (float)P : alpha, 1.0f, c->recon_stream, nullptr, bias, &bias_done,
+                                  mom ? &km : nullptr, /*bias_from_u=*/true);
+    if (err != cudaSuccess) return cuda_fail(err, "MN-major reconstruct+sgd launch");
+    if (bias && !bias_done) return fail(POSEIDON_ERR_STATE, "MN-major sync: bias not fused");
+    dst.ke_eff = dst.done;
+    if ((err = debug_sync(c->recon_stream, "K1 MN")) != cudaSuccess) return cuda_fail(err, "K1 MN");
+    CU_TRY(evrec(c, dst.done, c->recon_stream));
+    return POSEIDON_OK;
+  }
   if (mom && L.recon == POSEIDON_RECON_TF32 && recon_tcgen05_supported(g.U, g.V, L.ldk, L.M, L.N, W)) {
     // f4 fused into K1's epilogue: W and its velocity streamed once, v' = mu v + (lr/P) acc + lr wd w,
     // w' = w - v' (16 B / element); the bias likewise on idle lanes
@@ -934,14 +957,22 @@ poseidon_status_t pack_sfb(poseidon_ctx_t c, Layer& L, const float* U, int64_t l
                            cudaStream_t producer) {
   const bool round = (L.recon == POSEIDON_RECON_TF32);
   const GatherSet g = gather_set(L, next_set(c, L));
-  float* u_slot = g.U + (size_t)c->rank * L.M * L.ldk;
-  float* v_slot = g.V + (size_t)c->rank * L.N * L.ldk;
+  float* u_slot = g.U + (size_t)c->rank * slot_u(L);
+  float* v_slot = g.V + (size_t)c->rank * slot_v(L);
   float* b_slot = g.B + (size_t)c->rank * L.M;
   // U (+ bias column sums) and, unless the early input broadcast already packed it, V: one launch
   EvSet& e = L.ev[c->iter % RING];
   CU_TRY(evrec(c, e.pstart, producer));
   e.packed = true;
   e.pack_async = false;
+  if (L.mn) {   // MN-major gather: the slot is the layer's own [K x M] / [K x N] rows, copied by the copy engine
+    CU_TRY(cudaMemcpy2DAsync(u_slot, (size_t)L.M * 4, U, (size_t)ldU * 4, (size_t)L.M * 4, (size_t)L.K,
+                             cudaMemcpyDeviceToDevice, producer));
+    if (!L.v_posted)
+      CU_TRY(cudaMemcpy2DAsync(v_slot, (size_t)L.N * 4, V, (size_t)ldV * 4, (size_t)L.N * 4, (size_t)L.K,
+                               cudaMemcpyDeviceToDevice, producer));
+    return POSEIDON_OK;
+  }
   cudaError_t err = launch_pack_uv(U, ldU, u_slot, L.M, b_slot, L.v_posted ? nullptr : V, ldV, v_slot, L.N,
                                    L.ldk, L.K, round, producer);
   if (err != cudaSuccess) return cuda_fail(err, "pack U/V launch");
@@ -1164,6 +1195,9 @@ poseidon_status_t poseidon_register_layer(poseidon_ctx_t c, int32_t id, int32_t 
   }
   if (scheme != POSEIDON_SCHEME_PS) {
     L.ldk = round_up(K, 4);
+    L.mn = scheme == POSEIDON_SCHEME_SFB && c->world > 1 && !c->ssp && !(c->flags & POSEIDON_FLAG_DWBP_OFF) &&
+           (c->flags & POSEIDON_FLAG_INPLACE_FACTORS) && (c->flags & POSEIDON_FLAG_INPLACE_MN) && M % 4 == 0 &&
+           N % 4 == 0 && M < (1 << 30) && N < (1 << 30);
     const size_t P = (size_t)c->world;
     const size_t ub = P * (size_t)(M * L.ldk) * 4, vb = P * (size_t)(N * L.ldk) * 4, bb = P * (size_t)M * 4;
     const int nsets = c->ssp ? c->stale + 1 : 1;
@@ -1584,13 +1618,17 @@ poseidon_status_t poseidon_set_recon(poseidon_ctx_t c, int32_t id, int32_t recon
   if (st) return st;
   if (recon != POSEIDON_RECON_TF32 && recon != POSEIDON_RECON_FP32) return fail(POSEIDON_ERR_INVALID_ARG, "bad recon");
   if (id == -1) {
-    for (auto& L : c->layers) L.recon = recon;
+    for (auto& L : c->layers) {
+      L.recon = recon;
+      if (recon == POSEIDON_RECON_FP32) L.mn = false;
+    }
     return POSEIDON_OK;
   }
   Layer* L;
   st = check_layer(c, id, &L);
   if (st) return st;
   L->recon = recon;
+  if (recon == POSEIDON_RECON_FP32) L->mn = false;   // K1r reads the K-major layout (same buffer sizes)
   return POSEIDON_OK;
 }
 
@@ -1639,14 +1677,16 @@ poseidon_status_t poseidon_sfb_post_input(poseidon_ctx_t c, int32_t id, const fl
   if (st) return st;
   const int P = c->world;
   const bool round = (L->recon == POSEIDON_RECON_TF32);
-  float* v_slot = L->Vg + (size_t)c->rank * L->N * L->ldk;
-  cudaError_t err = launch_pack_t(V, ldV, v_slot, L->ldk, L->K, L->N, round, nullptr, ps);
+  float* v_slot = L->Vg + (size_t)c->rank * slot_v(*L);
+  cudaError_t err = L->mn ? cudaMemcpy2DAsync(v_slot, (size_t)L->N * 4, V, (size_t)ldV * 4, (size_t)L->N * 4,
+                                              (size_t)L->K, cudaMemcpyDeviceToDevice, ps)
+                          : launch_pack_t(V, ldV, v_slot, L->ldk, L->K, L->N, round, nullptr, ps);
   if (err != cudaSuccess) return cuda_fail(err, "pack V launch");
   EvSet& e = L->ev[c->iter % RING];
   CU_TRY(evrec(c, e.vready, ps));
   if (P > 1) {
     IterRecord& r = open_record(c);
-    const size_t vcount = (size_t)(L->N * L->ldk);
+    const size_t vcount = slot_v(*L);
     CU_TRY(evwait(c, c->comm_stream, e.vready));
     FZ(c->comm_stream);
     if (L->bcast) {

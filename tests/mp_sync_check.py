@@ -61,13 +61,30 @@ def allsame(t):
     return all(torch.equal(parts[0], p) for p in parts[1:])
 
 
+def wire_bytes(shapes, flags):
+    """Bytes one rank hands to the factor exchange of one iteration: K-major slots (M, N padded to ldk) plus the
+    bias sums, or, with FLAG_INPLACE_MN on layers with M, N multiples of 4, the MN-major slots K x (M + N)."""
+    mn = (flags & pz.FLAG_INPLACE_FACTORS) and (flags & pz.FLAG_INPLACE_MN)
+    out = 0
+    for _, M_, N_, K_ in shapes:
+        if mn and M_ % 4 == 0 and N_ % 4 == 0:
+            out += K_ * (M_ + N_) * 4
+        else:
+            ldk = (K_ + 3) // 4 * 4
+            out += (M_ * ldk + N_ * ldk + M_) * 4
+    return out
+
+
 def sfb_wire_checks(new_ctx, rank, P, dev):
     # ---- 1b. SFB on symmetric buffers: NCCL all-gather (SYMM_SFB) and the NVLS multicast broadcast
     #          (NVLS_SFB); odd M (bias slot not a multiple of 4), ldk padding, 3 iterations in a row
     #          (the broadcast's entry barrier guards the gather buffers the previous K1 read) ----
     # (+ FLAG_INPLACE_FACTORS: the pack reads U / V in place on the comm stream; the caller keeps them alive)
+    # (+ FLAG_INPLACE_MN: MN-major gather layout, copy-engine slot fill, K1 on MN-major operands, bias sums in
+    #  K1 -- for the layers with M, N multiples of 4; the 10 x 64 layer keeps the pack)
+    mnf = pz.FLAG_INPLACE_FACTORS | pz.FLAG_INPLACE_MN
     for flags in (pz.FLAG_SYMM_SFB, pz.FLAG_NVLS_SFB, pz.FLAG_NVLS_SFB | pz.FLAG_INPLACE_FACTORS,
-                  pz.FLAG_INPLACE_FACTORS):
+                  pz.FLAG_INPLACE_FACTORS, pz.FLAG_NVLS_SFB | mnf, mnf):
         cs = new_ctx(flags)
         shapes = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 1000, 4096, 33)]
         for lid, M_, N_, K_ in shapes:
@@ -89,9 +106,7 @@ def sfb_wire_checks(new_ctx, rank, P, dev):
                 assert np.array_equal(bd.cpu().numpy().astype(np.float64), b1)
                 assert allsame(Wd) and allsame(bd)
             st = cs.iteration_end(stats=True)
-            ldks = [(K_ + 3) // 4 * 4 for _, _, _, K_ in shapes]
-            per = sum((M_ * l + N_ * l + M_) * 4 for (_, M_, N_, _), l in zip(shapes, ldks))
-            assert st["nccl_bytes_recv"] == per * (P - 1), st
+            assert st["nccl_bytes_recv"] == wire_bytes(shapes, flags) * (P - 1), st
         cs.close()
 
 
@@ -100,7 +115,8 @@ def early_v_checks(new_ctx, rank, P, dev):
     #          argument is garbage here); NCCL and broadcast-kernel wires; integer bit-exact vs O4, two
     #          iterations, and the same NCCL byte total as the plain sync ----
     for flags in (pz.FLAG_EARLY_V, pz.FLAG_EARLY_V | pz.FLAG_NVLS_SFB,
-                  pz.FLAG_EARLY_V | pz.FLAG_NVLS_SFB | pz.FLAG_INPLACE_FACTORS):
+                  pz.FLAG_EARLY_V | pz.FLAG_NVLS_SFB | pz.FLAG_INPLACE_FACTORS,
+                  pz.FLAG_EARLY_V | pz.FLAG_NVLS_SFB | pz.FLAG_INPLACE_FACTORS | pz.FLAG_INPLACE_MN):
         ce = new_ctx(flags)
         keep = []   # FLAG_INPLACE_FACTORS: the factors stay alive until the syncs are done
         shapes = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 1000, 4096, 33)]
@@ -130,9 +146,7 @@ def early_v_checks(new_ctx, rank, P, dev):
                 assert np.array_equal(Wd.cpu().numpy().astype(np.float64), W1), f"early V flags={flags} lid={lid}"
                 assert np.array_equal(bd.cpu().numpy().astype(np.float64), b1)
                 assert allsame(Wd) and allsame(bd)
-            ldks = [(K_ + 3) // 4 * 4 for _, _, _, K_ in shapes]
-            per = sum((M_ * l + N_ * l + M_) * 4 for (_, M_, N_, _), l in zip(shapes, ldks))
-            assert st["nccl_bytes_recv"] == per * (P - 1), st
+            assert st["nccl_bytes_recv"] == wire_bytes(shapes, flags) * (P - 1), st
         ce.close()
 
 
