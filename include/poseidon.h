@@ -114,11 +114,14 @@ typedef struct {
                                          sync (what the glue does).  (A torch caller could also record_stream the
                                          tensors on both poseidon_stream()s, but the caching allocator then defers
                                          and re-allocates blocks: measured step collapses.) */
-#define POSEIDON_FLAG_INPLACE_MN 0x200u /* with POSEIDON_FLAG_INPLACE_FACTORS, at world == 1 (TF32, 16-B aligned U / V,
-                                         M and N multiples of 4): no pack at all, K1 consumes U and V MN-major and
-                                         forms the bias sums itself; the tensor core then reads the fp32 factors as
-                                         TF32 (13 low mantissa bits dropped) instead of the pack's RN rounding
-                                         (reading Z12'). */
+#define POSEIDON_FLAG_INPLACE_MN 0x200u /* with POSEIDON_FLAG_INPLACE_FACTORS, for SFB layers with M and N multiples
+                                         of 4 (TF32): no K3 pack.  At world == 1 (16-B aligned U / V) K1 consumes U
+                                         and V MN-major where they are; at world > 1 the gather buffers are
+                                         MN-major [P][K][M] / [P][K][N], this rank's slot is filled by a
+                                         copy-engine memcpy and K1 reads them MN-major.  K1 forms the bias sums
+                                         itself; the tensor core reads the fp32 factors as TF32 (13 low mantissa
+                                         bits dropped) instead of the pack's RN rounding (reading Z12').  Set at
+                                         init; a layer switched to POSEIDON_RECON_FP32 keeps the K-major pack. */
 
 typedef struct poseidon_ctx* poseidon_ctx_t;
 
