@@ -76,6 +76,31 @@ def test_null_context_errors():
     assert B.lib.poseidon_finalize(None) == B.OK
 
 
+def test_round2_entry_points_error_paths():
+    """Host-side argument checks of the round-2 entry points (no CUDA call is reached on these paths)."""
+    import ctypes
+    assert B.lib.poseidon_set_staleness(None, 2) == B.ERR_NOT_INITIALIZED
+    assert B.lib.poseidon_stream(None, 0) is None
+    assert B.lib.poseidon_stream(None, 1) is None
+    fake = ctypes.c_void_p(0x1000)
+    f = B.lib.poseidon_reconstruct_sgd_mn
+    # NULL operand, P < 1, K < 0, M/N <= 0, ldu < M, ldv < N: all INVALID_ARG before any launch
+    bad = [
+        (None, 64, 0, fake, 64, 0, 1, 8, 64, 64, fake),
+        (fake, 64, 0, fake, 64, 0, 0, 8, 64, 64, fake),
+        (fake, 64, 0, fake, 64, 0, 1, -1, 64, 64, fake),
+        (fake, 64, 0, fake, 64, 0, 1, 8, 0, 64, fake),
+        (fake, 32, 0, fake, 64, 0, 1, 8, 64, 64, fake),
+        (fake, 64, 0, fake, 32, 0, 1, 8, 64, 64, fake),
+        (fake, 64, 0, fake, 64, 0, 1, 8, 64, 64, None),
+    ]
+    for a in bad:
+        assert f(*a, ctypes.c_float(-1e-3), None) == B.ERR_INVALID_ARG, a
+        assert "reconstruct_sgd_mn" in B.last_error()
+    # K == 0 is a no-op (nothing to reconstruct), accepted without touching the device
+    assert f(fake, 64, 0, fake, 64, 0, 1, 0, 64, 64, fake, ctypes.c_float(-1e-3), None) == B.OK
+
+
 def test_struct_layouts_match_header():
     import ctypes
     assert ctypes.sizeof(B.Topology) == 4 * 3 + 128 + 4
