@@ -4,7 +4,8 @@ iteration_end.  A replayed step must compute exactly what an eager step computes
 every reduction; cuDNN deterministic), and the statistics read after a replay must describe that replay.
 
   * CIFAR-quick (C2 model, PS layers through K2), and the same net with its FC layers on SFB (K1; with and
-    without POSEIDON_FLAG_INPLACE_FACTORS): 4 eager steps == 2 eager + 2 replays, bit for bit;
+    without POSEIDON_FLAG_INPLACE_FACTORS, and with momentum + weight decay fused into K1 / K2):
+    4 eager steps == 2 eager + 2 replays, bit for bit;
   * after a replay: every layer's sync has a positive duration, starts after its ready event, and DWBP still
     overlaps the backward (every layer above the first starts its sync before the backward ends).
 """
@@ -29,7 +30,7 @@ def _batches(dev, n):
                                                                                    generator=g)) for _ in range(n)]
 
 
-def _run(pz, scheme, flags, graph):
+def _run(pz, scheme, flags, graph, mom=False):
     import torch.nn.functional as F
     from paper_1512_06216_b200.dwbp import PoseidonSync
     from drivers.cnn import CifarQuick
@@ -41,6 +42,8 @@ def _run(pz, scheme, flags, graph):
     torch.manual_seed(6216)
     model = CifarQuick().to(dev)
     sync = PoseidonSync(model, ctx, K=100, lr=0.05, scheme=scheme)
+    if mom:   # f4: velocities live in the library; the fused-momentum K1 / K2 variants are captured
+        ctx.set_momentum(0.9, 5e-4)
     data = _batches(dev, 4)
     x = torch.empty_like(data[0][0])
     y = torch.empty_like(data[0][1])
@@ -79,11 +82,12 @@ def _run(pz, scheme, flags, graph):
     return flat, stats
 
 
-@pytest.mark.parametrize("scheme,flags", [("ps", 0), ("auto", 0), ("auto", "inplace")])
+@pytest.mark.parametrize("scheme,flags", [("ps", 0), ("auto", 0), ("auto", "inplace"), ("auto", "momentum")])
 def test_graph_replay_equals_eager(pz, scheme, flags):
-    fl = (pz.FLAG_INPLACE_FACTORS | pz.FLAG_INPLACE_MN) if flags == "inplace" else flags
-    w_eager, _ = _run(pz, scheme, fl, False)
-    w_graph, stats = _run(pz, scheme, fl, True)
+    fl = (pz.FLAG_INPLACE_FACTORS | pz.FLAG_INPLACE_MN) if flags == "inplace" else 0
+    mom = flags == "momentum"
+    w_eager, _ = _run(pz, scheme, fl, False, mom)
+    w_graph, stats = _run(pz, scheme, fl, True, mom)
     assert torch.equal(w_eager, w_graph)
     it = stats.pop("_iter")
     assert it["n_layers"] == len(stats) and it["sync_total_ms"] > 0
