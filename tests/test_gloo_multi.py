@@ -1,4 +1,4 @@
-"""World-size-2 CPU (gloo) tests of the N>1 host logic: NCCL-id broadcast as
+"""World-size-2 and -3 CPU (gloo) tests of the N>1 host logic: NCCL-id broadcast as
 bench.py does it, cross-rank agreement of the library's host decisions (SACP
 rule, shard map), and the exchange protocols' data layouts (rank-major
 all-gather of SFB factors; reduce-scatter / shard update / all-gather of PS;
@@ -139,8 +139,8 @@ def _worker(rank, world, port, q):
         q.put((rank, "".join(traceback.format_exception(ex))))
 
 
-def test_gloo_world2_host_logic_and_protocols():
-    world = 2
+@pytest.mark.parametrize("world", [2, 3])   # 3: ragged shard maps (padded / P not a multiple of the 4-float unit)
+def test_gloo_host_logic_and_protocols(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
