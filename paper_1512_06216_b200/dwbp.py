@@ -13,10 +13,11 @@ Every parameterised layer of a model becomes a Poseidon layer:
   post-accumulate-grad hook once all of the layer's gradients have landed.
 * A forward pre-hook makes the next forward of layer i wait for layer i's sync
   (``poseidon_wait_layer``): the only synchronisation DWBP needs.
-* With ``FLAG_SSP1`` (staleness 1) the library applies a layer's update one hook
-  later; PS gradients then alternate between two arena buffers, so the
-  parameters' ``.grad`` views are re-pointed after every iteration, and
-  ``flush()`` applies the last deferred updates.
+* With ``FLAG_SSP1`` (staleness s = 1, or 1..5 via ``Context.set_staleness``)
+  the library applies a layer's update s hooks later; PS gradients then rotate
+  through s + 1 arena buffers, so the parameters' ``.grad`` views are
+  re-pointed after every iteration, and ``flush()`` applies the deferred
+  updates.
 
 All arithmetic of the sync happens in the library; this module only moves
 pointers and streams.  The optimiser step IS the sync (SGD applied by K1/K2),
@@ -269,8 +270,8 @@ class PoseidonSync:
     def iteration_end(self, stats: bool = False):
         out = self.ctx.iteration_end(torch.cuda.current_stream(), stats=stats)
         if self.ssp:
-            # the next backward accumulates into the other gradient buffer (zeroed by the library
-            # before the next forward of the layer may start: poseidon_wait_layer orders it)
+            # the next backward accumulates into the next of the s + 1 gradient buffers (zeroed by the
+            # library before the next forward of the layer may start: poseidon_wait_layer orders it)
             for plan in self.plans:
                 if plan.scheme == B.SCHEME_PS:
                     gptr = self.ctx.ps_layer_buffers(plan.layer_id)[0]
@@ -279,8 +280,8 @@ class PoseidonSync:
         return out
 
     def flush(self, stream=None):
-        """SSP: apply the deferred updates of the last iteration on every rank, then order the
-        stream after them (no-op for BSP)."""
+        """SSP: apply every deferred update (the last s iterations' syncs) on every rank, then order
+        the stream after them (no-op for BSP)."""
         s = stream or torch.cuda.current_stream()
         self.ctx.flush(s)
         self.wait_all(s)
