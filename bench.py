@@ -135,7 +135,7 @@ METRIC = "images/sec (exposed sync ms/iter and % of roofline alongside)"
 
 def workload_config(args, cfg, world):
     """The `config` object both arms print (identical for the driver's ratio)."""
-    consistency = "" if not getattr(args, "ssp", 0) else ", SSP staleness 1"
+    consistency = "" if not getattr(args, "ssp", 0) else f", SSP staleness {args.ssp}"
     return {"workload": f"{args.config} {cfg['name']} data-parallel training step with Poseidon sync "
                         f"(SACP + DWBP{consistency}), synthetic data",
             "global_batch": world * cfg["batch"], "per_gpu_batch": cfg["batch"],

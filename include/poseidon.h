@@ -98,7 +98,8 @@ typedef struct {
                                          layer's hook of iteration t+1, after that backward has read W, so
                                          forward t+1 reads every update of iterations <= t-1.  Gradient and
                                          factor buffers are double-buffered; PS layers need the arena.
-                                         Incompatible with POSEIDON_FLAG_DWBP_OFF. */
+                                         s = 2..5: poseidon_set_staleness (s + 1 buffer sets, update of t
+                                         applied at hook t+s).  Incompatible with POSEIDON_FLAG_DWBP_OFF. */
 #define POSEIDON_FLAG_SFPS 0x40u       /* FC layers the rule sends to the server (Alg. 3 else-branch) run as
                                          sharded SF-PS (POSEIDON_SCHEME_SFPS) instead of full-gradient PS.
                                          Not combined with POSEIDON_FLAG_SSP1. */
