@@ -901,11 +901,12 @@ poseidon_status_t ps_update_local(poseidon_ctx_t c, Layer& L, float* grad, float
   return POSEIDON_OK;
 }
 
-// SSP s = 1 (reading Z19): this hook issues sync t's communication and applies the update of sync
-// t-1 — after this layer's backward t has finished reading W (e.ready) — so the forward of t+1 reads
-// W with every update of iterations <= t-1 (P:L123 with s = 1, at the staleness bound).  The update
-// is local (SFB: K1 on the gathered factors; PS: the all-reduced gradient), so a rank's next forward
-// waits for the other ranks' hook t-1, not hook t: one iteration of slack.
+// SSP with staleness s (reading Z19; s = 1 by FLAG_SSP1, 2..5 by poseidon_set_staleness): this hook issues
+// sync t's communication into gather / gradient set t mod (s+1) and applies the update of sync t-s —
+// after this layer's backward t has finished reading W (e.ready) — so the forward of t+1 reads W with every
+// update of iterations <= t-s (at the staleness bound).  The update is local (SFB: K1 on the
+// gathered factors; PS: the all-reduced gradient), so a rank's next forward waits for the other ranks'
+// hook t-s, not hook t: s iterations of slack.
 poseidon_status_t ssp_hook(poseidon_ctx_t c, int32_t id, Layer& L, float* W, float* bias, float* grad, float lr) {
   EvSet& e = L.ev[c->iter % RING];
   IterRecord& r = open_record(c);
