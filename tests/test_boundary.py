@@ -191,3 +191,18 @@ def test_binding_refuses_buffers_the_abi_would_misread():
         Bn._ptr(t.t())
     with pytest.raises(TypeError):
         Bn._ptr(torch.zeros(4, dtype=torch.float64))
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without libposeidon.so the package refuses to import (the product path never routes
+    through the oracle or PyTorch ops)."""
+    import shutil
+    import subprocess
+    import sys
+    src = os.path.join(ROOT, "paper_1512_06216_b200")
+    dst = tmp_path / "paper_1512_06216_b200"
+    shutil.copytree(src, dst, ignore=shutil.ignore_patterns("*.so", "csrc", "__pycache__", "build"))
+    assert not list(dst.glob("*.so"))
+    out = subprocess.run([sys.executable, "-c", "import paper_1512_06216_b200"], cwd=tmp_path,
+                         capture_output=True, text=True, timeout=120)
+    assert out.returncode != 0 and "libposeidon.so is missing" in out.stderr, out.stderr[-1500:]
