@@ -151,7 +151,9 @@ typedef struct {
 
 /* ======================= the five named entry points ======================= */
 
-/* Create a context for this process's GPU.  world must equal topo->world.
+/* Create a context for this process's GPU: one of the paper's P workers ("in a distributed setting with P
+ * workers"; Alg. 2 "at iteration t on worker p"), one process per GPU.  world must equal
+ * topo->world.
  * world > 1 creates an NCCL communicator from topo->nccl_id (collective over
  * all ranks) and requires single-node all-pairs peer access between the GPUs
  * the ranks actually use (their PCI bus ids are all-gathered through the new
@@ -210,8 +212,9 @@ poseidon_status_t poseidon_sync_ps(poseidon_ctx_t ctx, int32_t layer_id, float* 
  * POSEIDON_FLAG_DWBP_OFF). */
 poseidon_status_t poseidon_backprop_hook(poseidon_ctx_t ctx, int32_t layer_id, poseidon_stream_t stream);
 
-/* Early input broadcast (POSEIDON_FLAG_EARLY_V; DWBP's "communicate as soon as the data exists" applied to
- * the sufficient factors): V, the layer input a_i of Eq. 5 (K x N, row stride ldV >= N, device), is final
+/* Early input broadcast (POSEIDON_FLAG_EARLY_V; DWBP's "start its communication once its gradients are
+ * generated", applied to the half of the sufficient factors that exists before the backward): V, the
+ * layer input a_i of Eq. 5 (K x N, row stride ldV >= N, device), is final
  * once the forward pass has produced it, so it is packed into this rank's slot on `stream` and its
  * broadcast (all-gather / broadcast kernel, whichever wire the layer uses) starts on the comm stream right
  * away, overlapping the rest of the forward and the backward.  The layer's next sync (sync_fc_sfb or
@@ -224,8 +227,8 @@ poseidon_status_t poseidon_sfb_post_input(poseidon_ctx_t ctx, int32_t layer_id, 
 /* Hardware figures for the measured-cost model (GB/s, TFLOP/s, microseconds). */
 typedef struct {
   double nvlink_gbps;           /* per-direction peer bandwidth, e.g. 770 (measured peer copy) */
-  double hbm_gbps;              /* e.g. 6543.7 (MEASURED_PEAKS.json) */
-  double tensor_tflops;         /* TF32 dense, e.g. 669.6 (sustained) */
+  double hbm_gbps;              /* e.g. 6543.7 (round-1 MEASURED_PEAKS.json; the binding's default) */
+  double tensor_tflops;         /* TF32 dense, e.g. 669.6 (round-1 sustained; the binding's default) */
   double collective_latency_us; /* per collective launch + sync, e.g. 10 */
 } poseidon_hw_t;
 
@@ -249,13 +252,16 @@ int32_t poseidon_choose_scheme_model3(int32_t kind, int64_t M, int64_t N, int64_
 /* ncclGetUniqueId into out[128] (call on rank 0 only). */
 poseidon_status_t poseidon_get_unique_id(uint8_t out[128]);
 
-/* Shard map (reading Z11): S = 32*ceil(n/(32P)), padded_n = P*S, rank r owns
+/* Shard map of the PS path (Alg. 1: the master "updates the part of model parameters for which a
+ * corresponding gradient is received"; one shard per rank, reading Z11): S = 32*ceil(n/(32P)),
+ * padded_n = P*S, rank r owns
  * [min(rS,n), min((r+1)S,n)) (possibly empty).  Pure host code. */
 poseidon_status_t poseidon_shard_range(int64_t n, int32_t P, int32_t rank, int64_t* begin,
                                        int64_t* end, int64_t* padded_n);
 
 /* Register layer `layer_id` (0 <= id < 4096): kind, M x N weight, per-worker
- * batch K, has_bias.  scheme_override: -1 -> SACP rule, else the scheme to use
+ * batch K, has_bias; the SACP decision of Alg. 3 is taken here, once
+ * per layer.  scheme_override: -1 -> SACP rule, else the scheme to use
  * (C2 forces PS; 2 = SF-PS, FC only).  chosen_scheme may be NULL.  With
  * POSEIDON_FLAG_SFPS an FC layer the rule sends to PS is registered as SF-PS.
  * SFB and SF-PS layers get library-owned
@@ -306,7 +312,7 @@ poseidon_status_t poseidon_ps_arena(poseidon_ctx_t ctx, int32_t* nvls_active);
  * stays unbucketed.  Members' stats report the bucket's sync.  0 (default) disables bucketing. */
 poseidon_status_t poseidon_set_ps_buckets(poseidon_ctx_t ctx, int64_t bucket_bytes);
 /* A PS layer's arena segments: *grad = the gradient buffer the layer's NEXT sync reduces (with
- * POSEIDON_FLAG_SSP1 two buffers alternate: re-point the parameters' gradients after every
+ * POSEIDON_FLAG_SSP1 the s + 1 buffers rotate: re-point the parameters' gradients after every
  * iteration), *W = its parameters, *padded_n = segment length in floats. */
 poseidon_status_t poseidon_ps_layer_buffers(poseidon_ctx_t ctx, int32_t layer_id, float** grad, float** W,
                                             int64_t* padded_n);
@@ -324,7 +330,8 @@ poseidon_stream_t poseidon_stream(poseidon_ctx_t ctx, int32_t which);
 /* Human-readable state of the fused NVLS PS path ("active", "not requested", or the NCCL error). */
 const char* poseidon_nvls_status(poseidon_ctx_t ctx);
 
-/* lr used by poseidon_backprop_hook from the next hook on (sync_* take theirs as an argument).
+/* lr (the stepsize epsilon of Eq. 3) used by poseidon_backprop_hook from the next hook on
+ * (sync_* take theirs as an argument).
  * ERR_NOT_INITIALIZED for a NULL context. */
 poseidon_status_t poseidon_set_lr(poseidon_ctx_t ctx, float lr);
 
@@ -342,7 +349,7 @@ poseidon_status_t poseidon_set_momentum(poseidon_ctx_t ctx, int32_t layer_id, fl
  * packing).  Errors: ERR_INVALID_ARG (bad recon), ERR_STATE (unregistered layer). */
 poseidon_status_t poseidon_set_recon(poseidon_ctx_t ctx, int32_t layer_id /* -1: all */, int32_t recon);
 
-/* SSP (POSEIDON_FLAG_SSP1): apply every layer's deferred update now (in layer-id order, identical on
+/* SSP (POSEIDON_FLAG_SSP1, P:L123, P:L399-402): apply every layer's deferred update now (in layer-id order, identical on
  * every rank: collective).  Call it on all ranks after the last iteration (and before reading the
  * parameters); afterwards poseidon_wait_layer orders a consumer after the updates.  The flush is an
  * iteration record of its own: it closes and advances the iteration counter (its statistics are
@@ -358,10 +365,11 @@ poseidon_status_t poseidon_flush(poseidon_ctx_t ctx, poseidon_stream_t stream);
 poseidon_status_t poseidon_set_staleness(poseidon_ctx_t ctx, int32_t s);
 
 /* Next-forward barrier: `consumer` waits until layer_id's latest sync is done
- * (under DWBP_OFF: until every layer's sync of the last iteration is done). */
+ * (under DWBP_OFF: until every layer's sync of the last iteration is done).  DWBP "allows partial
+ * parameter updating on the layer": the next forward of layer i waits for layer i's sync only. */
 poseidon_status_t poseidon_wait_layer(poseidon_ctx_t ctx, int32_t layer_id, poseidon_stream_t consumer);
 
-/* Mark the end of backward on `compute` (records bwd_end; under DWBP_OFF
+/* Mark the end of backward on `compute` (the end of Alg. 2's loop over layers; records bwd_end; under DWBP_OFF
  * launches the deferred syncs), close the iteration and, if out != NULL,
  * block until its syncs are done and fill the statistics.
  * CUDA graphs (round 2): a whole training step may be captured by stream capture on the caller's stream
@@ -395,7 +403,7 @@ int32_t poseidon_version(void);
  * way the all-gather leaves it, so multi-worker arithmetic is exercised on
  * one GPU.  No context needed. */
 
-/* SFB with P_sim simulated workers on one GPU: U_all [P_sim*K x M] and
+/* SFB (P:L328-331 steps (1)-(3), Alg. 3 lines 6-8) with P_sim simulated workers on one GPU: U_all [P_sim*K x M] and
  * V_all [P_sim*K x N] (worker p = rows [pK,(p+1)K)), W [M x N], bias [M]|NULL.
  * Packs each worker block (K3, column sums, rounding for TF32) into scratch
  * gather buffers, then runs the reconstruction (K1 or K1r) and the bias
@@ -404,20 +412,21 @@ poseidon_status_t poseidon_sfb_simulated(const float* U_all, const float* V_all,
                                          int64_t K, int64_t M, int64_t N, float* W, float* bias,
                                          float lr, int32_t recon, poseidon_stream_t stream);
 
-/* PS with P_sim simulated workers: grads [P_sim x padded_n] (padded flat
+/* PS (Alg. 1 master P:L208-211, Alg. 3 lines 1-3) with P_sim simulated workers: grads [P_sim x padded_n] (padded flat
  * buffers), W [padded_n].  For every shard r of the map, W[b_r,e_r) +=
  * alpha * sum_p grads[p][b_r,e_r) summed in worker order (the fused
  * reduce + K2 a single GPU can do for all shards), alpha = -lr / P_sim. */
 poseidon_status_t poseidon_ps_simulated(const float* grads, int32_t P_sim, float* W, int64_t n,
                                         float lr, poseidon_stream_t stream);
 
-/* K2 alone: W[i] = fmaf(alpha, g[i], W[i]) for i in [0,count); if stats !=
+/* K2 alone (the master's update of its part of the parameters, Alg. 1):
+ * W[i] = fmaf(alpha, g[i], W[i]) for i in [0,count); if stats !=
  * NULL (2 floats, device, caller-zeroed) accumulates sum((alpha g)^2) and the
  * count of non-finite updates via warp-shuffle reductions. */
 poseidon_status_t poseidon_ps_shard_update(const float* g, float* W, int64_t count, float alpha,
                                            float* stats, poseidon_stream_t stream);
 
-/* Reconstruction alone (K1 / K1r) on already-gathered, already-rounded
+/* Reconstruction alone (K1 / K1r; SFB step (3), Alg. 3 line 8) on already-gathered, already-rounded
  * buffers in the gather layout: W[M x N] += alpha * sum_p sum_k<K
  * Ug[p][m][k] Vg[p][n][k], Ug [P][M][ldk], Vg [P][N][ldk], ldk >= K.  The
  * TF32 path needs ldk and N multiples of 4 and 16-byte aligned buffers. */
