@@ -56,7 +56,7 @@ def cost_full_ps(M: int, N: int, K: int, P: int) -> int:
 
 
 def costs(M: int, N: int, K: int, P: int) -> Tuple[int, int, int]:
-    """(C_sfb, C_sf_ps, C_full) as exact Python integers."""
+    """(C_sfb, C_sf_ps, C_full) of P:L333 / P:L335 as exact Python integers."""
     return cost_sfb(M, N, K, P), cost_sf_ps(M, N, K, P), cost_full_ps(M, N, K, P)
 
 
@@ -76,12 +76,15 @@ def choose_scheme(kind: int, M: int, N: int, K: int, P: int) -> int:
 # single "master node" P:L207-212)
 # --------------------------------------------------------------------------
 def shard_size(n: int, P: int) -> int:
-    """S(n, P) = 32 * ceil(n / (32 P))."""
+    """S(n, P) = 32 * ceil(n / (32 P)): one shard of the PS layer per rank (the master of Alg. 1,
+    P:L208-211, split over the P ranks; reading Z11)."""
     return SHARD_ALIGN * (-(-n // (SHARD_ALIGN * P)))
 
 
 def shard_range(n: int, P: int, rank: int) -> Tuple[int, int, int]:
-    """Rank ``rank`` owns [min(rS, n), min((r+1)S, n)); returns (begin, end, padded_n)."""
+    """Rank ``rank`` owns [min(rS, n), min((r+1)S, n)); returns (begin, end, padded_n) (reading Z11;
+    the master "updates the part of model parameters for which a corresponding gradient is
+    received", P:L210)."""
     S = shard_size(n, P)
     return min(rank * S, n), min((rank + 1) * S, n), P * S
 
@@ -90,18 +93,22 @@ def shard_range(n: int, P: int, rank: int) -> Tuple[int, int, int]:
 # The FC layer + softmax cross-entropy used by the brute-force pins (O3, O7)
 # --------------------------------------------------------------------------
 def fc_forward(W: np.ndarray, b: np.ndarray, X: np.ndarray) -> np.ndarray:
-    """y = W x + b for every row x of X (K x N) -> K x M."""
+    """y = W x + b for every row x of X (K x N) -> K x M: the FC layer of P:L322-324 (W is M x N,
+    E_{i+1} is M-dimensional, a_i N-dimensional)."""
     return X @ W.T + b[None, :]
 
 
 def softmax(z: np.ndarray) -> np.ndarray:
+    """Row-wise softmax: the loss layer on top of the FC layer in the brute-force pins (the paper's
+    models end in a softmax classifier, P:L436 / P:L481)."""
     z = z - z.max(axis=1, keepdims=True)
     e = np.exp(z)
     return e / e.sum(axis=1, keepdims=True)
 
 
 def mean_ce_loss(W: np.ndarray, b: np.ndarray, X: np.ndarray, labels: np.ndarray) -> float:
-    """l = (1/#samples) * sum_samples -log softmax(W x + b)[label]."""
+    """l = (1/#samples) * sum_samples -log softmax(W x + b)[label]: the loss l of Alg. 2,
+    a mean over the batch (reading Z2)."""
     y = fc_forward(W, b, X)
     y = y - y.max(axis=1, keepdims=True)
     logp = y - np.log(np.exp(y).sum(axis=1, keepdims=True))
@@ -110,8 +117,8 @@ def mean_ce_loss(W: np.ndarray, b: np.ndarray, X: np.ndarray, labels: np.ndarray
 
 def error_messages(W: np.ndarray, b: np.ndarray, X: np.ndarray, labels: np.ndarray,
                    denom: int) -> np.ndarray:
-    """Per-sample E_{i+1} = dl/dy for the mean CE loss with ``denom`` samples:
-    (softmax(y) - onehot(label)) / denom  (K x M)."""
+    """Per-sample E_{i+1} = dl/dy (the error message of P:L324) for the mean CE loss with ``denom``
+    samples: (softmax(y) - onehot(label)) / denom  (K x M)."""
     s = softmax(fc_forward(W, b, X))
     s[np.arange(len(labels)), labels] -= 1.0
     return s / float(denom)
@@ -119,8 +126,8 @@ def error_messages(W: np.ndarray, b: np.ndarray, X: np.ndarray, labels: np.ndarr
 
 def fd_gradient(W: np.ndarray, b: np.ndarray, X: np.ndarray, labels: np.ndarray,
                 h: float = 1e-6) -> Tuple[np.ndarray, np.ndarray]:
-    """O3: dl/dW and dl/db by central finite differences, element by element
-    (brute force; for tiny layers only)."""
+    """O3: dl/dW and dl/db by central finite differences, element by element (brute force; for tiny
+    layers only): the gradient that Eq. 5 claims the factors reconstruct exactly."""
     gW = np.zeros_like(W)
     gb = np.zeros_like(b)
     for i in range(W.shape[0]):
@@ -153,7 +160,7 @@ def reconstruct_loops(U: np.ndarray, V: np.ndarray) -> np.ndarray:
 
 
 def reconstruct(U: np.ndarray, V: np.ndarray) -> np.ndarray:
-    """sum_k u_k v_k^T = U^T V (Eq. 5), one library matmul in float64."""
+    """sum_k u_k v_k^T = U^T V (Eq. 5, P:L325), one library matmul in float64."""
     return np.asarray(U, dtype=np.float64).T @ np.asarray(V, dtype=np.float64)
 
 
@@ -162,8 +169,9 @@ def reconstruct(U: np.ndarray, V: np.ndarray) -> np.ndarray:
 # --------------------------------------------------------------------------
 def sync_step(W: np.ndarray, b, Us: Sequence[np.ndarray], Vs: Sequence[np.ndarray],
               lr: float) -> Tuple[np.ndarray, np.ndarray]:
-    """W' = W - lr * (1/P) * sum_p G_p,  G_p = sum_k U_p[k]^T V_p[k];
-    b' = b - lr * (1/P) * sum_p sum_k U_p[k].  Workers p = 0..P-1 in order."""
+    """Eq. 4 with readings Z1-Z4: W' = W - lr * (1/P) * sum_p G_p,
+    G_p = sum_k U_p[k]^T V_p[k] (Eq. 5); b' = b - lr * (1/P) * sum_p sum_k U_p[k].  Workers p = 0..P-1
+    in order."""
     P = len(Us)
     W = np.asarray(W, dtype=np.float64)
     G = np.zeros_like(W)
@@ -181,9 +189,9 @@ def sync_step(W: np.ndarray, b, Us: Sequence[np.ndarray], Vs: Sequence[np.ndarra
 # lines 366-368)
 # --------------------------------------------------------------------------
 def sfb_simulated(W, b, Us, Vs, lr):
-    """Every worker receives the rank-major concatenation [U_1..U_P], [V_1..V_P]
-    (the broadcast, step 2) and applies the reconstructed update locally
-    (step 3).  Returns the replica of worker 0 (all replicas are identical)."""
+    """SFB: every worker receives the rank-major concatenation [U_1..U_P], [V_1..V_P]
+    (the broadcast, step 2) and applies the reconstructed update locally (step 3; Alg. 3 lines 6-8,
+    P:L366-368).  Returns the replica of worker 0 (all replicas are identical)."""
     P = len(Us)
     Ug = np.concatenate([np.asarray(u, np.float64) for u in Us], axis=0)
     Vg = np.concatenate([np.asarray(v, np.float64) for v in Vs], axis=0)
@@ -197,7 +205,8 @@ def sfb_simulated(W, b, Us, Vs, lr):
 # Alg. 3, reading Z7/Z11)
 # --------------------------------------------------------------------------
 def flatten_params(W: np.ndarray, b) -> np.ndarray:
-    """Flat layout of a PS layer: W row-major, then bias."""
+    """Flat layout of a PS layer: W row-major, then bias (the buffer Alg. 1's master updates by parts,
+    P:L210; reading Z11)."""
     parts = [np.asarray(W, np.float64).reshape(-1)]
     if b is not None:
         parts.append(np.asarray(b, np.float64).reshape(-1))
@@ -205,10 +214,10 @@ def flatten_params(W: np.ndarray, b) -> np.ndarray:
 
 
 def ps_step_flat(w: np.ndarray, grads: Sequence[np.ndarray], lr: float) -> np.ndarray:
-    """Parameter-server step on a flat buffer of n elements from P workers'
-    flat gradients: each shard r is collected (summed over workers), updated
-    by alpha = -lr/P, and pushed back (concatenated).  Each index must be
-    owned by exactly one shard."""
+    """Alg. 1's master loop (collect gradients, update the part of the parameters they
+    cover, push the parameters back) on a flat buffer of n elements from P workers' flat gradients:
+    each shard r is collected (summed over workers), updated by alpha = -lr/P, and pushed back
+    (concatenated).  Each index must be owned by exactly one shard."""
     P = len(grads)
     n = w.shape[0]
     out = np.empty(n, dtype=np.float64)
@@ -226,8 +235,8 @@ def ps_step_flat(w: np.ndarray, grads: Sequence[np.ndarray], lr: float) -> np.nd
 
 
 def ps_simulated(W, b, Us, Vs, lr):
-    """Workers form their full gradients (G_p, gb_p) locally and go through
-    the sharded parameter server."""
+    """Alg. 3 lines 1-3: workers form their full gradients (G_p, gb_p) locally, "send
+    them to the master node" and "synchronize" the updated layer (the sharded server of ps_step_flat)."""
     grads = [flatten_params(reconstruct(u, v), np.asarray(u, np.float64).sum(axis=0)
                             if b is not None else None) for u, v in zip(Us, Vs)]
     w1 = ps_step_flat(flatten_params(W, b), grads, lr)
@@ -244,13 +253,14 @@ def ps_simulated(W, b, Us, Vs, lr):
 # master of the output rows [lo_r, hi_r) = O2's shard_range(M, P, r).
 # --------------------------------------------------------------------------
 def row_shard_range(M: int, P: int, rank: int) -> Tuple[int, int]:
-    """Output rows mastered by ``rank``: O2's shard map applied to the M rows."""
+    """Output rows mastered by ``rank``: O2's shard map applied to the M rows (reading Z20 of the
+    "master node" of P:L370-371)."""
     lo, hi, _ = shard_range(M, P, rank)
     return lo, hi
 
 
 def sf_ps_simulated(W, b, Us, Vs, lr):
-    """Every worker p sends its sufficient factors to the masters: to master r
+    """Alg. 3's else-branch: every worker p sends its sufficient factors to the masters: to master r
     the entries of its error messages for r's rows (columns [lo_r, hi_r) of
     U_p) and all of its inputs V_p.  Master r reconstructs its rows of
     sum_p U_p^T V_p, applies W[lo_r:hi_r] += (-lr/P) * (.) (and the bias rows),
@@ -294,8 +304,9 @@ def sf_ps_simulated(W, b, Us, Vs, lr):
 # batch ("converges to the same objective value as a single machine")
 # --------------------------------------------------------------------------
 def concat_batch_sgd(W, b, X_all: np.ndarray, labels_all: np.ndarray, lr: float):
-    """Single worker, all P*K samples, mean CE loss: W' = W - lr dl/dW with
-    dl/dW = sum_samples E a^T (Eq. 5) and E = (softmax - onehot)/(PK)."""
+    """P:L24 ("converges to the same objective value as a single machine"): single worker, all P*K
+    samples, mean CE loss: W' = W - lr dl/dW with dl/dW = sum_samples E a^T (Eq. 5) and
+    E = (softmax - onehot)/(PK)."""
     W = np.asarray(W, np.float64)
     b = np.asarray(b, np.float64)
     X = np.asarray(X_all, np.float64)
@@ -304,9 +315,9 @@ def concat_batch_sgd(W, b, X_all: np.ndarray, labels_all: np.ndarray, lr: float)
 
 
 def worker_factors(W, b, X_all, labels_all, P: int):
-    """Split the concatenated batch contiguously rank-major (reading Z14) and
-    let every worker form its mean-loss factors U_p = (softmax-onehot)/K,
-    V_p = X_p."""
+    """Data parallelism (worker p computes on its own batch D_p): split the concatenated
+    batch contiguously rank-major (reading Z14) and let every worker form its mean-loss factors
+    U_p = (softmax-onehot)/K (E_{i+1}, P:L324), V_p = X_p (a_i)."""
     X = np.asarray(X_all, np.float64)
     K = X.shape[0] // P
     Us, Vs = [], []
@@ -322,8 +333,8 @@ def worker_factors(W, b, X_all, labels_all, P: int):
 # Error metric of reading Z13 (gate on the update, not on W')
 # --------------------------------------------------------------------------
 def update_error(W0, W1_test, W1_ref) -> float:
-    """max_i |dW_test,i - dW_ref,i| / max_i |dW_ref,i| with dW = W' - W0,
-    computed in float64.  Returns 0 when the reference update is all zero and
+    """Reading Z13 (the north_star tolerances are stated on the update): max_i |dW_test,i - dW_ref,i|
+    / max_i |dW_ref,i| with dW = W' - W0, computed in float64.  Returns 0 when the reference update is all zero and
     the test update equals it."""
     W0 = np.asarray(W0, np.float64)
     d_t = np.asarray(W1_test, np.float64) - W0
@@ -370,9 +381,9 @@ def ulp_excuse(W0, W1_ref) -> float:
 
 
 def sync_step_rows(W_rows, b_rows, Us, Vs, lr, rows):
-    """O4 restricted to a subset of output rows m (each row of W' depends only
-    on column m of every U_p), so full-size layers can be checked one sampled
-    row at a time."""
+    """O4 (Eq. 4; Eq. 5) restricted to a subset of output rows m (each row of W'
+    depends only on column m of every U_p), so full-size layers can be checked one sampled row at a
+    time."""
     rows = np.asarray(rows)
     P = len(Us)
     G = np.zeros((len(rows), np.asarray(Vs[0]).shape[1]), dtype=np.float64)
@@ -393,8 +404,8 @@ def sync_step_rows(W_rows, b_rows, Us, Vs, lr, rows):
 # aggregation point; Caffe's SGD solver semantics, decay on every parameter)
 # --------------------------------------------------------------------------
 def sync_step_momentum(W, b, VW, Vb, Us, Vs, lr: float, mu: float, wd: float):
-    """g = (1/P) sum_p G_p;  V' = mu V + lr (g + wd W);  W' = W - V'   (same for the bias).
-    Returns (W', b', VW', Vb')."""
+    """Lambda of Eq. 3 / Alg. 3 line 8 (P:L141, P:L368; reading Z4b): g = (1/P) sum_p G_p;
+    V' = mu V + lr (g + wd W);  W' = W - V'   (same for the bias).  Returns (W', b', VW', Vb')."""
     P = len(Us)
     W = np.asarray(W, np.float64)
     G = np.zeros_like(W)
@@ -414,8 +425,8 @@ def sync_step_momentum(W, b, VW, Vb, Us, Vs, lr: float, mu: float, wd: float):
 
 
 def ps_step_flat_momentum(w, v, grads: Sequence[np.ndarray], lr: float, mu: float, wd: float):
-    """Parameter-server step with momentum/decay on a flat buffer: each shard owner keeps the
-    velocity of its own shard only.  Returns (w', v')."""
+    """Alg. 1's master step with Lambda = momentum/decay (reading Z4b) on a flat
+    buffer: each shard owner keeps the velocity of its own shard only.  Returns (w', v')."""
     P = len(grads)
     w = np.asarray(w, np.float64)
     v = np.asarray(v, np.float64)
@@ -438,7 +449,8 @@ def ps_step_flat_momentum(w, v, grads: Sequence[np.ndarray], lr: float, mu: floa
 # worker's forward of iteration t uses contain exactly the updates of iterations <= t-s-1.
 # --------------------------------------------------------------------------
 def ssp_visible_weights(W0, b0, steps, lr: float, s: int = 1):
-    """steps[t] = (Us, Vs): the sufficient factors every worker produces at iteration t (fixed
+    """SSP at the staleness bound (reading Z19).  steps[t] = (Us, Vs): the
+    sufficient factors every worker produces at iteration t (fixed
     inputs, independent of the parameters).  Returns vis with vis[t] = (W, b) the forward of
     iteration t reads, for t = 0 .. len(steps) + s (the last entries are what remains after all
     updates have been applied, i.e. after a flush)."""
