@@ -87,8 +87,8 @@ def sfb_wire_checks(new_ctx, rank, P, dev):
                   pz.FLAG_INPLACE_FACTORS, pz.FLAG_NVLS_SFB | mnf, mnf):
         cs = new_ctx(flags)
         shapes = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 1000, 4096, 33)]
-        for lid, M_, N_, K_ in shapes:
-            assert cs.register_layer(lid, pz.LAYER_FC, M_, N_, K_) == pz.SCHEME_SFB
+        for lid, M_, N_, K_ in shapes:   # SFB forced: the rule sends the 10 x 64, K = 4 layer to PS at P >= 5
+            assert cs.register_layer(lid, pz.LAYER_FC, M_, N_, K_, True, pz.SCHEME_SFB) == pz.SCHEME_SFB
         path = cs.sfb_path(0)
         assert path >= pz.SFB_PATH_NCCL_SYMM or not (flags & (pz.FLAG_SYMM_SFB | pz.FLAG_NVLS_SFB)), path
         if rank == 0:
@@ -120,8 +120,8 @@ def early_v_checks(new_ctx, rank, P, dev):
         ce = new_ctx(flags)
         keep = []   # FLAG_INPLACE_FACTORS: the factors stay alive until the syncs are done
         shapes = [(0, 128, 256, 8), (1, 10, 64, 4), (2, 1000, 4096, 33)]
-        for lid, M_, N_, K_ in shapes:
-            assert ce.register_layer(lid, pz.LAYER_FC, M_, N_, K_) == pz.SCHEME_SFB
+        for lid, M_, N_, K_ in shapes:   # SFB forced (the 10 x 64 layer is PS by the rule at P >= 5)
+            assert ce.register_layer(lid, pz.LAYER_FC, M_, N_, K_, True, pz.SCHEME_SFB) == pz.SCHEME_SFB
         for it in range(2):
             outs = []
             for lid, M_, N_, K_ in shapes:   # "forward": every layer posts its input
