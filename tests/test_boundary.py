@@ -206,3 +206,15 @@ def test_missing_library_fails_loudly(tmp_path):
     out = subprocess.run([sys.executable, "-c", "import paper_1512_06216_b200"], cwd=tmp_path,
                          capture_output=True, text=True, timeout=120)
     assert out.returncode != 0 and "libposeidon.so is missing" in out.stderr, out.stderr[-1500:]
+
+
+def test_rule_picks_the_multi_gpu_checks_rely_on():
+    """tests/mp_sync_check.py registers these layers with the rule's own pick at every world size the driver
+    runs (2, 4, 8): SFB for the wire / momentum / SSP / full-size layers, and the C2 ip2 layer's switch to the
+    server at P >= 3 (FLAG_SFPS auto-selection).  A layer whose pick changes with P must be forced instead."""
+    for P in (2, 4, 8):
+        for (M, N, K) in [(128, 256, 8), (1000, 4096, 33), (4096, 9216, 256), (96, 130, 8), (40, 72, 4)]:
+            assert pz.choose_scheme(B.LAYER_FC, M, N, K, P)[0] == B.SCHEME_SFB, (M, N, K, P)
+        assert pz.choose_scheme(B.LAYER_FC, 10, 64, 100, P)[0] == (B.SCHEME_SFB if P <= 2 else B.SCHEME_PS)
+    # the 10 x 64, K = 4 wire-check layer flips to PS at P >= 5: mp_sync_check forces SFB on it
+    assert [pz.choose_scheme(B.LAYER_FC, 10, 64, 4, P)[0] for P in (2, 4, 5, 8)] == [1, 1, 0, 0]
