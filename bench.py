@@ -275,11 +275,15 @@ def c1_step(pz, dev):
     wflat = torch.zeros(padded, device=dev)
     stream = torch.cuda.current_stream()
 
+    spin = int(os.environ.get("C1_SPIN_CYCLES", "10000000"))
+
     def gpu_ms(fn):
+        """Device time of one call: a device spin (~5 ms) lets the host enqueue the whole call (the simulated
+        entry points allocate their scratch stream-ordered) before e0 fires, so the events see the GPU work."""
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ts = []
-        for _ in range(51):
-            torch.cuda._sleep(20_000)
+        for _ in range(31):
+            torch.cuda._sleep(spin)
             e0.record(stream)
             fn()
             e1.record(stream)
@@ -287,10 +291,26 @@ def c1_step(pz, dev):
             ts.append(e0.elapsed_time(e1))
         return statistics.median(ts[1:])
 
-    out = {"workload": "C1: FC 256->128 (M=128, N=256), K=8, P=2 simulated workers, one sync step"}
-    out["gpu_sfb_tf32_ms"] = gpu_ms(lambda: pz.sfb_simulated(Ud, Vd, P, K, M, N, Wd, bd, lr, recon=pz.RECON_TF32))
-    out["gpu_sfb_fp32_ms"] = gpu_ms(lambda: pz.sfb_simulated(Ud, Vd, P, K, M, N, Wd, bd, lr, recon=pz.RECON_FP32))
-    out["gpu_ps_ms"] = gpu_ms(lambda: pz.ps_simulated(gd, P, wflat, n, lr))
+    def call_ms(fn):
+        """Host wall time of one call through the binding until its result is ready (what a caller waits)."""
+        ts = []
+        for _ in range(31):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        return statistics.median(ts[1:])
+
+    out = {"workload": "C1: FC 256->128 (M=128, N=256), K=8, P=2 simulated workers, one sync step",
+           "note": "gpu_*: device time of the call; call_*: host wall time until the result is ready (the "
+                   "simulated entry points are test helpers that allocate scratch per call)"}
+    sfb_tf32 = lambda: pz.sfb_simulated(Ud, Vd, P, K, M, N, Wd, bd, lr, recon=pz.RECON_TF32)  # noqa: E731
+    sfb_fp32 = lambda: pz.sfb_simulated(Ud, Vd, P, K, M, N, Wd, bd, lr, recon=pz.RECON_FP32)  # noqa: E731
+    ps = lambda: pz.ps_simulated(gd, P, wflat, n, lr)  # noqa: E731
+    for name, fn in (("sfb_tf32", sfb_tf32), ("sfb_fp32", sfb_fp32), ("ps", ps)):
+        out[f"gpu_{name}_ms"] = gpu_ms(fn)
+        out[f"call_{name}_ms"] = call_ms(fn)
 
     def cpu_ms(threads):
         with threadpool_limits(threads):
