@@ -5,12 +5,24 @@
 //
 // Ug: P blocks of M x ldk, Vg: P blocks of N x ldk (K contiguous, ldk =
 // roundup(K,4)): every worker's sufficient factors, rank-major, exactly as
-// the all-gather leaves them.  Both operands are K-major: on sm_100a the
-// MN-major (transposed) TF32 variant of tcgen05.mma was measured to produce
-// all-zero accumulators (tools/tc_probe.cu), so K3 transposes the factors
-// while packing them and the reduction index (p, k) is contiguous in memory.
+// the all-gather leaves them (K-major operands, packed by K3).  Round 2 adds
+// MN-major operands (template MNK): the factors as the layer wrote them,
+// U [P][K][M] / V [P][K][N], read through 4D TMA maps in the SWIZZLE_128B_BASE32B
+// layout (UMMA layout type 1, the only MN-major TF32 layout; tools/tc_probe_mn.cu)
+// -- no pack at all at P = 1 (POSEIDON_FLAG_INPLACE_MN).  Round 1's probe of the
+// MN-major TF32 variant used the 128B layout and read zeros; type 1 is exact.
 //
-// Design (sm_100a, one CTA per SM, persistent, 256 threads):
+// Two kernels live here:
+//  * recon_tcgen05_2sm_kernel (production, below): a 2-CTA cluster computes a
+//    256 x 256 tile with tcgen05.mma.cta_group::2; 12 warps -- warp 0 operand
+//    TMA producer, warp 1 MMA issuer, warp 2 W-chunk TMA producer (lanes 1-31:
+//    the bias update), warp 3 TMEM-empty relay (lanes 1-31: in-place bias column
+//    sums), warps 4-11 two epilogue groups on alternate 32-column W chunks.
+//    Ring configurations by slab count (32 k each): <4 stages, 6 W slots> for
+//    <= 8 slabs (HBM regime), <5, 4> for 9-31, the register-path RW epilogue for
+//    >= 32 (tensor regime); momentum variants carry the velocity in the W slot.
+//  * recon_tcgen05_kernel (round 1; kept as the POSEIDON_K1_VARIANT=1 baseline and
+//    for the debug dump of the tests), one CTA per SM, persistent:
 //   warp 0      TMA producer: Ug/Vg slabs of BK=32 k (128 B) -> 3-stage smem ring
 //               (128B swizzle; one 32x128 box for A, one 32x256 box for B; 48 KB/stage)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
@@ -21,8 +33,8 @@
 //               on the accumulator, so its HBM read overlaps the MMA)
 //   warps 4-7   epilogue: tcgen05.ld 32 accumulator columns per row,
 //               W = fmaf(alpha, acc, W) in shared memory, TMA store back.
-// The epilogue of tile i overlaps the MMAs of tile i+1 (TMEM double buffer),
-// which is what keeps the kernel at the HBM roofline when P*K is small
+// In both, the epilogue of tile i overlaps the MMAs of tile i+1 (TMEM double
+// buffer), which is what keeps the kernel at the HBM roofline when P*K is small
 // (W read-modify-write, 8 B/element) and at the tensor roofline when it is
 // large.  Tile order: N-tile fastest within an M-tile row.
 #include <cuda.h>
