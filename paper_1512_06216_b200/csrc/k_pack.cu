@@ -5,8 +5,9 @@
 // The factors already exist after the layer's backward (grad_out G [K x M] and
 // the layer input X [K x N], row-major).  K3 writes them TRANSPOSED into this
 // rank's slot of the gather buffers — [M x ldk] and [N x ldk], K contiguous,
-// ldk = roundup(K,4) — because the tensor cores consume TF32 operands K-major
-// (reading D1 in DESIGN.md), optionally rounding to TF32 (round-to-nearest,
+// ldk = roundup(K,4) — the K-major operands K1 reads fastest (reading D1 in
+// DESIGN.md; round 2: K1 also reads MN-major factors in place, so at P = 1 the
+// bench runs no K3 at all), optionally rounding to TF32 (round-to-nearest,
 // cvt.rna; the tensor core would otherwise truncate, reading Z12).  For U it
 // also emits the per-worker column sums sum_k G[k][m] (of the unrounded
 // values) that the bias update needs, so the bias costs M floats on the wire
